@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: distance queries/s (+ preprocessing seconds) on B200.
+
+Contract:
+  python bench.py --gpus N --steps K --warmup W [--impl ours|reference]
+Under torchrun (N > 1) each rank drives one GPU; rank 0 prints ONE JSON line.
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on that
+fits one GPU): Delaunay triangulation of 262,144 uniform points, integer
+weights 1..1024, k = 256 components, batches of 1,000,000 random pairs.
+A step = one batch of 1M queries through the hot path. Every rank builds
+the oracle (partition on the host, phases 2-3 on its GPU) and answers its
+own 1M-pair batches ("scaling": "weak", queries sharded by rank, no data-path
+collective: the query path does not need one when every GPU holds the
+tables — SURVEY §8e(i)).
+
+value  device-resident queries/s over all ranks (pairs already in HBM,
+       CUDA events on the launching stream, max over ranks)
+e2e    the same batches through psp_gpu_query_batch with pinned host pairs:
+       H2D of 8 B/pair and D2H of 8 B/distance inside the timed region
+Inputs (the 4.9 GB boundary-graph table) are far larger than the 126 MB L2,
+so no flush is needed between steps; each step uses a fresh slice of pairs.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "distance queries/sec + preprocessing s (1M-vertex planar) at 1/2/4/8 B200 vs CPU"
+CONFIG = "delaunay262k_k256"
+BATCH = 1_000_000
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def query_bytes_and_ops(o, v1, v2):
+    """Algorithmic bytes / ops per query: 4(B1 B2 + B1 + B2) + 28
+    bytes (u32 tables, no reuse; 8 B pair in, 4 B out, 16 B id lookups) and
+    B1 B2 + B2 relaxations (the reference's minplus_ops, src/query.cpp:73)."""
+    bsz = np.diff(o.boundary_offset).astype(np.float64)
+    comp = o.assignment[o.permutation]
+    b1 = bsz[comp[v1]]
+    b2 = bsz[comp[v2]]
+    byts = 4.0 * (b1 * b2 + b1 + b2) + 28.0
+    ops = b1 * b2 + b2
+    return float(byts.sum()), float(ops.sum())
+
+
+# ---------------------------------------------------------------- ours ----
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_1503_07192_b200 as P
+    from paper_1503_07192_b200 import graphs
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    t0 = time.time()
+    g, cfg = graphs.make(args.config)
+    gen_s = time.time() - t0
+    threads = max(1, (os.cpu_count() or 8) // max(1, world))
+    ctx = P.Context(local, 0, 1)
+    o = P.build_oracle(g, cfg["k"], threads, 0, ctx=ctx)
+    st = o.stats
+
+    stream = torch.cuda.Stream(device=dev)
+    batch = args.batch
+    nsteps = args.warmup + args.steps
+    # distinct pair slices per step and per rank (weak scaling)
+    v1, v2 = P.random_pairs(g.n, batch * nsteps, 1000 + rank)
+    d_v1 = torch.from_numpy(v1.view(np.int32)).to(dev)
+    d_v2 = torch.from_numpy(v2.view(np.int32)).to(dev)
+    d_out = torch.empty(batch, dtype=torch.float64, device=dev)
+
+    def step(i):
+        o.batch_query_device(d_v1[i * batch:].data_ptr(), d_v2[i * batch:].data_ptr(),
+                             d_out.data_ptr(), batch, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.warmup, nsteps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dev_ms = ev0.elapsed_time(ev1)
+    barrier()
+    # algorithmic bytes of the timed launches
+    tb, tops = query_bytes_and_ops(o, v1[args.warmup * batch:], v2[args.warmup * batch:])
+
+    # ---- e2e through the public host API (pinned host buffers)
+    h_v1 = torch.from_numpy(v1.view(np.int32)).pin_memory()
+    h_v2 = torch.from_numpy(v2.view(np.int32)).pin_memory()
+    h_out = torch.empty(batch, dtype=torch.float64).pin_memory()
+    lib = P._lib.lib()
+
+    def e2e_step(i):
+        P._lib.check(lib.psp_gpu_query_batch(
+            o.h, batch, h_v1[i * batch:].data_ptr(), h_v2[i * batch:].data_ptr(),
+            h_out.data_ptr(), None))
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    barrier()
+    t_e = time.perf_counter()
+    for i in range(args.warmup, nsteps):
+        e2e_step(i)
+    e2e_ms = (time.perf_counter() - t_e) * 1e3
+    barrier()
+
+    # correctness spot check of the last batch against the e2e path
+    ref_last = h_out.numpy().copy()
+    step(nsteps - 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy(), ref_last), "device/e2e query mismatch"
+
+    # max over ranks
+    vals = torch.tensor([dev_ms, e2e_ms, st["k2_device_ms"], st["k1_device_ms"]],
+                        dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms, k2_ms, k1_ms = vals.tolist()
+
+    if rank != 0:
+        return None
+    peaks = measured_peaks()
+    total_q = batch * args.steps * world
+    qps = total_q / (dev_ms / 1e3)
+    e2e_qps = total_q / (e2e_ms / 1e3)
+    per_launch_ms = dev_ms / args.steps
+    achieved_gbs = (tb / args.steps) / (per_launch_ms / 1e3) / 1e9
+    peak_u32, clock_mhz = ctx.minplus_peak(P.VALUE_U32)
+    k2_rate = st["k2_relaxations"] / (st["k2_device_ms"] / 1e3) if st["k2_device_ms"] else 0.0
+    line = {
+        "metric": METRIC,
+        "value": round(qps, 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32" if o.value_kind == P.VALUE_U32 else "f32",
+        "data": "synthetic (seeded Delaunay + mt19937_64 pairs)",
+        "config": {"workload": f"{args.config}: Delaunay n={g.n} m={g.m} k={cfg['k']} b={o.b}, "
+                               f"{batch} random pairs per step per GPU",
+                   "batch_per_gpu": batch, "l2_policy": "inputs >> L2 (BG table "
+                   f"{o.b * o.b * 4 / 1e9:.1f} GB), fresh pairs each step",
+                   "parallelism": f"queries sharded over {world} GPU(s), tables replicated"},
+        "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s",
+                "h2d_bytes_per_step": 8 * batch, "d2h_bytes_per_step": 8 * batch},
+        "gpu_launches": args.steps,
+        "roofline": {"kernel": "query_warp (K3)", "bound": "hbm",
+                     "achieved": round(achieved_gbs, 1),
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved_gbs / peaks["hbm_gbs"], 4),
+                     "traffic": None, "peak_source": peaks["source"],
+                     "bytes_per_query": round(tb / (batch * args.steps), 1),
+                     "alu_frac": round((tops / args.steps) / (per_launch_ms / 1e3) / peak_u32, 4)},
+        "preprocessing": {
+            "graph_gen_s": round(gen_s, 2),
+            "partition_s": round(st["partition_ms"] / 1e3, 3),
+            "component_apsp_s": round(st["component_apsp_ms"] / 1e3, 3),
+            "boundary_s": round(st["boundary_ms"] / 1e3, 3),
+            "k1_device_s": round(k1_ms / 1e3, 4), "k2_device_s": round(k2_ms / 1e3, 4),
+            "k2_relax_per_s": k2_rate, "k2_alu_frac": round(k2_rate / peak_u32, 4),
+            "minplus_peak_relax_per_s": peak_u32, "peak_source": "measured in-run "
+            "(minplus_peak_kernel, VIADDMNMX.U32)", "host_threads": threads,
+            "b": o.b, "bg_edges": st["bg_edges"], "stored_entries": st["stored_entries"]},
+        "clocks": clk.summary(),
+    }
+    if args.cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(g, cfg, args)
+    return line
+
+
+# ----------------------------------------------------------- reference ----
+def reference_oracle(g, cfg, workers):
+    import oracle
+    R = oracle.RefLib()
+    rg = R.graph(g.n, g.eu, g.ev, g.ew)
+    t0 = time.time()
+    ro = rg.build_oracle(cfg["k"], workers, 0)
+    return R, ro, time.time() - t0
+
+
+def cpu_baseline(g, cfg, args, sample=100_000):
+    """The reference's own CPU implementation (oracle/_ref, unmodified
+    sources) on this box's host cores: full build_oracle, then batch_query
+    over a bounded sample of the same random-pair workload."""
+    import paper_1503_07192_b200 as P
+    cores = os.cpu_count() or 1
+    R, ro, build_s = reference_oracle(g, cfg, cores)
+    v1, v2 = P.random_pairs(g.n, sample, 77)
+    ro.batch_query(v1[:1000], v2[:1000], cores)
+    t0 = time.perf_counter()
+    ro.batch_query(v1, v2, cores)
+    qs = sample / (time.perf_counter() - t0)
+    return {"value": round(qs, 1), "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": f"{sample} random pairs on the full reference oracle (build_oracle with "
+                      f"{cores} workers took {build_s:.1f} s: partition "
+                      f"{ro.stats['partition_ms'] / 1e3:.1f} s, component APSP "
+                      f"{ro.stats['component_apsp_ms'] / 1e3:.1f} s, boundary "
+                      f"{ro.stats['boundary_ms'] / 1e3:.1f} s)",
+            "build_s": round(build_s, 2),
+            "phases_ms": {k: ro.stats[k] for k in ("partition_ms", "component_apsp_ms",
+                                                   "boundary_ms")}}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import paper_1503_07192_b200 as P  # tooling only: graph + pair generators
+    from paper_1503_07192_b200 import graphs
+    g, cfg = graphs.make(args.config)
+    cores = os.cpu_count() or 1
+    R, ro, build_s = reference_oracle(g, cfg, cores)
+    sample = args.ref_sample
+    v1, v2 = P.random_pairs(g.n, sample * (args.warmup + args.steps), 1000)
+    for i in range(args.warmup):
+        ro.batch_query(v1[i * sample:(i + 1) * sample], v2[i * sample:(i + 1) * sample], cores)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        ro.batch_query(v1[i * sample:(i + 1) * sample], v2[i * sample:(i + 1) * sample], cores)
+    dt = time.perf_counter() - t0
+    qps = sample * args.steps / dt
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(qps, 1), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Delaunay + mt19937_64 pairs)",
+        "config": {"workload": f"{args.config}: Delaunay n={g.n} k={cfg['k']} b={ro.b}, "
+                               f"{sample} random pairs per step (bounded sample)"},
+        "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": cores,
+                         "kind": "reference",
+                         "sample": f"{sample} pairs per step, batch_query with {cores} threads"},
+        "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "preprocessing": {"build_s": round(build_s, 2),
+                          "partition_s": ro.stats["partition_ms"] / 1e3,
+                          "component_apsp_s": ro.stats["component_apsp_ms"] / 1e3,
+                          "boundary_s": ro.stats["boundary_ms"] / 1e3, "workers": cores},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--ref-sample", type=int, default=100_000)
+    ap.add_argument("--cpu-baseline", dest="cpu_baseline", action="store_true", default=True)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

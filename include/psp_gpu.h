@@ -1,0 +1,203 @@
+/* psp_gpu.h — C-ABI of the B200-native preprocessing + query engine for the
+ * partitioned planar shortest-path oracle (Chapuis & Djidjev, arXiv 1503.07192).
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * `psp` (/root/reference/proj). Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj). Signatures
+ * use only plain pointers and sizes; a C++ shim restores the reference's
+ * types (psp::Graph, psp::Oracle, psp::Matrix, exceptions) on top — see
+ * INTEGRATION.md.
+ *
+ * Semantics shared by all entry points
+ *  - Distances cross the boundary as IEEE f64 exactly like the reference
+ *    (include/psp/graph.hpp:14): unreachable = +infinity.
+ *  - Inside the library distances are u32 (exact: integral weights, or dyadic
+ *    weights w*2^q integral, "fixed point") or f32 (tolerance path, relative
+ *    error <= 1e-5). PSP_VALUE_AUTO picks u32 whenever it is exact.
+ *  - Errors: every call returns a psp_status; psp_gpu_last_error() gives a
+ *    thread-local message. The shim maps PSP_EINVAL / PSP_EOVERFLOW to
+ *    std::invalid_argument, PSP_EGRAPH to psp::GraphInvariantError and the
+ *    rest to std::runtime_error (reference conventions, include/psp/errors.hpp).
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with PSP_ECUDA.
+ */
+#ifndef PSP_GPU_H
+#define PSP_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSP_GPU_ABI_VERSION 1
+
+typedef enum psp_status {
+    PSP_OK = 0,
+    PSP_EINVAL = 1,     /* bad argument (reference: std::invalid_argument)      */
+    PSP_ENOMEM = 2,     /* device or host allocation failed                      */
+    PSP_ECUDA = 3,      /* CUDA runtime error / no device                        */
+    PSP_ENCCL = 4,      /* NCCL error (multi-GPU)                                */
+    PSP_EOVERFLOW = 5,  /* u32 requested but weights not representable exactly   */
+    PSP_EGRAPH = 6      /* graph invariant violated (psp::GraphInvariantError)   */
+} psp_status;
+
+enum {
+    PSP_VALUE_AUTO = 0, /* u32 when exact (integral or dyadic weights), else f32 */
+    PSP_VALUE_U32 = 1,  /* exact; fails with PSP_EOVERFLOW when not exact         */
+    PSP_VALUE_F32 = 2   /* tolerance path                                         */
+};
+
+typedef struct psp_gpu_ctx psp_gpu_ctx;
+typedef struct psp_gpu_oracle psp_gpu_oracle;
+
+/* BuildStats (include/psp/oracle.hpp:29-37) plus device-side detail. */
+typedef struct psp_build_stats {
+    double partition_ms;       /* phase 1: partition + reorder (host)          */
+    double component_apsp_ms;  /* phase 2: upload + K0 + K1 (wall clock)       */
+    double boundary_ms;        /* phase 3: BG init + K2 + query tables (wall)  */
+    uint64_t boundary_total;   /* b                                            */
+    uint64_t bg_edges;         /* cross edges + finite clique pairs            */
+    uint64_t stored_entries;   /* sum |C|^2 + |B(C)| * b                       */
+    uint64_t peak_table_entries_per_worker;
+    /* device detail (CUDA events on the build stream) */
+    double k1_device_ms;       /* batched component Floyd-Warshall             */
+    double k2_device_ms;       /* boundary-graph Floyd-Warshall                */
+    double init_device_ms;     /* K0 + BG init + query-table extraction        */
+    uint64_t k1_relaxations;   /* min-plus relaxations executed by K1 (padded) */
+    uint64_t k2_relaxations;   /* min-plus relaxations executed by K2 (padded) */
+    int32_t value_kind;        /* PSP_VALUE_U32 or PSP_VALUE_F32               */
+    int32_t fixed_point_shift; /* q: device value = weight * 2^q (u32 only)    */
+    uint64_t device_bytes;     /* device memory held by the oracle             */
+} psp_build_stats;
+
+typedef struct psp_oracle_info {
+    uint64_t n;
+    uint32_t k;
+    uint64_t b;
+    int32_t value_kind;
+    int32_t fixed_point_shift;
+    int32_t device;
+    int32_t tile; /* Floyd-Warshall tile edge T */
+} psp_oracle_info;
+
+/* ------------------------------------------------------------ runtime -- */
+int psp_gpu_abi_version(void);
+const char* psp_gpu_last_error(void);
+int psp_gpu_device_count(void);
+
+/* One context per GPU (one process per GPU). `rank`/`world` describe the
+ * job; world == 1 is a single GPU. For world > 1 pass the 128-byte NCCL
+ * unique id produced by psp_gpu_nccl_unique_id on rank 0 and broadcast by
+ * the caller (e.g. through torch.distributed). */
+psp_status psp_gpu_ctx_create(int device, int rank, int world, const void* nccl_id,
+                              psp_gpu_ctx** out);
+void psp_gpu_ctx_destroy(psp_gpu_ctx* ctx);
+psp_status psp_gpu_nccl_unique_id(void* out128);
+/* The context's CUDA stream (cudaStream_t) for callers that time kernels. */
+void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx);
+
+/* ------------------------------------------------------- preprocessing -- */
+/* psp::build_oracle (include/psp/oracle.hpp:85-86, src/oracle.cpp:144-194):
+ * partition + reorder on the host (identical assignment to the reference's
+ * partition_graph, include/psp/partition.hpp:42), then Phase 2 (K0+K1) and
+ * Phase 3 (BG init + K2) on the device. Edges are undirected, listed once
+ * (psp::Graph(n, edges), include/psp/graph.hpp:50). workers < 1 or k outside
+ * 1..n -> PSP_EINVAL (src/oracle.cpp:146, src/partition.cpp:261-262);
+ * `workers` sizes the host partitioner's thread pool only and never changes
+ * the result (include/psp/oracle.hpp:80-84). */
+psp_status psp_gpu_build_oracle(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* eu,
+                                const uint32_t* ev, const double* ew, uint32_t k,
+                                uint32_t workers, uint64_t seed, int value_kind,
+                                psp_gpu_oracle** out, psp_build_stats* stats);
+
+/* Same pipeline with the partition supplied by the caller as a component
+ * assignment in ORIGINAL ids (psp::make_partition semantics,
+ * include/psp/partition.hpp:61): boundary flags and the boundary-first
+ * permutation are derived here exactly as src/partition.cpp:196-240 does. */
+psp_status psp_gpu_build_partitioned(psp_gpu_ctx* ctx, uint64_t n, uint64_t m,
+                                     const uint32_t* eu, const uint32_t* ev, const double* ew,
+                                     uint32_t k, const uint32_t* assignment, int value_kind,
+                                     psp_gpu_oracle** out, psp_build_stats* stats);
+
+void psp_gpu_oracle_free(psp_gpu_oracle* o);
+psp_status psp_gpu_oracle_info(const psp_gpu_oracle* o, psp_oracle_info* out);
+
+/* Oracle id maps (include/psp/oracle.hpp:47-62). Any pointer may be NULL.
+ * permutation/inverse (n), assignment + boundary_flags in reordered ids (n),
+ * component_offset / boundary_offset (k+1), boundary_vertex (b). */
+psp_status psp_gpu_oracle_ids(const psp_gpu_oracle* o, uint32_t* permutation,
+                              uint32_t* inverse_permutation, uint32_t* assignment,
+                              uint8_t* boundary_flags, uint64_t* component_offset,
+                              uint64_t* boundary_offset, uint32_t* boundary_vertex);
+
+/* Materialise Oracle::component_tables[c] (|C| x |C|, row-major) and
+ * Oracle::boundary_tables[c] (|B(C)| x b) as f64, for parity checks and for
+ * persisting through save_oracle (include/psp/oracle_io.hpp). */
+psp_status psp_gpu_export_component(const psp_gpu_oracle* o, uint32_t c, double* dst);
+psp_status psp_gpu_export_boundary_rows(const psp_gpu_oracle* o, uint32_t c, double* dst);
+
+/* ------------------------------------------------------------- queries -- */
+/* psp::batch_query (include/psp/query.hpp:45-46, src/query.cpp:106-114) on
+ * HOST arrays: ids in the original space, distances out as f64 (+inf when
+ * unreachable), optional minplus_ops = |B(C1)|*|B(C2)| + |B(C2)|
+ * (src/query.cpp:73). Host<->device copies happen inside the call. Any id
+ * >= n -> PSP_EINVAL and no output (src/query.cpp:30). */
+psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
+                               const uint32_t* v2, double* dist, uint64_t* minplus_ops);
+
+/* Device-resident variant: v1, v2, dist are DEVICE pointers on the oracle's
+ * GPU; enqueued on `stream` (a cudaStream_t, NULL = the context stream) and
+ * returns without synchronising. Ids are not range-checked here. */
+psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
+                                      const uint32_t* v1, const uint32_t* v2, double* dist,
+                                      void* stream);
+
+/* ---------------------------------------------------------- primitives -- */
+/* psp::apsp_dense (include/psp/shortest_paths.hpp:43): dense APSP of one
+ * graph on the device (K0 + K1 with a batch of one). block_size is the
+ * reference's CPU tiling hint: ignored except that 0 -> PSP_EINVAL
+ * (src/shortest_paths.cpp:131). out: n*n f64 row-major. */
+psp_status psp_gpu_apsp_dense(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* eu,
+                              const uint32_t* ev, const double* ew, uint64_t block_size,
+                              int value_kind, double* out);
+
+/* psp::boundary_apsp (include/psp/oracle.hpp:94-96): all-pairs distances of
+ * a boundary graph given as an edge list over b vertices; out is b*b f64,
+ * rows in boundary-id order, i.e. the concatenation of the reference's
+ * per-component |B(C)| x b matrices. */
+psp_status psp_gpu_boundary_apsp(psp_gpu_ctx* ctx, uint64_t b, uint64_t m, const uint32_t* eu,
+                                 const uint32_t* ev, const double* ew, int value_kind,
+                                 double* out);
+
+/* Measured min-plus ALU peak of this GPU (relaxations/s) for the roofline:
+ * kind PSP_VALUE_U32 (VIADDMNMX) or PSP_VALUE_F32 (FADD + FMNMX). */
+psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_per_s,
+                                double* sm_clock_mhz);
+
+/* ------------------------------------------------------- host helpers -- */
+/* psp::partition_graph (include/psp/partition.hpp:42, src/partition.cpp:
+ * 259-450): identical assignment for identical (graph, k, seed); the eight
+ * independent restarts run on up to `threads` host threads. */
+psp_status psp_partition_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                               const double* ew, uint32_t k, uint64_t seed, uint32_t threads,
+                               uint32_t* assignment);
+
+/* Synthetic inputs: psp::generate_grid / generate_triangulated_grid
+ * (include/psp/generators.hpp:24-30; kind 0 / 1; unit != 0 -> unit weights,
+ * else the uniform 1/1024 lattice on [lo, hi]). Call with eu == NULL to get
+ * the edge count in *m. */
+psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, double lo,
+                             double hi, uint64_t seed, uint64_t* m, uint32_t* eu, uint32_t* ev,
+                             double* ew);
+
+/* ref::random_pairs / the CLI's random_pairs (tests/support/reference.hpp:
+ * 80-91, tools/psp_main.cpp:108-120): mt19937_64, v1 = rng() % n then v2. */
+void psp_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSP_GPU_H */

@@ -1,0 +1,284 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// A thin extern "C" wrapper over the UNMODIFIED reference library (`psp`,
+// compiled straight from /root/reference/proj/src/*.cpp by oracle/Makefile
+// into oracle/_ref/libpspref.so). Python tests and bench.py's CPU arm reach
+// the reference through these entry points with ctypes; nothing here
+// re-implements reference behaviour, it only marshals plain arrays in and out.
+//
+// Reference interfaces wrapped (paths under /root/reference/proj):
+//   generate_grid / generate_triangulated_grid   include/psp/generators.hpp:24-30
+//   Graph(n, edges)                              include/psp/graph.hpp:50
+//   partition_graph / reorder_vertices           include/psp/partition.hpp:42,57
+//   build_oracle + BuildStats                    include/psp/oracle.hpp:29-37,85-86
+//   build_boundary_graph / boundary_apsp         include/psp/oracle.hpp:90-96
+//   apsp_dense / dijkstra_sssp                   include/psp/shortest_paths.hpp:39-43
+//   query / batch_query                          include/psp/query.hpp:36-46
+
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "psp/generators.hpp"
+#include "psp/graph.hpp"
+#include "psp/oracle.hpp"
+#include "psp/partition.hpp"
+#include "psp/query.hpp"
+#include "psp/shortest_paths.hpp"
+#include "support/reference.hpp"  // ref::random_pairs (tests/support/reference.hpp:80-91)
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    } catch (...) {
+        g_err = "unknown C++ exception";
+        return 1;
+    }
+}
+
+struct RefGraph {
+    psp::Graph g;
+};
+
+struct RefOracle {
+    psp::Oracle o;
+    psp::BuildStats stats;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+void ref_graph_free(void* g) { delete static_cast<RefGraph*>(g); }
+void ref_oracle_free(void* o) { delete static_cast<RefOracle*>(o); }
+
+// kind: 0 grid, 1 triangulated grid. unit != 0 selects WeightModel::unit().
+int ref_generate(int kind, uint64_t rows, uint64_t cols, int unit, double lo, double hi,
+                 uint64_t seed, void** out) {
+    return guarded([&] {
+        const psp::WeightModel wm = unit ? psp::WeightModel::unit() : psp::WeightModel::uniform(lo, hi);
+        auto* rg = new RefGraph;
+        rg->g = kind == 0 ? psp::generate_grid(rows, cols, wm, seed)
+                          : psp::generate_triangulated_grid(rows, cols, wm, seed);
+        *out = rg;
+    });
+}
+
+int ref_graph_from_edges(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                         const double* ew, void** out) {
+    return guarded([&] {
+        std::vector<psp::Edge> edges(m);
+        for (uint64_t i = 0; i < m; ++i) edges[i] = {eu[i], ev[i], ew[i]};
+        auto* rg = new RefGraph;
+        rg->g = psp::Graph(n, edges);
+        *out = rg;
+    });
+}
+
+uint64_t ref_graph_n(const void* g) { return static_cast<const RefGraph*>(g)->g.num_vertices(); }
+uint64_t ref_graph_m(const void* g) { return static_cast<const RefGraph*>(g)->g.num_edges(); }
+
+// Edges with u < v in lexicographic order (Graph::edge_list, graph.hpp:66).
+int ref_graph_edges(const void* g, uint32_t* eu, uint32_t* ev, double* ew) {
+    return guarded([&] {
+        const auto el = static_cast<const RefGraph*>(g)->g.edge_list();
+        for (size_t i = 0; i < el.size(); ++i) {
+            eu[i] = el[i].u;
+            ev[i] = el[i].v;
+            ew[i] = el[i].weight;
+        }
+    });
+}
+
+int ref_partition(const void* g, uint32_t k, uint64_t seed, uint32_t* assignment,
+                  double* elapsed_ms) {
+    return guarded([&] {
+        auto t0 = std::chrono::steady_clock::now();
+        psp::Partition p = psp::partition_graph(static_cast<const RefGraph*>(g)->g, k, seed);
+        if (elapsed_ms)
+            *elapsed_ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        std::memcpy(assignment, p.assignment.data(), p.assignment.size() * sizeof(uint32_t));
+    });
+}
+
+int ref_apsp_dense(const void* g, uint64_t block, double* out) {
+    return guarded([&] {
+        psp::Matrix m = psp::apsp_dense(static_cast<const RefGraph*>(g)->g, block);
+        std::memcpy(out, m.data().data(), m.data().size() * sizeof(double));
+    });
+}
+
+int ref_dijkstra(const void* g, uint32_t src, double* out) {
+    return guarded([&] {
+        auto d = psp::dijkstra_sssp(static_cast<const RefGraph*>(g)->g, src);
+        std::memcpy(out, d.data(), d.size() * sizeof(double));
+    });
+}
+
+// stats: partition_ms, component_apsp_ms, boundary_ms, boundary_total,
+// bg_edges, stored_entries, peak_table_entries_per_worker (7 doubles).
+int ref_build_oracle(const void* g, uint32_t k, uint32_t workers, uint64_t seed, double* stats,
+                     void** out) {
+    return guarded([&] {
+        auto* ro = new RefOracle;
+        try {
+            ro->o = psp::build_oracle(static_cast<const RefGraph*>(g)->g, k, workers, seed,
+                                      &ro->stats);
+        } catch (...) {
+            delete ro;
+            throw;
+        }
+        if (stats) {
+            stats[0] = ro->stats.partition_ms;
+            stats[1] = ro->stats.component_apsp_ms;
+            stats[2] = ro->stats.boundary_ms;
+            stats[3] = static_cast<double>(ro->stats.boundary_total);
+            stats[4] = static_cast<double>(ro->stats.bg_edges);
+            stats[5] = static_cast<double>(ro->stats.stored_entries);
+            stats[6] = static_cast<double>(ro->stats.peak_table_entries_per_worker);
+        }
+        *out = ro;
+    });
+}
+
+// info: n, k, b
+void ref_oracle_info(const void* o, uint64_t* info) {
+    const psp::Oracle& r = static_cast<const RefOracle*>(o)->o;
+    info[0] = r.n;
+    info[1] = r.k;
+    info[2] = r.b();
+}
+
+// permutation (n), reordered assignment (n), component_offset (k+1),
+// boundary_offset (k+1), boundary_vertex (b), boundary_flags (n, reordered).
+void ref_oracle_ids(const void* o, uint32_t* perm, uint32_t* assign, uint64_t* comp_off,
+                    uint64_t* bnd_off, uint32_t* bvert, uint8_t* flags) {
+    const psp::Oracle& r = static_cast<const RefOracle*>(o)->o;
+    for (size_t i = 0; i < r.n; ++i) {
+        perm[i] = r.permutation[i];
+        assign[i] = r.partition.assignment[i];
+        flags[i] = r.partition.boundary_flags[i];
+    }
+    for (size_t c = 0; c <= r.k; ++c) {
+        comp_off[c] = r.component_offset[c];
+        bnd_off[c] = r.boundary_offset[c];
+    }
+    for (size_t i = 0; i < r.b(); ++i) bvert[i] = r.boundary_vertex[i];
+}
+
+void ref_oracle_component(const void* o, uint32_t c, double* out) {
+    const psp::Matrix& m = static_cast<const RefOracle*>(o)->o.component_tables[c];
+    std::memcpy(out, m.data().data(), m.data().size() * sizeof(double));
+}
+
+void ref_oracle_boundary_rows(const void* o, uint32_t c, double* out) {
+    const psp::Matrix& m = static_cast<const RefOracle*>(o)->o.boundary_tables[c];
+    std::memcpy(out, m.data().data(), m.data().size() * sizeof(double));
+}
+
+// dist (count doubles); ops (count u64, minplus_ops) may be null.
+int ref_batch_query(const void* o, uint64_t count, const uint32_t* v1, const uint32_t* v2,
+                    uint32_t workers, double* dist, uint64_t* ops, double* elapsed_ms) {
+    return guarded([&] {
+        std::vector<std::pair<psp::VertexId, psp::VertexId>> pairs(count);
+        for (uint64_t i = 0; i < count; ++i) pairs[i] = {v1[i], v2[i]};
+        auto t0 = std::chrono::steady_clock::now();
+        auto res = psp::batch_query(static_cast<const RefOracle*>(o)->o, pairs, workers);
+        if (elapsed_ms)
+            *elapsed_ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        for (uint64_t i = 0; i < count; ++i) {
+            dist[i] = res[i].distance;
+            if (ops) ops[i] = res[i].stats.minplus_ops;
+        }
+    });
+}
+
+// Phase-3 sampling for configurations whose full f64 boundary tables exceed
+// host RAM: partition + reorder + component APSP in full,
+// build the boundary graph, then time `rows` Dijkstra runs on it.
+// times: partition_ms, component_apsp_ms, bg_build_ms, sampled_dijkstra_ms
+// info: b, bg_edges
+int ref_sampled_build(const void* g, uint32_t k, uint32_t workers, uint64_t seed, uint32_t rows,
+                      uint64_t sample_seed, double* times, uint64_t* info) {
+    return guarded([&] {
+        using Clock = std::chrono::steady_clock;
+        auto ms = [](Clock::time_point t) {
+            return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+        };
+        const psp::Graph& gg = static_cast<const RefGraph*>(g)->g;
+        auto t0 = Clock::now();
+        psp::Partition op = psp::partition_graph(gg, k, seed);
+        auto [rg, part] = psp::reorder_vertices(gg, op);
+        times[0] = ms(t0);
+        std::vector<std::size_t> off(k + 1, 0);
+        for (uint32_t c = 0; c < k; ++c) off[c + 1] = off[c] + part.component_members[c].size();
+        // component tables via the public apsp_dense on each induced range
+        t0 = Clock::now();
+        std::vector<psp::Matrix> tables(k);
+        std::vector<std::thread> pool;
+        std::atomic<uint32_t> next{0};
+        for (uint32_t w = 0; w < workers; ++w) {
+            pool.emplace_back([&] {
+                for (;;) {
+                    uint32_t c = next.fetch_add(1);
+                    if (c >= k) return;
+                    const std::size_t base = off[c], size = off[c + 1] - off[c];
+                    std::vector<psp::Edge> edges;
+                    for (std::size_t i = 0; i < size; ++i) {
+                        for (const psp::Neighbor& nb : rg.neighbors(static_cast<psp::VertexId>(base + i))) {
+                            if (nb.to >= base && nb.to < base + size && nb.to > base + i)
+                                edges.push_back({static_cast<psp::VertexId>(i),
+                                                 static_cast<psp::VertexId>(nb.to - base), nb.weight});
+                        }
+                    }
+                    tables[c] = psp::apsp_dense(psp::Graph(size, edges));
+                }
+            });
+        }
+        for (auto& t : pool) t.join();
+        times[1] = ms(t0);
+        t0 = Clock::now();
+        psp::BoundaryGraph bg = psp::build_boundary_graph(rg, part, tables);
+        times[2] = ms(t0);
+        info[0] = bg.global_of.size();
+        info[1] = bg.graph.num_edges();
+        std::mt19937_64 rng(sample_seed);
+        const std::size_t b = bg.global_of.size();
+        t0 = Clock::now();
+        for (uint32_t r = 0; r < rows && b > 0; ++r) {
+            auto d = psp::dijkstra_sssp(bg.graph, static_cast<psp::VertexId>(rng() % b));
+            (void)d;
+        }
+        times[3] = ms(t0);
+    });
+}
+
+void ref_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2) {
+    const auto pairs = ref::random_pairs(n, count, seed);
+    for (uint64_t i = 0; i < count; ++i) {
+        v1[i] = pairs[i].first;
+        v2[i] = pairs[i].second;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,455 @@
+// fw_kernels.cuh — K0/K1/K2: batched, symmetric, tile-packed blocked
+// Floyd-Warshall (min-plus) for sm_100a.
+//
+// Replaces the reference's apsp_dense (src/shortest_paths.cpp:107-172, Phase 2)
+// and the Dijkstra-per-boundary-vertex boundary_apsp
+// (src/oracle.cpp:127-142, Phase 3) with one engine:
+//
+//   for each k-block kb (T = 128 intermediates):
+//     phase 1  diagonal tile (kb,kb): sequential FW over its 128 vertices,
+//              8x8 register block per thread, row/column k broadcast through
+//              double-buffered shared memory (one barrier per k).
+//     phase 2  row panel R_J = D[kb-rows][J-cols] for every J != kb, as the
+//              single min-plus product R_J <- Dkk* (x) R_J (the closed diagonal
+//              tile has a zero diagonal, so R_J itself is included). The
+//              updated panel is written to its home tile and to the per-matrix
+//              panel buffer in [k][j] layout.
+//     phase 3  every upper tile (I,J), I,J != kb:
+//              D_IJ <- min(D_IJ, R_I^T (x) R_J). Symmetry gives the column
+//              panel for free (D[i][k] = D[k][i] = R_I[k][i]), so both
+//              operands are panel slots, already in the k-major layout the
+//              register-blocked inner loop wants, and only the upper triangle
+//              is computed: half the relaxations and half the bytes of a
+//              full-matrix FW.
+//
+// Exactness: u32 min-plus is exact, so the result equals the reference's f64
+// tables bit for bit after conversion (every FW order yields the same exact
+// shortest-path distances). FW keeps the matrix exactly symmetric even in f32
+// because a + b == b + a.
+//
+// The inner loop (phase 2/3) per k: 2 LDS.128 for A (broadcast within a
+// warp), 2 LDS.128 for B, 64 fused add-min (VIADDMNMX.U32 / FADD+FMNMX).
+#pragma once
+#include "minplus.cuh"
+
+namespace pspg {
+
+// ------------------------------------------------------------ PTX utils --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D TMA: contiguous global -> shared bulk copy completing on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// --------------------------------------------------- register blocking --
+// Thread (ty, tx) of a 16x16 block owns rows {4ty..4ty+3, 64+4ty..64+4ty+3}
+// and the same pattern of columns with tx: two aligned 4-vectors per side.
+__device__ __forceinline__ int blk(int t, int a) { return (a < 4) ? 4 * t + a : 60 + 4 * t + a; }
+
+template <class V>
+__device__ __forceinline__ void ld4(const V* p, V* r) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    r[0] = Ops<V>::from_bits(u.x);
+    r[1] = Ops<V>::from_bits(u.y);
+    r[2] = Ops<V>::from_bits(u.z);
+    r[3] = Ops<V>::from_bits(u.w);
+}
+template <class V>
+__device__ __forceinline__ void st4(V* p, const V* r) {
+    uint4 u;
+    u.x = Ops<V>::to_bits(r[0]);
+    u.y = Ops<V>::to_bits(r[1]);
+    u.z = Ops<V>::to_bits(r[2]);
+    u.w = Ops<V>::to_bits(r[3]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+// acc <- 8x8 block of a row-major T x T tile
+template <class V>
+__device__ __forceinline__ void load_block(const V* tile, V (&acc)[8][8], int ty, int tx) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const V* row = tile + blk(ty, a) * T;
+        ld4(row + 4 * tx, &acc[a][0]);
+        ld4(row + 64 + 4 * tx, &acc[a][4]);
+    }
+}
+template <class V>
+__device__ __forceinline__ void store_block(V* tile, const V (&acc)[8][8], int ty, int tx) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        V* row = tile + blk(ty, a) * T;
+        st4(row + 4 * tx, &acc[a][0]);
+        st4(row + 64 + 4 * tx, &acc[a][4]);
+    }
+}
+// transposed store: tile[col][row] <- acc[row][col]; rows come in aligned
+// 4-groups, so every store is still a 16-byte vector.
+template <class V>
+__device__ __forceinline__ void store_block_t(V* tile, const V (&acc)[8][8], int ty, int tx) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        V* row = tile + blk(tx, b) * T;
+        V lo[4] = {acc[0][b], acc[1][b], acc[2][b], acc[3][b]};
+        V hi[4] = {acc[4][b], acc[5][b], acc[6][b], acc[7][b]};
+        st4(row + 4 * ty, lo);
+        st4(row + 64 + 4 * ty, hi);
+    }
+}
+
+// acc[a][b] <- min_k A(row a, k) + sB[k][col b] over k in [0, T).
+// A_KMAJOR: sA[k][row] (the panel layout); otherwise sA[row][k].
+template <class V, bool A_KMAJOR>
+__device__ __forceinline__ void minplus_tile(const V* __restrict__ sA, const V* __restrict__ sB,
+                                             V (&acc)[8][8], int ty, int tx) {
+#pragma unroll 2
+    for (int k = 0; k < T; ++k) {
+        V a[8], b[8];
+        if (A_KMAJOR) {
+            ld4(sA + k * T + 4 * ty, &a[0]);
+            ld4(sA + k * T + 64 + 4 * ty, &a[4]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = sA[blk(ty, i) * T + k];
+        }
+        ld4(sB + k * T + 4 * tx, &b[0]);
+        ld4(sB + k * T + 64 + 4 * tx, &b[4]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::addmin(a[i], b[j], acc[i][j]);
+    }
+}
+
+// ---------------------------------------------------------------- phase 1 --
+// grid: nmat CTAs; one diagonal tile each.
+template <class V>
+__global__ void __launch_bounds__(NTHREADS) fw_phase1(MatSet<V> ms, uint32_t kb) {
+    const uint32_t m = blockIdx.x;
+    const uint32_t nb = ms.nb[m];
+    if (kb >= nb) return;
+    __shared__ __align__(16) V rowbuf[2][T];
+    __shared__ __align__(16) V colbuf[2][T];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    V* tile = ms.tiles + ms.tile_base[m] + tidx(kb, kb, nb) * TT;
+    V acc[8][8];
+    load_block(tile, acc, ty, tx);
+
+    // k runs over the two halves; within a half, k = half*64 + 4*q + r is
+    // owned (as a row) by ty == q at register row a = 4*half + r, and (as a
+    // column) by tx == q at register column 4*half + r.
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll 1
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int k = half * 64 + 4 * q + r;
+                const int buf = k & 1;
+                const int a = 4 * half + r;
+                if (ty == q) {
+                    st4(&rowbuf[buf][4 * tx], &acc[a][0]);
+                    st4(&rowbuf[buf][64 + 4 * tx], &acc[a][4]);
+                }
+                if (tx == q) {
+                    V lo[4] = {acc[0][a], acc[1][a], acc[2][a], acc[3][a]};
+                    V hi[4] = {acc[4][a], acc[5][a], acc[6][a], acc[7][a]};
+                    st4(&colbuf[buf][4 * ty], lo);
+                    st4(&colbuf[buf][64 + 4 * ty], hi);
+                }
+                __syncthreads();
+                V cv[8], rv[8];
+                ld4(&colbuf[buf][4 * ty], &cv[0]);
+                ld4(&colbuf[buf][64 + 4 * ty], &cv[4]);
+                ld4(&rowbuf[buf][4 * tx], &rv[0]);
+                ld4(&rowbuf[buf][64 + 4 * tx], &rv[4]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::addmin(cv[i], rv[j], acc[i][j]);
+            }
+        }
+    }
+    store_block(tile, acc, ty, tx);
+}
+
+// ---------------------------------------------------------------- phase 2 --
+// grid: (nmat, nb_max). CTA (m, J) updates row-panel tile J of matrix m.
+template <class V>
+__global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t kb) {
+    const uint32_t m = blockIdx.x;
+    const uint32_t nb = ms.nb[m];
+    const uint32_t J = blockIdx.y;
+    if (kb >= nb || J >= nb || J == kb) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V* sA = reinterpret_cast<V*>(smem_raw);
+    V* sB = sA + TT;
+    __shared__ uint64_t bar;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    V* base = ms.tiles + ms.tile_base[m];
+    const V* diag = base + tidx(kb, kb, nb) * TT;
+    V* panel = ms.panel + ms.panel_base[m] + uint64_t(J) * TT;
+    const bool upper = J > kb;
+    V* home = base + (upper ? tidx(kb, J, nb) : tidx(J, kb, nb)) * TT;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, 2 * TT * sizeof(V));
+        if (upper) {
+            bulk_g2s(sA, diag, TT * sizeof(V), &bar);  // Dkk* (symmetric: [k'][k])
+            bulk_g2s(sB, home, TT * sizeof(V), &bar);  // R_J [k'][j]
+        } else {
+            bulk_g2s(sA, home, TT * sizeof(V), &bar);  // Y = R_J^T [j][k']
+            bulk_g2s(sB, diag, TT * sizeof(V), &bar);  // Dkk* [k'][k]
+        }
+    }
+    __syncthreads();
+    V acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::inf();
+    mbar_wait(&bar, 0);
+    if (upper) {
+        // out[k][j] = min_k' Dkk[k][k'] + R_J[k'][j]
+        minplus_tile<V, true>(sA, sB, acc, ty, tx);
+        store_block(home, acc, ty, tx);
+        store_block(panel, acc, ty, tx);
+    } else {
+        // out^T[j][k] = min_k' Y[j][k'] + Dkk[k'][k]; the home tile (J, kb)
+        // is stored [j][k] = out^T, the panel slot wants [k][j].
+        minplus_tile<V, false>(sA, sB, acc, ty, tx);
+        store_block(home, acc, ty, tx);
+        store_block_t(panel, acc, ty, tx);
+    }
+}
+
+// ---------------------------------------------------------------- phase 3 --
+// Persistent: gridDim.x CTAs split the flat list of (matrix, upper tile)
+// items into contiguous ranges, so consecutive items share the tile row I
+// and the A operand (panel slot I) is reloaded only when I changes.
+__device__ __forceinline__ uint32_t row_start(uint32_t I, uint32_t nb) {
+    return I * nb - (I * (I - 1u)) / 2u;  // first flat index of tile row I
+}
+
+template <class V>
+__global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t kb) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V* sA = reinterpret_cast<V*>(smem_raw);
+    V* sB = sA + TT;
+    __shared__ uint64_t bar;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+
+    const uint64_t total = ms.work_prefix[ms.nmat];
+    const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint64_t w0 = uint64_t(blockIdx.x) * per;
+    const uint64_t w1 = min(total, w0 + per);
+    if (w0 >= w1) return;
+
+    // locate the first item: matrix by binary search, tile row by solving
+    // row_start(I) <= t < row_start(I+1).
+    uint32_t lo = 0, hi = ms.nmat;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (ms.work_prefix[mid] <= w0) lo = mid; else hi = mid;
+    }
+    uint32_t m = lo;
+    uint32_t nb = ms.nb[m];
+    uint32_t I, J;
+    {
+        const uint32_t t = static_cast<uint32_t>(w0 - ms.work_prefix[m]);
+        const double b2 = 2.0 * nb + 1.0;
+        double est = floor((b2 - sqrt(b2 * b2 - 8.0 * t)) * 0.5);
+        I = est < 0 ? 0u : static_cast<uint32_t>(est);
+        if (I >= nb) I = nb - 1;
+        while (I > 0 && row_start(I, nb) > t) --I;
+        while (I + 1 < nb && row_start(I + 1, nb) <= t) ++I;
+        J = I + (t - row_start(I, nb));
+    }
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+
+    uint32_t parity = 0;
+    uint64_t a_key = ~0ull;
+    for (uint64_t w = w0; w < w1; ++w) {
+        if (kb < nb && I != kb && J != kb) {
+            const V* P = ms.panel + ms.panel_base[m];
+            V* C = ms.tiles + ms.tile_base[m] + tidx(I, J, nb) * TT;
+            const uint64_t key = (uint64_t(m) << 32) | I;
+            const bool needA = key != a_key;
+            a_key = key;
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&bar, (needA ? 2u : 1u) * TT * sizeof(V));
+                if (needA) bulk_g2s(sA, P + uint64_t(I) * TT, TT * sizeof(V), &bar);
+                bulk_g2s(sB, P + uint64_t(J) * TT, TT * sizeof(V), &bar);
+            }
+            V acc[8][8];
+            load_block(C, acc, ty, tx);
+            mbar_wait(&bar, parity);
+            parity ^= 1;
+            minplus_tile<V, true>(sA, sB, acc, ty, tx);
+            store_block(C, acc, ty, tx);
+            __syncthreads();  // all reads of sA/sB done before the next copy
+        }
+        // advance to the next item
+        if (++J == nb) {
+            if (++I == nb) {
+                do {
+                    ++m;
+                } while (m < ms.nmat && ms.nb[m] == 0);  // empty components own no tiles
+                if (m < ms.nmat) nb = ms.nb[m];
+                I = 0;
+            }
+            J = I;
+        }
+    }
+}
+
+// ------------------------------------------------------------- K0: init --
+template <class V>
+__global__ void fill_value(V* __restrict__ p, uint64_t count, V value) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+        p[i] = value;
+}
+
+// grid: nmat CTAs. Zero diagonal incl. padding vertices.
+template <class V>
+__global__ void set_diag_zero(MatSet<V> ms) {
+    const uint32_t m = blockIdx.x;
+    const uint32_t nb = ms.nb[m];
+    for (uint32_t v = threadIdx.x; v < nb * T; v += blockDim.x)
+        ms.tiles[ms.tile_base[m] + tidx(v / T, v / T, nb) * TT + uint64_t(v % T) * T + v % T] = V(0);
+}
+
+// Symmetric scatter of weighted pairs (i, j) into matrix mat[e] (or 0).
+template <class V>
+__global__ void scatter_pairs(MatSet<V> ms, const uint32_t* __restrict__ mat,
+                              const uint32_t* __restrict__ ii, const uint32_t* __restrict__ jj,
+                              const V* __restrict__ w, uint64_t count) {
+    const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const uint32_t m = mat ? mat[e] : 0u;
+    const uint32_t nb = ms.nb[m];
+    V* base = ms.tiles + ms.tile_base[m];
+    const uint32_t i = ii[e], j = jj[e];
+    if (i / T <= j / T) base[tidx(i / T, j / T, nb) * TT + uint64_t(i % T) * T + j % T] = w[e];
+    if (j / T <= i / T) base[tidx(j / T, i / T, nb) * TT + uint64_t(j % T) * T + i % T] = w[e];
+}
+
+// Phase 3 init, clique part (src/oracle.cpp:110-122): the |B(C)| x |B(C)|
+// boundary prefix of every component table lands on the BG block diagonal;
+// counts finite pairs i < j for BuildStats::bg_edges.
+// grid: k CTAs, one component each (block-stride over its B x B block)
+template <class V>
+__global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict__ bnd_off,
+                                     MatSet<V> bg, unsigned long long* clique_edges) {
+    const uint32_t c = blockIdx.x;
+    const uint32_t g = bnd_off[c];
+    const uint32_t B = bnd_off[c + 1] - g;
+    const uint64_t total = uint64_t(B) * B;
+    uint32_t finite = 0;
+    for (uint64_t base = 0; base < total; base += blockDim.x) {
+        const uint64_t idx = base + threadIdx.x;
+        if (idx < total) {
+            const uint32_t i = static_cast<uint32_t>(idx / B), j = static_cast<uint32_t>(idx % B);
+            const V val = comps.tiles[comps.tile_base[c] + sym_off(i, j, comps.nb[c])];
+            const uint32_t gi = g + i, gj = g + j;
+            if (gi / T <= gj / T)
+                bg.tiles[tidx(gi / T, gj / T, bg.nb[0]) * TT + uint64_t(gi % T) * T + gj % T] = val;
+            finite += (i < j && val < Ops<V>::inf()) ? 1u : 0u;
+        }
+    }
+    const uint32_t warp_total = __reduce_add_sync(0xffffffffu, finite);
+    if ((threadIdx.x & 31) == 0 && warp_total) atomicAdd(clique_edges, warp_total);
+}
+
+// Query side table CB[c] = rows 0..|C| of component c restricted to its
+// boundary columns, |C| x |B(C)| row-major: row1/col2 of Algorithm 2
+// (src/query.cpp:29-45) become contiguous reads.  grid: k CTAs
+template <class V>
+__global__ void extract_to_boundary(MatSet<V> comps, const uint32_t* __restrict__ comp_off,
+                                    const uint32_t* __restrict__ bnd_off,
+                                    const uint64_t* __restrict__ cb_off, V* __restrict__ cb) {
+    const uint32_t c = blockIdx.x;
+    const uint32_t S = comp_off[c + 1] - comp_off[c];
+    const uint32_t B = bnd_off[c + 1] - bnd_off[c];
+    const uint64_t total = uint64_t(S) * B;
+    for (uint64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const uint32_t l = static_cast<uint32_t>(idx / B), j = static_cast<uint32_t>(idx % B);
+        cb[cb_off[c] + idx] = comps.tiles[comps.tile_base[c] + sym_off(l, j, comps.nb[c])];
+    }
+}
+
+// Dense export of a row/column window of matrix m: out[r][c] = D[row0+r][col0+c].
+template <class V>
+__global__ void unpack_window(MatSet<V> ms, uint32_t m, uint32_t row0, uint32_t nrows,
+                              uint32_t col0, uint32_t ncols, V* __restrict__ out) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= uint64_t(nrows) * ncols) return;
+    const uint32_t r = static_cast<uint32_t>(idx / ncols), c = static_cast<uint32_t>(idx % ncols);
+    out[idx] = ms.tiles[ms.tile_base[m] + sym_off(row0 + r, col0 + c, ms.nb[m])];
+}
+
+// ------------------------------------------------------ ALU peak probe ----
+// The phase-3 inner loop without memory: 64 independent add-min chains per
+// thread, operands rotated through the accumulators so nothing folds.
+template <class V>
+__global__ void __launch_bounds__(NTHREADS) minplus_peak_kernel(V* out, uint32_t iters, V seed) {
+    V acc[8][8];
+    V a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        a[i] = seed + V(threadIdx.x & 7) + V(i);
+        b[i] = seed + V(i * 3);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = seed + V(1000 + i * 8 + j);
+    }
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::addmin(a[i], b[j], acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            a[i] = acc[i][(i + 1) & 7];
+            b[i] = acc[(i + 3) & 7][i];
+        }
+    }
+    V s = acc[0][0];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s = Ops<V>::vmin(s, acc[i][j]);
+    if (s == V(12345)) out[blockIdx.x] = s;
+}
+
+}  // namespace pspg

@@ -1,0 +1,189 @@
+// host_graph.cpp — CSR build, boundary flags, boundary-first reordering and
+// the synthetic grid generators. See host_graph.hpp for the reference
+// interfaces each routine reproduces.
+#include "host_graph.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <random>
+
+namespace pspg {
+
+namespace {
+std::string pair_str(uint32_t u, uint32_t v) {
+    return "(" + std::to_string(u) + "," + std::to_string(v) + ")";
+}
+}  // namespace
+
+Csr build_csr(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev, const double* ew) {
+    Csr g;
+    g.n = n;
+    g.off.assign(n + 1, 0);
+    // validation order of src/graph.cpp:22-36: range, self-loop, NaN/inf, negative
+    for (uint64_t e = 0; e < m; ++e) {
+        const uint32_t u = eu[e], v = ev[e];
+        const double w = ew[e];
+        if (u >= n || v >= n)
+            throw GraphError("edge " + pair_str(u, v) + " references vertex outside 0.." +
+                             std::to_string(n ? n - 1 : 0));
+        if (u == v) throw GraphError("self-loop at vertex " + std::to_string(u));
+        if (std::isnan(w) || std::isinf(w))
+            throw GraphError("non-finite weight on edge " + pair_str(u, v));
+        if (w < 0.0) throw GraphError("negative weight on edge " + pair_str(u, v));
+        ++g.off[u + 1];
+        ++g.off[v + 1];
+    }
+    for (uint64_t v = 0; v < n; ++v) g.off[v + 1] += g.off[v];
+    g.to.resize(2 * m);
+    g.w.resize(2 * m);
+    std::vector<uint64_t> cur(g.off.begin(), g.off.end() - 1);
+    for (uint64_t e = 0; e < m; ++e) {
+        const uint64_t a = cur[eu[e]]++, b = cur[ev[e]]++;
+        g.to[a] = ev[e];
+        g.w[a] = ew[e];
+        g.to[b] = eu[e];
+        g.w[b] = ew[e];
+    }
+    std::vector<std::pair<uint32_t, double>> tmp;
+    for (uint64_t v = 0; v < n; ++v) {
+        const uint64_t lo = g.off[v], hi = g.off[v + 1];
+        tmp.clear();
+        for (uint64_t e = lo; e < hi; ++e) tmp.emplace_back(g.to[e], g.w[e]);
+        std::sort(tmp.begin(), tmp.end(),
+                  [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (uint64_t e = lo; e < hi; ++e) {
+            g.to[e] = tmp[e - lo].first;
+            g.w[e] = tmp[e - lo].second;
+            if (e > lo && g.to[e] == g.to[e - 1])
+                throw GraphError("duplicate edge " + pair_str(static_cast<uint32_t>(v), g.to[e]));
+        }
+    }
+    return g;
+}
+
+std::vector<uint8_t> compute_boundary(const Csr& g, const std::vector<uint32_t>& a) {
+    std::vector<uint8_t> flags(g.n, 0);
+    for (uint64_t v = 0; v < g.n; ++v)
+        for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e)
+            if (a[g.to[e]] != a[v]) {
+                flags[v] = 1;
+                break;
+            }
+    return flags;
+}
+
+std::vector<uint32_t> reorder_permutation(uint32_t k, const std::vector<uint32_t>& a,
+                                          const std::vector<uint8_t>& flags) {
+    const uint64_t n = a.size();
+    std::vector<uint64_t> bsize(k, 0), tsize(k, 0);
+    for (uint64_t v = 0; v < n; ++v) {
+        ++tsize[a[v]];
+        if (flags[v]) ++bsize[a[v]];
+    }
+    std::vector<uint64_t> bcur(k), icur(k);
+    uint64_t start = 0;
+    for (uint32_t c = 0; c < k; ++c) {
+        bcur[c] = start;
+        icur[c] = start + bsize[c];
+        start += tsize[c];
+    }
+    std::vector<uint32_t> perm(n);
+    for (uint64_t v = 0; v < n; ++v)
+        perm[v] = static_cast<uint32_t>(flags[v] ? bcur[a[v]]++ : icur[a[v]]++);
+    return perm;
+}
+
+Reordered reorder(const Csr& g, uint32_t k, const std::vector<uint32_t>& assignment) {
+    const uint64_t n = g.n;
+    if (assignment.size() != n) throw ArgError("reorder: assignment must cover all vertices");
+    for (uint64_t v = 0; v < n; ++v)
+        if (assignment[v] >= k) throw ArgError("reorder: component id out of range");
+    Reordered r;
+    r.n = n;
+    r.k = k;
+    const std::vector<uint8_t> flags0 = compute_boundary(g, assignment);
+    r.perm = reorder_permutation(k, assignment, flags0);
+    r.inv.resize(n);
+    for (uint64_t v = 0; v < n; ++v) r.inv[r.perm[v]] = static_cast<uint32_t>(v);
+    r.assign.resize(n);
+    r.flags.resize(n);
+    for (uint64_t v = 0; v < n; ++v) {
+        r.assign[r.perm[v]] = assignment[v];
+        r.flags[r.perm[v]] = flags0[v];
+    }
+    // relabelled CSR, neighbour lists re-sorted by new id (:458-470)
+    Csr& rg = r.g;
+    rg.n = n;
+    rg.off.assign(n + 1, 0);
+    for (uint64_t v = 0; v < n; ++v) rg.off[r.perm[v] + 1] = g.degree(static_cast<uint32_t>(v));
+    for (uint64_t v = 0; v < n; ++v) rg.off[v + 1] += rg.off[v];
+    rg.to.resize(g.to.size());
+    rg.w.resize(g.w.size());
+    std::vector<std::pair<uint32_t, double>> tmp;
+    for (uint64_t v = 0; v < n; ++v) {
+        tmp.clear();
+        for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) tmp.emplace_back(r.perm[g.to[e]], g.w[e]);
+        std::sort(tmp.begin(), tmp.end(),
+                  [](const auto& a, const auto& b) { return a.first < b.first; });
+        uint64_t at = rg.off[r.perm[v]];
+        for (const auto& t : tmp) {
+            rg.to[at] = t.first;
+            rg.w[at++] = t.second;
+        }
+    }
+    r.comp_off.assign(k + 1, 0);
+    r.bnd_off.assign(k + 1, 0);
+    for (uint64_t v = 0; v < n; ++v) {
+        ++r.comp_off[r.assign[v] + 1];
+        if (r.flags[v]) ++r.bnd_off[r.assign[v] + 1];
+    }
+    for (uint32_t c = 0; c < k; ++c) {
+        r.comp_off[c + 1] += r.comp_off[c];
+        r.bnd_off[c + 1] += r.bnd_off[c];
+    }
+    return r;
+}
+
+void generate_grid(int kind, uint64_t rows, uint64_t cols, bool unit, double lo, double hi,
+                   uint64_t seed, std::vector<uint32_t>& eu, std::vector<uint32_t>& ev,
+                   std::vector<double>& ew) {
+    // checked_vertex_count (src/generators.cpp:28-35), WeightModel::uniform (:39-47)
+    if (rows == 0 || cols == 0) throw ArgError("grid dimensions must be positive");
+    if (cols > std::numeric_limits<uint64_t>::max() / rows ||
+        rows * cols > std::numeric_limits<uint32_t>::max())
+        throw ArgError("rows*cols exceeds the supported vertex-count range");
+    if (!unit && (lo < 0.0 || hi < lo || std::isnan(lo) || std::isnan(hi) || std::isinf(hi)))
+        throw ArgError("uniform weight bounds must satisfy 0 <= lo <= hi < inf");
+    std::mt19937_64 rng(seed);
+    // WeightDrawer (:14-26): 1025 lattice points including both endpoints
+    auto draw = [&]() -> double {
+        if (unit) return 1.0;
+        const double step = static_cast<double>(rng() % 1025u);
+        return lo + (hi - lo) * (step / 1024.0);
+    };
+    eu.clear();
+    ev.clear();
+    ew.clear();
+    auto push = [&](uint64_t a, uint64_t b, double w) {
+        eu.push_back(static_cast<uint32_t>(a));
+        ev.push_back(static_cast<uint32_t>(b));
+        ew.push_back(w);
+    };
+    for (uint64_t r = 0; r < rows; ++r)
+        for (uint64_t c = 0; c < cols; ++c) {
+            const uint64_t v = r * cols + c;
+            // argument evaluation order matters for the rng stream: the
+            // reference draws the weight inside push_back({v, v+1, draw()})
+            if (c + 1 < cols) push(v, v + 1, draw());
+            if (r + 1 < rows) push(v, v + cols, draw());
+            if (kind == 1 && c + 1 < cols && r + 1 < rows) {
+                const bool down_right = (rng() & 1u) != 0;
+                if (down_right) push(v, v + cols + 1, draw());
+                else push(v + 1, v + cols, draw());
+            }
+        }
+}
+
+}  // namespace pspg

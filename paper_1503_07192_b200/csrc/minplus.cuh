@@ -1,0 +1,89 @@
+// minplus.cuh — value semantics and tile geometry shared by every kernel.
+//
+// Two value kinds (BASELINE.json north_star):
+//   u32  exact. INF = 0x7FFFFFFF so INF + INF = 0xFFFFFFFE never wraps; the
+//        host guarantees every finite distance < 2^31 - 1
+//        (max_w * 2^q * (n - 1) < 2^31 - 1), so one add of two stored values
+//        never wraps either, and min() clamps anything >= INF back to <= INF.
+//        min(a + b, c) compiles to one VIADDMNMX.U32 on sm_100a.
+//   f32  tolerance path. INF = +inf; fminf(a + b, c) -> FADD + FMNMX.
+//
+// The reference skips unreachable rows explicitly
+// (src/shortest_paths.cpp:117, src/query.cpp:53); with these encodings the
+// skip is implicit because INF + x >= INF never wins a min.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pspg {
+
+constexpr int T = 128;          // Floyd-Warshall tile edge
+constexpr int TT = T * T;       // elements per tile
+constexpr int NTHREADS = 256;   // 16 x 16 threads, 8 x 8 register block each
+constexpr uint32_t U32_INF = 0x7FFFFFFFu;
+
+template <class V> struct Ops;
+
+template <> struct Ops<uint32_t> {
+    static __host__ __device__ __forceinline__ uint32_t inf() { return U32_INF; }
+    static __device__ __forceinline__ uint32_t addmin(uint32_t a, uint32_t b, uint32_t c) {
+        return min(a + b, c);
+    }
+    static __device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return min(a, b); }
+    static __device__ __forceinline__ uint32_t from_bits(uint32_t u) { return u; }
+    static __device__ __forceinline__ uint32_t to_bits(uint32_t v) { return v; }
+    static __device__ __forceinline__ double to_f64(uint32_t v, double scale) {
+        return v >= U32_INF ? __longlong_as_double(0x7ff0000000000000ll) : double(v) * scale;
+    }
+};
+
+template <> struct Ops<float> {
+    static __host__ __device__ __forceinline__ float inf() { return __builtin_huge_valf(); }
+    static __device__ __forceinline__ float addmin(float a, float b, float c) {
+        return fminf(a + b, c);
+    }
+    static __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+    static __device__ __forceinline__ float from_bits(uint32_t u) { return __uint_as_float(u); }
+    static __device__ __forceinline__ uint32_t to_bits(float v) { return __float_as_uint(v); }
+    static __device__ __forceinline__ double to_f64(float v, double) { return double(v); }
+};
+
+// ---------------------------------------------------------------- layout --
+// A symmetric n x n distance matrix is stored as the upper triangle of its
+// nb x nb grid of T x T tiles (nb = ceil(n / T)), "tile-packed": tile (I, J)
+// with I <= J is one contiguous T*T row-major block at index
+//   tidx(I, J) = I * (2 nb - I + 1) / 2 + (J - I).
+// Diagonal tiles hold both triangles. Padding rows/columns (>= n) are
+// isolated dummy vertices (INF, 0 on the diagonal) that never shorten a
+// path. Element (i, j) lives in tile (min(I,J), max(I,J)); the rule for
+// writers is: write (i, j) iff i / T <= j / T.
+__host__ __device__ __forceinline__ uint64_t tidx(uint32_t I, uint32_t J, uint32_t nb) {
+    return uint64_t(I) * (2ull * nb - I + 1) / 2 + (J - I);
+}
+__host__ __device__ __forceinline__ uint64_t ntiles_upper(uint32_t nb) {
+    return uint64_t(nb) * (nb + 1) / 2;
+}
+// Offset (in elements, relative to the matrix's first tile) of element (i, j).
+__host__ __device__ __forceinline__ uint64_t sym_off(uint32_t i, uint32_t j, uint32_t nb) {
+    if (i / T > j / T) {
+        const uint32_t t = i;
+        i = j;
+        j = t;
+    }
+    return tidx(i / T, j / T, nb) * TT + uint64_t(i % T) * T + (j % T);
+}
+
+// A batch of matrices sharing one tile arena (component tables: k matrices;
+// boundary graph: one). Arrays are device pointers indexed by matrix.
+template <class V> struct MatSet {
+    V* tiles;                   // tile arena
+    V* panel;                   // per-matrix row-panel slots (nb * T*T each)
+    const uint64_t* tile_base;  // element offset of matrix m's first tile
+    const uint64_t* panel_base; // element offset of matrix m's panel slots
+    const uint64_t* work_prefix;// prefix sum of upper-tile counts (nmat + 1)
+    const uint32_t* nb;         // tiles per side
+    uint32_t nmat;
+    uint32_t nb_max;
+};
+
+}  // namespace pspg

@@ -1,0 +1,388 @@
+// partition.cpp — host k-way partitioner with output identical to the
+// reference's partition_graph (src/partition.cpp:259-450).
+//
+// Why restate it: BASELINE.json keeps the reference's partition + boundary
+// extraction on the host "so component assignment matches the oracle"; the
+// product library must not link reference sources, so the algorithm is
+// re-expressed here and checked for identical assignments against the
+// reference build (tests/test_partition.py).
+//
+// What is the same (bit for bit): the mt19937_64 stream and its order of use,
+// seed selection (farthest-point first restart, best-of-8 candidates after),
+// hop-count Voronoi growth with smallest-id tie breaking, recentering,
+// finalize = fill unreached + rebalance + refine sweeps, the cost
+// sum |B(C)|^2 and the first-strict-minimum candidate choice over
+// (restart, round).
+//
+// What differs (speed only):
+//  * the 8 restarts are independent once their seed sets are drawn, so the
+//    seed draws run first (sequentially, they share the rng and the id
+//    shuffle) and the 8 grow/recenter/finalize chains run on a thread pool;
+//    the winner is the first minimum in (restart, round) order exactly as
+//    the reference's strict `<` scan picks it.
+//  * rebalance collects each oversized component's members from per-
+//    component buckets instead of rescanning all n vertices; the member
+//    order is fixed by the reference's total (hop desc, id asc) sort anyway.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <exception>
+#include <limits>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "host_graph.hpp"
+
+namespace pspg {
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;   // kUnassigned (:14)
+constexpr int kMaxRefineSweeps = 10;      // (:15)
+constexpr int kRecenterRounds = 12;       // (:16)
+constexpr int kRestarts = 8;              // (:17)
+constexpr uint64_t kSeedCandidates = 8;   // (:18)
+
+// balance_cap (:191-194): ceil(1.1 n / k) in integers
+uint64_t cap_of(uint64_t n, uint32_t k) { return (11 * n + 10 * uint64_t(k) - 1) / (10 * uint64_t(k)); }
+
+struct Part {
+    const Csr& g;
+    uint32_t k;
+    uint64_t cap;
+
+    // is_boundary_with_move (:22-31): u's boundary status with `moved`
+    // placed in component `to`.
+    bool boundary_if(const std::vector<uint32_t>& a, uint32_t u, uint32_t moved, uint32_t to) const {
+        const uint32_t cu = (u == moved) ? to : a[u];
+        for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+            const uint32_t x = g.to[e];
+            if (((x == moved) ? to : a[x]) != cu) return true;
+        }
+        return false;
+    }
+
+    // voronoi_grow (:40-72)
+    void grow(const std::vector<uint32_t>& seeds, std::vector<uint32_t>& assign,
+              std::vector<uint32_t>& hop) const {
+        const uint64_t n = g.n;
+        assign.assign(n, kNone);
+        hop.assign(n, kNone);
+        std::vector<uint32_t> frontier, next, claimed(n, kNone);
+        for (uint32_t c = 0; c < seeds.size(); ++c) {
+            assign[seeds[c]] = c;
+            hop[seeds[c]] = 0;
+            frontier.push_back(seeds[c]);
+        }
+        std::sort(frontier.begin(), frontier.end());
+        uint32_t round = 0;
+        while (!frontier.empty()) {
+            ++round;
+            next.clear();
+            for (uint32_t u : frontier)
+                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                    const uint32_t x = g.to[e];
+                    if (assign[x] != kNone || claimed[x] != kNone) continue;
+                    claimed[x] = assign[u];
+                    next.push_back(x);
+                }
+            for (uint32_t v : next) {
+                assign[v] = claimed[v];
+                hop[v] = round;
+            }
+            std::sort(next.begin(), next.end());
+            frontier.swap(next);
+        }
+    }
+
+    // recenter (:77-119)
+    std::vector<uint32_t> recenter(const std::vector<uint32_t>& a,
+                                   const std::vector<uint32_t>& old) const {
+        const uint64_t n = g.n;
+        std::vector<uint32_t> seeds(old);
+        const std::vector<uint8_t> flags = compute_boundary(g, a);
+        std::vector<uint32_t> best_hop(seeds.size(), 0), best(seeds.size(), kNone);
+        std::vector<uint8_t> visited(n, 0);
+        std::vector<uint32_t> frontier, next;
+        for (uint64_t v = 0; v < n; ++v)
+            if (flags[v]) {
+                visited[v] = 1;
+                frontier.push_back(static_cast<uint32_t>(v));
+                if (best[a[v]] == kNone) best[a[v]] = static_cast<uint32_t>(v);
+            }
+        uint32_t round = 0;
+        while (!frontier.empty()) {
+            ++round;
+            next.clear();
+            for (uint32_t u : frontier)
+                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                    const uint32_t x = g.to[e];
+                    if (visited[x] || a[x] != a[u]) continue;
+                    visited[x] = 1;
+                    next.push_back(x);
+                }
+            std::sort(next.begin(), next.end());
+            for (uint32_t v : next) {
+                const uint32_t c = a[v];
+                if (round > best_hop[c]) {
+                    best_hop[c] = round;
+                    best[c] = v;
+                }
+            }
+            frontier.swap(next);
+        }
+        for (uint32_t c = 0; c < seeds.size(); ++c)
+            if (best[c] != kNone) seeds[c] = best[c];
+        return seeds;
+    }
+
+    // rebalance (:125-175)
+    void rebalance(std::vector<uint32_t>& a, const std::vector<uint32_t>& hop,
+                   std::vector<uint64_t>& size) const {
+        const uint64_t n = g.n;
+        bool any = false;
+        for (uint32_t c = 0; c < k; ++c) any |= size[c] > cap;
+        if (!any) return;
+        auto smallest_with_room = [&](uint32_t exclude) {
+            uint32_t target = kNone;
+            for (uint32_t t = 0; t < k; ++t) {
+                if (t == exclude || size[t] + 1 > cap) continue;
+                if (target == kNone || size[t] < size[target]) target = t;
+            }
+            return target;
+        };
+        // members of c when c is processed = its vertices at entry plus
+        // those moved into it while earlier components were trimmed
+        std::vector<std::vector<uint32_t>> bucket(k);
+        for (uint64_t v = 0; v < n; ++v)
+            if (size[a[v]] > cap) bucket[a[v]].push_back(static_cast<uint32_t>(v));
+        std::vector<std::vector<uint32_t>> moved_in(k);
+        std::vector<uint32_t> members;
+        for (uint32_t c = 0; c < k; ++c) {
+            if (size[c] <= cap) continue;
+            members.clear();
+            for (uint32_t v : bucket[c]) if (a[v] == c) members.push_back(v);
+            for (uint32_t v : moved_in[c]) if (a[v] == c) members.push_back(v);
+            std::sort(members.begin(), members.end(), [&](uint32_t x, uint32_t y) {
+                if (hop[x] != hop[y]) return hop[x] > hop[y];
+                return x < y;
+            });
+            for (uint32_t v : members) {
+                if (size[c] <= cap) break;
+                uint32_t target = kNone;
+                for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                    const uint32_t t = a[g.to[e]];
+                    if (t == c || t == kNone || size[t] + 1 > cap) continue;
+                    if (target == kNone || size[t] < size[target] ||
+                        (size[t] == size[target] && t < target))
+                        target = t;
+                }
+                if (target == kNone) target = smallest_with_room(c);
+                a[v] = target;
+                --size[c];
+                ++size[target];
+                if (target > c) moved_in[target].push_back(v);
+            }
+        }
+    }
+
+    // the refine lambda (:334-387)
+    void refine(std::vector<uint32_t>& a, std::vector<uint64_t>& size,
+                std::vector<uint8_t>& flags) const {
+        const uint64_t n = g.n;
+        std::vector<uint32_t> targets;
+        for (int sweep = 0; sweep < kMaxRefineSweeps; ++sweep) {
+            bool improved = false;
+            for (uint64_t step = 0; step < n; ++step) {
+                const uint32_t v = static_cast<uint32_t>((sweep % 2 == 0) ? step : n - 1 - step);
+                if (!flags[v]) continue;
+                const uint32_t from = a[v];
+                if (size[from] <= 1) continue;
+                targets.clear();
+                for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                    const uint32_t c = a[g.to[e]];
+                    if (c != from && std::find(targets.begin(), targets.end(), c) == targets.end())
+                        targets.push_back(c);
+                }
+                std::sort(targets.begin(), targets.end());
+                int best_delta = 0;
+                uint32_t best_to = kNone;
+                for (uint32_t to : targets) {
+                    if (size[to] + 1 > cap) continue;
+                    int delta = (boundary_if(a, v, v, to) ? 1 : 0) - (flags[v] ? 1 : 0);
+                    for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                        const uint32_t x = g.to[e];
+                        delta += (boundary_if(a, x, v, to) ? 1 : 0) - (flags[x] ? 1 : 0);
+                    }
+                    if (delta < best_delta) {
+                        best_delta = delta;
+                        best_to = to;
+                    }
+                }
+                if (best_to != kNone) {
+                    a[v] = best_to;
+                    --size[from];
+                    ++size[best_to];
+                    flags[v] = boundary_if(a, v, v, best_to) ? 1 : 0;
+                    for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                        const uint32_t x = g.to[e];
+                        flags[x] = boundary_if(a, x, v, best_to) ? 1 : 0;
+                    }
+                    improved = true;
+                }
+            }
+            if (!improved) break;
+        }
+    }
+
+    // the finalize lambda (:393-420); returns the candidate's cost
+    uint64_t finalize(std::vector<uint32_t> assign, const std::vector<uint32_t>& hop,
+                      std::vector<uint32_t>& out) const {
+        const uint64_t n = g.n;
+        std::vector<uint64_t> sz(k, 0);
+        for (uint64_t v = 0; v < n; ++v)
+            if (assign[v] != kNone) ++sz[assign[v]];
+        for (uint64_t v = 0; v < n; ++v) {
+            if (assign[v] != kNone) continue;
+            uint32_t best = kNone;
+            for (uint32_t c = 0; c < k; ++c)
+                if (sz[c] < cap && (best == kNone || sz[c] < sz[best])) best = c;
+            assign[v] = best;
+            ++sz[best];
+        }
+        rebalance(assign, hop, sz);
+        std::vector<uint8_t> flags = compute_boundary(g, assign);
+        refine(assign, sz, flags);
+        std::vector<uint64_t> bsz(k, 0);
+        for (uint64_t v = 0; v < n; ++v)
+            if (flags[v]) ++bsz[assign[v]];
+        uint64_t cost = 0;
+        for (uint32_t c = 0; c < k; ++c) cost += bsz[c] * bsz[c];
+        out = std::move(assign);
+        return cost;
+    }
+};
+
+}  // namespace
+
+std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, unsigned threads) {
+    const uint64_t n = g.n;
+    if (k < 1) throw ArgError("partition_graph: k must be at least 1");
+    if (k > n) throw ArgError("partition_graph: k exceeds vertex count");
+    Part P{g, k, cap_of(n, k)};
+
+    // --- seed sets for all restarts, in the reference's rng order (:268-329)
+    std::mt19937_64 rng(seed);
+    std::vector<uint32_t> ids(n);
+    std::iota(ids.begin(), ids.end(), 0u);
+    std::vector<uint32_t> dist(n);
+    std::vector<uint32_t> q;
+    auto relax_from = [&](uint32_t s) {  // relax_seed_dist (:272-284)
+        dist[s] = 0;
+        q.assign(1, s);
+        for (size_t head = 0; head < q.size(); ++head) {
+            const uint32_t u = q[head];
+            for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                const uint32_t x = g.to[e];
+                if (dist[x] > dist[u] + 1) {
+                    dist[x] = dist[u] + 1;
+                    q.push_back(x);
+                }
+            }
+        }
+    };
+    std::vector<std::vector<uint32_t>> seed_sets(kRestarts, std::vector<uint32_t>(k));
+    {  // farthest_seeds (:315-329)
+        auto& s = seed_sets[0];
+        std::fill(dist.begin(), dist.end(), kNone);
+        s[0] = static_cast<uint32_t>(rng() % n);
+        relax_from(s[0]);
+        for (uint32_t c = 1; c < k; ++c) {
+            uint32_t pick = 0;
+            for (uint32_t v = 1; v < n; ++v)
+                if (dist[v] > dist[pick]) pick = v;
+            s[c] = pick;
+            relax_from(pick);
+        }
+    }
+    for (int r = 1; r < kRestarts; ++r) {  // draw_seeds (:285-306)
+        auto& s = seed_sets[r];
+        std::fill(dist.begin(), dist.end(), kNone);
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint64_t m = std::min<uint64_t>(kSeedCandidates, n - c);
+            for (uint64_t t = 0; t < m; ++t) {
+                const uint64_t j = c + t + static_cast<uint64_t>(rng() % (n - c - t));
+                std::swap(ids[c + t], ids[j]);
+            }
+            uint64_t best = c;
+            for (uint64_t t = 1; t < m; ++t) {
+                const uint32_t cand = ids[c + t], cur = ids[best];
+                if (dist[cand] > dist[cur] || (dist[cand] == dist[cur] && cand < cur)) best = c + t;
+            }
+            std::swap(ids[c], ids[best]);
+            s[c] = ids[c];
+            relax_from(s[c]);
+        }
+    }
+
+    // --- independent restart chains (:430-444)
+    struct Best {
+        uint64_t cost = std::numeric_limits<uint64_t>::max();
+        std::vector<uint32_t> assign;
+    };
+    std::vector<Best> best(kRestarts);
+    auto chain = [&](int r) {
+        std::vector<uint32_t> seeds = seed_sets[r];
+        std::vector<uint32_t> assign, hop, cand;
+        P.grow(seeds, assign, hop);
+        for (int round = 0;; ++round) {
+            const uint64_t cost = P.finalize(assign, hop, cand);
+            if (cost < best[r].cost) {
+                best[r].cost = cost;
+                best[r].assign = cand;
+            }
+            if (round == kRecenterRounds) break;
+            seeds = P.recenter(assign, seeds);
+            P.grow(seeds, assign, hop);
+        }
+    };
+    const unsigned nthreads = std::max(1u, std::min<unsigned>(threads, kRestarts));
+    if (nthreads == 1) {
+        for (int r = 0; r < kRestarts; ++r) chain(r);
+    } else {
+        std::atomic<int> next{0};
+        std::exception_ptr err;
+        std::mutex mu;
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nthreads; ++t)
+            pool.emplace_back([&] {
+                for (;;) {
+                    const int r = next.fetch_add(1);
+                    if (r >= kRestarts) return;
+                    try {
+                        chain(r);
+                    } catch (...) {
+                        std::lock_guard<std::mutex> lock(mu);
+                        if (!err) err = std::current_exception();
+                        return;
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+        if (err) std::rethrow_exception(err);
+    }
+    int win = 0;
+    for (int r = 1; r < kRestarts; ++r)
+        if (best[r].cost < best[win].cost) win = r;
+    std::vector<uint64_t> sz(k, 0);
+    for (uint32_t c : best[win].assign) ++sz[c];
+    for (uint32_t c = 0; c < k; ++c)
+        if (sz[c] > P.cap) throw std::logic_error("partition_graph: balance cap violated");
+    return std::move(best[win].assign);
+}
+
+}  // namespace pspg

@@ -1,0 +1,859 @@
+// psp_gpu.cu — C-ABI (include/psp_gpu.h) over the sm_100a kernels.
+//
+// Device build pipeline (replaces src/oracle.cpp:144-194 Phases 2 and 3):
+//   host   partition_graph + reorder            (identical ids to the reference)
+//   K0     component tiles <- INF / 0 diagonal / intra-component edge weights
+//   K1     batched symmetric blocked FW over all k component matrices
+//   BG     BG tiles <- INF / 0 diagonal / component boundary blocks (clique
+//          edges, src/oracle.cpp:110-122) / cross edges (:103-109)
+//   K2     symmetric blocked FW on the b x b boundary-graph matrix (replaces
+//          one Dijkstra per boundary vertex, :127-142; equal distances)
+//   CB     |C| x |B(C)| to-boundary tables for the query kernel
+// Queries (K3, src/query.cpp:85-114) read CB, the BG tiles and, for
+// same-component pairs, the component tiles.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <type_traits>
+#include <string>
+#include <vector>
+
+#include "fw_kernels.cuh"
+#include "host_graph.hpp"
+#include "minplus.cuh"
+#include "psp_gpu.h"
+#include "query_kernels.cuh"
+
+using namespace pspg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    psp_status st;
+    std::string msg;
+};
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? PSP_ENOMEM : PSP_ECUDA,       \
+                       std::string(#x) + ": " + cudaGetErrorString(e_)};               \
+    } while (0)
+#define CK_LAUNCH(what) CK(cudaGetLastError())
+
+template <typename F>
+psp_status guarded(F&& f) {
+    try {
+        f();
+        return PSP_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.st;
+    } catch (const GraphError& e) {
+        g_err = e.what();
+        return PSP_EGRAPH;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return PSP_EINVAL;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return PSP_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PSP_ECUDA;
+    }
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+}
+
+// ------------------------------------------------------ device buffers --
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    explicit DBuf(size_t n) { alloc(n); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void alloc(size_t n) {
+        reset();
+        if (n == 0) n = 16;
+        CK(cudaMalloc(&p, n));
+        bytes = n;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+DBuf upload(const std::vector<T>& h, cudaStream_t s) {
+    DBuf d(h.size() * sizeof(T));
+    if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+// A batch of symmetric tile-packed matrices (see minplus.cuh).
+struct MatArena {
+    uint32_t nmat = 0, nb_max = 0;
+    size_t vbytes = 4;
+    std::vector<uint32_t> nb;
+    std::vector<uint64_t> tile_base, panel_base, work_prefix;
+    uint64_t tile_elems = 0, panel_elems = 0;
+    DBuf tiles, panel, d_tile_base, d_panel_base, d_work_prefix, d_nb;
+
+    void create(const std::vector<uint64_t>& sizes, size_t value_bytes, bool with_panel,
+                cudaStream_t s) {
+        vbytes = value_bytes;
+        nmat = static_cast<uint32_t>(sizes.size());
+        nb.resize(nmat);
+        tile_base.resize(nmat);
+        panel_base.resize(nmat);
+        work_prefix.assign(nmat + 1, 0);
+        tile_elems = panel_elems = 0;
+        nb_max = 0;
+        for (uint32_t m = 0; m < nmat; ++m) {
+            nb[m] = static_cast<uint32_t>((sizes[m] + T - 1) / T);
+            nb_max = std::max(nb_max, nb[m]);
+            tile_base[m] = tile_elems;
+            panel_base[m] = panel_elems;
+            tile_elems += ntiles_upper(nb[m]) * TT;
+            panel_elems += uint64_t(nb[m]) * TT;
+            work_prefix[m + 1] = work_prefix[m] + ntiles_upper(nb[m]);
+        }
+        tiles.alloc(tile_elems * vbytes);
+        if (with_panel) panel.alloc(panel_elems * vbytes);
+        d_tile_base = upload(tile_base, s);
+        d_panel_base = upload(panel_base, s);
+        d_work_prefix = upload(work_prefix, s);
+        d_nb = upload(nb, s);
+    }
+    template <class V> MatSet<V> view() const {
+        MatSet<V> v;
+        v.tiles = tiles.as<V>();
+        v.panel = panel.as<V>();
+        v.tile_base = d_tile_base.as<uint64_t>();
+        v.panel_base = d_panel_base.as<uint64_t>();
+        v.work_prefix = d_work_prefix.as<uint64_t>();
+        v.nb = d_nb.as<uint32_t>();
+        v.nmat = nmat;
+        v.nb_max = nb_max;
+        return v;
+    }
+    // relaxations the FW executes on the padded matrices: per k-block the
+    // diagonal tile, the nb-1 panel tiles and the upper tiles off row/col kb
+    uint64_t relaxations() const {
+        uint64_t r = 0;
+        for (uint32_t m = 0; m < nmat; ++m) r += ntiles_upper(nb[m]) * nb[m];
+        return r * uint64_t(T) * T * T;
+    }
+    size_t bytes() const { return tiles.bytes + panel.bytes; }
+};
+
+}  // namespace
+
+// --------------------------------------------------------------- ctx ----
+struct psp_gpu_ctx {
+    int device = 0;
+    int rank = 0, world = 1;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+int g_attr_done[2] = {0, 0};
+
+template <class V>
+void set_kernel_attrs() {
+    const int idx = std::is_same<V, float>::value ? 1 : 0;
+    if (g_attr_done[idx]) return;
+    const int smem = 2 * TT * sizeof(V);
+    CK(cudaFuncSetAttribute(fw_phase2<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(fw_phase3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    g_attr_done[idx] = 1;
+}
+
+template <class V>
+void fill_arena(MatArena& a, cudaStream_t s, int sms) {
+    const uint64_t n = a.tile_elems;
+    const int blocks = int(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 32));
+    fill_value<V><<<std::max(blocks, 1), 256, 0, s>>>(a.tiles.as<V>(), n, Ops<V>::inf());
+    CK_LAUNCH();
+    if (a.nmat) {
+        set_diag_zero<V><<<a.nmat, 256, 0, s>>>(a.view<V>());
+        CK_LAUNCH();
+    }
+}
+
+// The blocked FW driver: 3 launches per k-block on one stream.
+template <class V>
+void run_fw(const MatArena& a, cudaStream_t s, int sms) {
+    if (a.nmat == 0 || a.nb_max == 0) return;
+    set_kernel_attrs<V>();
+    const MatSet<V> v = a.view<V>();
+    const int smem = 2 * TT * sizeof(V);
+    const uint64_t work = a.work_prefix[a.nmat];
+    const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
+    for (uint32_t kb = 0; kb < a.nb_max; ++kb) {
+        fw_phase1<V><<<a.nmat, NTHREADS, 0, s>>>(v, kb);
+        CK_LAUNCH();
+        if (a.nb_max > 1) {
+            fw_phase2<V><<<dim3(a.nmat, a.nb_max), NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+            fw_phase3<V><<<g3, NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+        }
+    }
+}
+
+// Value kind selection: u32 when integral or dyadic weights keep
+// every finite distance below INF; f32 otherwise.
+struct Kind {
+    int kind;
+    int shift;
+};
+Kind choose_kind(int requested, const double* w, uint64_t m, uint64_t n) {
+    if (requested != PSP_VALUE_AUTO && requested != PSP_VALUE_U32 && requested != PSP_VALUE_F32)
+        throw ArgError("value_kind must be PSP_VALUE_AUTO, PSP_VALUE_U32 or PSP_VALUE_F32");
+    if (requested == PSP_VALUE_F32) return {PSP_VALUE_F32, 0};
+    double maxw = 0.0;
+    for (uint64_t e = 0; e < m; ++e) maxw = std::max(maxw, w[e]);
+    const double hops = n > 1 ? double(n - 1) : 1.0;
+    for (int q = 0; q <= 24; ++q) {
+        const double scale = std::ldexp(1.0, q);
+        if (maxw * scale * hops >= double(U32_INF)) break;
+        bool integral = true;
+        for (uint64_t e = 0; e < m && integral; ++e) {
+            const double x = w[e] * scale;
+            integral = std::floor(x) == x;
+        }
+        if (integral) return {PSP_VALUE_U32, q};
+    }
+    if (requested == PSP_VALUE_U32)
+        throw Fail{PSP_EOVERFLOW,
+                   "u32 distances are not exact for these weights (non-dyadic weights or "
+                   "max_w * 2^q * (n-1) >= 2^31-1)"};
+    return {PSP_VALUE_F32, 0};
+}
+
+template <class V>
+V to_value(double w, int shift) {
+    if (std::is_same<V, float>::value) return V(float(w));
+    return V(static_cast<uint32_t>(std::ldexp(w, shift)));
+}
+
+template <class V>
+void to_f64(const std::vector<V>& src, double* dst, double scale) {
+    for (size_t i = 0; i < src.size(); ++i) {
+        if (std::is_same<V, float>::value) {
+            dst[i] = double(src[i]);
+        } else {
+            const uint32_t v = static_cast<uint32_t>(src[i]);
+            dst[i] = v >= U32_INF ? HUGE_VAL : double(v) * scale;
+        }
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ oracle ----
+struct psp_gpu_oracle {
+    psp_gpu_ctx* ctx = nullptr;
+    Kind kind{PSP_VALUE_U32, 0};
+    double scale = 1.0;
+    Reordered R;
+    MatArena comps, bg;
+    DBuf d_perm, d_assign, d_comp_off, d_bnd_off, d_cb_off, d_cb;
+    uint64_t device_bytes = 0;
+};
+
+namespace {
+
+struct EdgeLists {
+    std::vector<uint32_t> mat, ii, jj;  // intra-component (local ids)
+    std::vector<double> w;
+    std::vector<uint32_t> bi, bj;       // cross edges (boundary ids)
+    std::vector<double> bw;
+};
+
+EdgeLists split_edges(const Reordered& R) {
+    EdgeLists L;
+    const Csr& g = R.g;
+    for (uint64_t u = 0; u < R.n; ++u) {
+        const uint32_t cu = R.assign[u];
+        for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+            const uint32_t v = g.to[e];
+            if (v <= u) continue;
+            const uint32_t cv = R.assign[v];
+            if (cu == cv) {
+                L.mat.push_back(cu);
+                L.ii.push_back(static_cast<uint32_t>(u - R.comp_off[cu]));
+                L.jj.push_back(v - R.comp_off[cv]);
+                L.w.push_back(g.w[e]);
+            } else {
+                // endpoints of a cross edge are boundary vertices, whose
+                // boundary id is base + local id (src/oracle.cpp:95-100)
+                L.bi.push_back(static_cast<uint32_t>(R.bnd_off[cu] + (u - R.comp_off[cu])));
+                L.bj.push_back(R.bnd_off[cv] + (v - R.comp_off[cv]));
+                L.bw.push_back(g.w[e]);
+            }
+        }
+    }
+    return L;
+}
+
+template <class V>
+std::vector<V> convert(const std::vector<double>& w, int shift) {
+    std::vector<V> out(w.size());
+    for (size_t i = 0; i < w.size(); ++i) out[i] = to_value<V>(w[i], shift);
+    return out;
+}
+
+template <class V>
+void scatter(MatArena& a, const std::vector<uint32_t>* mat, const std::vector<uint32_t>& ii,
+             const std::vector<uint32_t>& jj, const std::vector<double>& w, int shift,
+             cudaStream_t s) {
+    if (ii.empty()) return;
+    DBuf dm = mat ? upload(*mat, s) : DBuf();
+    DBuf di = upload(ii, s), dj = upload(jj, s), dw = upload(convert<V>(w, shift), s);
+    const uint64_t cnt = ii.size();
+    scatter_pairs<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(
+        a.view<V>(), mat ? dm.as<uint32_t>() : nullptr, di.as<uint32_t>(), dj.as<uint32_t>(),
+        dw.as<V>(), cnt);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));  // keep staging buffers alive until consumed
+}
+
+struct EventTimer {
+    cudaEvent_t a{}, b{};
+    EventTimer() {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+    }
+    ~EventTimer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    void start(cudaStream_t s) { CK(cudaEventRecord(a, s)); }
+    void stop(cudaStream_t s) { CK(cudaEventRecord(b, s)); }
+    double ms() {
+        CK(cudaEventSynchronize(b));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, a, b));
+        return t;
+    }
+};
+
+template <class V>
+void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
+    psp_gpu_ctx* ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
+    const Reordered& R = o->R;
+    const uint32_t k = R.k;
+    const int q = o->kind.shift;
+    EventTimer t_init, t_k1, t_k2, t_post;
+
+    // ---- Phase 2: K0 + K1
+    auto t0 = Clock::now();
+    std::vector<uint64_t> sizes(k);
+    for (uint32_t c = 0; c < k; ++c) sizes[c] = R.comp_off[c + 1] - R.comp_off[c];
+    EdgeLists L = split_edges(R);
+    t_init.start(s);
+    o->comps.create(sizes, sizeof(V), true, s);
+    fill_arena<V>(o->comps, s, ctx->sms);
+    scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
+    t_init.stop(s);
+    t_k1.start(s);
+    run_fw<V>(o->comps, s, ctx->sms);
+    t_k1.stop(s);
+    CK(cudaStreamSynchronize(s));
+    const double k1_ms = t_k1.ms();
+    double init_ms = t_init.ms();
+    const double component_ms = ms_since(t0);
+
+    // ---- Phase 3: BG init + K2 + query tables
+    t0 = Clock::now();
+    const uint64_t b = R.b();
+    DBuf d_bnd = upload(R.bnd_off, s);
+    unsigned long long clique = 0;
+    double k2_ms = 0.0;
+    if (b > 0) {
+        t_post.start(s);
+        o->bg.create({b}, sizeof(V), true, s);
+        fill_arena<V>(o->bg, s, ctx->sms);
+        DBuf d_clique(sizeof(unsigned long long));
+        CK(cudaMemsetAsync(d_clique.p, 0, sizeof(unsigned long long), s));
+        copy_boundary_blocks<V><<<k, 256, 0, s>>>(o->comps.view<V>(), d_bnd.as<uint32_t>(),
+                                                  o->bg.view<V>(),
+                                                  d_clique.as<unsigned long long>());
+        CK_LAUNCH();
+        scatter<V>(o->bg, nullptr, L.bi, L.bj, L.bw, q, s);
+        CK(cudaMemcpyAsync(&clique, d_clique.p, sizeof(clique), cudaMemcpyDeviceToHost, s));
+        t_post.stop(s);
+        CK(cudaStreamSynchronize(s));
+        init_ms += t_post.ms();
+        t_k2.start(s);
+        run_fw<V>(o->bg, s, ctx->sms);
+        t_k2.stop(s);
+        CK(cudaStreamSynchronize(s));
+        k2_ms = t_k2.ms();
+    }
+    // query-side tables
+    std::vector<uint64_t> cb_off(k + 1, 0);
+    for (uint32_t c = 0; c < k; ++c)
+        cb_off[c + 1] = cb_off[c] + sizes[c] * (R.bnd_off[c + 1] - R.bnd_off[c]);
+    t_post.start(s);
+    o->d_cb.alloc(cb_off[k] * sizeof(V));
+    o->d_cb_off = upload(cb_off, s);
+    o->d_comp_off = upload(R.comp_off, s);
+    o->d_bnd_off = std::move(d_bnd);
+    o->d_perm = upload(R.perm, s);
+    o->d_assign = upload(R.assign, s);
+    extract_to_boundary<V><<<k, 256, 0, s>>>(o->comps.view<V>(), o->d_comp_off.as<uint32_t>(),
+                                             o->d_bnd_off.as<uint32_t>(),
+                                             o->d_cb_off.as<uint64_t>(), o->d_cb.as<V>());
+    CK_LAUNCH();
+    t_post.stop(s);
+    CK(cudaStreamSynchronize(s));
+    init_ms += t_post.ms();
+    // panels are build-time scratch
+    o->comps.panel.reset();
+    o->bg.panel.reset();
+    const double boundary_ms = ms_since(t0);
+
+    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->d_cb_off.bytes +
+                      o->d_comp_off.bytes + o->d_bnd_off.bytes + o->d_perm.bytes +
+                      o->d_assign.bytes;
+    if (st) {
+        st->component_apsp_ms = component_ms;
+        st->boundary_ms = boundary_ms;
+        st->k1_device_ms = k1_ms;
+        st->k2_device_ms = k2_ms;
+        st->init_device_ms = init_ms;
+        st->k1_relaxations = o->comps.relaxations();
+        st->k2_relaxations = b ? o->bg.relaxations() : 0;
+        st->boundary_total = b;
+        st->bg_edges = L.bi.size() + clique;
+        uint64_t stored = 0;
+        for (uint32_t c = 0; c < k; ++c)
+            stored += sizes[c] * sizes[c] + (R.bnd_off[c + 1] - R.bnd_off[c]) * b;
+        st->stored_entries = stored;
+        st->value_kind = o->kind.kind;
+        st->fixed_point_shift = o->kind.shift;
+        st->device_bytes = o->device_bytes;
+    }
+}
+
+void set_peak_entries(const Reordered& R, unsigned workers, psp_build_stats* st) {
+    if (!st) return;
+    // RoundRobin placement over min(workers, k) (src/oracle.cpp:181-191)
+    const uint32_t p = std::max<uint32_t>(1, std::min<uint32_t>(workers, R.k));
+    std::vector<uint64_t> per(p, 0);
+    for (uint32_t c = 0; c < R.k; ++c) {
+        const uint64_t s = R.comp_off[c + 1] - R.comp_off[c];
+        per[c % p] += s * s + (R.bnd_off[c + 1] - R.bnd_off[c]) * R.b();
+    }
+    st->peak_table_entries_per_worker = *std::max_element(per.begin(), per.end());
+}
+
+psp_gpu_oracle* build_from_csr(psp_gpu_ctx* ctx, const Csr& g, uint32_t k,
+                               const std::vector<uint32_t>& assignment, const double* ew,
+                               uint64_t m, int value_kind, double partition_ms,
+                               psp_build_stats* st) {
+    auto o = std::make_unique<psp_gpu_oracle>();
+    o->ctx = ctx;
+    o->kind = choose_kind(value_kind, ew, m, g.n);
+    o->scale = std::ldexp(1.0, -o->kind.shift);
+    auto t0 = Clock::now();
+    o->R = reorder(g, k, assignment);
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->partition_ms = partition_ms + ms_since(t0);
+    }
+    CK(cudaSetDevice(ctx->device));
+    if (o->kind.kind == PSP_VALUE_U32) device_build<uint32_t>(o.get(), st);
+    else device_build<float>(o.get(), st);
+    return o.release();
+}
+
+template <class V>
+void dense_apsp(psp_gpu_ctx* ctx, const Csr& g, const double* ew, uint64_t m, Kind kind,
+                double* out) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = g.n;
+    if (n == 0) return;
+    if (n > 0xffffffffull / 2) throw ArgError("apsp: vertex count too large");
+    MatArena a;
+    a.create({n}, sizeof(V), true, s);
+    fill_arena<V>(a, s, ctx->sms);
+    std::vector<uint32_t> ii, jj;
+    std::vector<double> w;
+    for (uint64_t u = 0; u < n; ++u)
+        for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e)
+            if (g.to[e] > u) {
+                ii.push_back(static_cast<uint32_t>(u));
+                jj.push_back(g.to[e]);
+                w.push_back(g.w[e]);
+            }
+    (void)ew;
+    (void)m;
+    scatter<V>(a, nullptr, ii, jj, w, kind.shift, s);
+    run_fw<V>(a, s, ctx->sms);
+    DBuf d(n * n * sizeof(V));
+    const uint64_t cnt = n * n;
+    unpack_window<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(a.view<V>(), 0, 0, uint32_t(n), 0,
+                                                                 uint32_t(n), d.as<V>());
+    CK_LAUNCH();
+    std::vector<V> h(cnt);
+    CK(cudaMemcpyAsync(h.data(), d.p, cnt * sizeof(V), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    to_f64(h, out, std::ldexp(1.0, -kind.shift));
+}
+
+template <class V>
+void export_window(const psp_gpu_oracle* o, const MatArena& a, uint32_t m, uint32_t row0,
+                   uint32_t nrows, uint32_t ncols, double* dst) {
+    const uint64_t cnt = uint64_t(nrows) * ncols;
+    if (cnt == 0) return;
+    cudaStream_t s = o->ctx->stream;
+    CK(cudaSetDevice(o->ctx->device));
+    DBuf d(cnt * sizeof(V));
+    unpack_window<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(a.view<V>(), m, row0, nrows, 0,
+                                                                 ncols, d.as<V>());
+    CK_LAUNCH();
+    std::vector<V> h(cnt);
+    CK(cudaMemcpyAsync(h.data(), d.p, cnt * sizeof(V), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    to_f64(h, dst, o->scale);
+}
+
+template <class V>
+void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
+                    const uint32_t* v2, double* dist, cudaStream_t s) {
+    if (count == 0) return;
+    QueryView<V> q;
+    q.perm = o->d_perm.as<uint32_t>();
+    q.assign = o->d_assign.as<uint32_t>();
+    q.comp_off = o->d_comp_off.as<uint32_t>();
+    q.bnd_off = o->d_bnd_off.as<uint32_t>();
+    q.cb_off = o->d_cb_off.as<uint64_t>();
+    q.cb = o->d_cb.as<V>();
+    q.comps = o->comps.view<V>();
+    q.bg = o->bg.tiles.as<V>();
+    q.bg_nb = o->bg.nmat ? o->bg.nb[0] : 0;
+    q.scale = o->scale;
+    const uint64_t warps_per_block = 8;
+    const uint64_t want = (count + warps_per_block - 1) / warps_per_block;
+    const unsigned blocks =
+        unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(o->ctx->sms) * 16)));
+    query_warp<V><<<blocks, 256, 0, s>>>(q, v1, v2, count, dist);
+    CK_LAUNCH();
+}
+
+}  // namespace
+
+// ================================================================ C-ABI ==
+extern "C" {
+
+int psp_gpu_abi_version(void) { return PSP_GPU_ABI_VERSION; }
+const char* psp_gpu_last_error(void) { return g_err.c_str(); }
+
+int psp_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+psp_status psp_gpu_ctx_create(int device, int rank, int world, const void* nccl_id,
+                              psp_gpu_ctx** out) {
+    return guarded([&] {
+        if (!out) throw ArgError("ctx_create: out is NULL");
+        if (world < 1 || rank < 0 || rank >= world) throw ArgError("ctx_create: bad rank/world");
+        if (world > 1 && !nccl_id) throw ArgError("ctx_create: world > 1 needs an NCCL id");
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw ArgError("ctx_create: no such CUDA device");
+        CK(cudaSetDevice(device));
+        auto c = std::make_unique<psp_gpu_ctx>();
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+void psp_gpu_ctx_destroy(psp_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+psp_status psp_gpu_nccl_unique_id(void* out128) {
+    return guarded([&] {
+        (void)out128;
+        throw Fail{PSP_ENCCL, "NCCL sharding is not built into this library version"};
+    });
+}
+
+void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+psp_status psp_gpu_build_oracle(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* eu,
+                                const uint32_t* ev, const double* ew, uint32_t k,
+                                uint32_t workers, uint64_t seed, int value_kind,
+                                psp_gpu_oracle** out, psp_build_stats* stats) {
+    return guarded([&] {
+        if (!ctx || !out) throw ArgError("build_oracle: NULL ctx/out");
+        if (workers < 1) throw ArgError("build_oracle: workers must be at least 1");
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        auto t0 = Clock::now();
+        const std::vector<uint32_t> a = partition_graph(g, k, seed, workers);
+        const double part_ms = ms_since(t0);
+        psp_gpu_oracle* o = build_from_csr(ctx, g, k, a, ew, m, value_kind, part_ms, stats);
+        set_peak_entries(o->R, workers, stats);
+        *out = o;
+    });
+}
+
+psp_status psp_gpu_build_partitioned(psp_gpu_ctx* ctx, uint64_t n, uint64_t m,
+                                     const uint32_t* eu, const uint32_t* ev, const double* ew,
+                                     uint32_t k, const uint32_t* assignment, int value_kind,
+                                     psp_gpu_oracle** out, psp_build_stats* stats) {
+    return guarded([&] {
+        if (!ctx || !out || (!assignment && n)) throw ArgError("build_partitioned: NULL argument");
+        if (k < 1 || k > n) throw ArgError("build_partitioned: k must be in 1..n");
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        std::vector<uint32_t> a(assignment, assignment + n);
+        psp_gpu_oracle* o = build_from_csr(ctx, g, k, a, ew, m, value_kind, 0.0, stats);
+        set_peak_entries(o->R, 1, stats);
+        *out = o;
+    });
+}
+
+void psp_gpu_oracle_free(psp_gpu_oracle* o) {
+    if (!o) return;
+    cudaSetDevice(o->ctx->device);
+    delete o;
+}
+
+psp_status psp_gpu_oracle_info(const psp_gpu_oracle* o, psp_oracle_info* out) {
+    return guarded([&] {
+        if (!o || !out) throw ArgError("oracle_info: NULL argument");
+        out->n = o->R.n;
+        out->k = o->R.k;
+        out->b = o->R.b();
+        out->value_kind = o->kind.kind;
+        out->fixed_point_shift = o->kind.shift;
+        out->device = o->ctx->device;
+        out->tile = T;
+    });
+}
+
+psp_status psp_gpu_oracle_ids(const psp_gpu_oracle* o, uint32_t* permutation,
+                              uint32_t* inverse_permutation, uint32_t* assignment,
+                              uint8_t* boundary_flags, uint64_t* component_offset,
+                              uint64_t* boundary_offset, uint32_t* boundary_vertex) {
+    return guarded([&] {
+        if (!o) throw ArgError("oracle_ids: NULL oracle");
+        const Reordered& R = o->R;
+        if (permutation) std::copy(R.perm.begin(), R.perm.end(), permutation);
+        if (inverse_permutation) std::copy(R.inv.begin(), R.inv.end(), inverse_permutation);
+        if (assignment) std::copy(R.assign.begin(), R.assign.end(), assignment);
+        if (boundary_flags) std::copy(R.flags.begin(), R.flags.end(), boundary_flags);
+        if (component_offset) std::copy(R.comp_off.begin(), R.comp_off.end(), component_offset);
+        if (boundary_offset) std::copy(R.bnd_off.begin(), R.bnd_off.end(), boundary_offset);
+        if (boundary_vertex) {
+            // boundary id -> reordered vertex (src/oracle.cpp:80-85)
+            uint64_t at = 0;
+            for (uint64_t v = 0; v < R.n; ++v)
+                if (R.flags[v]) boundary_vertex[at++] = static_cast<uint32_t>(v);
+        }
+    });
+}
+
+psp_status psp_gpu_export_component(const psp_gpu_oracle* o, uint32_t c, double* dst) {
+    return guarded([&] {
+        if (!o || !dst) throw ArgError("export_component: NULL argument");
+        if (c >= o->R.k) throw ArgError("export_component: component out of range");
+        const uint32_t s = o->R.comp_off[c + 1] - o->R.comp_off[c];
+        if (o->kind.kind == PSP_VALUE_U32) export_window<uint32_t>(o, o->comps, c, 0, s, s, dst);
+        else export_window<float>(o, o->comps, c, 0, s, s, dst);
+    });
+}
+
+psp_status psp_gpu_export_boundary_rows(const psp_gpu_oracle* o, uint32_t c, double* dst) {
+    return guarded([&] {
+        if (!o || !dst) throw ArgError("export_boundary_rows: NULL argument");
+        if (c >= o->R.k) throw ArgError("export_boundary_rows: component out of range");
+        const uint32_t g = o->R.bnd_off[c], B = o->R.bnd_off[c + 1] - g;
+        const uint32_t b = static_cast<uint32_t>(o->R.b());
+        if (B == 0 || b == 0) return;
+        if (o->kind.kind == PSP_VALUE_U32) export_window<uint32_t>(o, o->bg, 0, g, B, b, dst);
+        else export_window<float>(o, o->bg, 0, g, B, b, dst);
+    });
+}
+
+psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
+                               const uint32_t* v2, double* dist, uint64_t* minplus_ops) {
+    return guarded([&] {
+        if (!o) throw ArgError("query_batch: NULL oracle");
+        if (count == 0) return;
+        if (!v1 || !v2 || !dist) throw ArgError("query_batch: NULL array");
+        const Reordered& R = o->R;
+        for (uint64_t i = 0; i < count; ++i)
+            if (v1[i] >= R.n || v2[i] >= R.n)
+                throw ArgError("query: vertex id out of range");  // src/query.cpp:30
+        cudaStream_t s = o->ctx->stream;
+        CK(cudaSetDevice(o->ctx->device));
+        DBuf d(count * (sizeof(double) + 2 * sizeof(uint32_t)));
+        double* dd = d.as<double>();
+        uint32_t* d1 = reinterpret_cast<uint32_t*>(dd + count);
+        uint32_t* d2 = d1 + count;
+        CK(cudaMemcpyAsync(d1, v1, count * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d2, v2, count * 4, cudaMemcpyHostToDevice, s));
+        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, d1, d2, dd, s);
+        else launch_queries<float>(o, count, d1, d2, dd, s);
+        CK(cudaMemcpyAsync(dist, dd, count * 8, cudaMemcpyDeviceToHost, s));
+        if (minplus_ops) {
+            for (uint64_t i = 0; i < count; ++i) {
+                const uint32_t c1 = R.assign[R.perm[v1[i]]], c2 = R.assign[R.perm[v2[i]]];
+                const uint64_t b1 = R.bnd_off[c1 + 1] - R.bnd_off[c1];
+                const uint64_t b2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
+                minplus_ops[i] = b1 * b2 + b2;  // src/query.cpp:73
+            }
+        }
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
+                                      const uint32_t* v1, const uint32_t* v2, double* dist,
+                                      void* stream) {
+    return guarded([&] {
+        if (!o) throw ArgError("query_batch_device: NULL oracle");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : o->ctx->stream;
+        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, v1, v2, dist, s);
+        else launch_queries<float>(o, count, v1, v2, dist, s);
+    });
+}
+
+psp_status psp_gpu_apsp_dense(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* eu,
+                              const uint32_t* ev, const double* ew, uint64_t block_size,
+                              int value_kind, double* out) {
+    return guarded([&] {
+        if (!ctx) throw ArgError("apsp_dense: NULL ctx");
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        if (n == 0) return;
+        if (block_size == 0) throw ArgError("apsp_dense: block size must be positive");
+        const Kind kind = choose_kind(value_kind, ew, m, n);
+        CK(cudaSetDevice(ctx->device));
+        if (kind.kind == PSP_VALUE_U32) dense_apsp<uint32_t>(ctx, g, ew, m, kind, out);
+        else dense_apsp<float>(ctx, g, ew, m, kind, out);
+    });
+}
+
+psp_status psp_gpu_boundary_apsp(psp_gpu_ctx* ctx, uint64_t b, uint64_t m, const uint32_t* eu,
+                                 const uint32_t* ev, const double* ew, int value_kind,
+                                 double* out) {
+    // The boundary graph's all-pairs table is exactly the dense APSP of the
+    // boundary graph; rows are already in boundary-id (component) order.
+    return psp_gpu_apsp_dense(ctx, b, m, eu, ev, ew, 64, value_kind, out);
+}
+
+psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_per_s,
+                                double* sm_clock_mhz) {
+    return guarded([&] {
+        if (!ctx || !relax_per_s) throw ArgError("minplus_peak: NULL argument");
+        CK(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        DBuf out(ctx->sms * 64 * sizeof(uint32_t));
+        const int blocks = ctx->sms * 4;
+        const uint32_t iters = 1 << 14;
+        EventTimer t;
+        for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+            t.start(s);
+            if (value_kind == PSP_VALUE_F32)
+                minplus_peak_kernel<float><<<blocks, NTHREADS, 0, s>>>(out.as<float>(), iters, 1.0f);
+            else
+                minplus_peak_kernel<uint32_t><<<blocks, NTHREADS, 0, s>>>(out.as<uint32_t>(), iters, 1u);
+            CK_LAUNCH();
+            t.stop(s);
+        }
+        const double ms = t.ms();
+        *relax_per_s = double(blocks) * NTHREADS * 64.0 * iters / (ms * 1e-3);
+        if (sm_clock_mhz) {
+            int khz = 0;
+            CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device));
+            *sm_clock_mhz = khz / 1000.0;
+        }
+    });
+}
+
+psp_status psp_partition_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                               const double* ew, uint32_t k, uint64_t seed, uint32_t threads,
+                               uint32_t* assignment) {
+    return guarded([&] {
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        const std::vector<uint32_t> a = partition_graph(g, k, seed, std::max(1u, threads));
+        std::copy(a.begin(), a.end(), assignment);
+    });
+}
+
+psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, double lo,
+                             double hi, uint64_t seed, uint64_t* m, uint32_t* eu, uint32_t* ev,
+                             double* ew) {
+    return guarded([&] {
+        if (!m) throw ArgError("generate_grid: NULL m");
+        if (kind != 0 && kind != 1) throw ArgError("generate_grid: kind must be 0 or 1");
+        if (!eu) {
+            if (rows == 0 || cols == 0) throw ArgError("grid dimensions must be positive");
+            *m = rows * (cols - 1) + (rows - 1) * cols + (kind == 1 ? (rows - 1) * (cols - 1) : 0);
+            return;
+        }
+        std::vector<uint32_t> a, b;
+        std::vector<double> w;
+        generate_grid(kind, rows, cols, unit != 0, lo, hi, seed, a, b, w);
+        std::copy(a.begin(), a.end(), eu);
+        std::copy(b.begin(), b.end(), ev);
+        std::copy(w.begin(), w.end(), ew);
+        *m = a.size();
+    });
+}
+
+void psp_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2) {
+    std::mt19937_64 rng(seed);
+    for (uint64_t i = 0; i < count; ++i) {
+        v1[i] = static_cast<uint32_t>(rng() % n);
+        v2[i] = static_cast<uint32_t>(rng() % n);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""Synthetic planar inputs for the BASELINE.json configurations.
+
+The reference only generates (triangulated) grids (include/psp/generators.hpp:
+23-30) but loads any edge list (src/graph_io.cpp:50-91); the Delaunay and
+road-like families named in BASELINE.json are defined here, seeded and
+deterministic, and emitted as plain edge lists that both the GPU build and
+the CPU reference consume.
+
+* delaunay(n, seed): Delaunay triangulation (scipy Qhull) of n uniform points
+  in [0,1)^2 drawn with numpy default_rng(seed); unique undirected edges in
+  lexicographic order; integer weights rng.integers(1, 1025) drawn after the
+  points.
+* road_grid(rows, cols, seed): "road-like perturbed grid": a 4-neighbour grid
+  with ~10% of edges deleted (kept connected via a random spanning tree) and
+  jittered coordinates; f32-representable weights = Euclidean length of the
+  jittered embedding times U[1,2) rounded to f32 (the tolerance path).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import Graph
+
+
+def delaunay(n: int, seed: int = 1) -> Graph:
+    from scipy.spatial import Delaunay
+
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 2))
+    tri = Delaunay(pts)
+    s = tri.simplices.astype(np.int64)
+    e = np.concatenate([s[:, [0, 1]], s[:, [1, 2]], s[:, [0, 2]]])
+    e.sort(axis=1)
+    e = np.unique(e, axis=0)
+    w = rng.integers(1, 1025, size=len(e)).astype(np.float64)
+    return Graph(n, e[:, 0].astype(np.uint32), e[:, 1].astype(np.uint32), w)
+
+
+def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10) -> Graph:
+    rng = np.random.default_rng(seed)
+    n = rows * cols
+    r, c = np.divmod(np.arange(n, dtype=np.int64), cols)
+    xy = np.stack([c + rng.uniform(-0.3, 0.3, n), r + rng.uniform(-0.3, 0.3, n)], axis=1)
+    right = np.arange(n)[c + 1 < cols]
+    down = np.arange(n)[r + 1 < rows]
+    eu = np.concatenate([right, down])
+    ev = np.concatenate([right + 1, down + cols])
+    # keep a random spanning tree (randomised Kruskal on a shuffled order) so
+    # deletions never disconnect the network, then drop a fraction of the rest
+    order = rng.permutation(len(eu))
+    parent = np.arange(n)
+
+    def find(x):
+        root = x
+        while parent[root] != root:
+            root = parent[root]
+        while parent[x] != root:
+            parent[x], x = root, parent[x]
+        return root
+
+    in_tree = np.zeros(len(eu), bool)
+    for idx in order:
+        a, b = find(eu[idx]), find(ev[idx])
+        if a != b:
+            parent[a] = b
+            in_tree[idx] = True
+    keep = in_tree | (rng.random(len(eu)) >= drop)
+    eu, ev = eu[keep], ev[keep]
+    length = np.linalg.norm(xy[eu] - xy[ev], axis=1)
+    w = (length * rng.uniform(1.0, 2.0, len(eu))).astype(np.float32).astype(np.float64)
+    return Graph(n, eu.astype(np.uint32), ev.astype(np.uint32), w)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]: runs on the CPU reference too
+    "grid64_k16": dict(family="grid", rows=64, cols=64, weights=(1, 1025), seed=1, k=16,
+                       queries=10_000),
+    # configs[1]
+    "delaunay262k_k256": dict(family="delaunay", n=262_144, seed=1, k=256, queries=1_000_000),
+    # configs[2]
+    "delaunay1m_k1024": dict(family="delaunay", n=1_048_576, seed=1, k=1024,
+                             queries=10_000_000),
+}
+
+
+def make(name: str) -> tuple[Graph, dict]:
+    cfg = dict(CONFIGS[name])
+    fam = cfg["family"]
+    if fam == "grid":
+        from . import generate_grid
+        g = generate_grid(cfg["rows"], cfg["cols"], cfg["weights"], cfg["seed"])
+    elif fam == "delaunay":
+        g = delaunay(cfg["n"], cfg["seed"])
+    else:
+        raise ValueError(fam)
+    return g, cfg

@@ -1,0 +1,261 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference.
+
+Checkers: the committed reference fixtures (tests/golden/), the live
+reference build (oracle/_ref, travels to the GPU box as a .so) and the C
+restatement (oracle/). Integer and dyadic-lattice weights are compared bit
+for bit; the f32 path within relative 1e-5 (BASELINE.json north_star).
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1503_07192_b200 as P
+from conftest import graph_of
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+F32_RTOL = 1e-5  # north_star tolerance for float32 weights
+
+SMALL = ["grid2x3_k2", "grid2x3_k1", "cycle8_k2_s4", "two_squares_k2", "isolated2_k2",
+         "grid16_k4", "grid16_k8_lattice", "tri9_k6", "grid10_k2", "tri20_k20_w0",
+         "grid32_k32_unit"]
+
+
+def assert_same_oracle(o: P.GpuOracle, case: dict, full_tables: bool = True):
+    k = int(case["k"])
+    assert o.k == k and o.n == int(case["n"])
+    assert np.array_equal(o.permutation, case["permutation"])
+    assert np.array_equal(o.component_offset, case["component_offset"])
+    assert np.array_equal(o.boundary_offset, case["boundary_offset"])
+    assert np.array_equal(o.boundary_vertex, case["boundary_vertex"])
+    assert o.b == int(case["b"])
+    assert o.stats["bg_edges"] == int(case["bg_edges"])
+    assert o.stats["stored_entries"] == int(case["stored_entries"])
+    assert o.stored_entries() == int(case["stored_entries"])
+    h = hashlib.sha256()
+    for c in range(k):
+        ct, bt = o.component_table(c), o.boundary_rows(c)
+        if full_tables:
+            assert np.array_equal(ct, case[f"ct{c}"]), f"component table {c}"
+            assert np.array_equal(bt, case[f"bt{c}"]), f"boundary rows {c}"
+        h.update(ct.tobytes())
+        h.update(bt.tobytes())
+    assert h.digest() == case["tables_sha256"].tobytes()
+    d, ops = o.batch_query(case["q_v1"], case["q_v2"], with_ops=True)
+    assert np.array_equal(d, case["q_dist"])
+    assert np.array_equal(ops, case["q_ops"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_build_oracle_matches_reference_fixture(golden_small, name):
+    case = golden_small[name]
+    o = P.build_oracle(graph_of(case), int(case["k"]), 1, int(case["seed"]))
+    assert o.value_kind == P.VALUE_U32  # integral or dyadic -> exact path
+    assert_same_oracle(o, case)
+    assert o.stats["peak_table_entries_per_worker"] == int(case["peak_table_entries_per_worker"])
+
+
+def test_grid2x3_golden_vectors(golden_small):
+    # tests/test_oracle.cpp:28-79 and tests/test_query.cpp:30-62
+    o = P.build_oracle(P.generate_grid(2, 3), 2, 1, 0)
+    path = [0, 2, 1, 2, 0, 1, 1, 1, 0]
+    assert o.component_table(0).ravel().tolist() == path
+    assert o.component_table(1).ravel().tolist() == path
+    assert o.boundary_rows(0).ravel().tolist() == [0, 2, 1, 1, 2, 0, 3, 1]
+    assert o.boundary_rows(1).ravel().tolist() == [1, 3, 0, 2, 1, 1, 2, 0]
+    assert o.stats["bg_edges"] == 5 and o.stats["stored_entries"] == 34
+    assert o.query(0, 5) == (3.0, 6)
+    g = P.generate_grid(2, 3)
+    truth = oracle.apsp_dense(6, g.eu, g.ev, g.ew)
+    v1, v2 = np.divmod(np.arange(36), 6)
+    assert np.array_equal(o.batch_query(v1, v2), truth[v1, v2])
+
+
+def test_same_component_escape_route():
+    # tests/test_query.cpp:64-89
+    g = P.Graph(8, [0, 1, 2, 3, 4, 5, 6, 0], [1, 2, 3, 4, 5, 6, 7, 7],
+                [1, 1, 1, 10, 1, 1, 1, 1])
+    o = P.build_oracle(g, 2, 1, 4)
+    assert o.query(2, 5)[0] == 5.0
+    assert o.query(3, 3)[0] == 0.0
+
+
+def test_unreachable_and_errors():
+    # tests/test_query.cpp:155-172
+    o = P.build_oracle(P.Graph(2, [], [], []), 2, 1, 0)
+    d, ops = o.query(0, 1)
+    assert d == INF and ops == 0
+    assert o.query(0, 0)[0] == 0.0
+    o2 = P.build_oracle(P.generate_grid(2, 3), 2, 1, 0)
+    with pytest.raises(ValueError):
+        o2.query(0, 6)
+    with pytest.raises(ValueError):
+        o2.query(6, 0)
+    with pytest.raises(ValueError):
+        P.build_oracle(P.generate_grid(2, 3), 7, 1, 0)       # k > n
+    with pytest.raises(ValueError):
+        P.build_oracle(P.generate_grid(2, 3), 2, 0, 0)       # workers < 1
+
+
+def test_workers_do_not_change_the_oracle(golden_cfg1):
+    # include/psp/oracle.hpp:80-84; tests/test_oracle.cpp:151-160
+    g = graph_of(golden_cfg1)
+    a = P.build_oracle(g, 16, 1, 0)
+    b = P.build_oracle(g, 16, 8, 0)
+    for c in range(16):
+        assert np.array_equal(a.component_table(c), b.component_table(c))
+        assert np.array_equal(a.boundary_rows(c), b.boundary_rows(c))
+
+
+def test_cfg1_matches_reference(golden_cfg1):
+    # BASELINE.json configs[0]: 64x64 grid, integer weights 1..1025, k=16
+    case = golden_cfg1
+    o = P.build_oracle(graph_of(case), 16, 8, 0)
+    assert_same_oracle(o, case, full_tables=False)
+
+
+def test_cfg1_matches_live_reference_and_restatement(ref):
+    rg = ref.generate("grid", 64, 64, (1, 1025), 1)
+    ro = rg.build_oracle(16, 8, 0)
+    eu, ev, ew = rg.edges()
+    g = P.Graph(rg.n, eu, ev, ew)
+    o = P.build_oracle(g, 16, 8, 0)
+    po = oracle.Oracle(rg.n, eu, ev, ew, 16, ro.permutation, ro.assignment, ro.boundary_flags)
+    for c in range(16):
+        ct = o.component_table(c)
+        assert np.array_equal(ct, ro.component_table(c))
+        assert np.array_equal(ct, po.component_table(c))
+        bt = o.boundary_rows(c)
+        assert np.array_equal(bt, ro.boundary_rows(c))
+        assert np.array_equal(bt, po.boundary_rows(c))
+    v1, v2 = ref.random_pairs(rg.n, 50_000, 3)
+    d, ops = o.batch_query(v1, v2, with_ops=True)
+    rd, rops = ro.batch_query(v1, v2, 8, with_ops=True)
+    assert np.array_equal(d, rd) and np.array_equal(ops, rops)
+
+
+@pytest.mark.parametrize("kind,rows,cols,w,gseed", [
+    ("grid", 4, 4, None, 0), ("grid", 9, 9, (0.25, 2.0), 5), ("tri", 7, 8, (1.0, 3.0), 1)])
+def test_apsp_dense_bitwise(ref, kind, rows, cols, w, gseed):
+    # tests/test_shortest_paths.cpp:55-74 (FW == triple loop, any block size)
+    rg = ref.generate(kind, rows, cols, w, gseed)
+    eu, ev, ew = rg.edges()
+    g = P.Graph(rg.n, eu, ev, ew)
+    want = rg.apsp_dense(64)
+    for bs in (1, 3, 41, 64, 4096):
+        assert np.array_equal(P.apsp_dense(g, bs), want)
+    d = P.apsp_dense(g)
+    assert (np.diag(d) == 0).all() and np.array_equal(d, d.T)
+    with pytest.raises(ValueError):
+        P.apsp_dense(g, 0)
+
+
+def test_apsp_dense_disconnected_and_tiles():
+    # tests/test_shortest_paths.cpp:59-60 plus sizes straddling the 128 tile
+    g = P.Graph(6, [0, 1, 4], [1, 2, 5], [1, 1, 7])
+    want = oracle.apsp_dense(6, g.eu, g.ev, g.ew)
+    assert np.array_equal(P.apsp_dense(g), want)
+    for rows, cols in ((8, 16), (13, 20), (16, 17), (20, 26), (30, 30)):
+        gg = P.generate_triangulated_grid(rows, cols, (0.0, 1024.0), rows * cols)
+        assert np.array_equal(P.apsp_dense(gg), oracle.apsp_dense(gg.n, gg.eu, gg.ev, gg.ew))
+
+
+def test_boundary_apsp_clique_omission():
+    # tests/test_oracle.cpp:90-112: BG over 3 boundary vertices, clique pair
+    # (0,1) omitted because it is unreachable inside its component
+    bg = P.Graph(3, [0, 1], [2, 2], [1.0, 1.0])
+    t = P.boundary_apsp(bg)
+    assert t[:2].ravel().tolist() == [0, 2, 1, 2, 0, 1]
+    assert t[2:].ravel().tolist() == [1, 1, 0]
+
+
+@pytest.mark.parametrize("side,k", [(20, 1), (20, 2), (20, 4), (20, 20), (33, 6), (44, 44)])
+def test_exhaustive_all_pairs(side, k):
+    # acceptance criterion 1 (acceptance_main.cpp:79-123): all n^2 queries
+    g = P.generate_triangulated_grid(side, side, (1.0, 9.0), side)
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    o = P.build_oracle(g, k, 4, 0)
+    v1, v2 = np.divmod(np.arange(g.n * g.n, dtype=np.int64), g.n)
+    d = o.batch_query(v1, v2)
+    assert np.array_equal(d, truth[v1, v2])
+
+
+def test_boundary_rows_equal_full_graph_distances():
+    # Lemma 1 / acceptance criterion 3 (acceptance_main.cpp:157-180)
+    g = P.generate_grid(40, 40, (1, 1025), 8)
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    o = P.build_oracle(g, 40, 4, 0)
+    orig_of_b = o.inverse_permutation[o.boundary_vertex]
+    for c in range(o.k):
+        rows = o.boundary_rows(c)
+        lo = int(o.boundary_offset[c])
+        want = truth[np.ix_(orig_of_b[lo: lo + rows.shape[0]], orig_of_b)]
+        assert np.array_equal(rows, want)
+
+
+def test_large_grid_sampled_against_dijkstra():
+    # acceptance criterion 2 (acceptance_main.cpp:127-153): 256x256 unit grid,
+    # k=128, random queries vs per-source Dijkstra on the original graph
+    g = P.generate_grid(256, 256)
+    o = P.build_oracle(g, 128, 8, 0)
+    v1, v2 = P.random_pairs(g.n, 4000, 17)
+    d = o.batch_query(v1, v2)
+    order = np.argsort(v1, kind="stable")
+    last, truth = -1, None
+    for i in order[:1500]:
+        if v1[i] != last:
+            truth = oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(v1[i]))
+            last = v1[i]
+        assert d[i] == truth[v2[i]]
+    # undirected symmetry (tests/test_query.cpp:144-153)
+    assert np.array_equal(o.batch_query(v2, v1), d)
+
+
+def test_delaunay_sampled_against_dijkstra():
+    from paper_1503_07192_b200 import graphs
+    g = graphs.delaunay(20_000, 5)
+    o = P.build_oracle(g, 141, 8, 0)
+    assert o.value_kind == P.VALUE_U32
+    v1, v2 = P.random_pairs(g.n, 20_000, 9)
+    d = o.batch_query(v1, v2)
+    for s in np.unique(v1)[:25]:
+        truth = oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(s))
+        sel = v1 == s
+        assert np.array_equal(d[sel], truth[v2[sel]])
+
+
+def test_f32_tolerance_path():
+    # non-dyadic weights -> f32 kernels; relative error <= 1e-5 vs f64
+    rng = np.random.default_rng(3)
+    g = P.generate_grid(48, 48)
+    g = P.Graph(g.n, g.eu, g.ev, rng.uniform(1.0, 2.0, g.m).astype(np.float32).astype(np.float64))
+    o = P.build_oracle(g, 24, 4, 0)
+    assert o.value_kind == P.VALUE_F32
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    v1, v2 = np.divmod(np.arange(g.n * g.n, dtype=np.int64)[::7], g.n)
+    d = o.batch_query(v1, v2)
+    t = truth[v1, v2]
+    rel = np.abs(d - t) / np.maximum(t, 1e-300)
+    rel[t == 0] = np.abs(d[t == 0])
+    assert rel.max() <= F32_RTOL, rel.max()
+    # forcing u32 on non-dyadic weights is refused, not silently rounded
+    with pytest.raises(ValueError):
+        P.build_oracle(g, 24, 1, 0, value_kind=P.VALUE_U32)
+
+
+def test_disconnected_components_give_empty_boundary_graph(golden_small):
+    # tests/test_oracle.cpp:114-122
+    case = golden_small["two_squares_k2"]
+    o = P.build_oracle(graph_of(case), 2, 1, 0)
+    assert o.b == 0 and o.stats["bg_edges"] == 0 and o.stored_entries() == 32
+
+
+def test_minplus_peak_probe(ctx):
+    r_u32, mhz = ctx.minplus_peak(P.VALUE_U32)
+    r_f32, _ = ctx.minplus_peak(P.VALUE_F32)
+    assert r_u32 > 1e12 and r_f32 > 1e12 and mhz > 500

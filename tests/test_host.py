@@ -1,0 +1,134 @@
+"""Host-side logic of the product library (no GPU needed): graph
+validation, generators, the restated partitioner and the C-ABI surface."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1503_07192_b200 as P
+from paper_1503_07192_b200 import _lib
+from conftest import GOLDEN, ROOT, graph_of
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "psp_gpu.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(psp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    # and the Python binding covers exactly that surface
+    assert set(syms) == set(_lib.SIGNATURES)
+    assert L.psp_gpu_abi_version() == 1
+
+
+def test_no_gpu_fails_loudly_or_works():
+    # Without a device the context must fail with PSP_ECUDA/EINVAL, never
+    # fall back to the CPU.
+    L = _lib.lib()
+    if L.psp_gpu_device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(P.PspError) as ei:
+        P.Context(0)
+    assert ei.value.status in (_lib.PSP_ECUDA, _lib.PSP_EINVAL)
+
+
+def test_random_pairs_stream_matches_reference():
+    # ref::random_pairs (tests/support/reference.hpp:86-88) evaluates
+    # emplace_back(rng() % n, rng() % n) right to left under g++, so its v2 is
+    # the first draw; the CLI's random_pairs (tools/psp_main.cpp:113-117)
+    # draws v1 first. psp_random_pairs follows the CLI; order="tests" swaps.
+    z = np.load(os.path.join(GOLDEN, "random_pairs_n1000_s123.npz"))
+    v1, v2 = P.random_pairs(1000, 16, 123)
+    assert np.array_equal(v2, z["v1"]) and np.array_equal(v1, z["v2"])
+    t1, t2 = P.random_pairs(1000, 16, 123, order="tests")
+    assert np.array_equal(t1, z["v1"]) and np.array_equal(t2, z["v2"])
+
+
+@pytest.mark.parametrize("kind,rows,cols,w,seed", [
+    ("grid", 64, 64, (1, 1025), 1), ("grid", 2, 3, None, 0), ("tri", 9, 9, (1.0, 3.0), 4),
+    ("tri", 20, 20, (0.0, 1024.0), 3), ("grid", 16, 16, (0.5, 2.0), 9)])
+def test_generators_match_reference(ref, kind, rows, cols, w, seed):
+    g = (P.generate_grid if kind == "grid" else P.generate_triangulated_grid)(rows, cols, w, seed)
+    eu, ev, ew = ref.generate(kind, rows, cols, w, seed).edges()
+    a, b = np.minimum(g.eu, g.ev), np.maximum(g.eu, g.ev)
+    o = np.lexsort((b, a))
+    assert np.array_equal(a[o], eu) and np.array_equal(b[o], ev) and np.array_equal(g.ew[o], ew)
+
+
+def test_generator_argument_errors():
+    with pytest.raises(ValueError):
+        P.generate_grid(0, 3)
+    with pytest.raises(ValueError):
+        P.generate_grid(3, 3, (2.0, 1.0))
+
+
+@pytest.mark.parametrize("name", ["grid2x3_k2", "cycle8_k2_s4", "two_squares_k2", "isolated2_k2",
+                                  "grid16_k4", "grid16_k8_lattice", "tri9_k6", "grid10_k2",
+                                  "tri20_k20_w0", "grid32_k32_unit"])
+def test_partition_matches_reference_fixtures(golden_small, name):
+    case = golden_small[name]
+    g = graph_of(case)
+    a = P.partition_graph(g, int(case["k"]), int(case["seed"]), threads=4)
+    assert np.array_equal(a, case["assignment"])
+
+
+def test_partition_cfg1_fixture(golden_cfg1):
+    g = graph_of(golden_cfg1)
+    for threads in (1, 8):  # worker count never changes the result
+        a = P.partition_graph(g, 16, 0, threads=threads)
+        assert np.array_equal(a, golden_cfg1["assignment"])
+
+
+@pytest.mark.parametrize("kind,rows,cols,w,gseed,k,seed", [
+    ("grid", 40, 40, None, 0, 40, 0), ("tri", 25, 31, (1.0, 4.0), 2, 17, 3),
+    ("grid", 33, 47, (1, 1025), 5, 64, 9), ("tri", 50, 50, (0.0, 1024.0), 1, 50, 1),
+    ("grid", 7, 7, None, 0, 49, 0),  # k = n: every vertex its own component
+])
+def test_partition_matches_live_reference(ref, kind, rows, cols, w, gseed, k, seed):
+    rg = ref.generate(kind, rows, cols, w, gseed)
+    want, _ = rg.partition(k, seed)
+    eu, ev, ew = rg.edges()
+    got = P.partition_graph(P.Graph(rg.n, eu, ev, ew), k, seed, threads=8)
+    assert np.array_equal(got, want)
+
+
+def test_partition_disconnected_matches_reference(ref):
+    # unreached vertices + isolated vertices exercise finalize's fill step
+    eu = np.array([0, 1, 2, 5, 6, 8], np.uint32)
+    ev = np.array([1, 2, 3, 6, 7, 9], np.uint32)
+    ew = np.ones(6)
+    rg = ref.graph(12, eu, ev, ew)
+    for k, seed in ((2, 0), (3, 1), (5, 2), (12, 0)):
+        want, _ = rg.partition(k, seed)
+        got = P.partition_graph(P.Graph(12, eu, ev, ew), k, seed, threads=4)
+        assert np.array_equal(got, want), (k, seed)
+
+
+def test_partition_argument_errors():
+    g = P.generate_grid(2, 3)
+    with pytest.raises(ValueError):
+        P.partition_graph(g, 0)
+    with pytest.raises(ValueError):
+        P.partition_graph(g, 7)
+
+
+@pytest.mark.parametrize("edges,msg", [
+    (([0], [0], [1.0]), "self-loop"), (([0], [1], [-1.0]), "negative"),
+    (([0], [1], [np.nan]), "non-finite"), (([0, 1], [1, 0], [1.0, 1.0]), "duplicate"),
+    (([0], [9], [1.0]), "outside"),
+])
+def test_graph_invariants_rejected(edges, msg):
+    eu, ev, ew = edges
+    g = P.Graph(3, eu, ev, ew)
+    with pytest.raises(P.GraphInvariantError, match=msg):
+        P.partition_graph(g, 1)
