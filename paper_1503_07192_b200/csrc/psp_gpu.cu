@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <type_traits>
 #include <string>
@@ -291,6 +292,10 @@ struct psp_gpu_oracle {
     MatArena comps, bg;
     DBuf d_perm, d_assign, d_comp_off, d_bnd_off, d_cb_off, d_cb;
     uint64_t device_bytes = 0;
+    // grow-only staging for the host-pointer query API (one call at a time;
+    // the tables themselves are read-only, src/query.cpp is re-entrant too)
+    std::mutex query_mu;
+    DBuf query_stage;
 };
 
 namespace {
@@ -733,8 +738,11 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
                 throw ArgError("query: vertex id out of range");  // src/query.cpp:30
         cudaStream_t s = o->ctx->stream;
         CK(cudaSetDevice(o->ctx->device));
-        DBuf d(count * (sizeof(double) + 2 * sizeof(uint32_t)));
-        double* dd = d.as<double>();
+        psp_gpu_oracle* mo = const_cast<psp_gpu_oracle*>(o);
+        std::lock_guard<std::mutex> lock(mo->query_mu);
+        const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t));
+        if (mo->query_stage.bytes < need) mo->query_stage.alloc(need);
+        double* dd = mo->query_stage.as<double>();
         uint32_t* d1 = reinterpret_cast<uint32_t*>(dd + count);
         uint32_t* d2 = d1 + count;
         CK(cudaMemcpyAsync(d1, v1, count * 4, cudaMemcpyHostToDevice, s));
