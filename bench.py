@@ -191,13 +191,15 @@ def run_ours(args, rank, world, local):
             import torch.distributed as dist
             dist.barrier()
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # the sampler runs from the warm-up through the timed region so that
+    # even a sub-second region carries clock evidence
     with ClockSampler(local) as clk:
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for i in range(args.warmup, nsteps):
@@ -371,7 +373,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)

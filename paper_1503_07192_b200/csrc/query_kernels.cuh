@@ -4,16 +4,24 @@
 //   through[j] = min_i row1[i] + BG[g1 + i][g2 + j]     (stitch_into :49-59)
 //   d          = min_j through[j] + col2[j]             (min_plus_combine :61-65)
 //   d          = min(d, CT[c1](l1, l2)) if c1 == c2     (finish :70-72)
-// One warp per query: lanes own target boundary columns j, the source
-// boundary row values row1[i] are fetched 32 at a time and broadcast with
-// SHFL, the final min is a warp reduction (REDUX.MIN for u32).
 //
 // Undirected symmetry (dist(v,w) = dist(w,v), tests/test_query.cpp:144-153)
-// lets every query be turned around so that c1 <= c2: the B1 x B2 block
-// BG[g1.., g2..] then lies in the stored upper triangle (g1 + B1 <= g2), and
-// rows advance by a constant stride inside a tile. In u32 the result is
-// exact either way; in f32 the three-term sums may round differently, which
-// the 1e-5 tolerance covers.
+// turns every query around so that c1 <= c2: the B1 x B2 block
+// BG[g1.., g2..] then lies in the stored upper triangle (g1 + B1 <= g2 when
+// c1 < c2). In u32 the result is exact either way; in f32 the three-term sums
+// may round differently, which the 1e-5 tolerance covers.
+//
+// Two kernels:
+//  * query_grouped (dense batches): queries are counting-sorted by the
+//    component pair (c1, c2). One CTA takes up to QT queries of one pair and
+//    streams that pair's B1 x B2 boundary block through shared memory ONCE
+//    for all of them, as a register-blocked min-plus product
+//    (QT queries x B1) (x) (B1 x B2) followed by the combine with col2.
+//    HBM traffic drops from B1*B2*4 bytes per query to per (pair, 32
+//    queries); the kernel is then bound by the min-plus ALU rate.
+//  * query_warp (sparse batches, < ~4 queries per pair): one warp per query,
+//    lanes own target columns, every row segment of the block is fetched by
+//    the whole warp at once so DRAM sees full contiguous segments.
 #pragma once
 #include "minplus.cuh"
 
@@ -29,6 +37,7 @@ template <class V> struct QueryView {
     MatSet<V> comps;            // full component tables (same-component cap)
     const V* bg;                // boundary-graph tiles
     uint32_t bg_nb;
+    uint32_t k;
     double scale;               // 2^-q (u32 fixed point) or 1
 };
 
@@ -46,75 +55,360 @@ __device__ __forceinline__ float warp_min<float>(float v) {
 }
 
 template <class V>
+__device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_t c,
+                                                  uint32_t l1, uint32_t l2) {
+    return q.comps.tiles[q.comps.tile_base[c] + sym_off(l1, l2, q.comps.nb[c])];
+}
+
+// Resolve a query to (c1 <= c2, l1, l2).
+template <class V>
+__device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
+                                        uint32_t& c1, uint32_t& c2, uint32_t& l1, uint32_t& l2) {
+    uint32_t r1 = q.perm[v1], r2 = q.perm[v2];
+    c1 = q.assign[r1];
+    c2 = q.assign[r2];
+    if (c1 > c2) {
+        uint32_t t = r1; r1 = r2; r2 = t;
+        t = c1; c1 = c2; c2 = t;
+    }
+    l1 = r1 - q.comp_off[c1];
+    l2 = r2 - q.comp_off[c2];
+}
+
+// ---------------------------------------------------- sparse: warp/query --
+constexpr int WQ_SLOTS = 16;  // up to 512 target boundary columns in registers
+
+template <class V>
 __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t* __restrict__ v1,
                                                   const uint32_t* __restrict__ v2, uint64_t count,
                                                   double* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint32_t nb = q.bg_nb;
     for (uint64_t qi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; qi < count;
          qi += nwarps) {
-        uint32_t r1 = q.perm[v1[qi]], r2 = q.perm[v2[qi]];
-        uint32_t c1 = q.assign[r1], c2 = q.assign[r2];
-        if (c1 > c2) {
-            uint32_t t = r1; r1 = r2; r2 = t;
-            t = c1; c1 = c2; c2 = t;
-        }
-        const uint32_t l1 = r1 - q.comp_off[c1], l2 = r2 - q.comp_off[c2];
+        uint32_t c1, c2, l1, l2;
+        resolve(q, v1[qi], v2[qi], c1, c2, l1, l2);
         const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
         const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
         const V* row1 = q.cb + q.cb_off[c1] + uint64_t(l1) * B1;
         const V* col2 = q.cb + q.cb_off[c2] + uint64_t(l2) * B2;
-        const uint32_t nb = q.bg_nb;
         V best = Ops<V>::inf();
-        for (uint32_t j0 = 0; j0 < B2; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            const bool active = j < B2;
-            const uint32_t gj = g2 + (active ? j : B2 - 1);
-            const uint32_t Jt = gj / T, jj = gj % T;
-            V acc = Ops<V>::inf();
+        for (uint32_t j0 = 0; j0 < B2; j0 += 32 * WQ_SLOTS) {
+            const uint32_t nslot = min(uint32_t(WQ_SLOTS), (B2 - j0 + 31) / 32);
+            V acc[WQ_SLOTS];
+#pragma unroll
+            for (int s = 0; s < WQ_SLOTS; ++s) acc[s] = Ops<V>::inf();
+            uint64_t colbase[WQ_SLOTS];
+            uint32_t cur_I = 0xffffffffu;
             for (uint32_t i0 = 0; i0 < B1; i0 += 32) {
                 const uint32_t ni = min(32u, B1 - i0);
-                const V rv = (lane < ni) ? row1[i0 + lane] : Ops<V>::inf();
-                const uint32_t gi0 = g1 + i0;
-                if (c1 != c2) {
-                    // rows gi0.. cross at most one tile boundary (32 < T)
-                    const uint32_t It = gi0 / T;
-                    const uint32_t split = min(ni, T - gi0 % T);
-                    const V* pa = q.bg + tidx(It, Jt, nb) * TT + uint64_t(gi0 % T) * T + jj;
-                    const V* pb = q.bg + tidx(It + 1 < nb ? It + 1 : It, Jt, nb) * TT + jj;
-                    pb -= uint64_t(split) * T;
-                    if (ni == 32) {
+                const V rv = (uint32_t(lane) < ni) ? row1[i0 + lane] : Ops<V>::inf();
+                for (uint32_t t = 0; t < ni; ++t) {
+                    const V r = __shfl_sync(0xffffffffu, rv, t);
+                    const uint32_t gi = g1 + i0 + t;
+                    if (c1 != c2) {
+                        if ((gi >> 7) != cur_I) {  // new tile row: per-slot tile bases
+                            cur_I = gi >> 7;
 #pragma unroll
-                        for (uint32_t t = 0; t < 32; ++t) {
-                            const V* p = (t < split) ? pa : pb;
-                            acc = Ops<V>::addmin(__shfl_sync(0xffffffffu, rv, t), p[t * T], acc);
+                            for (int s = 0; s < WQ_SLOTS; ++s) {
+                                const uint32_t gj = g2 + min(j0 + s * 32 + lane, B2 - 1);
+                                colbase[s] = tidx(cur_I, gj >> 7, nb) * TT + (gj & 127);
+                            }
                         }
+                        const uint32_t roff = (gi & 127) * T;
+#pragma unroll
+                        for (int s = 0; s < WQ_SLOTS; ++s)
+                            if (s < nslot) acc[s] = Ops<V>::addmin(r, q.bg[colbase[s] + roff], acc[s]);
                     } else {
-                        for (uint32_t t = 0; t < ni; ++t) {
-                            const V* p = (t < split) ? pa : pb;
-                            acc = Ops<V>::addmin(__shfl_sync(0xffffffffu, rv, t), p[t * T], acc);
-                        }
-                    }
-                } else {
-                    // diagonal block: both triangles, symmetric lookup
-                    for (uint32_t t = 0; t < ni; ++t) {
-                        const V e = q.bg[sym_off(gi0 + t, gj, nb)];
-                        acc = Ops<V>::addmin(__shfl_sync(0xffffffffu, rv, t), e, acc);
+#pragma unroll
+                        for (int s = 0; s < WQ_SLOTS; ++s)
+                            if (s < nslot) {
+                                const uint32_t gj = g2 + min(j0 + s * 32 + lane, B2 - 1);
+                                acc[s] = Ops<V>::addmin(r, q.bg[sym_off(gi, gj, nb)], acc[s]);
+                            }
                     }
                 }
             }
-            if (active) best = Ops<V>::addmin(acc, col2[j], best);
+#pragma unroll
+            for (int s = 0; s < WQ_SLOTS; ++s) {
+                const uint32_t j = j0 + s * 32 + lane;
+                if (s < nslot && j < B2) best = Ops<V>::addmin(acc[s], col2[j], best);
+            }
         }
         best = warp_min<V>(best);
         if (lane == 0) {
-            if (c1 == c2) {
-                const V same =
-                    q.comps.tiles[q.comps.tile_base[c1] + sym_off(l1, l2, q.comps.nb[c1])];
-                best = Ops<V>::vmin(best, same);
-            }
+            if (c1 == c2) best = Ops<V>::vmin(best, same_component_entry(q, c1, l1, l2));
             out[qi] = Ops<V>::to_f64(best, q.scale);
         }
     }
+}
+
+// ------------------------------------------- dense: grouped by (c1, c2) --
+// Scheduling unit = one WARP TASK (item, column group): an item is up to 32
+// queries of one component pair (c1 <= c2); a column group is 32 consecutive
+// target boundary columns j of that pair. Lane = column. Each lane streams
+// its own column of the B1 x B2 block straight from HBM/L2 (a warp reads one
+// 128-byte row segment per load), and keeps one accumulator per query. The
+// queries' row1 values for a 32-row chunk are staged once per warp in shared
+// memory with an XOR swizzle (word (kk, q) at column q ^ (kk & 7)) that the
+// compute reads as LDS.128 broadcasts at compile-time offsets (the row loop
+// is unrolled by 8). Per row: Q/4 LDS.128 +
+// Q VIADDMNMX for Q queries (Q = m rounded up to 4, templated), no padding
+// in the query or row dimensions. Partial results of the column groups of a
+// query meet in a global atomicMin (value bits are order-preserving: all
+// distances are >= 0), a last tiny kernel applies the same-component cap.
+constexpr int GQ = 32;           // queries per item (= max Q)
+constexpr int GK = 32;           // rows per staged chunk
+constexpr int GWARPS = 4;        // warps per CTA
+constexpr int GTHREADS = 32 * GWARPS;
+
+// Per-batch workspace (device pointers), all sized by the caller.
+struct GroupWork {
+    uint32_t* key;        // [count] c1 * k + c2
+    uint32_t* l1;         // [count]
+    uint32_t* l2;         // [count]
+    uint32_t* best;       // [count] running min (value bits)
+    uint32_t* sorted;     // [count] query ids ordered by key
+    uint32_t* s_l1;       // [count] l1 in sorted order
+    uint32_t* s_l2;       // [count] l2 in sorted order
+    uint32_t* bin_cnt;    // [nbins + 1] counts, then reused as scatter cursors
+    uint32_t* bin_start;  // [nbins + 1]
+    uint32_t* task_cnt;   // [nbins + 1] warp tasks per bin
+    uint32_t* task_start; // [nbins + 1]
+    uint4* tasks;         // [max tasks] (c1, c2, first sorted query, m | cg << 8)
+    uint32_t nbins;
+};
+
+template <class V>
+__global__ void group_prep(QueryView<V> q, const uint32_t* __restrict__ v1,
+                           const uint32_t* __restrict__ v2, uint64_t count, GroupWork w) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint32_t c1, c2, l1, l2;
+    resolve(q, v1[i], v2[i], c1, c2, l1, l2);
+    const uint32_t key = c1 * q.k + c2;
+    w.key[i] = key;
+    w.l1[i] = l1;
+    w.l2[i] = l2;
+    w.best[i] = Ops<V>::to_bits(Ops<V>::inf());
+    atomicAdd(&w.bin_cnt[key], 1u);
+}
+
+__global__ void group_tasks(GroupWork w, const uint32_t* __restrict__ bnd_off, uint32_t k) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < w.nbins) {
+        const uint32_t c2 = b % k;
+        const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2];
+        w.task_cnt[b] = ((w.bin_cnt[b] + GQ - 1) / GQ) * ((B2 + 31) / 32);
+    } else if (b == w.nbins) {
+        w.task_cnt[b] = 0;
+    }
+}
+
+// one thread per bin writes the bin's complete (item, column group) task
+// records, so a warp starts a task with one 16-byte load
+__global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, uint32_t k) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= w.nbins) return;
+    const uint32_t n = w.task_cnt[b];
+    if (n == 0) return;
+    const uint32_t c1 = b / k, c2 = b % k;
+    const uint32_t ncg = (bnd_off[c2 + 1] - bnd_off[c2] + 31) / 32;
+    const uint32_t start = w.bin_start[b], end = w.bin_start[b + 1];
+    uint4* out = w.tasks + w.task_start[b];
+    for (uint32_t t = 0; t < n; ++t) {
+        const uint32_t item = t / ncg, cg = t % ncg;
+        const uint32_t q0 = start + item * GQ;
+        const uint32_t m = min(uint32_t(GQ), end - q0);
+        out[t] = make_uint4(c1, c2, q0, m | (cg << 8));
+    }
+}
+
+__global__ void group_scatter(uint64_t count, GroupWork w) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t key = w.key[i];
+    const uint32_t pos = w.bin_start[key] + atomicAdd(&w.bin_cnt[key], 1u);
+    w.sorted[pos] = static_cast<uint32_t>(i);
+    w.s_l1[pos] = w.l1[i];
+    w.s_l2[pos] = w.l2[i];
+}
+
+template <class V>
+__device__ __forceinline__ void atomic_min_bits(uint32_t* p, V v) {
+    atomicMin(p, Ops<V>::to_bits(v));  // non-negative: bit order == value order
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+    // 4-byte asynchronous global->shared copy; invalid lanes zero-fill (their
+    // values never reach a used accumulator)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One chunk for NQ4*4 queries: acc[q] <- min_kk sA[kk][q] + sB[kk][lane]
+// over kk < rows8 (rows rounded up to 8; staged rows past the block end hold
+// INF in sA, so they never win). Row kk of sA stores query q at column
+// q ^ (kk & 7): with kk = k8 + r (k8 a multiple of 8, r unrolled) every
+// shared address below is a compile-time offset from one base register and
+// the in-vector permutation t ^ (r & 3) is free, so the ALU pipe sees only
+// the add-min instructions.
+template <class V, int NQ4>
+__device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* __restrict__ sB,
+                                            V (&acc)[4 * NQ4], uint32_t rows8, int lane) {
+    for (uint32_t k8 = 0; k8 < rows8; k8 += 8) {
+        const V* a8 = sA + k8 * GQ;
+        const V* b8 = sB + k8 * 32 + lane;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const V b = b8[r * 32];
+#pragma unroll
+            for (int i = 0; i < NQ4; ++i) {
+                const uint4 u = *reinterpret_cast<const uint4*>(a8 + r * GQ + 4 * (i ^ (r >> 2)));
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    acc[4 * i + t] =
+                        Ops<V>::addmin(Ops<V>::from_bits(w4[t ^ (r & 3)]), b, acc[4 * i + t]);
+            }
+        }
+    }
+}
+
+// Per-warp shared state: two staged chunks of row1 values (A) and block
+// rows (B), and the item's query ids / local ids.
+template <class V> struct WarpStage {
+    V a[2][GK * GQ];
+    V b[2][GK * 32];
+    uint32_t id[GQ], a_off[GQ], l2[GQ];
+};
+
+template <class V, int NQ4>
+__device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWork& w,
+                                           WarpStage<V>* st, uint32_t c1, uint32_t c2,
+                                           uint32_t q0, uint32_t m, uint32_t cg) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nb = q.bg_nb;
+    const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
+    const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
+    const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
+    const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
+    const uint32_t j = cg * 32 + lane;
+    const bool col_ok = j < B2;
+    const uint32_t gj = g2 + (col_ok ? j : B2 - 1);
+    const uint32_t Jt = gj >> 7, jc = gj & (T - 1);
+    __syncwarp();
+    if (uint32_t(lane) < m) {
+        st->id[lane] = w.sorted[q0 + lane];
+        st->a_off[lane] = w.s_l1[q0 + lane] * B1;
+        st->l2[lane] = w.s_l2[q0 + lane];
+    }
+    __syncwarp();
+
+    // enqueue the chunk starting at row k0 into buffer `buf`
+    auto issue = [&](uint32_t k0, int buf) {
+        const uint32_t rows = min(uint32_t(GK), B1 - k0);
+        V* sa = st->a[buf];
+        V* sb = st->b[buf];
+        const bool row_ok = uint32_t(lane) < rows;
+#pragma unroll 4
+        for (int qq = 0; qq < 4 * NQ4; ++qq) {
+            V* dst = sa + lane * GQ + (qq ^ (lane & 7));  // 4-way bank conflict, async
+            if (row_ok && uint32_t(qq) < m) cp_async4(dst, cb1 + st->a_off[qq] + k0 + lane, true);
+            else *dst = Ops<V>::inf();  // padding rows / query slots never win
+        }
+        if (c1 != c2) {
+            const uint32_t gi0 = g1 + k0;
+            const uint32_t split = T - (gi0 & (T - 1));
+            const V* p0 = q.bg + tidx(gi0 >> 7, Jt, nb) * TT + uint64_t(gi0 & (T - 1)) * T + jc;
+            const uint32_t I1 = (gi0 >> 7) + 1;
+            const V* p1 = (I1 <= Jt) ? q.bg + tidx(I1, Jt, nb) * TT + jc - uint64_t(split) * T : p0;
+#pragma unroll 8
+            for (int kk = 0; kk < GK; ++kk) {
+                const bool ok = col_ok && uint32_t(kk) < rows;
+                const V* src = ((uint32_t(kk) < split) ? p0 : p1) + kk * T;
+                cp_async4(sb + kk * 32 + lane, ok ? src : p0, ok);
+            }
+        } else {  // diagonal block (c1 == c2, 1/k of the pairs): generic lookup
+#pragma unroll 1
+            for (int kk = 0; kk < GK; ++kk) {
+                const bool ok = col_ok && uint32_t(kk) < rows;
+                const V* src = q.bg + (ok ? sym_off(g1 + k0 + kk, gj, nb) : 0);
+                cp_async4(sb + kk * 32 + lane, src, ok);
+            }
+        }
+        cp_async_commit();
+    };
+
+    V acc[4 * NQ4];
+#pragma unroll
+    for (int i = 0; i < 4 * NQ4; ++i) acc[i] = Ops<V>::inf();
+    if (B1 > 0) issue(0, 0);
+    // col2_q[j] for every query, fetched now so the loads overlap the task
+    V c2v[4 * NQ4];
+#pragma unroll
+    for (int i = 0; i < 4 * NQ4; ++i)
+        c2v[i] = (col_ok && uint32_t(i) < m) ? cb2[uint64_t(st->l2[i]) * B2 + j] : Ops<V>::inf();
+    int buf = 0;
+    for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
+        const bool more = k0 + GK < B1;
+        if (more) issue(k0 + GK, buf ^ 1);
+        if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+        __syncwarp();
+        group_chunk<V, NQ4>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 7) & ~7u,
+                            lane);
+        __syncwarp();  // buffer `buf` is refilled two chunks later
+        buf ^= 1;
+    }
+    // combine with col2 (t_q = acc_q + col2_q[j]), then per-query minimum over
+    // the 32 columns through a padded shared transpose (conflict free)
+    V* sT = st->a[0];  // 32 x 33 words, free after the last chunk
+#pragma unroll
+    for (int i = 0; i < 4 * NQ4; ++i) {
+        sT[i * 33 + lane] = Ops<V>::addmin(acc[i], c2v[i], Ops<V>::inf());
+    }
+    __syncwarp();
+    if (uint32_t(lane) < m) {
+        V mine = Ops<V>::inf();
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) mine = Ops<V>::vmin(mine, sT[lane * 33 + c]);
+        atomic_min_bits<V>(&w.best[st->id[lane]], mine);
+    }
+}
+
+template <class V>
+__global__ void __launch_bounds__(GTHREADS) query_grouped(QueryView<V> q, GroupWork w) {
+    extern __shared__ __align__(16) unsigned char g_smem[];
+    WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
+    const uint32_t total = w.task_start[w.nbins];
+    const uint32_t nwarps = gridDim.x * GWARPS;
+    for (uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5); task < total; task += nwarps) {
+        const uint4 rec = w.tasks[task];
+        const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0xffu, cg = rec.w >> 8;
+        if (m > 16) group_task<V, 8>(q, w, st, c1, c2, q0, m, cg);
+        else if (m > 8) group_task<V, 4>(q, w, st, c1, c2, q0, m, cg);
+        else group_task<V, 2>(q, w, st, c1, c2, q0, m, cg);
+    }
+}
+
+// out[i] = min(best[i], same-component entry) as f64 (src/query.cpp:70-72).
+template <class V>
+__global__ void group_finish(QueryView<V> q, const uint32_t* __restrict__ v1,
+                             const uint32_t* __restrict__ v2, uint64_t count, GroupWork w,
+                             double* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    V d = Ops<V>::from_bits(w.best[i]);
+    const uint32_t key = w.key[i];
+    const uint32_t c1 = key / q.k, c2 = key % q.k;
+    if (c1 == c2) d = Ops<V>::vmin(d, same_component_entry(q, c1, w.l1[i], w.l2[i]));
+    out[i] = Ops<V>::to_f64(d, q.scale);
 }
 
 }  // namespace pspg

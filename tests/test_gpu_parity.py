@@ -259,3 +259,48 @@ def test_minplus_peak_probe(ctx):
     r_u32, mhz = ctx.minplus_peak(P.VALUE_U32)
     r_f32, _ = ctx.minplus_peak(P.VALUE_F32)
     assert r_u32 > 1e12 and r_f32 > 1e12 and mhz > 500
+
+
+@pytest.mark.parametrize("kernel", ["warp", "grouped"])
+def test_both_query_kernels_bitwise(monkeypatch, golden_cfg1, kernel):
+    # the dense (grouped by component pair) and sparse (warp per query)
+    # kernels must return the reference's distances bit for bit
+    monkeypatch.setenv("PSP_QUERY_KERNEL", kernel)
+    case = golden_cfg1
+    o = P.build_oracle(graph_of(case), 16, 8, 0)
+    d, ops = o.batch_query(case["q_v1"], case["q_v2"], with_ops=True)
+    assert np.array_equal(d, case["q_dist"]) and np.array_equal(ops, case["q_ops"])
+    g = P.generate_triangulated_grid(33, 33, (1.0, 9.0), 4)
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    o2 = P.build_oracle(g, 11, 4, 0)
+    v1, v2 = np.divmod(np.arange(g.n * g.n, dtype=np.int64)[::3], g.n)
+    assert np.array_equal(o2.batch_query(v1, v2), truth[v1, v2])
+    # f32 tolerance path through the same kernel
+    rng = np.random.default_rng(5)
+    gf = P.Graph(g.n, g.eu, g.ev, rng.uniform(1.0, 2.0, g.m).astype(np.float32).astype(np.float64))
+    tf = oracle.apsp_dense(gf.n, gf.eu, gf.ev, gf.ew)
+    of = P.build_oracle(gf, 11, 4, 0)
+    assert of.value_kind == P.VALUE_F32
+    df = of.batch_query(v1, v2)
+    t = tf[v1, v2]
+    assert (np.abs(df - t) <= F32_RTOL * np.maximum(t, 1e-300)).all()
+
+
+def test_large_boundaries_query_paths(monkeypatch):
+    # few components -> boundaries far above one 64-column pass / 32-row
+    # chunk / 512-column warp window; exercises every loop boundary
+    g = P.generate_grid(90, 90, (1, 1025), 6)
+    o = P.build_oracle(g, 3, 8, 0)
+    assert max(np.diff(o.boundary_offset)) > 64
+    v1, v2 = P.random_pairs(g.n, 3000, 8)
+    want = np.array([oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(s))[int(t)]
+                     for s, t in zip(v1[:200], v2[:200])])
+    dw = None
+    for kernel in ("warp", "grouped"):
+        monkeypatch.setenv("PSP_QUERY_KERNEL", kernel)
+        d = o.batch_query(v1, v2)
+        assert np.array_equal(d[:200], want)
+        if dw is None:
+            dw = d
+        else:
+            assert np.array_equal(d, dw)
