@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, GraphInvariantError, PspError,
                    PspValueError)
 
-__all__ = ["Graph", "Context", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
+__all__ = ["Graph", "Context", "nccl_unique_id", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
            "random_pairs", "VALUE_AUTO", "VALUE_U32", "VALUE_F32", "PspError", "PspValueError",
            "GraphInvariantError", "UNREACHABLE"]
@@ -78,6 +78,14 @@ class Context:
         r, mhz = C.c_double(), C.c_double()
         _lib.check(_lib.lib().psp_gpu_minplus_peak(self.h, value_kind, C.byref(r), C.byref(mhz)))
         return r.value, mhz.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for a multi-GPU Context (create on rank 0 and
+    broadcast, e.g. with torch.distributed.broadcast_object_list)."""
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.lib().psp_gpu_nccl_unique_id(buf))
+    return buf.raw
 
 
 _default_ctx: Context | None = None

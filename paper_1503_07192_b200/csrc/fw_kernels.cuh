@@ -209,6 +209,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
     const uint32_t nb = ms.nb[m];
     const uint32_t J = blockIdx.y;
     if (kb >= nb || J >= nb || J == kb) return;
+    if (ms.world > 1) {
+        // the panel tile's home row is kb (J > kb) or J (J < kb); its owner
+        // computes it, every other rank contributes INF to the min-allreduce
+        const uint32_t home_row = J > kb ? kb : J;
+        if (home_row % ms.world != ms.rank) {
+            V* panel = ms.panel + ms.panel_base[m] + uint64_t(J) * TT;
+            for (int e = threadIdx.x * 4; e < TT; e += NTHREADS * 4) {
+                const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
+                st4(panel + e, inf4);
+            }
+            return;
+        }
+    }
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* sA = reinterpret_cast<V*>(smem_raw);
     V* sB = sA + TT;
@@ -267,23 +280,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
     __shared__ uint64_t bar;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 
-    const uint64_t total = ms.work_prefix[ms.nmat];
+    const bool rowlist = ms.rows != nullptr;
+    const uint64_t total = rowlist ? ms.row_prefix[ms.nrows] : ms.work_prefix[ms.nmat];
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t w0 = uint64_t(blockIdx.x) * per;
     const uint64_t w1 = min(total, w0 + per);
     if (w0 >= w1) return;
 
-    // locate the first item: matrix by binary search, tile row by solving
-    // row_start(I) <= t < row_start(I+1).
-    uint32_t lo = 0, hi = ms.nmat;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) / 2;
-        if (ms.work_prefix[mid] <= w0) lo = mid; else hi = mid;
-    }
-    uint32_t m = lo;
-    uint32_t nb = ms.nb[m];
-    uint32_t I, J;
-    {
+    uint32_t m = 0, ri = 0;  // matrix, index into the owned-row list
+    uint32_t nb, I, J;
+    if (rowlist) {
+        // owned rows only (multi-GPU boundary graph): binary search the row
+        uint32_t lo = 0, hi = ms.nrows;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (ms.row_prefix[mid] <= w0) lo = mid; else hi = mid;
+        }
+        ri = lo;
+        nb = ms.nb[0];
+        I = ms.rows[ri];
+        J = I + static_cast<uint32_t>(w0 - ms.row_prefix[ri]);
+    } else {
+        // locate the first item: matrix by binary search, tile row by solving
+        // row_start(I) <= t < row_start(I+1).
+        uint32_t lo = 0, hi = ms.nmat;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (ms.work_prefix[mid] <= w0) lo = mid; else hi = mid;
+        }
+        m = lo;
+        nb = ms.nb[m];
         const uint32_t t = static_cast<uint32_t>(w0 - ms.work_prefix[m]);
         const double b2 = 2.0 * nb + 1.0;
         double est = floor((b2 - sqrt(b2 * b2 - 8.0 * t)) * 0.5);
@@ -320,7 +346,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
             __syncthreads();  // all reads of sA/sB done before the next copy
         }
         // advance to the next item
-        if (++J == nb) {
+        if (rowlist) {
+            if (++J == nb && ++ri < ms.nrows) {
+                I = ms.rows[ri];
+                J = I;
+            }
+        } else if (++J == nb) {
             if (++I == nb) {
                 do {
                     ++m;

@@ -84,6 +84,12 @@ template <class V> struct MatSet {
     const uint32_t* nb;         // tiles per side
     uint32_t nmat;
     uint32_t nb_max;
+    // multi-GPU boundary graph (nmat == 1): tile rows owned by this rank
+    // (owner(I) = I mod world), phase 3 walks only these rows
+    const uint32_t* rows;       // owned tile rows, ascending (nullptr: all rows)
+    const uint64_t* row_prefix; // prefix of their upper-tile counts (nrows + 1)
+    uint32_t nrows;
+    uint32_t rank, world;
 };
 
 }  // namespace pspg

@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -29,6 +30,7 @@
 #include "fw_kernels.cuh"
 #include "host_graph.hpp"
 #include "minplus.cuh"
+#include "nccl_api.hpp"
 #include "psp_gpu.h"
 #include "query_kernels.cuh"
 
@@ -129,6 +131,23 @@ struct MatArena {
     std::vector<uint64_t> tile_base, panel_base, work_prefix;
     uint64_t tile_elems = 0, panel_elems = 0;
     DBuf tiles, panel, d_tile_base, d_panel_base, d_work_prefix, d_nb;
+    // row ownership for the multi-GPU boundary graph (nmat == 1)
+    uint32_t rank = 0, world = 1, nrows = 0;
+    DBuf d_rows, d_row_prefix;
+
+    void shard_rows(uint32_t r, uint32_t g, cudaStream_t s) {
+        rank = r;
+        world = g;
+        std::vector<uint32_t> rows;
+        std::vector<uint64_t> prefix(1, 0);
+        for (uint32_t I = r; I < nb[0]; I += g) {
+            rows.push_back(I);
+            prefix.push_back(prefix.back() + (nb[0] - I));
+        }
+        nrows = static_cast<uint32_t>(rows.size());
+        d_rows = upload(rows, s);
+        d_row_prefix = upload(prefix, s);
+    }
 
     void create(const std::vector<uint64_t>& sizes, size_t value_bytes, bool with_panel,
                 cudaStream_t s) {
@@ -166,6 +185,11 @@ struct MatArena {
         v.nb = d_nb.as<uint32_t>();
         v.nmat = nmat;
         v.nb_max = nb_max;
+        v.rows = world > 1 ? d_rows.as<uint32_t>() : nullptr;
+        v.row_prefix = world > 1 ? d_row_prefix.as<uint64_t>() : nullptr;
+        v.nrows = world > 1 ? nrows : 0;
+        v.rank = rank;
+        v.world = world;
         return v;
     }
     // relaxations the FW executes on the padded matrices: per k-block the
@@ -186,6 +210,7 @@ struct psp_gpu_ctx {
     int rank = 0, world = 1;
     int sms = 148;
     cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;  // world > 1 only
 };
 
 namespace {
@@ -232,6 +257,101 @@ void run_fw(const MatArena& a, cudaStream_t s, int sms) {
             fw_phase3<V><<<g3, NTHREADS, smem, s>>>(v, kb);
             CK_LAUNCH();
         }
+    }
+}
+
+#define NCK(x)                                                                         \
+    do {                                                                               \
+        ncclResult_t r_ = (x);                                                         \
+        if (r_ != ncclSuccess)                                                         \
+            throw Fail{PSP_ENCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)}; \
+    } while (0)
+
+template <class V> ncclDataType_t nccl_type();
+template <> ncclDataType_t nccl_type<uint32_t>() { return ncclUint32; }
+template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+
+// Row-sharded blocked FW of the boundary graph over ctx->world GPUs
+// (SURVEY §8e): tile row I is owned by rank I mod world. Per k-block the
+// owner closes the diagonal tile and broadcasts it; every rank updates the
+// panel tiles whose home row it owns (others contribute INF) and one
+// min-allreduce assembles the full row panel; phase 3 then touches owned rows
+// only. At the end every row is broadcast from its owner so each GPU holds
+// the complete table (queries stay replicated, no per-query traffic).
+template <class V>
+void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    const uint32_t nb = a.nb[0];
+    set_kernel_attrs<V>();
+    a.shard_rows(ctx->rank, ctx->world, s);
+    const MatSet<V> v = a.view<V>();
+    const int smem = 2 * TT * sizeof(V);
+    const uint64_t my_work = std::max<uint64_t>(1, a.nrows ? (a.nrows * uint64_t(nb)) : 1);
+    const int g3 = int(std::min<uint64_t>(my_work, uint64_t(ctx->sms)));
+    const ncclDataType_t dt = nccl_type<V>();
+    V* tiles = a.tiles.as<V>();
+    // PSP_FW_PROFILE=1: per-phase CUDA-event breakdown on stderr (diagnostics)
+    const bool prof = std::getenv("PSP_FW_PROFILE") != nullptr;
+    const char* dm = std::getenv("PSP_DIAG_MODE");
+    const bool diag_allreduce = dm && std::strcmp(dm, "allreduce") == 0;
+    cudaEvent_t ev[5];
+    double acc_ms[4] = {0, 0, 0, 0};
+    if (prof)
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (uint32_t kb = 0; kb < nb; ++kb) {
+        const int owner = int(kb % ctx->world);
+        V* diag = tiles + tidx(kb, kb, nb) * TT;
+        if (prof) CK(cudaEventRecord(ev[0], s));
+        if (owner == ctx->rank) {
+            fw_phase1<V><<<1, NTHREADS, 0, s>>>(v, kb);
+            CK_LAUNCH();
+        }
+        if (diag_allreduce) {
+            // owners contribute the closed tile, everyone else INF
+            if (owner != ctx->rank) fill_value<V><<<16, 256, 0, s>>>(diag, TT, Ops<V>::inf());
+            NCK(nccl().AllReduce(diag, diag, TT, dt, ncclMin, ctx->comm, s));
+        } else {
+            NCK(nccl().Broadcast(diag, diag, TT, dt, owner, ctx->comm, s));
+        }
+        if (prof) CK(cudaEventRecord(ev[1], s));
+        if (nb > 1) {
+            fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+            if (prof) CK(cudaEventRecord(ev[2], s));
+            NCK(nccl().AllReduce(a.panel.p, a.panel.p, uint64_t(nb) * TT, dt, ncclMin, ctx->comm, s));
+            if (prof) CK(cudaEventRecord(ev[3], s));
+            if (a.nrows) {
+                fw_phase3<V><<<g3, NTHREADS, smem, s>>>(v, kb);
+                CK_LAUNCH();
+            }
+            if (prof) {
+                CK(cudaEventRecord(ev[4], s));
+                CK(cudaEventSynchronize(ev[4]));
+                for (int i = 0; i < 4; ++i) {
+                    float t = 0;
+                    CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+                    acc_ms[i] += t;
+                }
+            }
+        }
+    }
+    if (prof) {
+        std::fprintf(stderr,
+                     "[psp] rank %d sharded FW nb=%u: phase1+bcast %.1f ms, phase2 %.1f ms, "
+                     "allreduce %.1f ms, phase3 %.1f ms\n",
+                     ctx->rank, nb, acc_ms[0], acc_ms[1], acc_ms[2], acc_ms[3]);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
+    const uint32_t batch = 64;
+    for (uint32_t I0 = 0; I0 < nb; I0 += batch) {
+        NCK(nccl().GroupStart());
+        for (uint32_t I = I0; I < std::min(nb, I0 + batch); ++I) {
+            V* row = tiles + tidx(I, I, nb) * TT;
+            NCK(nccl().Broadcast(row, row, uint64_t(nb - I) * TT, dt, int(I % ctx->world),
+                                 ctx->comm, s));
+        }
+        NCK(nccl().GroupEnd());
     }
 }
 
@@ -435,7 +555,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         CK(cudaStreamSynchronize(s));
         init_ms += t_post.ms();
         t_k2.start(s);
-        run_fw<V>(o->bg, s, ctx->sms);
+        if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
+        else run_fw<V>(o->bg, s, ctx->sms);
         t_k2.stop(s);
         CK(cudaStreamSynchronize(s));
         k2_ms = t_k2.ms();
@@ -716,6 +837,28 @@ psp_status psp_gpu_ctx_create(int device, int rank, int world, const void* nccl_
         c->world = world;
         CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        if (world > 1) {
+            NcclApi& api = nccl();
+            if (!api.ok) throw Fail{PSP_ENCCL, api.err};
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NCK(api.CommInitRank(&c->comm, world, id, rank));
+            // NCCL connects lazily; run the collectives the sharded build
+            // uses once here (every root for the 64 KB tile broadcast, a
+            // panel-sized min-allreduce, the row broadcasts) so that one-time
+            // setup is part of context creation, not of the first build.
+            DBuf tmp(size_t(32) << 20);
+            CK(cudaMemsetAsync(tmp.p, 0, tmp.bytes, c->stream));
+            for (int root = 0; root < world; ++root)
+                NCK(api.Broadcast(tmp.p, tmp.p, TT, ncclUint32, root, c->comm, c->stream));
+            for (size_t elems : {size_t(TT), size_t(8) << 20})
+                NCK(api.AllReduce(tmp.p, tmp.p, elems, ncclUint32, ncclMin, c->comm, c->stream));
+            NCK(api.GroupStart());
+            for (int root = 0; root < world; ++root)
+                NCK(api.Broadcast(tmp.p, tmp.p, size_t(1) << 20, ncclUint32, root, c->comm, c->stream));
+            NCK(api.GroupEnd());
+            CK(cudaStreamSynchronize(c->stream));
+        }
         *out = c.release();
     });
 }
@@ -723,14 +866,20 @@ psp_status psp_gpu_ctx_create(int device, int rank, int world, const void* nccl_
 void psp_gpu_ctx_destroy(psp_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    if (ctx->comm) nccl().CommDestroy(ctx->comm);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
 
 psp_status psp_gpu_nccl_unique_id(void* out128) {
     return guarded([&] {
-        (void)out128;
-        throw Fail{PSP_ENCCL, "NCCL sharding is not built into this library version"};
+        if (!out128) throw ArgError("nccl_unique_id: NULL output");
+        NcclApi& api = nccl();
+        if (!api.ok) throw Fail{PSP_ENCCL, api.err};
+        static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+        ncclUniqueId id;
+        NCK(api.GetUniqueId(&id));
+        std::memcpy(out128, &id, sizeof(id));
     });
 }
 
