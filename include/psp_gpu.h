@@ -121,6 +121,22 @@ psp_status psp_gpu_build_partitioned(psp_gpu_ctx* ctx, uint64_t n, uint64_t m,
                                      uint32_t k, const uint32_t* assignment, int value_kind,
                                      psp_gpu_oracle** out, psp_build_stats* stats);
 
+/* Import a host oracle into device memory for queries: e.g. one read by
+ * psp::load_oracle (include/psp/oracle_io.hpp:22-34) or copied by value.
+ * permutation: original -> reordered (n); assignment: reordered vertex ->
+ * component (n); component_offset / boundary_offset (k+1);
+ * component_tables[c]: |C| x |C| f64 row-major; boundary_tables[c]:
+ * |B(C)| x b f64 (Oracle::component_tables / boundary_tables,
+ * include/psp/oracle.hpp:59-60). PSP_VALUE_AUTO stores u32 when every finite
+ * entry is exact in u32 fixed point, else f32. */
+psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
+                                 const uint32_t* permutation, const uint32_t* assignment,
+                                 const uint64_t* component_offset,
+                                 const uint64_t* boundary_offset,
+                                 const double* const* component_tables,
+                                 const double* const* boundary_tables, int value_kind,
+                                 psp_gpu_oracle** out);
+
 void psp_gpu_oracle_free(psp_gpu_oracle* o);
 psp_status psp_gpu_oracle_info(const psp_gpu_oracle* o, psp_oracle_info* out);
 

@@ -1,0 +1,247 @@
+// psp_gpu_shim.cpp — reference-side binding: the hot-path symbols of the
+// reference library `psp` (/root/reference/proj/include/psp) implemented on
+// top of the C-ABI in include/psp_gpu.h. A maintainer compiles this file into
+// libpsp INSTEAD OF the reference's definitions of exactly these functions
+// (see INTEGRATION.md for the build lines); everything else in psp (graph,
+// partitioner, I/O, cluster simulation, Dijkstra, min_plus_combine,
+// build_boundary_graph, Oracle::stored_entries/same_data) stays as it is.
+//
+//   psp::apsp_dense            include/psp/shortest_paths.hpp:43
+//   psp::build_oracle          include/psp/oracle.hpp:85-86
+//   psp::boundary_apsp         include/psp/oracle.hpp:94-96
+//   psp::query                 include/psp/query.hpp:36
+//   psp::query_parallel_inner  include/psp/query.hpp:40
+//   psp::batch_query           include/psp/query.hpp:45-46
+//
+// Error mapping (include/psp/errors.hpp conventions): PSP_EINVAL and
+// PSP_EOVERFLOW -> std::invalid_argument, PSP_EGRAPH -> psp::GraphInvariantError,
+// anything else -> std::runtime_error.
+//
+// Device-resident oracles: build_oracle returns a fully populated host
+// psp::Oracle (the reference tests and save_oracle read its tables) and keeps
+// the device tables alive in a registry keyed by the oracle's table storage;
+// query/batch_query look the device oracle up there (an Oracle copied or
+// loaded from a file is imported once with psp_gpu_oracle_import).
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "psp/errors.hpp"
+#include "psp/graph.hpp"
+#include "psp/oracle.hpp"
+#include "psp/placement.hpp"
+#include "psp/query.hpp"
+#include "psp/shortest_paths.hpp"
+#include "psp_gpu.h"
+
+namespace {
+
+void check(psp_status st) {
+    if (st == PSP_OK) return;
+    const std::string msg = psp_gpu_last_error();
+    if (st == PSP_EINVAL || st == PSP_EOVERFLOW) throw std::invalid_argument(msg);
+    if (st == PSP_EGRAPH) throw psp::GraphInvariantError(msg);
+    throw std::runtime_error(msg);
+}
+
+psp_gpu_ctx* context() {
+    static psp_gpu_ctx* ctx = [] {
+        psp_gpu_ctx* c = nullptr;
+        check(psp_gpu_ctx_create(0, 0, 1, nullptr, &c));
+        return c;
+    }();
+    return ctx;
+}
+
+struct EdgeArrays {
+    std::vector<uint32_t> u, v;
+    std::vector<double> w;
+};
+
+EdgeArrays edges_of(const psp::Graph& g) {
+    EdgeArrays e;
+    for (const psp::Edge& x : g.edge_list()) {
+        e.u.push_back(x.u);
+        e.v.push_back(x.v);
+        e.w.push_back(x.weight);
+    }
+    return e;
+}
+
+// registry: table storage of a host Oracle -> its device oracle
+struct Entry {
+    std::shared_ptr<psp_gpu_oracle> dev;
+    std::size_t n, k, b;
+};
+std::mutex g_mu;
+std::map<const void*, Entry> g_registry;
+
+const void* key_of(const psp::Oracle& o) { return o.component_tables.data(); }
+
+std::shared_ptr<psp_gpu_oracle> adopt(psp_gpu_oracle* h) {
+    return std::shared_ptr<psp_gpu_oracle>(h, psp_gpu_oracle_free);
+}
+
+std::shared_ptr<psp_gpu_oracle> device_of(const psp::Oracle& o) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_registry.find(key_of(o));
+    if (it != g_registry.end() && it->second.n == o.n && it->second.k == o.k &&
+        it->second.b == o.b())
+        return it->second.dev;
+    // an Oracle we did not build (copied, or read by load_oracle): import it
+    std::vector<uint64_t> co(o.component_offset.begin(), o.component_offset.end());
+    std::vector<uint64_t> bo(o.boundary_offset.begin(), o.boundary_offset.end());
+    std::vector<const double*> ct(o.k), bt(o.k);
+    for (uint32_t c = 0; c < o.k; ++c) {
+        ct[c] = o.component_tables[c].data().data();
+        bt[c] = o.boundary_tables[c].data().data();
+    }
+    psp_gpu_oracle* h = nullptr;
+    check(psp_gpu_oracle_import(context(), o.n, o.k, o.permutation.data(),
+                                o.partition.assignment.data(), co.data(), bo.data(), ct.data(),
+                                bt.data(), PSP_VALUE_AUTO, &h));
+    auto dev = adopt(h);
+    g_registry[key_of(o)] = Entry{dev, o.n, o.k, o.b()};
+    return dev;
+}
+
+}  // namespace
+
+namespace psp {
+
+Matrix apsp_dense(const Graph& g, std::size_t block_size) {
+    const std::size_t n = g.num_vertices();
+    if (n == 0) return Matrix();
+    if (block_size == 0) throw std::invalid_argument("apsp_dense: block size must be positive");
+    EdgeArrays e = edges_of(g);
+    Matrix m(n, n, kUnreachable);
+    check(psp_gpu_apsp_dense(context(), n, e.u.size(), e.u.data(), e.v.data(), e.w.data(),
+                             block_size, PSP_VALUE_AUTO, m.data().data()));
+    return m;
+}
+
+std::vector<Matrix> boundary_apsp(const BoundaryGraph& bg, const Partition& p, unsigned) {
+    const std::size_t b = bg.global_of.size();
+    EdgeArrays e = edges_of(bg.graph);
+    std::vector<double> all(b * b);
+    if (b) check(psp_gpu_boundary_apsp(context(), b, e.u.size(), e.u.data(), e.v.data(),
+                                       e.w.data(), PSP_VALUE_AUTO, all.data()));
+    std::vector<Matrix> tables(p.k);
+    for (uint32_t c = 0; c < p.k; ++c) {
+        const std::size_t lo = bg.component_offset[c], hi = bg.component_offset[c + 1];
+        Matrix t(hi - lo, b, kUnreachable);
+        std::memcpy(t.data().data(), all.data() + lo * b, (hi - lo) * b * sizeof(double));
+        tables[c] = std::move(t);
+    }
+    return tables;
+}
+
+Oracle build_oracle(const Graph& g, std::uint32_t k, unsigned workers, std::uint64_t seed,
+                    BuildStats* stats) {
+    if (workers < 1) throw std::invalid_argument("build_oracle: workers must be at least 1");
+    EdgeArrays e = edges_of(g);
+    psp_gpu_oracle* h = nullptr;
+    psp_build_stats st{};
+    check(psp_gpu_build_oracle(context(), g.num_vertices(), e.u.size(), e.u.data(), e.v.data(),
+                               e.w.data(), k, workers, seed, PSP_VALUE_AUTO, &h, &st));
+    auto dev = adopt(h);
+    psp_oracle_info info{};
+    check(psp_gpu_oracle_info(h, &info));
+    Oracle o;
+    o.n = info.n;
+    o.k = info.k;
+    const std::size_t n = o.n, b = info.b;
+    o.permutation.resize(n);
+    o.inverse_permutation.resize(n);
+    std::vector<uint32_t> assign(n);
+    std::vector<uint64_t> co(k + 1), bo(k + 1);
+    std::vector<uint8_t> flags(n);
+    o.boundary_vertex.resize(b);
+    check(psp_gpu_oracle_ids(h, o.permutation.data(), o.inverse_permutation.data(), assign.data(),
+                             flags.data(), co.data(), bo.data(), o.boundary_vertex.data()));
+    o.component_offset.assign(co.begin(), co.end());
+    o.boundary_offset.assign(bo.begin(), bo.end());
+    // Partition in the reordered id space, as reorder_vertices returns it
+    o.partition.k = k;
+    o.partition.assignment = assign;
+    o.partition.boundary_flags = flags;
+    o.partition.component_members.assign(k, {});
+    for (VertexId v = 0; v < n; ++v) o.partition.component_members[assign[v]].push_back(v);
+    o.partition.permutation.resize(n);
+    o.partition.inverse_permutation.resize(n);
+    for (VertexId v = 0; v < n; ++v) o.partition.permutation[v] = o.partition.inverse_permutation[v] = v;
+    o.component_tables.resize(k);
+    o.boundary_tables.resize(k);
+    for (uint32_t c = 0; c < k; ++c) {
+        const std::size_t s = co[c + 1] - co[c], bc = bo[c + 1] - bo[c];
+        o.component_tables[c] = Matrix(s, s, kUnreachable);
+        if (s) check(psp_gpu_export_component(h, c, o.component_tables[c].data().data()));
+        o.boundary_tables[c] = Matrix(bc, b, kUnreachable);
+        if (bc && b) check(psp_gpu_export_boundary_rows(h, c, o.boundary_tables[c].data().data()));
+    }
+    o.placement = place_components(k, 1);
+    if (stats) {
+        stats->partition_ms = st.partition_ms;
+        stats->component_apsp_ms = st.component_apsp_ms;
+        stats->boundary_ms = st.boundary_ms;
+        stats->boundary_total = st.boundary_total;
+        stats->bg_edges = st.bg_edges;
+        stats->stored_entries = st.stored_entries;
+        stats->peak_table_entries_per_worker = st.peak_table_entries_per_worker;
+    }
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_registry[key_of(o)] = Entry{dev, o.n, o.k, o.b()};
+    return o;
+}
+
+namespace {
+
+QueryResult result_for(const Oracle& o, VertexId v1, VertexId v2, double d) {
+    // QueryStats exactly as src/query.cpp:67-81 derives them from the frame
+    QueryResult r;
+    r.distance = d;
+    const uint32_t c1 = o.partition.assignment[o.permutation[v1]];
+    const uint32_t c2 = o.partition.assignment[o.permutation[v2]];
+    r.stats.boundary_size_1 = o.boundary_size(c1);
+    r.stats.boundary_size_2 = o.boundary_size(c2);
+    r.stats.minplus_ops = r.stats.boundary_size_1 * r.stats.boundary_size_2 + r.stats.boundary_size_2;
+    r.stats.same_component = c1 == c2;
+    if (o.placement.owner[c1] != o.placement.owner[c2]) r.stats.transfer_entries = r.stats.boundary_size_2;
+    return r;
+}
+
+}  // namespace
+
+std::vector<QueryResult> batch_query(const Oracle& o,
+                                     std::span<const std::pair<VertexId, VertexId>> pairs,
+                                     unsigned) {
+    std::vector<uint32_t> v1(pairs.size()), v2(pairs.size());
+    for (std::size_t i = 0; i < pairs.size(); ++i) {
+        if (pairs[i].first >= o.n || pairs[i].second >= o.n)
+            throw std::invalid_argument("query: vertex id out of range");
+        v1[i] = pairs[i].first;
+        v2[i] = pairs[i].second;
+    }
+    std::vector<double> d(pairs.size());
+    if (!pairs.empty())
+        check(psp_gpu_query_batch(device_of(o).get(), pairs.size(), v1.data(), v2.data(), d.data(),
+                                  nullptr));
+    std::vector<QueryResult> out(pairs.size());
+    for (std::size_t i = 0; i < pairs.size(); ++i) out[i] = result_for(o, v1[i], v2[i], d[i]);
+    return out;
+}
+
+QueryResult query(const Oracle& o, VertexId v1, VertexId v2) {
+    const std::pair<VertexId, VertexId> p{v1, v2};
+    return batch_query(o, std::span<const std::pair<VertexId, VertexId>>(&p, 1), 1)[0];
+}
+
+QueryResult query_parallel_inner(const Oracle& o, VertexId v1, VertexId v2, unsigned) {
+    return query(o, v1, v2);  // one device query is already parallel
+}
+
+}  // namespace psp

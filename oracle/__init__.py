@@ -26,6 +26,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libpspref.so")
 ORACLE_SO = os.path.join(HERE, "_build", "libpsporacle.so")
+SHIM_DIR = os.path.join(HERE, "_ref", "shim")
+SHIM_TESTS = ("test_shortest_paths", "test_oracle", "test_query", "test_cluster")
 REF_SRC = "/root/reference/proj"
 
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
@@ -38,10 +40,10 @@ def build(force: bool = False) -> None:
     """Compile the checkers (the reference part only where its sources exist)."""
     targets = ["oracle"]
     if os.path.isdir(REF_SRC):
-        targets.append("ref")
-    elif not os.path.exists(REF_SO):
-        targets = ["oracle"]
-    args = ["make", "-s", "-C", HERE] + (["-B"] if force else []) + targets
+        # the reference build and its own unit tests against the reference
+        # and against the GPU shim (needs the product library built first)
+        targets += ["ref", "shimtests"]
+    args = ["make", "-s", "-j", "8", "-C", HERE] + (["-B"] if force else []) + targets
     subprocess.run(args, check=True)
 
 

@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, GraphInvariantError, PspError,
                    PspValueError)
 
-__all__ = ["Graph", "Context", "nccl_unique_id", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
+__all__ = ["Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
            "random_pairs", "VALUE_AUTO", "VALUE_U32", "VALUE_F32", "PspError", "PspValueError",
            "GraphInvariantError", "UNREACHABLE"]
@@ -207,6 +207,28 @@ def build_partitioned(g: Graph, k: int, assignment, value_kind: int = VALUE_AUTO
     _lib.check(_lib.lib().psp_gpu_build_partitioned(ctx.h, g.n, g.m, g.eu, g.ev, g.ew, k, a,
                                                     value_kind, C.byref(h), C.byref(st)))
     return GpuOracle(ctx, h, st)
+
+
+def import_oracle(n: int, k: int, permutation, assignment_reordered, component_offset,
+                  boundary_offset, component_tables, boundary_tables,
+                  value_kind: int = VALUE_AUTO, ctx: Context | None = None) -> GpuOracle:
+    """Device oracle from host tables (e.g. a psp::Oracle read by load_oracle,
+    include/psp/oracle_io.hpp:22-34): psp_gpu_oracle_import."""
+    ctx = ctx or default_context()
+    perm = np.ascontiguousarray(permutation, np.uint32)
+    asg = np.ascontiguousarray(assignment_reordered, np.uint32)
+    co = np.ascontiguousarray(component_offset, np.uint64)
+    bo = np.ascontiguousarray(boundary_offset, np.uint64)
+    cts = [np.ascontiguousarray(t, np.float64) for t in component_tables]
+    bts = [np.ascontiguousarray(t, np.float64) for t in boundary_tables]
+    if len(cts) != k or len(bts) != k:
+        raise ValueError("one component table and one boundary table per component")
+    cp = (C.c_void_p * k)(*[t.ctypes.data for t in cts])
+    bp = (C.c_void_p * k)(*[t.ctypes.data for t in bts])
+    h = C.c_void_p()
+    _lib.check(_lib.lib().psp_gpu_oracle_import(ctx.h, n, k, perm, asg, co, bo, cp, bp,
+                                                value_kind, C.byref(h)))
+    return GpuOracle(ctx, h, BuildStats())
 
 
 def apsp_dense(g: Graph, block_size: int = 64, value_kind: int = VALUE_AUTO,

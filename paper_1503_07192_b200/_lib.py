@@ -91,6 +91,8 @@ SIGNATURES = {
     "psp_gpu_build_partitioned": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
                                             C.c_uint32, _u32p, C.c_int, C.POINTER(_vp),
                                             C.POINTER(BuildStats)]),
+    "psp_gpu_oracle_import": (C.c_int, [_vp, C.c_uint64, C.c_uint32, _u32p, _u32p, _u64p, _u64p,
+                                        _vp, _vp, C.c_int, C.POINTER(_vp)]),
     "psp_gpu_oracle_free": (None, [_vp]),
     "psp_gpu_oracle_info": (C.c_int, [_vp, C.POINTER(OracleInfo)]),
     "psp_gpu_oracle_ids": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

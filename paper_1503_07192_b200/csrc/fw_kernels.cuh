@@ -440,6 +440,20 @@ __global__ void extract_to_boundary(MatSet<V> comps, const uint32_t* __restrict_
     }
 }
 
+// Dense import of a row window of matrix m (rows row0.., columns 0..ncols):
+// writes element (i, j) iff its tile is in the stored upper triangle.
+template <class V>
+__global__ void pack_window(MatSet<V> ms, uint32_t m, uint32_t row0, uint32_t nrows,
+                            uint32_t ncols, const V* __restrict__ dense) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= uint64_t(nrows) * ncols) return;
+    const uint32_t i = row0 + static_cast<uint32_t>(idx / ncols);
+    const uint32_t j = static_cast<uint32_t>(idx % ncols);
+    if (i / T <= j / T)
+        ms.tiles[ms.tile_base[m] + tidx(i / T, j / T, ms.nb[m]) * TT + uint64_t(i % T) * T + j % T] =
+            dense[idx];
+}
+
 // Dense export of a row/column window of matrix m: out[r][c] = D[row0+r][col0+c].
 template <class V>
 __global__ void unpack_window(MatSet<V> ms, uint32_t m, uint32_t row0, uint32_t nrows,

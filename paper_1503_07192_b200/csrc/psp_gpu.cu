@@ -506,6 +506,27 @@ struct EventTimer {
     }
 };
 
+// Query-side tables and id maps on the device (shared by build and import).
+template <class V>
+void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
+    const Reordered& R = o->R;
+    const uint32_t k = R.k;
+    std::vector<uint64_t> cb_off(k + 1, 0);
+    for (uint32_t c = 0; c < k; ++c)
+        cb_off[c + 1] = cb_off[c] + uint64_t(R.comp_off[c + 1] - R.comp_off[c]) *
+                                        (R.bnd_off[c + 1] - R.bnd_off[c]);
+    o->d_cb.alloc(cb_off[k] * sizeof(V));
+    o->d_cb_off = upload(cb_off, s);
+    o->d_comp_off = upload(R.comp_off, s);
+    o->d_bnd_off = std::move(d_bnd);
+    o->d_perm = upload(R.perm, s);
+    o->d_assign = upload(R.assign, s);
+    extract_to_boundary<V><<<std::max(k, 1u), 256, 0, s>>>(
+        o->comps.view<V>(), o->d_comp_off.as<uint32_t>(), o->d_bnd_off.as<uint32_t>(),
+        o->d_cb_off.as<uint64_t>(), o->d_cb.as<V>());
+    CK_LAUNCH();
+}
+
 template <class V>
 void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     psp_gpu_ctx* ctx = o->ctx;
@@ -562,20 +583,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         k2_ms = t_k2.ms();
     }
     // query-side tables
-    std::vector<uint64_t> cb_off(k + 1, 0);
-    for (uint32_t c = 0; c < k; ++c)
-        cb_off[c + 1] = cb_off[c] + sizes[c] * (R.bnd_off[c + 1] - R.bnd_off[c]);
     t_post.start(s);
-    o->d_cb.alloc(cb_off[k] * sizeof(V));
-    o->d_cb_off = upload(cb_off, s);
-    o->d_comp_off = upload(R.comp_off, s);
-    o->d_bnd_off = std::move(d_bnd);
-    o->d_perm = upload(R.perm, s);
-    o->d_assign = upload(R.assign, s);
-    extract_to_boundary<V><<<k, 256, 0, s>>>(o->comps.view<V>(), o->d_comp_off.as<uint32_t>(),
-                                             o->d_bnd_off.as<uint32_t>(),
-                                             o->d_cb_off.as<uint64_t>(), o->d_cb.as<V>());
-    CK_LAUNCH();
+    finish_query_tables<V>(o, std::move(d_bnd), s);
     t_post.stop(s);
     CK(cudaStreamSynchronize(s));
     init_ms += t_post.ms();
@@ -605,6 +614,76 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         st->fixed_point_shift = o->kind.shift;
         st->device_bytes = o->device_bytes;
     }
+}
+
+// Kind for imported tables: u32 when every finite entry is exact in fixed
+// point 2^q (q <= 24) below INF, else f32.
+Kind choose_kind_tables(int requested, const std::vector<const double*>& ptr,
+                        const std::vector<uint64_t>& len) {
+    if (requested == PSP_VALUE_F32) return {PSP_VALUE_F32, 0};
+    double maxv = 0.0;
+    for (size_t t = 0; t < ptr.size(); ++t)
+        for (uint64_t i = 0; i < len[t]; ++i)
+            if (std::isfinite(ptr[t][i])) maxv = std::max(maxv, ptr[t][i]);
+    for (int q = 0; q <= 24; ++q) {
+        const double scale = std::ldexp(1.0, q);
+        if (2.0 * maxv * scale >= double(U32_INF)) break;
+        bool ok = true;
+        for (size_t t = 0; t < ptr.size() && ok; ++t)
+            for (uint64_t i = 0; i < len[t] && ok; ++i) {
+                const double x = ptr[t][i];
+                if (std::isinf(x)) continue;
+                if (!(x >= 0) || std::floor(x * scale) != x * scale) ok = false;
+            }
+        if (ok) return {PSP_VALUE_U32, q};
+    }
+    if (requested == PSP_VALUE_U32)
+        throw Fail{PSP_EOVERFLOW, "import: tables are not exact in u32 fixed point"};
+    return {PSP_VALUE_F32, 0};
+}
+
+template <class V>
+void import_tables(psp_gpu_oracle* o, const double* const* ct, const double* const* bt) {
+    cudaStream_t s = o->ctx->stream;
+    const Reordered& R = o->R;
+    const uint32_t k = R.k;
+    const uint64_t b = R.b();
+    std::vector<uint64_t> sizes(k);
+    for (uint32_t c = 0; c < k; ++c) sizes[c] = R.comp_off[c + 1] - R.comp_off[c];
+    o->comps.create(sizes, sizeof(V), false, s);
+    fill_arena<V>(o->comps, s, o->ctx->sms);
+    auto to_v = [&](const double* src, uint64_t cnt) {
+        std::vector<V> h(cnt);
+        for (uint64_t i = 0; i < cnt; ++i)
+            h[i] = std::isinf(src[i]) ? Ops<V>::inf() : to_value<V>(src[i], o->kind.shift);
+        return h;
+    };
+    for (uint32_t c = 0; c < k; ++c) {
+        const uint64_t cnt = sizes[c] * sizes[c];
+        if (!cnt) continue;
+        DBuf d = upload(to_v(ct[c], cnt), s);
+        pack_window<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(o->comps.view<V>(), c, 0,
+                                                                   uint32_t(sizes[c]),
+                                                                   uint32_t(sizes[c]), d.as<V>());
+        CK_LAUNCH();
+        CK(cudaStreamSynchronize(s));
+    }
+    if (b > 0) {
+        o->bg.create({b}, sizeof(V), false, s);
+        fill_arena<V>(o->bg, s, o->ctx->sms);
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint64_t rows = R.bnd_off[c + 1] - R.bnd_off[c], cnt = rows * b;
+            if (!cnt) continue;
+            DBuf d = upload(to_v(bt[c], cnt), s);
+            pack_window<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(
+                o->bg.view<V>(), 0, R.bnd_off[c], uint32_t(rows), uint32_t(b), d.as<V>());
+            CK_LAUNCH();
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    finish_query_tables<V>(o, upload(R.bnd_off, s), s);
+    CK(cudaStreamSynchronize(s));
+    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes;
 }
 
 void set_peak_entries(const Reordered& R, unsigned workers, psp_build_stats* st) {
@@ -914,6 +993,68 @@ psp_status psp_gpu_build_partitioned(psp_gpu_ctx* ctx, uint64_t n, uint64_t m,
         psp_gpu_oracle* o = build_from_csr(ctx, g, k, a, ew, m, value_kind, 0.0, stats);
         set_peak_entries(o->R, 1, stats);
         *out = o;
+    });
+}
+
+psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
+                                 const uint32_t* permutation, const uint32_t* assignment,
+                                 const uint64_t* component_offset,
+                                 const uint64_t* boundary_offset,
+                                 const double* const* component_tables,
+                                 const double* const* boundary_tables, int value_kind,
+                                 psp_gpu_oracle** out) {
+    return guarded([&] {
+        if (!ctx || !out || (n && (!permutation || !assignment)) || !component_offset ||
+            !boundary_offset || (k && (!component_tables || !boundary_tables)))
+            throw ArgError("oracle_import: NULL argument");
+        if (k < 1 || k > n) throw ArgError("oracle_import: k must be in 1..n");
+        auto o = std::make_unique<psp_gpu_oracle>();
+        o->ctx = ctx;
+        Reordered& R = o->R;
+        R.n = n;
+        R.k = k;
+        R.perm.assign(permutation, permutation + n);
+        R.inv.assign(n, 0);
+        std::vector<uint8_t> seen(n, 0);
+        for (uint64_t v = 0; v < n; ++v) {
+            if (R.perm[v] >= n || seen[R.perm[v]]++) throw ArgError("oracle_import: bad permutation");
+            R.inv[R.perm[v]] = static_cast<uint32_t>(v);
+        }
+        R.assign.assign(assignment, assignment + n);
+        R.comp_off.resize(k + 1);
+        R.bnd_off.resize(k + 1);
+        for (uint32_t c = 0; c <= k; ++c) {
+            R.comp_off[c] = static_cast<uint32_t>(component_offset[c]);
+            R.bnd_off[c] = static_cast<uint32_t>(boundary_offset[c]);
+        }
+        if (R.comp_off[0] != 0 || R.comp_off[k] != n || R.bnd_off[0] != 0)
+            throw ArgError("oracle_import: offsets do not cover the graph");
+        R.flags.assign(n, 0);
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint32_t s = R.comp_off[c + 1] - R.comp_off[c];
+            const uint32_t bc = R.bnd_off[c + 1] - R.bnd_off[c];
+            if (R.comp_off[c + 1] < R.comp_off[c] || R.bnd_off[c + 1] < R.bnd_off[c] || bc > s)
+                throw ArgError("oracle_import: inconsistent offsets");
+            for (uint32_t i = 0; i < s; ++i) {
+                if (R.assign[R.comp_off[c] + i] != c) throw ArgError("oracle_import: assignment/offset mismatch");
+                R.flags[R.comp_off[c] + i] = i < bc;  // boundary-first local ids
+            }
+        }
+        std::vector<const double*> ptr;
+        std::vector<uint64_t> len;
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint64_t s = R.comp_off[c + 1] - R.comp_off[c];
+            ptr.push_back(component_tables[c]);
+            len.push_back(s * s);
+            ptr.push_back(boundary_tables[c]);
+            len.push_back(uint64_t(R.bnd_off[c + 1] - R.bnd_off[c]) * R.b());
+        }
+        o->kind = choose_kind_tables(value_kind, ptr, len);
+        o->scale = std::ldexp(1.0, -o->kind.shift);
+        CK(cudaSetDevice(ctx->device));
+        if (o->kind.kind == PSP_VALUE_U32) import_tables<uint32_t>(o.get(), component_tables, boundary_tables);
+        else import_tables<float>(o.get(), component_tables, boundary_tables);
+        *out = o.release();
     });
 }
 

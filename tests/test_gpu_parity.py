@@ -321,3 +321,22 @@ def test_multigpu_sharded_build():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("bit-exact") == min(n, 4)
+
+
+@pytest.mark.parametrize("name", ["grid2x3_k2", "cycle8_k2_s4", "grid16_k8_lattice", "tri20_k20_w0",
+                                  "isolated2_k2", "two_squares_k2"])
+def test_import_oracle_from_reference_tables(golden_small, name):
+    # psp_gpu_oracle_import: device oracle from host (reference-built) tables
+    case = golden_small[name]
+    n, k = int(case["n"]), int(case["k"])
+    perm = case["permutation"]
+    assign_r = np.empty(n, np.uint32)
+    assign_r[perm] = case["assignment"]
+    o = P.import_oracle(n, k, perm, assign_r, case["component_offset"], case["boundary_offset"],
+                        [case[f"ct{c}"] for c in range(k)], [case[f"bt{c}"] for c in range(k)])
+    assert o.value_kind == P.VALUE_U32
+    for c in range(k):
+        assert np.array_equal(o.component_table(c), case[f"ct{c}"])
+        assert np.array_equal(o.boundary_rows(c), case[f"bt{c}"])
+    d, ops = o.batch_query(case["q_v1"], case["q_v2"], with_ops=True)
+    assert np.array_equal(d, case["q_dist"]) and np.array_equal(ops, case["q_ops"])
