@@ -165,7 +165,8 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
 
 /* Device-resident variant: v1, v2, dist are DEVICE pointers on the oracle's
  * GPU; enqueued on `stream` (a cudaStream_t, NULL = the context stream) and
- * returns without synchronising. Ids are not range-checked here. */
+ * returns without synchronising. Out-of-range ids are answered as (0, 0)
+ * and not reported (the host variant reports them). */
 psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       const uint32_t* v1, const uint32_t* v2, double* dist,
                                       void* stream);

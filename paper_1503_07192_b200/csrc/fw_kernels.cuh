@@ -268,16 +268,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
 // Persistent: gridDim.x CTAs split the flat list of (matrix, upper tile)
 // items into contiguous ranges, so consecutive items share the tile row I
 // and the A operand (panel slot I) is reloaded only when I changes.
+// Software pipeline per CTA: the B operand is double-buffered in shared
+// memory and the next item's panel slot is fetched by 1-D TMA while the
+// current item computes; the C tile is loaded into registers alongside the
+// min-plus product and folded in at the end (min is associative), so the
+// ALU pipe no longer waits for either transfer. Shared memory: A 64 KB +
+// 2 x B 64 KB.
 __device__ __forceinline__ uint32_t row_start(uint32_t I, uint32_t nb) {
     return I * nb - (I * (I - 1u)) / 2u;  // first flat index of tile row I
+}
+
+struct P3Cursor {
+    uint64_t w;
+    uint32_t m, ri, nb, I, J;
+};
+
+template <class V>
+__device__ __forceinline__ void p3_advance(const MatSet<V>& ms, P3Cursor& c) {
+    ++c.w;
+    if (ms.rows != nullptr) {
+        if (++c.J == c.nb && ++c.ri < ms.nrows) {
+            c.I = ms.rows[c.ri];
+            c.J = c.I;
+        }
+    } else if (++c.J == c.nb) {
+        if (++c.I == c.nb) {
+            do {
+                ++c.m;
+            } while (c.m < ms.nmat && ms.nb[c.m] == 0);  // empty components own no tiles
+            if (c.m < ms.nmat) c.nb = ms.nb[c.m];
+            c.I = 0;
+        }
+        c.J = c.I;
+    }
+}
+
+template <class V>
+__device__ __forceinline__ bool p3_valid(const P3Cursor& c, uint64_t w1, uint32_t kb) {
+    return c.w < w1 && kb < c.nb && c.I != kb && c.J != kb;
 }
 
 template <class V>
 __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t kb) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* sA = reinterpret_cast<V*>(smem_raw);
-    V* sB = sA + TT;
-    __shared__ uint64_t bar;
+    V* sB0 = sA + TT;  // two B buffers: sB0, sB0 + TT
+    __shared__ uint64_t bars[2];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 
     const bool rowlist = ms.rows != nullptr;
@@ -287,8 +323,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
     const uint64_t w1 = min(total, w0 + per);
     if (w0 >= w1) return;
 
-    uint32_t m = 0, ri = 0;  // matrix, index into the owned-row list
-    uint32_t nb, I, J;
+    P3Cursor cur;
+    cur.w = w0;
+    cur.m = 0;
+    cur.ri = 0;
     if (rowlist) {
         // owned rows only (multi-GPU boundary graph): binary search the row
         uint32_t lo = 0, hi = ms.nrows;
@@ -296,10 +334,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
             const uint32_t mid = (lo + hi) / 2;
             if (ms.row_prefix[mid] <= w0) lo = mid; else hi = mid;
         }
-        ri = lo;
-        nb = ms.nb[0];
-        I = ms.rows[ri];
-        J = I + static_cast<uint32_t>(w0 - ms.row_prefix[ri]);
+        cur.ri = lo;
+        cur.nb = ms.nb[0];
+        cur.I = ms.rows[lo];
+        cur.J = cur.I + static_cast<uint32_t>(w0 - ms.row_prefix[lo]);
     } else {
         // locate the first item: matrix by binary search, tile row by solving
         // row_start(I) <= t < row_start(I+1).
@@ -308,59 +346,82 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
             const uint32_t mid = (lo + hi) / 2;
             if (ms.work_prefix[mid] <= w0) lo = mid; else hi = mid;
         }
-        m = lo;
-        nb = ms.nb[m];
-        const uint32_t t = static_cast<uint32_t>(w0 - ms.work_prefix[m]);
+        cur.m = lo;
+        cur.nb = ms.nb[lo];
+        const uint32_t nb = cur.nb;
+        const uint32_t t = static_cast<uint32_t>(w0 - ms.work_prefix[lo]);
         const double b2 = 2.0 * nb + 1.0;
         double est = floor((b2 - sqrt(b2 * b2 - 8.0 * t)) * 0.5);
-        I = est < 0 ? 0u : static_cast<uint32_t>(est);
+        uint32_t I = est < 0 ? 0u : static_cast<uint32_t>(est);
         if (I >= nb) I = nb - 1;
         while (I > 0 && row_start(I, nb) > t) --I;
         while (I + 1 < nb && row_start(I + 1, nb) <= t) ++I;
-        J = I + (t - row_start(I, nb));
+        cur.I = I;
+        cur.J = I + (t - row_start(I, nb));
     }
-    if (tid == 0) mbar_init(&bar, 1);
+    while (cur.w < w1 && !p3_valid<V>(cur, w1, kb)) p3_advance(ms, cur);
+    if (cur.w >= w1) return;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+    }
     __syncthreads();
 
-    uint32_t parity = 0;
-    uint64_t a_key = ~0ull;
-    for (uint64_t w = w0; w < w1; ++w) {
-        if (kb < nb && I != kb && J != kb) {
-            const V* P = ms.panel + ms.panel_base[m];
-            V* C = ms.tiles + ms.tile_base[m] + tidx(I, J, nb) * TT;
-            const uint64_t key = (uint64_t(m) << 32) | I;
-            const bool needA = key != a_key;
-            a_key = key;
-            if (tid == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(&bar, (needA ? 2u : 1u) * TT * sizeof(V));
-                if (needA) bulk_g2s(sA, P + uint64_t(I) * TT, TT * sizeof(V), &bar);
-                bulk_g2s(sB, P + uint64_t(J) * TT, TT * sizeof(V), &bar);
-            }
-            V acc[8][8];
-            load_block(C, acc, ty, tx);
-            mbar_wait(&bar, parity);
-            parity ^= 1;
-            minplus_tile<V, true>(sA, sB, acc, ty, tx);
-            store_block(C, acc, ty, tx);
-            __syncthreads();  // all reads of sA/sB done before the next copy
+    auto panel_of = [&](const P3Cursor& c) { return ms.panel + ms.panel_base[c.m]; };
+    uint32_t parity[2] = {0, 0};
+    int buf = 0;
+    uint64_t a_key = (uint64_t(cur.m) << 32) | cur.I;
+    if (tid == 0) {
+        const V* P = panel_of(cur);
+        mbar_expect_tx(&bars[0], 2u * TT * sizeof(V));
+        bulk_g2s(sA, P + uint64_t(cur.I) * TT, TT * sizeof(V), &bars[0]);
+        bulk_g2s(sB0, P + uint64_t(cur.J) * TT, TT * sizeof(V), &bars[0]);
+    }
+    while (cur.w < w1) {
+        P3Cursor nxt = cur;
+        do {
+            p3_advance(ms, nxt);
+        } while (nxt.w < w1 && !p3_valid<V>(nxt, w1, kb));
+        const bool has_next = nxt.w < w1;
+        const uint64_t next_key = (uint64_t(nxt.m) << 32) | nxt.I;
+        const bool next_needs_a = has_next && next_key != a_key;
+        V* sBcur = sB0 + buf * TT;
+        V* sBnxt = sB0 + (buf ^ 1) * TT;
+        // same tile row next: its B slot can stream in during this compute
+        // (sBnxt was last read by the previous item, before its barrier)
+        if (has_next && !next_needs_a && tid == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[buf ^ 1], TT * sizeof(V));
+            bulk_g2s(sBnxt, panel_of(nxt) + uint64_t(nxt.J) * TT, TT * sizeof(V), &bars[buf ^ 1]);
         }
-        // advance to the next item
-        if (rowlist) {
-            if (++J == nb && ++ri < ms.nrows) {
-                I = ms.rows[ri];
-                J = I;
-            }
-        } else if (++J == nb) {
-            if (++I == nb) {
-                do {
-                    ++m;
-                } while (m < ms.nmat && ms.nb[m] == 0);  // empty components own no tiles
-                if (m < ms.nmat) nb = ms.nb[m];
-                I = 0;
-            }
-            J = I;
+        V* C = ms.tiles + ms.tile_base[cur.m] + tidx(cur.I, cur.J, cur.nb) * TT;
+        V cr[8][8];
+        load_block(C, cr, ty, tx);  // in flight during the product
+        V acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::inf();
+        mbar_wait(&bars[buf], parity[buf]);
+        parity[buf] ^= 1;
+        minplus_tile<V, true>(sA, sBcur, acc, ty, tx);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::vmin(acc[i][j], cr[i][j]);
+        store_block(C, acc, ty, tx);
+        __syncthreads();  // all reads of sA / sBcur done
+        if (next_needs_a && tid == 0) {
+            const V* P = panel_of(nxt);
+            fence_proxy_async();
+            mbar_expect_tx(&bars[buf ^ 1], 2u * TT * sizeof(V));
+            bulk_g2s(sA, P + uint64_t(nxt.I) * TT, TT * sizeof(V), &bars[buf ^ 1]);
+            bulk_g2s(sBnxt, P + uint64_t(nxt.J) * TT, TT * sizeof(V), &bars[buf ^ 1]);
         }
+        if (next_needs_a) a_key = next_key;
+        cur = nxt;
+        buf ^= 1;
     }
 }
 

@@ -216,6 +216,7 @@ struct psp_gpu_ctx {
 namespace {
 
 int g_attr_done[2] = {0, 0};
+template <class V> constexpr int P3_SMEM = 3 * TT * sizeof(V);  // A + 2 x B
 
 template <class V>
 void set_kernel_attrs() {
@@ -223,7 +224,7 @@ void set_kernel_attrs() {
     if (g_attr_done[idx]) return;
     const int smem = 2 * TT * sizeof(V);
     CK(cudaFuncSetAttribute(fw_phase2<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(fw_phase3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(fw_phase3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_SMEM<V>));
     g_attr_done[idx] = 1;
 }
 
@@ -254,7 +255,7 @@ void run_fw(const MatArena& a, cudaStream_t s, int sms) {
         if (a.nb_max > 1) {
             fw_phase2<V><<<dim3(a.nmat, a.nb_max), NTHREADS, smem, s>>>(v, kb);
             CK_LAUNCH();
-            fw_phase3<V><<<g3, NTHREADS, smem, s>>>(v, kb);
+            fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
             CK_LAUNCH();
         }
     }
@@ -321,7 +322,7 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
             NCK(nccl().AllReduce(a.panel.p, a.panel.p, uint64_t(nb) * TT, dt, ncclMin, ctx->comm, s));
             if (prof) CK(cudaEventRecord(ev[3], s));
             if (a.nrows) {
-                fw_phase3<V><<<g3, NTHREADS, smem, s>>>(v, kb);
+                fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
                 CK_LAUNCH();
             }
             if (prof) {
@@ -852,9 +853,11 @@ constexpr double GROUP_MIN_DENSITY = 2.0;
 
 template <class V>
 void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
-                    const uint32_t* v2, double* dist, cudaStream_t s) {
+                    const uint32_t* v2, double* dist, cudaStream_t s, uint32_t* bad_id) {
     if (count == 0) return;
     QueryView<V> q;
+    q.n = static_cast<uint32_t>(o->R.n);
+    q.bad_id = bad_id;
     q.perm = o->d_perm.as<uint32_t>();
     q.assign = o->d_assign.as<uint32_t>();
     q.comp_off = o->d_comp_off.as<uint32_t>();
@@ -1128,22 +1131,27 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
         if (count == 0) return;
         if (!v1 || !v2 || !dist) throw ArgError("query_batch: NULL array");
         const Reordered& R = o->R;
-        for (uint64_t i = 0; i < count; ++i)
-            if (v1[i] >= R.n || v2[i] >= R.n)
-                throw ArgError("query: vertex id out of range");  // src/query.cpp:30
         cudaStream_t s = o->ctx->stream;
         CK(cudaSetDevice(o->ctx->device));
         psp_gpu_oracle* mo = const_cast<psp_gpu_oracle*>(o);
         std::lock_guard<std::mutex> lock(mo->query_mu);
-        const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t));
+        // ids are range-checked on the device (src/query.cpp:30 semantics:
+        // any bad id -> PSP_EINVAL and no output)
+        const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t)) + 16;
         if (mo->query_stage.bytes < need) mo->query_stage.alloc(need);
         double* dd = mo->query_stage.as<double>();
         uint32_t* d1 = reinterpret_cast<uint32_t*>(dd + count);
         uint32_t* d2 = d1 + count;
+        uint32_t* dbad = d2 + count;
+        CK(cudaMemsetAsync(dbad, 0, sizeof(uint32_t), s));
         CK(cudaMemcpyAsync(d1, v1, count * 4, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d2, v2, count * 4, cudaMemcpyHostToDevice, s));
-        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, d1, d2, dd, s);
-        else launch_queries<float>(o, count, d1, d2, dd, s);
+        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, d1, d2, dd, s, dbad);
+        else launch_queries<float>(o, count, d1, d2, dd, s, dbad);
+        uint32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, dbad, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (bad) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
         CK(cudaMemcpyAsync(dist, dd, count * 8, cudaMemcpyDeviceToHost, s));
         if (minplus_ops) {
             for (uint64_t i = 0; i < count; ++i) {
@@ -1163,8 +1171,8 @@ psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
     return guarded([&] {
         if (!o) throw ArgError("query_batch_device: NULL oracle");
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : o->ctx->stream;
-        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, v1, v2, dist, s);
-        else launch_queries<float>(o, count, v1, v2, dist, s);
+        if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, v1, v2, dist, s, nullptr);
+        else launch_queries<float>(o, count, v1, v2, dist, s, nullptr);
     });
 }
 

@@ -38,6 +38,8 @@ template <class V> struct QueryView {
     const V* bg;                // boundary-graph tiles
     uint32_t bg_nb;
     uint32_t k;
+    uint32_t n;                 // vertex count: ids >= n are rejected
+    uint32_t* bad_id;           // set to 1 when a query id is out of range
     double scale;               // 2^-q (u32 fixed point) or 1
 };
 
@@ -64,6 +66,12 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
 template <class V>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
                                         uint32_t& c1, uint32_t& c2, uint32_t& l1, uint32_t& l2) {
+    // src/query.cpp:30: out-of-range ids invalidate the batch (the host API
+    // reports PSP_EINVAL); the query is answered as (0, 0) meanwhile
+    if (v1 >= q.n || v2 >= q.n) {
+        if (q.bad_id) *q.bad_id = 1u;
+        v1 = v2 = 0;
+    }
     uint32_t r1 = q.perm[v1], r2 = q.perm[v2];
     c1 = q.assign[r1];
     c2 = q.assign[r2];
