@@ -221,12 +221,27 @@ def run_ours(args, rank, world, local):
     t0 = time.time()
     g, cfg = graphs.make(args.config)
     gen_s = time.time() - t0
-    threads = max(1, (os.cpu_count() or 8) // max(1, world))
-    o = P.build_oracle(g, cfg["k"], threads, 0, ctx=ctx)
+    threads = os.cpu_count() or 8
+    if world > 1:
+        # one host partition (all cores, rank 0), broadcast, then the
+        # collective device build with the boundary-graph FW row-sharded
+        import torch.distributed as dist
+        part = torch.empty(g.n, dtype=torch.int32, device=dev)
+        part_s = 0.0
+        if rank == 0:
+            t0 = time.time()
+            a = P.partition_graph(g, cfg["k"], 0, threads)
+            part_s = time.time() - t0
+            part.copy_(torch.from_numpy(a.view(np.int32)))
+        dist.broadcast(part, src=0)
+        o = P.build_partitioned(g, cfg["k"], part.cpu().numpy().view(np.uint32), ctx=ctx)
+        o.stats["partition_ms"] = part_s * 1e3 + o.stats["partition_ms"]
+    else:
+        o = P.build_oracle(g, cfg["k"], threads, 0, ctx=ctx)
     st = o.stats
 
     stream = torch.cuda.Stream(device=dev)
-    batch = args.batch
+    batch = args.batch or cfg["queries"]
     nsteps = args.warmup + args.steps
     # distinct pair slices per step and per rank (weak scaling)
     v1, v2 = P.random_pairs(g.n, batch * nsteps, 1000 + rank)
@@ -323,7 +338,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{args.config}: Delaunay n={g.n} m={g.m} k={cfg['k']} b={o.b}, "
                                f"{batch} random pairs per step per GPU",
                    "batch_per_gpu": batch, "l2_policy": "inputs >> L2 (BG table "
-                   f"{o.b * o.b * 4 / 1e9:.1f} GB), fresh pairs each step",
+                   f"{o.b * (o.b + 128) * 2 / 1e9:.1f} GB symmetric u32), fresh pairs each step",
                    "parallelism": (f"boundary-graph FW row-sharded over {world} GPUs (NCCL "
                                    f"panel min-allreduce), queries sharded by rank, tables "
                                    f"replicated" if world > 1 else "1 GPU")},
@@ -426,7 +441,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)
-    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--batch", type=int, default=0,
+                    help="pairs per step per GPU (default: the config's query count)")
     ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--cpu-baseline", dest="cpu_baseline", action="store_true", default=True)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
