@@ -485,8 +485,10 @@ __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict
 }
 
 // Query side table CB[c] = rows 0..|C| of component c restricted to its
-// boundary columns, |C| x |B(C)| row-major: row1/col2 of Algorithm 2
-// (src/query.cpp:29-45) become contiguous reads.  grid: k CTAs
+// boundary columns, |C| x cb_stride(|B(C)|) row-major (rows padded to a
+// multiple of 4 with INF so each row starts 16-byte aligned): row1/col2 of
+// Algorithm 2 (src/query.cpp:29-45) become contiguous, vector-loadable
+// reads.  grid: k CTAs
 template <class V>
 __global__ void extract_to_boundary(MatSet<V> comps, const uint32_t* __restrict__ comp_off,
                                     const uint32_t* __restrict__ bnd_off,
@@ -494,10 +496,12 @@ __global__ void extract_to_boundary(MatSet<V> comps, const uint32_t* __restrict_
     const uint32_t c = blockIdx.x;
     const uint32_t S = comp_off[c + 1] - comp_off[c];
     const uint32_t B = bnd_off[c + 1] - bnd_off[c];
-    const uint64_t total = uint64_t(S) * B;
+    const uint32_t Bp = cb_stride(B);  // rows padded to 16 bytes with INF
+    const uint64_t total = uint64_t(S) * Bp;
     for (uint64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const uint32_t l = static_cast<uint32_t>(idx / B), j = static_cast<uint32_t>(idx % B);
-        cb[cb_off[c] + idx] = comps.tiles[comps.tile_base[c] + sym_off(l, j, comps.nb[c])];
+        const uint32_t l = static_cast<uint32_t>(idx / Bp), j = static_cast<uint32_t>(idx % Bp);
+        cb[cb_off[c] + idx] =
+            j < B ? comps.tiles[comps.tile_base[c] + sym_off(l, j, comps.nb[c])] : Ops<V>::inf();
     }
 }
 

@@ -515,7 +515,7 @@ void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
     std::vector<uint64_t> cb_off(k + 1, 0);
     for (uint32_t c = 0; c < k; ++c)
         cb_off[c + 1] = cb_off[c] + uint64_t(R.comp_off[c + 1] - R.comp_off[c]) *
-                                        (R.bnd_off[c + 1] - R.bnd_off[c]);
+                                        cb_stride(R.bnd_off[c + 1] - R.bnd_off[c]);
     o->d_cb.alloc(cb_off[k] * sizeof(V));
     o->d_cb_off = upload(cb_off, s);
     o->d_comp_off = upload(R.comp_off, s);
@@ -840,7 +840,7 @@ void launch_grouped(psp_gpu_oracle* o, const QueryView<V>& q, uint64_t count, co
         CK(cudaFuncSetAttribute(query_grouped<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
         attr_set[std::is_same<V, float>::value] = true;
     }
-    query_grouped<V><<<o->ctx->sms * 3, GTHREADS, gsmem, s>>>(q, w);
+    query_grouped<V><<<o->ctx->sms * 2, GTHREADS, gsmem, s>>>(q, w);
     CK_LAUNCH();
     group_finish<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w, dist);
     CK_LAUNCH();

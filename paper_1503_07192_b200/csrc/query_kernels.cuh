@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
         resolve(q, v1[qi], v2[qi], c1, c2, l1, l2);
         const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
         const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
-        const V* row1 = q.cb + q.cb_off[c1] + uint64_t(l1) * B1;
-        const V* col2 = q.cb + q.cb_off[c2] + uint64_t(l2) * B2;
+        const V* row1 = q.cb + q.cb_off[c1] + uint64_t(l1) * cb_stride(B1);
+        const V* col2 = q.cb + q.cb_off[c2] + uint64_t(l2) * cb_stride(B2);
         V best = Ops<V>::inf();
         for (uint32_t j0 = 0; j0 < B2; j0 += 32 * WQ_SLOTS) {
             const uint32_t nslot = min(uint32_t(WQ_SLOTS), (B2 - j0 + 31) / 32);
@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
 // query meet in a global atomicMin (value bits are order-preserving: all
 // distances are >= 0), a last tiny kernel applies the same-component cap.
 constexpr int GQ = 32;           // queries per item (= max Q)
-constexpr int GK = 32;           // rows per staged chunk
-constexpr int GWARPS = 4;        // warps per CTA
+constexpr int GK = 16;           // rows per staged chunk
+constexpr int GWARPS = 8;        // warps per CTA
 constexpr int GTHREADS = 32 * GWARPS;
 
 // Per-batch workspace (device pointers), all sized by the caller.
@@ -260,42 +260,53 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// One chunk for NQ4*4 queries: acc[q] <- min_kk sA[kk][q] + sB[kk][lane]
-// over kk < rows8 (rows rounded up to 8; staged rows past the block end hold
-// INF in sA, so they never win). Row kk of sA stores query q at column
-// q ^ (kk & 7): with kk = k8 + r (k8 a multiple of 8, r unrolled) every
-// shared address below is a compile-time offset from one base register and
-// the in-vector permutation t ^ (r & 3) is free, so the ALU pipe sees only
-// the add-min instructions.
+// Shared staging per warp and chunk (GK = 16 rows):
+//   A [query][row]  : row1_q[k0 + kk], GK + 4 word rows (16-byte aligned, the
+//                     lane-per-query async fill is 4-way conflicted at most)
+//   B [row][column] : block rows for the 36-column, 16-byte-aligned superset
+//                     [A0, A0 + 36) of this task's 32 columns starting at
+//                     G0 = A0 + shift; lane j reads column shift + j.
+// Rows past the block end hold INF in B (their A values are don't-care), so
+// the compute never needs a row predicate; it walks rows in groups of 4,
+// reading each query's 4 row values as one broadcast LDS.128.
+constexpr int GA_STRIDE = GK + 4;  // 16-byte aligned rows, <= 4-way conflicted fill
+constexpr int GB_STRIDE = 36;  // the 9 staged 4-column chunks, conflict-free reads
+
 template <class V, int NQ4>
 __device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* __restrict__ sB,
-                                            V (&acc)[4 * NQ4], uint32_t rows8, int lane) {
-    for (uint32_t k8 = 0; k8 < rows8; k8 += 8) {
-        const V* a8 = sA + k8 * GQ;
-        const V* b8 = sB + k8 * 32 + lane;
+                                            V (&acc)[4 * NQ4], uint32_t rows4, uint32_t shift,
+                                            int lane) {
+    const V* bcol = sB + shift + lane;
+    for (uint32_t k4 = 0; k4 < rows4; k4 += 4) {
+        V b[4];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const V b = b8[r * 32];
+        for (int r = 0; r < 4; ++r) b[r] = bcol[(k4 + r) * GB_STRIDE];
 #pragma unroll
-            for (int i = 0; i < NQ4; ++i) {
-                const uint4 u = *reinterpret_cast<const uint4*>(a8 + r * GQ + 4 * (i ^ (r >> 2)));
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    acc[4 * i + t] =
-                        Ops<V>::addmin(Ops<V>::from_bits(w4[t ^ (r & 3)]), b, acc[4 * i + t]);
-            }
+        for (int qq = 0; qq < 4 * NQ4; ++qq) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sA + qq * GA_STRIDE + k4);
+            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.x), b[0], acc[qq]);
+            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.y), b[1], acc[qq]);
+            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.z), b[2], acc[qq]);
+            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.w), b[3], acc[qq]);
         }
     }
 }
 
-// Per-warp shared state: two staged chunks of row1 values (A) and block
-// rows (B), and the item's query ids / local ids.
+// Per-warp shared state: two staged chunks of A and B, the item's query
+// ids and col2 row offsets.
 template <class V> struct WarpStage {
-    V a[2][GK * GQ];
-    V b[2][GK * 32];
-    uint32_t id[GQ], a_off[GQ], l2[GQ];
+    V a[2][GQ * GA_STRIDE];
+    V b[2][GK * GB_STRIDE];
+    V c2[GQ * 32];  // col2_q[j] per (query, lane), fetched at task start
+    uint32_t id[GQ], c2off[GQ];
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
 
 template <class V, int NQ4>
 __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWork& w,
@@ -305,81 +316,103 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     const uint32_t nb = q.bg_nb;
     const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
     const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
+    const uint32_t Bp1 = cb_stride(B1), Bp2 = cb_stride(B2);
     const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
     const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
     const uint32_t j = cg * 32 + lane;
     const bool col_ok = j < B2;
-    const uint32_t gj = g2 + (col_ok ? j : B2 - 1);
-    const uint32_t Jt = gj >> 7, jc = gj & (T - 1);
+    // 16-byte-aligned column superset of this task's 32 columns
+    const uint32_t G0 = g2 + cg * 32, A0 = G0 & ~3u, shift = G0 - A0;
+    const uint32_t Jlo = A0 >> 7;
+    // this lane's staging slots for B: e = t*32 + lane -> (row kk, chunk u)
+    // over the 32 x 9 chunks of 4 columns
     __syncwarp();
+    const V* my_row1 = cb1;  // lane q: its query's row1 (16-byte aligned)
     if (uint32_t(lane) < m) {
-        st->id[lane] = w.sorted[q0 + lane];
-        st->a_off[lane] = w.s_l1[q0 + lane] * B1;
-        st->l2[lane] = w.s_l2[q0 + lane];
+        const uint32_t id = w.sorted[q0 + lane];
+        st->id[lane] = id;
+        st->c2off[lane] = w.s_l2[q0 + lane] * Bp2;
+        my_row1 = cb1 + uint64_t(w.s_l1[q0 + lane]) * Bp1;
     }
     __syncwarp();
 
-    // enqueue the chunk starting at row k0 into buffer `buf`
     auto issue = [&](uint32_t k0, int buf) {
         const uint32_t rows = min(uint32_t(GK), B1 - k0);
-        V* sa = st->a[buf];
-        V* sb = st->b[buf];
-        const bool row_ok = uint32_t(lane) < rows;
-#pragma unroll 4
-        for (int qq = 0; qq < 4 * NQ4; ++qq) {
-            V* dst = sa + lane * GQ + (qq ^ (lane & 7));  // 4-way bank conflict, async
-            if (row_ok && uint32_t(qq) < m) cp_async4(dst, cb1 + st->a_off[qq] + k0 + lane, true);
-            else *dst = Ops<V>::inf();  // padding rows / query slots never win
+        V* sa = st->a[buf] + lane * GA_STRIDE;
+        // A: lane q copies row1_q[k0 .. k0+32) (padding past Bp1 zero-fills;
+        // those rows meet INF in B)
+        if (uint32_t(lane) < m) {
+#pragma unroll
+            for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
         }
+        V* sb = st->b[buf];
         if (c1 != c2) {
             const uint32_t gi0 = g1 + k0;
-            const uint32_t split = T - (gi0 & (T - 1));
-            const V* p0 = q.bg + tidx(gi0 >> 7, Jt, nb) * TT + uint64_t(gi0 & (T - 1)) * T + jc;
-            const uint32_t I1 = (gi0 >> 7) + 1;
-            const V* p1 = (I1 <= Jt) ? q.bg + tidx(I1, Jt, nb) * TT + jc - uint64_t(split) * T : p0;
-#pragma unroll 8
-            for (int kk = 0; kk < GK; ++kk) {
-                const bool ok = col_ok && uint32_t(kk) < rows;
-                const V* src = ((uint32_t(kk) < split) ? p0 : p1) + kk * T;
-                cp_async4(sb + kk * 32 + lane, ok ? src : p0, ok);
+            const uint32_t I0 = gi0 >> 7, r0 = gi0 & (T - 1);
+#pragma unroll
+            for (int t = 0; t < (GK * 9 + 31) / 32; ++t) {
+                const uint32_t e = t * 32 + lane;
+                if (e >= uint32_t(GK * 9)) break;
+                const uint32_t kk = e / 9, u = e - kk * 9;
+                const uint32_t I = I0 + ((r0 + kk) >> 7);
+                const uint32_t col = A0 + 4 * u, J = col >> 7;
+                V* dst = sb + kk * GB_STRIDE + 4 * u;
+                if (kk < rows && I <= J && J < nb) {
+                    const V* src = q.bg + tidx(I, J, nb) * TT + uint64_t((r0 + kk) & (T - 1)) * T +
+                                   (col & (T - 1));
+                    cp_async16(dst, src, true);
+                } else {
+                    const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
+                    st4(dst, inf4);
+                }
             }
         } else {  // diagonal block (c1 == c2, 1/k of the pairs): generic lookup
 #pragma unroll 1
             for (int kk = 0; kk < GK; ++kk) {
-                const bool ok = col_ok && uint32_t(kk) < rows;
-                const V* src = q.bg + (ok ? sym_off(g1 + k0 + kk, gj, nb) : 0);
-                cp_async4(sb + kk * 32 + lane, src, ok);
+                const uint32_t col = G0 + lane;
+                V v = Ops<V>::inf();
+                if (uint32_t(kk) < rows && col_ok) v = q.bg[sym_off(g1 + k0 + kk, col, nb)];
+                sb[kk * GB_STRIDE + shift + lane] = v;
             }
         }
         cp_async_commit();
     };
+    (void)Jlo;
 
     V acc[4 * NQ4];
 #pragma unroll
     for (int i = 0; i < 4 * NQ4; ++i) acc[i] = Ops<V>::inf();
+    // col2_q[j] for every query, fetched asynchronously now (first commit
+    // group, so it has landed by the first chunk's wait) into shared memory
+#pragma unroll 4
+    for (int i = 0; i < 4 * NQ4; ++i) {
+        const bool ok = col_ok && uint32_t(i) < m;
+        cp_async4(st->c2 + i * 32 + lane, cb2 + (ok ? st->c2off[i] + j : 0), ok);
+    }
+    cp_async_commit();
     if (B1 > 0) issue(0, 0);
-    // col2_q[j] for every query, fetched now so the loads overlap the task
-    V c2v[4 * NQ4];
-#pragma unroll
-    for (int i = 0; i < 4 * NQ4; ++i)
-        c2v[i] = (col_ok && uint32_t(i) < m) ? cb2[uint64_t(st->l2[i]) * B2 + j] : Ops<V>::inf();
     int buf = 0;
     for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
         const bool more = k0 + GK < B1;
         if (more) issue(k0 + GK, buf ^ 1);
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncwarp();
-        group_chunk<V, NQ4>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 7) & ~7u,
-                            lane);
+        group_chunk<V, NQ4>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u,
+                            shift, lane);
         __syncwarp();  // buffer `buf` is refilled two chunks later
         buf ^= 1;
     }
     // combine with col2 (t_q = acc_q + col2_q[j]), then per-query minimum over
     // the 32 columns through a padded shared transpose (conflict free)
-    V* sT = st->a[0];  // 32 x 33 words, free after the last chunk
+    cp_async_wait<0>();  // col2 group (also covers B1 == 0)
+    __syncwarp();
+    static_assert(2 * GQ * GA_STRIDE >= 32 * 33, "transpose scratch fits both A buffers");
+    V* sT = st->a[0];  // 32 x 33 words over a[0..1], free after the last chunk
 #pragma unroll
     for (int i = 0; i < 4 * NQ4; ++i) {
-        sT[i * 33 + lane] = Ops<V>::addmin(acc[i], c2v[i], Ops<V>::inf());
+        const V c2v = st->c2[i * 32 + lane];  // zero-filled when !ok: masked below
+        const bool ok = col_ok && uint32_t(i) < m;
+        sT[i * 33 + lane] = ok ? Ops<V>::addmin(acc[i], c2v, Ops<V>::inf()) : Ops<V>::inf();
     }
     __syncwarp();
     if (uint32_t(lane) < m) {
@@ -391,7 +424,7 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
 }
 
 template <class V>
-__global__ void __launch_bounds__(GTHREADS) query_grouped(QueryView<V> q, GroupWork w) {
+__global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, GroupWork w) {
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
     const uint32_t total = w.task_start[w.nbins];
