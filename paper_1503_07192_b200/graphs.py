@@ -37,6 +37,14 @@ def delaunay(n: int, seed: int = 1) -> Graph:
 
 
 def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10) -> Graph:
+    """Road-like perturbed grid: jittered 4-neighbour grid, a random spanning
+    tree kept (minimum spanning tree under random keys, so deletions never
+    disconnect the network) and ~`drop` of the remaining edges removed;
+    weights = Euclidean length of the jittered embedding x U[1, 2), rounded to
+    f32 (the tolerance path: not dyadic, so the device computes in f32)."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import minimum_spanning_tree
+
     rng = np.random.default_rng(seed)
     n = rows * cols
     r, c = np.divmod(np.arange(n, dtype=np.int64), cols)
@@ -45,26 +53,16 @@ def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10) -> Graph:
     down = np.arange(n)[r + 1 < rows]
     eu = np.concatenate([right, down])
     ev = np.concatenate([right + 1, down + cols])
-    # keep a random spanning tree (randomised Kruskal on a shuffled order) so
-    # deletions never disconnect the network, then drop a fraction of the rest
-    order = rng.permutation(len(eu))
-    parent = np.arange(n)
-
-    def find(x):
-        root = x
-        while parent[root] != root:
-            root = parent[root]
-        while parent[x] != root:
-            parent[x], x = root, parent[x]
-        return root
-
-    in_tree = np.zeros(len(eu), bool)
-    for idx in order:
-        a, b = find(eu[idx]), find(ev[idx])
-        if a != b:
-            parent[a] = b
-            in_tree[idx] = True
-    keep = in_tree | (rng.random(len(eu)) >= drop)
+    key = rng.random(len(eu)) + 1.0  # distinct positive keys -> random spanning tree
+    mst = minimum_spanning_tree(coo_matrix((key, (eu, ev)), shape=(n, n)).tocsr()).tocoo()
+    tree = np.zeros(len(eu), bool)
+    # map MST edges back to edge ids (the grid edge (u, v) is unique)
+    lin = eu * n + ev
+    order = np.argsort(lin)
+    mlin = np.minimum(mst.row, mst.col).astype(np.int64) * n + np.maximum(mst.row, mst.col)
+    pos = np.searchsorted(lin[order], mlin)
+    tree[order[pos]] = True
+    keep = tree | (rng.random(len(eu)) >= drop)
     eu, ev = eu[keep], ev[keep]
     length = np.linalg.norm(xy[eu] - xy[ev], axis=1)
     w = (length * rng.uniform(1.0, 2.0, len(eu))).astype(np.float32).astype(np.float64)
@@ -80,6 +78,13 @@ CONFIGS = {
     # configs[2]
     "delaunay1m_k1024": dict(family="delaunay", n=1_048_576, seed=1, k=1024,
                              queries=10_000_000),
+    # configs[3]: road-like grid, float32 weights (tolerance path), for
+    # preprocessing scaling. k = 512 keeps the u32/f32 tables at ~121 GB per
+    # GPU (components 70 GB + boundary graph 51 GB) and minimises FW work.
+    "road4m_k512": dict(family="road", rows=2048, cols=2048, seed=7, k=512,
+                        queries=10_000_000),
+    # small road grid for tests
+    "road64k_k64": dict(family="road", rows=256, cols=256, seed=7, k=64, queries=1_000_000),
 }
 
 
@@ -91,6 +96,8 @@ def make(name: str) -> tuple[Graph, dict]:
         g = generate_grid(cfg["rows"], cfg["cols"], cfg["weights"], cfg["seed"])
     elif fam == "delaunay":
         g = delaunay(cfg["n"], cfg["seed"])
+    elif fam == "road":
+        g = road_grid(cfg["rows"], cfg["cols"], cfg["seed"])
     else:
         raise ValueError(fam)
     return g, cfg
