@@ -40,7 +40,10 @@ typedef enum psp_status {
     PSP_ECUDA = 3,      /* CUDA runtime error / no device                        */
     PSP_ENCCL = 4,      /* NCCL error (multi-GPU)                                */
     PSP_EOVERFLOW = 5,  /* u32 requested but weights not representable exactly   */
-    PSP_EGRAPH = 6      /* graph invariant violated (psp::GraphInvariantError)   */
+    PSP_EGRAPH = 6,     /* graph invariant violated (psp::GraphInvariantError)   */
+    PSP_EIO = 7,        /* file unreadable / truncated / inconsistent (psp::IoError) */
+    PSP_EFORMAT = 8,    /* not a PSP1 file or wrong version (psp::FormatVersionError) */
+    PSP_ECHECKSUM = 9   /* CRC-64 mismatch (psp::ChecksumError)                  */
 } psp_status;
 
 enum {
@@ -136,6 +139,15 @@ psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
                                  const double* const* component_tables,
                                  const double* const* boundary_tables, int value_kind,
                                  psp_gpu_oracle** out);
+
+/* psp::save_oracle / load_oracle (include/psp/oracle_io.hpp:22-34,
+ * src/oracle_io.cpp:106-255): the PSP1 file written straight from the device
+ * tables (f64 conversion and CRC-64/XZ on the GPU), byte-identical to the
+ * reference's image of the same oracle; and read back (same validation and
+ * error classes as read_oracle) into a device oracle for queries. */
+psp_status psp_gpu_oracle_save(const psp_gpu_oracle* o, const char* path);
+psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kind,
+                               psp_gpu_oracle** out);
 
 void psp_gpu_oracle_free(psp_gpu_oracle* o);
 psp_status psp_gpu_oracle_info(const psp_gpu_oracle* o, psp_oracle_info* out);

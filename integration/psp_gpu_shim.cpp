@@ -15,7 +15,8 @@
 //
 // Error mapping (include/psp/errors.hpp conventions): PSP_EINVAL and
 // PSP_EOVERFLOW -> std::invalid_argument, PSP_EGRAPH -> psp::GraphInvariantError,
-// anything else -> std::runtime_error.
+// PSP_EIO / PSP_EFORMAT / PSP_ECHECKSUM -> psp::IoError / FormatVersionError /
+// ChecksumError, anything else -> std::runtime_error.
 //
 // Device-resident oracles: build_oracle returns a fully populated host
 // psp::Oracle (the reference tests and save_oracle read its tables) and keeps
@@ -45,6 +46,9 @@ void check(psp_status st) {
     const std::string msg = psp_gpu_last_error();
     if (st == PSP_EINVAL || st == PSP_EOVERFLOW) throw std::invalid_argument(msg);
     if (st == PSP_EGRAPH) throw psp::GraphInvariantError(msg);
+    if (st == PSP_ECHECKSUM) throw psp::ChecksumError(msg);
+    if (st == PSP_EFORMAT) throw psp::FormatVersionError(msg);
+    if (st == PSP_EIO) throw psp::IoError(msg);
     throw std::runtime_error(msg);
 }
 

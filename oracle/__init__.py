@@ -91,6 +91,8 @@ class RefLib:
             lib.ref_sampled_build.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64,
                                               C.c_uint32, C.c_uint64, _f64p, _u64p]
             lib.ref_random_pairs.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]
+            lib.ref_save_oracle.argtypes = [vp, C.c_char_p]
+            lib.ref_load_oracle.argtypes = [C.c_char_p, C.POINTER(vp)]
             RefLib._lib = lib
         self.lib = RefLib._lib
 
@@ -104,6 +106,12 @@ class RefLib:
         v2 = np.empty(count, np.uint32)
         self.lib.ref_random_pairs(n, count, seed, v1, v2)
         return v1, v2
+
+    def load_oracle(self, path: str) -> "RefOracle":
+        """psp::load_oracle on the reference."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_load_oracle(os.fsencode(path), C.byref(h)))
+        return RefOracle(self, h, np.zeros(7))
 
     # graphs ------------------------------------------------------------
     def generate(self, kind: str, rows: int, cols: int, weights=None, seed: int = 0) -> "RefGraph":
@@ -207,6 +215,10 @@ class RefOracle:
 
     def boundary_size(self, c: int) -> int:
         return int(self.boundary_offset[c + 1] - self.boundary_offset[c])
+
+    def save(self, path: str) -> None:
+        """psp::save_oracle on the reference."""
+        self.ref._check(self.ref.lib.ref_save_oracle(self.h, os.fsencode(path)))
 
     def component_table(self, c: int) -> np.ndarray:
         s = self.component_size(c)

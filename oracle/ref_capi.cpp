@@ -29,6 +29,7 @@
 #include "psp/generators.hpp"
 #include "psp/graph.hpp"
 #include "psp/oracle.hpp"
+#include "psp/oracle_io.hpp"
 #include "psp/partition.hpp"
 #include "psp/query.hpp"
 #include "psp/shortest_paths.hpp"
@@ -270,6 +271,24 @@ int ref_sampled_build(const void* g, uint32_t k, uint32_t workers, uint64_t seed
             (void)d;
         }
         times[3] = ms(t0);
+    });
+}
+
+// save_oracle / load_oracle (include/psp/oracle_io.hpp:31-32)
+int ref_save_oracle(const void* o, const char* path) {
+    return guarded([&] { psp::save_oracle(static_cast<const RefOracle*>(o)->o, path); });
+}
+
+int ref_load_oracle(const char* path, void** out) {
+    return guarded([&] {
+        auto* ro = new RefOracle;
+        try {
+            ro->o = psp::load_oracle(path);
+        } catch (...) {
+            delete ro;
+            throw;
+        }
+        *out = ro;
     });
 }
 

@@ -15,17 +15,19 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import os
 
 import numpy as np
 
 from . import _lib
-from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, GraphInvariantError, PspError,
-                   PspValueError)
+from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, ChecksumError,
+                   FormatVersionError, GraphInvariantError, OracleIoError, PspError, PspValueError)
 
 __all__ = ["Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
            "random_pairs", "VALUE_AUTO", "VALUE_U32", "VALUE_F32", "PspError", "PspValueError",
-           "GraphInvariantError", "UNREACHABLE"]
+           "GraphInvariantError", "OracleIoError", "FormatVersionError", "ChecksumError",
+           "load_oracle", "UNREACHABLE"]
 
 UNREACHABLE = float("inf")  # kUnreachable (include/psp/graph.hpp:14)
 
@@ -177,6 +179,11 @@ class GpuOracle:
         d, ops = self.batch_query([v1], [v2], with_ops=True)
         return float(d[0]), int(ops[0])
 
+    def save(self, path: str) -> None:
+        """psp::save_oracle (include/psp/oracle_io.hpp:31): PSP1 file written
+        from the device tables, byte-identical to the reference's image."""
+        _lib.check(_lib.lib().psp_gpu_oracle_save(self.h, os.fsencode(path)))
+
     def batch_query_device(self, v1_ptr: int, v2_ptr: int, dist_ptr: int, count: int,
                            stream: int | None = None) -> None:
         """Device-resident queries: raw device pointers, enqueued on `stream`."""
@@ -228,6 +235,14 @@ def import_oracle(n: int, k: int, permutation, assignment_reordered, component_o
     h = C.c_void_p()
     _lib.check(_lib.lib().psp_gpu_oracle_import(ctx.h, n, k, perm, asg, co, bo, cp, bp,
                                                 value_kind, C.byref(h)))
+    return GpuOracle(ctx, h, BuildStats())
+
+
+def load_oracle(path: str, value_kind: int = VALUE_AUTO, ctx: Context | None = None) -> GpuOracle:
+    """psp::load_oracle (include/psp/oracle_io.hpp:32) into device memory."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _lib.check(_lib.lib().psp_gpu_oracle_load(ctx.h, os.fsencode(path), value_kind, C.byref(h)))
     return GpuOracle(ctx, h, BuildStats())
 
 

@@ -14,7 +14,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpsp_gpu.so")
 
-PSP_OK, PSP_EINVAL, PSP_ENOMEM, PSP_ECUDA, PSP_ENCCL, PSP_EOVERFLOW, PSP_EGRAPH = range(7)
+(PSP_OK, PSP_EINVAL, PSP_ENOMEM, PSP_ECUDA, PSP_ENCCL, PSP_EOVERFLOW, PSP_EGRAPH, PSP_EIO,
+ PSP_EFORMAT, PSP_ECHECKSUM) = range(10)
 VALUE_AUTO, VALUE_U32, VALUE_F32 = 0, 1, 2
 VALUE_NAMES = {VALUE_U32: "u32", VALUE_F32: "f32"}
 
@@ -33,6 +34,19 @@ class GraphInvariantError(PspError):
 
 class PspValueError(PspError, ValueError):
     """std::invalid_argument / PSP_EINVAL and PSP_EOVERFLOW."""
+
+
+class OracleIoError(PspError, OSError):
+    """psp::IoError (include/psp/errors.hpp:28-31): unreadable, truncated or
+    inconsistent oracle file."""
+
+
+class FormatVersionError(OracleIoError):
+    """psp::FormatVersionError (include/psp/errors.hpp:34-37)."""
+
+
+class ChecksumError(OracleIoError):
+    """psp::ChecksumError (include/psp/errors.hpp:40-43)."""
 
 
 class BuildStats(C.Structure):
@@ -93,6 +107,8 @@ SIGNATURES = {
                                             C.POINTER(BuildStats)]),
     "psp_gpu_oracle_import": (C.c_int, [_vp, C.c_uint64, C.c_uint32, _u32p, _u32p, _u64p, _u64p,
                                         _vp, _vp, C.c_int, C.POINTER(_vp)]),
+    "psp_gpu_oracle_save": (C.c_int, [_vp, C.c_char_p]),
+    "psp_gpu_oracle_load": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
     "psp_gpu_oracle_free": (None, [_vp]),
     "psp_gpu_oracle_info": (C.c_int, [_vp, C.POINTER(OracleInfo)]),
     "psp_gpu_oracle_ids": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -141,4 +157,10 @@ def check(status: int) -> None:
         raise PspValueError(status, msg)
     if status == PSP_EGRAPH:
         raise GraphInvariantError(status, msg)
+    if status == PSP_ECHECKSUM:
+        raise ChecksumError(status, msg)
+    if status == PSP_EFORMAT:
+        raise FormatVersionError(status, msg)
+    if status == PSP_EIO:
+        raise OracleIoError(status, msg)
     raise PspError(status, msg)

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <fstream>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -31,6 +32,7 @@
 #include "host_graph.hpp"
 #include "minplus.cuh"
 #include "nccl_api.hpp"
+#include "oracle_file.cuh"
 #include "psp_gpu.h"
 #include "query_kernels.cuh"
 
@@ -891,6 +893,69 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
 
 }  // namespace
 
+// --------------------------------------------------------- PSP1 files --
+struct PinnedBuf {
+    void* p = nullptr;
+    explicit PinnedBuf(size_t n) { CK(cudaMallocHost(&p, n)); }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+constexpr size_t IO_CHUNK = size_t(64) << 20;  // bytes per device/host staging chunk
+
+// Append `len` bytes at device pointer d (8-byte aligned) to the running CRC:
+// per-segment raw CRCs on the GPU, folded on the host.
+void crc_device_bytes(Crc64Stream& crc, const uint8_t* d, uint64_t len, DBuf& seg,
+                      std::vector<uint64_t>& hseg, cudaStream_t s) {
+    if (len == 0) return;
+    const uint64_t nseg = (len + CRC_SEG - 1) / CRC_SEG;
+    if (seg.bytes < nseg * 8) seg.alloc(nseg * 8);
+    crc64_segments<<<unsigned((nseg + 127) / 128), 128, 0, s>>>(d, len, crc.table(),
+                                                                seg.as<uint64_t>());
+    CK_LAUNCH();
+    hseg.resize(nseg);
+    CK(cudaMemcpyAsync(hseg.data(), seg.p, nseg * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < nseg; ++i)
+        crc.append_raw(hseg[i], std::min<uint64_t>(CRC_SEG, len - i * CRC_SEG));
+}
+
+template <class V>
+void save_tables(const psp_gpu_oracle* o, std::FILE* f, Crc64Stream& crc) {
+    cudaStream_t s = o->ctx->stream;
+    DBuf chunk(IO_CHUNK), seg;
+    PinnedBuf host(IO_CHUNK);
+    std::vector<uint64_t> hseg;
+    auto emit = [&](const MatArena& a, uint32_t m, uint32_t row0, uint32_t nrows, uint32_t ncols) {
+        if (!nrows || !ncols) return;
+        const uint32_t per = uint32_t(std::max<uint64_t>(1, IO_CHUNK / (uint64_t(ncols) * 8)));
+        for (uint32_t r0 = 0; r0 < nrows; r0 += per) {
+            const uint32_t nr = std::min(per, nrows - r0);
+            const uint64_t cnt = uint64_t(nr) * ncols, bytes = cnt * 8;
+            window_to_f64<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(
+                a.view<V>(), m, row0 + r0, nr, ncols, o->scale, chunk.as<double>());
+            CK_LAUNCH();
+            CK(cudaMemcpyAsync(host.p, chunk.p, bytes, cudaMemcpyDeviceToHost, s));
+            crc_device_bytes(crc, chunk.as<uint8_t>(), bytes, seg, hseg, s);  // syncs
+            if (std::fwrite(host.p, 1, bytes, f) != bytes) throw Fail{PSP_EIO, "oracle write failed"};
+        }
+    };
+    const Reordered& R = o->R;
+    for (uint32_t c = 0; c < R.k; ++c) {
+        const uint32_t sz = R.comp_off[c + 1] - R.comp_off[c];
+        emit(o->comps, c, 0, sz, sz);
+    }
+    for (uint32_t c = 0; c < R.k; ++c)
+        emit(o->bg, 0, R.bnd_off[c], R.bnd_off[c + 1] - R.bnd_off[c], uint32_t(R.b()));
+}
+
+void put_u64s(std::vector<uint8_t>& buf, uint64_t v) {
+    const size_t at = buf.size();
+    buf.resize(at + 8);
+    std::memcpy(buf.data() + at, &v, 8);
+}
+
 // ================================================================ C-ABI ==
 extern "C" {
 
@@ -1058,6 +1123,159 @@ psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
         if (o->kind.kind == PSP_VALUE_U32) import_tables<uint32_t>(o.get(), component_tables, boundary_tables);
         else import_tables<float>(o.get(), component_tables, boundary_tables);
         *out = o.release();
+    });
+}
+
+psp_status psp_gpu_oracle_save(const psp_gpu_oracle* o, const char* path) {
+    return guarded([&] {
+        if (!o || !path) throw ArgError("oracle_save: NULL argument");
+        CK(cudaSetDevice(o->ctx->device));
+        const Reordered& R = o->R;
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw Fail{PSP_EIO, std::string(path) + ": cannot open for writing"};
+        std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, std::fclose);
+        Crc64Stream crc;
+        // header and id sections (src/oracle_io.cpp:106-127)
+        std::vector<uint8_t> head = {'P', 'S', 'P', '1', 1, 0, 0, 0};
+        put_u64s(head, R.n);
+        put_u64s(head, R.k);
+        put_u64s(head, R.b());
+        for (uint64_t v = 0; v < R.n; ++v) put_u64s(head, R.perm[v]);
+        for (uint64_t v = 0; v < R.n; ++v) put_u64s(head, R.assign[v]);
+        std::vector<uint8_t> packed((R.n + 7) / 8, 0);
+        for (uint64_t v = 0; v < R.n; ++v)
+            if (R.flags[v]) packed[v / 8] |= uint8_t(1u << (v % 8));
+        head.insert(head.end(), packed.begin(), packed.end());
+        for (uint32_t c = 0; c <= R.k; ++c) put_u64s(head, R.comp_off[c]);
+        crc.update(head.data(), head.size());
+        if (std::fwrite(head.data(), 1, head.size(), f) != head.size())
+            throw Fail{PSP_EIO, "oracle write failed"};
+        if (o->kind.kind == PSP_VALUE_U32) save_tables<uint32_t>(o, f, crc);
+        else save_tables<float>(o, f, crc);
+        const uint64_t sum = crc.value();
+        if (std::fwrite(&sum, 1, 8, f) != 8 || std::fflush(f) != 0)
+            throw Fail{PSP_EIO, "oracle write failed"};
+    });
+}
+
+psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kind,
+                               psp_gpu_oracle** out) {
+    return guarded([&] {
+        if (!ctx || !path || !out) throw ArgError("oracle_load: NULL argument");
+        const std::string name(path);
+        auto io = [&](const std::string& msg) { return Fail{PSP_EIO, name + ": " + msg}; };
+        std::ifstream in(name, std::ios::binary);
+        if (!in) throw io("cannot open for reading");
+        in.seekg(0, std::ios::end);
+        const int64_t total = in.tellg();
+        in.seekg(0, std::ios::beg);
+        if (total < 4 + 4 + 8) throw io("truncated oracle file");
+        // validation order and messages follow read_oracle (src/oracle_io.cpp:129-255)
+        uint8_t head[28] = {0};
+        in.read(reinterpret_cast<char*>(head), std::min<int64_t>(28, total));
+        if (std::memcmp(head, "PSP1", 4) != 0) throw Fail{PSP_EFORMAT, name + ": not an oracle file"};
+        uint32_t version;
+        std::memcpy(&version, head + 4, 4);
+        if (version != 1)
+            throw Fail{PSP_EFORMAT, name + ": unsupported oracle format version " + std::to_string(version)};
+        const uint64_t payload = uint64_t(total) - 8;
+        if (payload < 28) throw io("truncated oracle file");
+        uint64_t n, k, b;
+        std::memcpy(&n, head + 8, 8);
+        std::memcpy(&k, head + 16, 8);
+        std::memcpy(&b, head + 24, 8);
+        const uint64_t remaining = payload - 28;
+        if (n > remaining / 16 || k > remaining / 8) throw io("truncated oracle file");
+        if (k < 1 || k > n || b > n || n > 0xffffffffull) throw io("inconsistent oracle header");
+        const uint64_t fixed = 16 * n + (n + 7) / 8 + 8 * (k + 1);
+        if (remaining < fixed) throw io("truncated oracle file");
+        // read everything with the table section 8-byte aligned in memory
+        const uint64_t table_at = 28 + fixed;
+        const size_t pad = (8 - table_at % 8) % 8;
+        std::vector<uint64_t> store((uint64_t(total) + pad + 7) / 8 + 1);
+        uint8_t* buf = reinterpret_cast<uint8_t*>(store.data()) + pad;
+        in.seekg(0, std::ios::beg);
+        in.read(reinterpret_cast<char*>(buf), total);
+        if (in.gcount() != total) throw io("truncated oracle file");
+        const uint8_t* p = buf + 28;
+        auto rd64 = [&](const uint8_t* q) {
+            uint64_t v;
+            std::memcpy(&v, q, 8);
+            return v;
+        };
+        std::vector<uint32_t> perm(n), assign(n);
+        for (uint64_t v = 0; v < n; ++v) {
+            const uint64_t t = rd64(p + 8 * v);
+            if (t >= n) throw io("permutation entry out of range");
+            perm[v] = uint32_t(t);
+        }
+        p += 8 * n;
+        for (uint64_t v = 0; v < n; ++v) {
+            const uint64_t c = rd64(p + 8 * v);
+            if (c >= k) throw io("component assignment out of range");
+            assign[v] = uint32_t(c);
+        }
+        p += 8 * n;
+        const uint8_t* packed = p;
+        p += (n + 7) / 8;
+        std::vector<uint64_t> co(k + 1), bo(k + 1, 0);
+        for (uint64_t c = 0; c <= k; ++c) co[c] = rd64(p + 8 * c);
+        p += 8 * (k + 1);
+        if (co[0] != 0 || co[k] != n) throw io("inconsistent component offsets");
+        for (uint64_t c = 0; c < k; ++c) {
+            if (co[c + 1] < co[c] || co[c + 1] > n) throw io("inconsistent component offsets");
+            bool interior = false;
+            uint64_t nbnd = 0;
+            for (uint64_t v = co[c]; v < co[c + 1]; ++v) {
+                if (assign[v] != c) throw io("assignment does not match component offsets");
+                if ((packed[v / 8] >> (v % 8)) & 1u) {
+                    if (interior) throw io("boundary vertices must prefix each component");
+                    ++nbnd;
+                } else {
+                    interior = true;
+                }
+            }
+            bo[c + 1] = bo[c] + nbnd;
+        }
+        if (bo[k] != b) throw io("boundary count does not match flags");
+        uint64_t table_bytes = 0;
+        for (uint64_t c = 0; c < k; ++c) {
+            const uint64_t sz = co[c + 1] - co[c];
+            table_bytes += 8 * (sz * sz + (bo[c + 1] - bo[c]) * b);
+        }
+        if (payload - table_at != table_bytes)
+            throw io(payload - table_at < table_bytes ? "truncated oracle file"
+                                                      : "oracle file has trailing data");
+        // checksum: header on the host, tables on the device
+        CK(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        Crc64Stream crc;
+        crc.update(buf, table_at);
+        {
+            DBuf chunk(IO_CHUNK), seg;
+            std::vector<uint64_t> hseg;
+            for (uint64_t at = 0; at < table_bytes; at += IO_CHUNK) {
+                const uint64_t len = std::min<uint64_t>(IO_CHUNK, table_bytes - at);
+                CK(cudaMemcpyAsync(chunk.p, buf + table_at + at, len, cudaMemcpyHostToDevice, s));
+                crc_device_bytes(crc, chunk.as<uint8_t>(), len, seg, hseg, s);
+            }
+        }
+        if (rd64(buf + payload) != crc.value())
+            throw Fail{PSP_ECHECKSUM, name + ": oracle checksum mismatch"};
+        std::vector<const double*> ct(k), bt(k);
+        const double* tp = reinterpret_cast<const double*>(buf + table_at);
+        for (uint64_t c = 0; c < k; ++c) {
+            ct[c] = tp;
+            tp += (co[c + 1] - co[c]) * (co[c + 1] - co[c]);
+        }
+        for (uint64_t c = 0; c < k; ++c) {
+            bt[c] = tp;
+            tp += (bo[c + 1] - bo[c]) * b;
+        }
+        const psp_status st = psp_gpu_oracle_import(ctx, n, uint32_t(k), perm.data(), assign.data(),
+                                                    co.data(), bo.data(), ct.data(), bt.data(),
+                                                    value_kind, out);
+        if (st != PSP_OK) throw Fail{st, g_err};
     });
 }
 
