@@ -175,8 +175,9 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
     minplus_ops) per second per GPU against the in-run VIADDMNMX peak; the
     no-reuse HBM figure is reported beside it, never as a fraction > 1.
     Sparse batches run query_warp, which is HBM bound."""
+    import paper_1503_07192_b200 as P
     pairs = o.k * (o.k + 1) / 2
-    dense = batch >= 2.0 * pairs and os.environ.get("PSP_QUERY_KERNEL") != "warp"
+    dense = batch >= P.GROUP_MIN_DENSITY * pairs and os.environ.get("PSP_QUERY_KERNEL") != "warp"
     secs = per_launch_ms / 1e3
     ops_launch = tops / steps
     bytes_launch = tb / steps

@@ -30,6 +30,10 @@ __all__ = ["Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "
            "load_oracle", "UNREACHABLE"]
 
 UNREACHABLE = float("inf")  # kUnreachable (include/psp/graph.hpp:14)
+# queries per component pair at which batches switch from the warp-per-query
+# kernel to the pair-grouped kernel (must match psp_gpu.cu GROUP_MIN_DENSITY):
+# 0 = always grouped (it wins at every measured batch size)
+GROUP_MIN_DENSITY = 0.0
 
 
 @dataclasses.dataclass

@@ -849,9 +849,11 @@ void launch_grouped(psp_gpu_oracle* o, const QueryView<V>& q, uint64_t count, co
     CK(cudaEventRecord(o->gw_done, s));
 }
 
-// Dense batches (>= GROUP_MIN_DENSITY queries per component pair on average)
-// go through the grouped kernel; sparse ones through one warp per query.
-constexpr double GROUP_MIN_DENSITY = 2.0;
+// Every batch goes through the pair-grouped kernel: measured on cfg2/cfg3 it
+// beats one-warp-per-query from 1K pairs up (8.4M vs 3.4M q/s at 1K, 393M vs
+// 17M at 1M; profiles/bench/r1_kernel_crossover.jsonl). query_warp remains
+// for k*k beyond 32-bit bin keys and as the PSP_QUERY_KERNEL=warp check.
+constexpr double GROUP_MIN_DENSITY = 0.0;
 
 template <class V>
 void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
@@ -1171,33 +1173,33 @@ psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kin
         in.seekg(0, std::ios::beg);
         if (total < 4 + 4 + 8) throw io("truncated oracle file");
         // validation order and messages follow read_oracle (src/oracle_io.cpp:129-255)
-        uint8_t head[28] = {0};
-        in.read(reinterpret_cast<char*>(head), std::min<int64_t>(28, total));
+        uint8_t head[32] = {0};  // magic, version, n, k, b
+        in.read(reinterpret_cast<char*>(head), std::min<int64_t>(32, total));
         if (std::memcmp(head, "PSP1", 4) != 0) throw Fail{PSP_EFORMAT, name + ": not an oracle file"};
         uint32_t version;
         std::memcpy(&version, head + 4, 4);
         if (version != 1)
             throw Fail{PSP_EFORMAT, name + ": unsupported oracle format version " + std::to_string(version)};
         const uint64_t payload = uint64_t(total) - 8;
-        if (payload < 28) throw io("truncated oracle file");
+        if (payload < 32) throw io("truncated oracle file");
         uint64_t n, k, b;
         std::memcpy(&n, head + 8, 8);
         std::memcpy(&k, head + 16, 8);
         std::memcpy(&b, head + 24, 8);
-        const uint64_t remaining = payload - 28;
+        const uint64_t remaining = payload - 32;
         if (n > remaining / 16 || k > remaining / 8) throw io("truncated oracle file");
         if (k < 1 || k > n || b > n || n > 0xffffffffull) throw io("inconsistent oracle header");
         const uint64_t fixed = 16 * n + (n + 7) / 8 + 8 * (k + 1);
         if (remaining < fixed) throw io("truncated oracle file");
         // read everything with the table section 8-byte aligned in memory
-        const uint64_t table_at = 28 + fixed;
+        const uint64_t table_at = 32 + fixed;
         const size_t pad = (8 - table_at % 8) % 8;
         std::vector<uint64_t> store((uint64_t(total) + pad + 7) / 8 + 1);
         uint8_t* buf = reinterpret_cast<uint8_t*>(store.data()) + pad;
         in.seekg(0, std::ios::beg);
         in.read(reinterpret_cast<char*>(buf), total);
         if (in.gcount() != total) throw io("truncated oracle file");
-        const uint8_t* p = buf + 28;
+        const uint8_t* p = buf + 32;
         auto rd64 = [&](const uint8_t* q) {
             uint64_t v;
             std::memcpy(&v, q, 8);

@@ -84,7 +84,11 @@ __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint
 }
 
 // ---------------------------------------------------- sparse: warp/query --
-constexpr int WQ_SLOTS = 16;  // up to 512 target boundary columns in registers
+// One warp per query. Lanes own target columns (a window of 32 x WQ_SLOTS);
+// source rows are walked in chunks of 32 with row1 broadcast by SHFL, and
+// rows are unrolled by 4 so 4 x WQ_SLOTS independent row-segment loads are
+// in flight per warp (each a full 128-byte row segment of the block).
+constexpr int WQ_SLOTS = 8;  // 256 target boundary columns per window
 
 template <class V>
 __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t* __restrict__ v1,
@@ -107,33 +111,46 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
             V acc[WQ_SLOTS];
 #pragma unroll
             for (int s = 0; s < WQ_SLOTS; ++s) acc[s] = Ops<V>::inf();
-            uint64_t colbase[WQ_SLOTS];
-            uint32_t cur_I = 0xffffffffu;
             for (uint32_t i0 = 0; i0 < B1; i0 += 32) {
                 const uint32_t ni = min(32u, B1 - i0);
                 const V rv = (uint32_t(lane) < ni) ? row1[i0 + lane] : Ops<V>::inf();
-                for (uint32_t t = 0; t < ni; ++t) {
-                    const V r = __shfl_sync(0xffffffffu, rv, t);
-                    const uint32_t gi = g1 + i0 + t;
-                    if (c1 != c2) {
-                        if ((gi >> 7) != cur_I) {  // new tile row: per-slot tile bases
-                            cur_I = gi >> 7;
+                const uint32_t gi0 = g1 + i0;
+                if (c1 != c2) {
+                    // rows gi0.. span at most two tile rows (32 < T): per slot
+                    // a pointer for each, p1 pre-shifted so p[t * T] works
+                    const uint32_t I0 = gi0 >> 7, split = T - (gi0 & (T - 1));
+                    const V* p0[WQ_SLOTS];
+                    const V* p1[WQ_SLOTS];
 #pragma unroll
-                            for (int s = 0; s < WQ_SLOTS; ++s) {
-                                const uint32_t gj = g2 + min(j0 + s * 32 + lane, B2 - 1);
-                                colbase[s] = tidx(cur_I, gj >> 7, nb) * TT + (gj & 127);
+                    for (int s = 0; s < WQ_SLOTS; ++s) {
+                        const uint32_t gj = g2 + min(j0 + s * 32 + lane, B2 - 1);
+                        const uint32_t Jt = gj >> 7;
+                        p0[s] = q.bg + tidx(I0, Jt, nb) * TT + uint64_t(gi0 & (T - 1)) * T + (gj & (T - 1));
+                        p1[s] = (I0 + 1 <= Jt) ? q.bg + tidx(I0 + 1, Jt, nb) * TT + (gj & (T - 1)) -
+                                                     uint64_t(split) * T
+                                               : p0[s];
+                    }
+                    for (uint32_t t0 = 0; t0 < ni; t0 += 4) {
+#pragma unroll
+                        for (uint32_t dt = 0; dt < 4; ++dt) {
+                            const uint32_t t = t0 + dt;
+                            const V r = __shfl_sync(0xffffffffu, rv, t & 31);
+                            if (t < ni) {
+#pragma unroll
+                                for (int s = 0; s < WQ_SLOTS; ++s)
+                                    if (uint32_t(s) < nslot)
+                                        acc[s] = Ops<V>::addmin(r, (t < split ? p0[s] : p1[s])[t * T], acc[s]);
                             }
                         }
-                        const uint32_t roff = (gi & 127) * T;
+                    }
+                } else {  // diagonal block: both triangles, generic lookup
+                    for (uint32_t t = 0; t < ni; ++t) {
+                        const V r = __shfl_sync(0xffffffffu, rv, t);
 #pragma unroll
                         for (int s = 0; s < WQ_SLOTS; ++s)
-                            if (s < nslot) acc[s] = Ops<V>::addmin(r, q.bg[colbase[s] + roff], acc[s]);
-                    } else {
-#pragma unroll
-                        for (int s = 0; s < WQ_SLOTS; ++s)
-                            if (s < nslot) {
+                            if (uint32_t(s) < nslot) {
                                 const uint32_t gj = g2 + min(j0 + s * 32 + lane, B2 - 1);
-                                acc[s] = Ops<V>::addmin(r, q.bg[sym_off(gi, gj, nb)], acc[s]);
+                                acc[s] = Ops<V>::addmin(r, q.bg[sym_off(gi0 + t, gj, nb)], acc[s]);
                             }
                     }
                 }
@@ -141,7 +158,7 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
 #pragma unroll
             for (int s = 0; s < WQ_SLOTS; ++s) {
                 const uint32_t j = j0 + s * 32 + lane;
-                if (s < nslot && j < B2) best = Ops<V>::addmin(acc[s], col2[j], best);
+                if (uint32_t(s) < nslot && j < B2) best = Ops<V>::addmin(acc[s], col2[j], best);
             }
         }
         best = warp_min<V>(best);

@@ -35,7 +35,11 @@ def main():
     ap.add_argument("--config", default="delaunay1m_k1024")
     ap.add_argument("--sizes", default="1e3,1e4,1e5,1e6,1e7,1e8")
     ap.add_argument("--min-time", type=float, default=0.25, help="seconds per measurement")
+    ap.add_argument("--kernel", choices=["auto", "warp", "grouped"], default="auto",
+                    help="force a query kernel (PSP_QUERY_KERNEL) instead of the density rule")
     args = ap.parse_args()
+    if args.kernel != "auto":
+        os.environ["PSP_QUERY_KERNEL"] = args.kernel
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -114,7 +118,8 @@ def main():
         if dist:
             dist.all_reduce(times, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = times.tolist()
-        dense = size >= 2.0 * o.k * (o.k + 1) / 2
+        dense = (size >= P.GROUP_MIN_DENSITY * o.k * (o.k + 1) / 2 if args.kernel == "auto"
+                 else args.kernel == "grouped")
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "batch_per_gpu": size,
                               "kernel": "query_grouped" if dense else "query_warp",
