@@ -1,0 +1,207 @@
+// engine_fw.cuh — contexts and the blocked Floyd-Warshall drivers (1 GPU and row-sharded over NCCL), value-kind selection.
+// Internal to libpsp_gpu.so (one translation unit: psp_gpu.cu includes the
+// engine headers in dependency order).
+#pragma once
+
+// --------------------------------------------------------------- ctx ----
+struct psp_gpu_ctx {
+    int device = 0;
+    int rank = 0, world = 1;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;  // world > 1 only
+};
+
+namespace {
+
+int g_attr_done[2] = {0, 0};
+template <class V> constexpr int P3_SMEM = 3 * TT * sizeof(V);  // A + 2 x B
+
+template <class V>
+void set_kernel_attrs() {
+    const int idx = std::is_same<V, float>::value ? 1 : 0;
+    if (g_attr_done[idx]) return;
+    const int smem = 2 * TT * sizeof(V);
+    CK(cudaFuncSetAttribute(fw_phase2<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(fw_phase3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_SMEM<V>));
+    g_attr_done[idx] = 1;
+}
+
+template <class V>
+void fill_arena(MatArena& a, cudaStream_t s, int sms) {
+    const uint64_t n = a.tile_elems;
+    const int blocks = int(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 32));
+    fill_value<V><<<std::max(blocks, 1), 256, 0, s>>>(a.tiles.as<V>(), n, Ops<V>::inf());
+    CK_LAUNCH();
+    if (a.nmat) {
+        set_diag_zero<V><<<a.nmat, 256, 0, s>>>(a.view<V>());
+        CK_LAUNCH();
+    }
+}
+
+// The blocked FW driver: 3 launches per k-block on one stream.
+template <class V>
+void run_fw(const MatArena& a, cudaStream_t s, int sms) {
+    if (a.nmat == 0 || a.nb_max == 0) return;
+    set_kernel_attrs<V>();
+    const MatSet<V> v = a.view<V>();
+    const int smem = 2 * TT * sizeof(V);
+    const uint64_t work = a.work_prefix[a.nmat];
+    const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
+    for (uint32_t kb = 0; kb < a.nb_max; ++kb) {
+        fw_phase1<V><<<a.nmat, NTHREADS, 0, s>>>(v, kb);
+        CK_LAUNCH();
+        if (a.nb_max > 1) {
+            fw_phase2<V><<<dim3(a.nmat, a.nb_max), NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+            fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
+            CK_LAUNCH();
+        }
+    }
+}
+
+#define NCK(x)                                                                         \
+    do {                                                                               \
+        ncclResult_t r_ = (x);                                                         \
+        if (r_ != ncclSuccess)                                                         \
+            throw Fail{PSP_ENCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)}; \
+    } while (0)
+
+template <class V> ncclDataType_t nccl_type();
+template <> ncclDataType_t nccl_type<uint32_t>() { return ncclUint32; }
+template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+
+// Row-sharded blocked FW of the boundary graph over ctx->world GPUs
+// (SURVEY §8e): tile row I is owned by rank I mod world. Per k-block the
+// owner closes the diagonal tile and broadcasts it; every rank updates the
+// panel tiles whose home row it owns (others contribute INF) and one
+// min-allreduce assembles the full row panel; phase 3 then touches owned rows
+// only. At the end every row is broadcast from its owner so each GPU holds
+// the complete table (queries stay replicated, no per-query traffic).
+template <class V>
+void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    const uint32_t nb = a.nb[0];
+    set_kernel_attrs<V>();
+    a.shard_rows(ctx->rank, ctx->world, s);
+    const MatSet<V> v = a.view<V>();
+    const int smem = 2 * TT * sizeof(V);
+    const uint64_t my_work = std::max<uint64_t>(1, a.nrows ? (a.nrows * uint64_t(nb)) : 1);
+    const int g3 = int(std::min<uint64_t>(my_work, uint64_t(ctx->sms)));
+    const ncclDataType_t dt = nccl_type<V>();
+    V* tiles = a.tiles.as<V>();
+    // PSP_FW_PROFILE=1: per-phase CUDA-event breakdown on stderr (diagnostics)
+    const bool prof = std::getenv("PSP_FW_PROFILE") != nullptr;
+    const char* dm = std::getenv("PSP_DIAG_MODE");
+    const bool diag_allreduce = dm && std::strcmp(dm, "allreduce") == 0;
+    cudaEvent_t ev[5];
+    double acc_ms[4] = {0, 0, 0, 0};
+    if (prof)
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (uint32_t kb = 0; kb < nb; ++kb) {
+        const int owner = int(kb % ctx->world);
+        V* diag = tiles + tidx(kb, kb, nb) * TT;
+        if (prof) CK(cudaEventRecord(ev[0], s));
+        if (owner == ctx->rank) {
+            fw_phase1<V><<<1, NTHREADS, 0, s>>>(v, kb);
+            CK_LAUNCH();
+        }
+        if (diag_allreduce) {
+            // owners contribute the closed tile, everyone else INF
+            if (owner != ctx->rank) fill_value<V><<<16, 256, 0, s>>>(diag, TT, Ops<V>::inf());
+            NCK(nccl().AllReduce(diag, diag, TT, dt, ncclMin, ctx->comm, s));
+        } else {
+            NCK(nccl().Broadcast(diag, diag, TT, dt, owner, ctx->comm, s));
+        }
+        if (prof) CK(cudaEventRecord(ev[1], s));
+        if (nb > 1) {
+            fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+            if (prof) CK(cudaEventRecord(ev[2], s));
+            NCK(nccl().AllReduce(a.panel.p, a.panel.p, uint64_t(nb) * TT, dt, ncclMin, ctx->comm, s));
+            if (prof) CK(cudaEventRecord(ev[3], s));
+            if (a.nrows) {
+                fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
+                CK_LAUNCH();
+            }
+            if (prof) {
+                CK(cudaEventRecord(ev[4], s));
+                CK(cudaEventSynchronize(ev[4]));
+                for (int i = 0; i < 4; ++i) {
+                    float t = 0;
+                    CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+                    acc_ms[i] += t;
+                }
+            }
+        }
+    }
+    if (prof) {
+        std::fprintf(stderr,
+                     "[psp] rank %d sharded FW nb=%u: phase1+bcast %.1f ms, phase2 %.1f ms, "
+                     "allreduce %.1f ms, phase3 %.1f ms\n",
+                     ctx->rank, nb, acc_ms[0], acc_ms[1], acc_ms[2], acc_ms[3]);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
+    const uint32_t batch = 64;
+    for (uint32_t I0 = 0; I0 < nb; I0 += batch) {
+        NCK(nccl().GroupStart());
+        for (uint32_t I = I0; I < std::min(nb, I0 + batch); ++I) {
+            V* row = tiles + tidx(I, I, nb) * TT;
+            NCK(nccl().Broadcast(row, row, uint64_t(nb - I) * TT, dt, int(I % ctx->world),
+                                 ctx->comm, s));
+        }
+        NCK(nccl().GroupEnd());
+    }
+}
+
+// Value kind selection: u32 when integral or dyadic weights keep
+// every finite distance below INF; f32 otherwise.
+struct Kind {
+    int kind;
+    int shift;
+};
+Kind choose_kind(int requested, const double* w, uint64_t m, uint64_t n) {
+    if (requested != PSP_VALUE_AUTO && requested != PSP_VALUE_U32 && requested != PSP_VALUE_F32)
+        throw ArgError("value_kind must be PSP_VALUE_AUTO, PSP_VALUE_U32 or PSP_VALUE_F32");
+    if (requested == PSP_VALUE_F32) return {PSP_VALUE_F32, 0};
+    double maxw = 0.0;
+    for (uint64_t e = 0; e < m; ++e) maxw = std::max(maxw, w[e]);
+    const double hops = n > 1 ? double(n - 1) : 1.0;
+    for (int q = 0; q <= 24; ++q) {
+        const double scale = std::ldexp(1.0, q);
+        if (maxw * scale * hops >= double(U32_INF)) break;
+        bool integral = true;
+        for (uint64_t e = 0; e < m && integral; ++e) {
+            const double x = w[e] * scale;
+            integral = std::floor(x) == x;
+        }
+        if (integral) return {PSP_VALUE_U32, q};
+    }
+    if (requested == PSP_VALUE_U32)
+        throw Fail{PSP_EOVERFLOW,
+                   "u32 distances are not exact for these weights (non-dyadic weights or "
+                   "max_w * 2^q * (n-1) >= 2^31-1)"};
+    return {PSP_VALUE_F32, 0};
+}
+
+template <class V>
+V to_value(double w, int shift) {
+    if (std::is_same<V, float>::value) return V(float(w));
+    return V(static_cast<uint32_t>(std::ldexp(w, shift)));
+}
+
+template <class V>
+void to_f64(const std::vector<V>& src, double* dst, double scale) {
+    for (size_t i = 0; i < src.size(); ++i) {
+        if (std::is_same<V, float>::value) {
+            dst[i] = double(src[i]);
+        } else {
+            const uint32_t v = static_cast<uint32_t>(src[i]);
+            dst[i] = v >= U32_INF ? HUGE_VAL : double(v) * scale;
+        }
+    }
+}
+
+}  // namespace
+

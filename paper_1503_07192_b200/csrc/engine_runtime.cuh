@@ -1,0 +1,173 @@
+// engine_runtime.cuh — error plumbing, device buffers, tile arenas.
+// Internal to libpsp_gpu.so (one translation unit: psp_gpu.cu includes the
+// engine headers in dependency order).
+#pragma once
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    psp_status st;
+    std::string msg;
+};
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? PSP_ENOMEM : PSP_ECUDA,       \
+                       std::string(#x) + ": " + cudaGetErrorString(e_)};               \
+    } while (0)
+#define CK_LAUNCH(what) CK(cudaGetLastError())
+
+template <typename F>
+psp_status guarded(F&& f) {
+    try {
+        f();
+        return PSP_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.st;
+    } catch (const GraphError& e) {
+        g_err = e.what();
+        return PSP_EGRAPH;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return PSP_EINVAL;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return PSP_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PSP_ECUDA;
+    }
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+}
+
+// ------------------------------------------------------ device buffers --
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    explicit DBuf(size_t n) { alloc(n); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void alloc(size_t n) {
+        reset();
+        if (n == 0) n = 16;
+        CK(cudaMalloc(&p, n));
+        bytes = n;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+DBuf upload(const std::vector<T>& h, cudaStream_t s) {
+    DBuf d(h.size() * sizeof(T));
+    if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+// A batch of symmetric tile-packed matrices (see minplus.cuh).
+struct MatArena {
+    uint32_t nmat = 0, nb_max = 0;
+    size_t vbytes = 4;
+    std::vector<uint32_t> nb;
+    std::vector<uint64_t> tile_base, panel_base, work_prefix;
+    uint64_t tile_elems = 0, panel_elems = 0;
+    DBuf tiles, panel, d_tile_base, d_panel_base, d_work_prefix, d_nb;
+    // row ownership for the multi-GPU boundary graph (nmat == 1)
+    uint32_t rank = 0, world = 1, nrows = 0;
+    DBuf d_rows, d_row_prefix;
+
+    void shard_rows(uint32_t r, uint32_t g, cudaStream_t s) {
+        rank = r;
+        world = g;
+        std::vector<uint32_t> rows;
+        std::vector<uint64_t> prefix(1, 0);
+        for (uint32_t I = r; I < nb[0]; I += g) {
+            rows.push_back(I);
+            prefix.push_back(prefix.back() + (nb[0] - I));
+        }
+        nrows = static_cast<uint32_t>(rows.size());
+        d_rows = upload(rows, s);
+        d_row_prefix = upload(prefix, s);
+    }
+
+    void create(const std::vector<uint64_t>& sizes, size_t value_bytes, bool with_panel,
+                cudaStream_t s) {
+        vbytes = value_bytes;
+        nmat = static_cast<uint32_t>(sizes.size());
+        nb.resize(nmat);
+        tile_base.resize(nmat);
+        panel_base.resize(nmat);
+        work_prefix.assign(nmat + 1, 0);
+        tile_elems = panel_elems = 0;
+        nb_max = 0;
+        for (uint32_t m = 0; m < nmat; ++m) {
+            nb[m] = static_cast<uint32_t>((sizes[m] + T - 1) / T);
+            nb_max = std::max(nb_max, nb[m]);
+            tile_base[m] = tile_elems;
+            panel_base[m] = panel_elems;
+            tile_elems += ntiles_upper(nb[m]) * TT;
+            panel_elems += uint64_t(nb[m]) * TT;
+            work_prefix[m + 1] = work_prefix[m] + ntiles_upper(nb[m]);
+        }
+        tiles.alloc(tile_elems * vbytes);
+        if (with_panel) panel.alloc(panel_elems * vbytes);
+        d_tile_base = upload(tile_base, s);
+        d_panel_base = upload(panel_base, s);
+        d_work_prefix = upload(work_prefix, s);
+        d_nb = upload(nb, s);
+    }
+    template <class V> MatSet<V> view() const {
+        MatSet<V> v;
+        v.tiles = tiles.as<V>();
+        v.panel = panel.as<V>();
+        v.tile_base = d_tile_base.as<uint64_t>();
+        v.panel_base = d_panel_base.as<uint64_t>();
+        v.work_prefix = d_work_prefix.as<uint64_t>();
+        v.nb = d_nb.as<uint32_t>();
+        v.nmat = nmat;
+        v.nb_max = nb_max;
+        v.rows = world > 1 ? d_rows.as<uint32_t>() : nullptr;
+        v.row_prefix = world > 1 ? d_row_prefix.as<uint64_t>() : nullptr;
+        v.nrows = world > 1 ? nrows : 0;
+        v.rank = rank;
+        v.world = world;
+        return v;
+    }
+    // relaxations the FW executes on the padded matrices: per k-block the
+    // diagonal tile, the nb-1 panel tiles and the upper tiles off row/col kb
+    uint64_t relaxations() const {
+        uint64_t r = 0;
+        for (uint32_t m = 0; m < nmat; ++m) r += ntiles_upper(nb[m]) * nb[m];
+        return r * uint64_t(T) * T * T;
+    }
+    size_t bytes() const { return tiles.bytes + panel.bytes; }
+};
+
+}  // namespace
+
