@@ -128,24 +128,34 @@ __device__ __forceinline__ void store_block_t(V* tile, const V (&acc)[8][8], int
 // acc[a][b] <- min_k A(row a, k) + sB[k][col b] over k in [0, T).
 // A_KMAJOR: sA[k][row] (the panel layout); otherwise sA[row][k].
 template <class V, bool A_KMAJOR>
+__device__ __forceinline__ void load_ab(const V* __restrict__ sA, const V* __restrict__ sB, int k,
+                                        int ty, int tx, V (&a)[8], V (&b)[8]) {
+    if (A_KMAJOR) {
+        ld4(sA + k * T + 4 * ty, &a[0]);
+        ld4(sA + k * T + 64 + 4 * ty, &a[4]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = sA[blk(ty, i) * T + k];
+    }
+    ld4(sB + k * T + 4 * tx, &b[0]);
+    ld4(sB + k * T + 64 + 4 * tx, &b[4]);
+}
+
+// k advances in pairs so each accumulator takes two relaxations per update
+// (Ops::addmin2: 2 x VIADDMNMX for u32, FADD x2 + FMNMX3 for f32).
+template <class V, bool A_KMAJOR>
 __device__ __forceinline__ void minplus_tile(const V* __restrict__ sA, const V* __restrict__ sB,
                                              V (&acc)[8][8], int ty, int tx) {
-#pragma unroll 2
-    for (int k = 0; k < T; ++k) {
-        V a[8], b[8];
-        if (A_KMAJOR) {
-            ld4(sA + k * T + 4 * ty, &a[0]);
-            ld4(sA + k * T + 64 + 4 * ty, &a[4]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = sA[blk(ty, i) * T + k];
-        }
-        ld4(sB + k * T + 4 * tx, &b[0]);
-        ld4(sB + k * T + 64 + 4 * tx, &b[4]);
+#pragma unroll 1
+    for (int k = 0; k < T; k += 2) {
+        V a0[8], b0[8], a1[8], b1[8];
+        load_ab<V, A_KMAJOR>(sA, sB, k, ty, tx, a0, b0);
+        load_ab<V, A_KMAJOR>(sA, sB, k + 1, ty, tx, a1, b1);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::addmin(a[i], b[j], acc[i][j]);
+            for (int j = 0; j < 8; ++j)
+                acc[i][j] = Ops<V>::addmin2(a0[i], b0[j], a1[i], b1[j], acc[i][j]);
     }
 }
 

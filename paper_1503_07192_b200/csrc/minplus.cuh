@@ -6,7 +6,8 @@
 //        (max_w * 2^q * (n - 1) < 2^31 - 1), so one add of two stored values
 //        never wraps either, and min() clamps anything >= INF back to <= INF.
 //        min(a + b, c) compiles to one VIADDMNMX.U32 on sm_100a.
-//   f32  tolerance path. INF = +inf; fminf(a + b, c) -> FADD + FMNMX.
+//   f32  tolerance path. INF = +inf; relaxations are paired so that two of
+//        them cost FADD + FADD + one 3-input FMNMX3 (addmin2).
 //
 // The reference skips unreachable rows explicitly
 // (src/shortest_paths.cpp:117, src/query.cpp:53); with these encodings the
@@ -29,6 +30,11 @@ template <> struct Ops<uint32_t> {
     static __device__ __forceinline__ uint32_t addmin(uint32_t a, uint32_t b, uint32_t c) {
         return min(a + b, c);
     }
+    // two relaxations of one accumulator: two VIADDMNMX
+    static __device__ __forceinline__ uint32_t addmin2(uint32_t a0, uint32_t b0, uint32_t a1,
+                                                       uint32_t b1, uint32_t c) {
+        return min(a1 + b1, min(a0 + b0, c));
+    }
     static __device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return min(a, b); }
     static __device__ __forceinline__ uint32_t from_bits(uint32_t u) { return u; }
     static __device__ __forceinline__ uint32_t to_bits(uint32_t v) { return v; }
@@ -41,6 +47,14 @@ template <> struct Ops<float> {
     static __host__ __device__ __forceinline__ float inf() { return __builtin_huge_valf(); }
     static __device__ __forceinline__ float addmin(float a, float b, float c) {
         return fminf(a + b, c);
+    }
+    // two relaxations of one accumulator: FADD x2 + one 3-input FMNMX3
+    // (1.5 instructions per relaxation instead of 2)
+    static __device__ __forceinline__ float addmin2(float a0, float b0, float a1, float b1,
+                                                    float c) {
+        float d;
+        asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(c), "f"(a0 + b0), "f"(a1 + b1));
+        return d;
     }
     static __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
     static __device__ __forceinline__ float from_bits(uint32_t u) { return __uint_as_float(u); }

@@ -301,10 +301,10 @@ __device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* _
 #pragma unroll
         for (int qq = 0; qq < 4 * NQ4; ++qq) {
             const uint4 u = *reinterpret_cast<const uint4*>(sA + qq * GA_STRIDE + k4);
-            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.x), b[0], acc[qq]);
-            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.y), b[1], acc[qq]);
-            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.z), b[2], acc[qq]);
-            acc[qq] = Ops<V>::addmin(Ops<V>::from_bits(u.w), b[3], acc[qq]);
+            acc[qq] = Ops<V>::addmin2(Ops<V>::from_bits(u.x), b[0], Ops<V>::from_bits(u.y), b[1],
+                                      acc[qq]);
+            acc[qq] = Ops<V>::addmin2(Ops<V>::from_bits(u.z), b[2], Ops<V>::from_bits(u.w), b[3],
+                                      acc[qq]);
         }
     }
 }

@@ -83,6 +83,8 @@ CONFIGS = {
     # GPU (components 70 GB + boundary graph 51 GB) and minimises FW work.
     "road4m_k512": dict(family="road", rows=2048, cols=2048, seed=7, k=512,
                         queries=10_000_000),
+    # mid-size road grid (f32 kernels at a scale that builds in seconds)
+    "road1m_k256": dict(family="road", rows=1024, cols=1024, seed=7, k=256, queries=1_000_000),
     # small road grid for tests
     "road64k_k64": dict(family="road", rows=256, cols=256, seed=7, k=64, queries=1_000_000),
 }
