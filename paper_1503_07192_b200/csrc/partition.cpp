@@ -17,13 +17,19 @@
 // What differs (speed only):
 //  * the 8 restarts are independent once their seed sets are drawn, so the
 //    seed draws run first (sequentially, they share the rng and the id
-//    shuffle) and the 8 grow/recenter/finalize chains run on a thread pool;
-//    the winner is the first minimum in (restart, round) order exactly as
-//    the reference's strict `<` scan picks it.
+//    shuffle); then the 8 grow/recenter chains run in parallel and all
+//    8 x 13 finalize calls (the expensive part, independent of each other
+//    because recentering reads the un-finalized growth) run as separate
+//    tasks on every host thread; the winner is the first minimum in
+//    (restart, round) order exactly as the reference's strict `<` scan
+//    picks it.
 //  * rebalance collects each oversized component's members from per-
 //    component buckets instead of rescanning all n vertices; the member
 //    order is fixed by the reference's total (hop desc, id asc) sort anyway.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <exception>
@@ -49,6 +55,38 @@ constexpr uint64_t kSeedCandidates = 8;   // (:18)
 
 // balance_cap (:191-194): ceil(1.1 n / k) in integers
 uint64_t cap_of(uint64_t n, uint32_t k) { return (11 * n + 10 * uint64_t(k) - 1) / (10 * uint64_t(k)); }
+
+// Run fn(i) for i in [0, count) on up to `workers` threads; the first
+// exception is rethrown after all threads join (cf. psp::parallel_for,
+// include/psp/parallel.hpp:15-47).
+template <typename Fn>
+void parallel_tasks(size_t count, unsigned workers, Fn&& fn) {
+    workers = std::max(1u, std::min<unsigned>(workers, unsigned(count)));
+    if (workers == 1) {
+        for (size_t i = 0; i < count; ++i) fn(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::exception_ptr err;
+    std::mutex mu;
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < workers; ++t)
+        pool.emplace_back([&] {
+            for (;;) {
+                const size_t i = next.fetch_add(1);
+                if (i >= count) return;
+                try {
+                    fn(i);
+                } catch (...) {
+                    std::lock_guard<std::mutex> lock(mu);
+                    if (!err) err = std::current_exception();
+                    return;
+                }
+            }
+        });
+    for (auto& t : pool) t.join();
+    if (err) std::rethrow_exception(err);
+}
 
 struct Part {
     const Csr& g;
@@ -275,6 +313,7 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     if (k > n) throw ArgError("partition_graph: k exceeds vertex count");
     Part P{g, k, cap_of(n, k)};
 
+    const auto t_start = std::chrono::steady_clock::now();
     // --- seed sets for all restarts, in the reference's rng order (:268-329)
     std::mt19937_64 rng(seed);
     std::vector<uint32_t> ids(n);
@@ -329,60 +368,60 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
         }
     }
 
-    // --- independent restart chains (:430-444)
-    struct Best {
-        uint64_t cost = std::numeric_limits<uint64_t>::max();
-        std::vector<uint32_t> assign;
+    // --- restart chains (:430-444), two parallel stages. finalize() never
+    // feeds back into the chain (recenter reads the un-finalized growth), so
+    //   stage 1: per restart, the cheap grow/recenter chain, keeping every
+    //            round's grown state (8 restarts in parallel);
+    //   stage 2: all 8 x 13 finalize() calls, independent tasks on every
+    //            host thread, costs only;
+    // then the reference's winner -- the first strict minimum in (restart,
+    // round) order -- is finalized once more to materialise its assignment.
+    if (std::getenv("PSP_PART_PROFILE"))
+        std::fprintf(stderr, "[partition] seeds %.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
+    constexpr int kRounds = kRecenterRounds + 1;
+    struct Grown {
+        std::vector<uint32_t> assign, hop;
     };
-    std::vector<Best> best(kRestarts);
-    auto chain = [&](int r) {
+    std::vector<std::vector<Grown>> grown(kRestarts, std::vector<Grown>(kRounds));
+    const unsigned pool = std::max(1u, threads);
+    const bool prof = std::getenv("PSP_PART_PROFILE") != nullptr;
+    auto t_mark = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[partition] %s %.3f s\n", what,
+                     std::chrono::duration<double>(now - t_mark).count());
+        t_mark = now;
+    };
+    parallel_tasks(kRestarts, std::min<unsigned>(pool, kRestarts), [&](size_t r) {
         std::vector<uint32_t> seeds = seed_sets[r];
-        std::vector<uint32_t> assign, hop, cand;
-        P.grow(seeds, assign, hop);
-        for (int round = 0;; ++round) {
-            const uint64_t cost = P.finalize(assign, hop, cand);
-            if (cost < best[r].cost) {
-                best[r].cost = cost;
-                best[r].assign = cand;
-            }
-            if (round == kRecenterRounds) break;
-            seeds = P.recenter(assign, seeds);
-            P.grow(seeds, assign, hop);
+        P.grow(seeds, grown[r][0].assign, grown[r][0].hop);
+        for (int round = 1; round < kRounds; ++round) {
+            seeds = P.recenter(grown[r][round - 1].assign, seeds);
+            P.grow(seeds, grown[r][round].assign, grown[r][round].hop);
         }
-    };
-    const unsigned nthreads = std::max(1u, std::min<unsigned>(threads, kRestarts));
-    if (nthreads == 1) {
-        for (int r = 0; r < kRestarts; ++r) chain(r);
-    } else {
-        std::atomic<int> next{0};
-        std::exception_ptr err;
-        std::mutex mu;
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < nthreads; ++t)
-            pool.emplace_back([&] {
-                for (;;) {
-                    const int r = next.fetch_add(1);
-                    if (r >= kRestarts) return;
-                    try {
-                        chain(r);
-                    } catch (...) {
-                        std::lock_guard<std::mutex> lock(mu);
-                        if (!err) err = std::current_exception();
-                        return;
-                    }
-                }
-            });
-        for (auto& t : pool) t.join();
-        if (err) std::rethrow_exception(err);
-    }
-    int win = 0;
-    for (int r = 1; r < kRestarts; ++r)
-        if (best[r].cost < best[win].cost) win = r;
+    });
+    lap("grow/recenter chains");
+    std::vector<uint64_t> cost(size_t(kRestarts) * kRounds);
+    parallel_tasks(cost.size(), pool, [&](size_t t) {
+        std::vector<uint32_t> cand;
+        const Grown& gr = grown[t / kRounds][t % kRounds];
+        cost[t] = P.finalize(gr.assign, gr.hop, cand);
+    });
+    lap("finalize tasks");
+    size_t win = 0;
+    for (size_t t = 1; t < cost.size(); ++t)
+        if (cost[t] < cost[win]) win = t;
+    std::vector<uint32_t> assignment;
+    const Grown& gw = grown[win / kRounds][win % kRounds];
+    P.finalize(gw.assign, gw.hop, assignment);
+    lap("winner");
     std::vector<uint64_t> sz(k, 0);
-    for (uint32_t c : best[win].assign) ++sz[c];
+    for (uint32_t c : assignment) ++sz[c];
     for (uint32_t c = 0; c < k; ++c)
         if (sz[c] > P.cap) throw std::logic_error("partition_graph: balance cap violated");
-    return std::move(best[win].assign);
+    return assignment;
 }
 
 }  // namespace pspg
