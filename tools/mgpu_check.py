@@ -40,6 +40,15 @@ def main():
     d = o.batch_query(z["q_v1"], z["q_v2"])
     ok &= bool(np.array_equal(d, z["q_dist"]))
 
+    # tiny boundary graphs: fewer tile rows than ranks (ranks with no rows)
+    for rows, cols, k in ((2, 3, 2), (8, 8, 4), (20, 20, 9)):
+        gt = P.generate_grid(rows, cols, (1, 9), rows)
+        ot = P.build_oracle(gt, k, 2, 0, ctx=ctx)
+        st = P.build_oracle(gt, k, 2, 0, ctx=solo)
+        for c in range(k):
+            ok &= bool(np.array_equal(ot.component_table(c), st.component_table(c)))
+            ok &= bool(np.array_equal(ot.boundary_rows(c), st.boundary_rows(c)))
+
     gd = graphs.delaunay(30_000, 3)
     od = P.build_oracle(gd, 173, 4, 0, ctx=ctx)
     os_ = P.build_oracle(gd, 173, 4, 0, ctx=solo)
