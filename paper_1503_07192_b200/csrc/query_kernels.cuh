@@ -277,11 +277,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// tidx(I, J, nb) = row_base(I, nb) + J
-__device__ __forceinline__ uint64_t row_base(uint32_t I, uint32_t nb) {
-    return uint64_t(I) * (2ull * nb - I + 1) / 2 - I;
-}
-
 // Shared staging per warp and chunk (GK = 16 rows):
 //   A [query][row]  : row1_q[k0 + kk], GK + 4 word rows (16-byte aligned, the
 //                     lane-per-query async fill is 4-way conflicted at most)
@@ -345,14 +340,9 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     const bool col_ok = j < B2;
     // 16-byte-aligned column superset of this task's 32 columns
     const uint32_t G0 = g2 + cg * 32, A0 = G0 & ~3u, shift = G0 - A0;
-    // this lane's B staging piece (lanes 0..26: 3 rows x 9 pieces of 4
-    // columns per instruction; lanes 27..31 idle): fixed for the task
-    const uint32_t lane_row = lane < 27 ? uint32_t(lane) / 9u : uint32_t(GK);  // >= GK: idle
-    const uint32_t piece = uint32_t(lane) % 9u;
-    const uint32_t piece_colg = A0 + 4 * piece;  // BG column of the piece
-    const uint32_t piece_J = piece_colg >> 7, piece_off = piece_colg & (T - 1);
-    const uint32_t piece_col = 4 * piece;        // staging column
-    const bool piece_ok = piece_J < nb;
+    const uint32_t Jlo = A0 >> 7;
+    // this lane's staging slots for B: e = t*32 + lane -> (row kk, chunk u)
+    // over the 32 x 9 chunks of 4 columns
     __syncwarp();
     const V* my_row1 = cb1;  // lane q: its query's row1 (16-byte aligned)
     if (uint32_t(lane) < m) {
@@ -374,29 +364,23 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
         }
         V* sb = st->b[buf];
         if (c1 != c2) {
-            // 9 lanes per block row (one 16-byte piece each), 3 rows per
-            // warp instruction; this lane's piece is fixed for the task
-            // (lane_row, piece address parts precomputed), the tile row is
-            // one of two warp-uniform bases per chunk
             const uint32_t gi0 = g1 + k0;
             const uint32_t I0 = gi0 >> 7, r0 = gi0 & (T - 1);
-            const V* base0 = q.bg + (row_base(I0, nb) + piece_J) * TT;
-            const V* base1 = q.bg + (row_base(I0 + 1, nb) + piece_J) * TT;
-            const bool ok0 = piece_ok && I0 <= piece_J;
-            const bool ok1 = piece_ok && I0 + 1 <= piece_J;
 #pragma unroll
-            for (int t = 0; t < (GK + 2) / 3; ++t) {
-                const uint32_t kk = 3 * t + lane_row;
-                if (kk < uint32_t(GK)) {
-                    const uint32_t r = r0 + kk;
-                    const bool hi = r >= uint32_t(T);
-                    V* dst = sb + kk * GB_STRIDE + piece_col;
-                    if (kk < rows && (hi ? ok1 : ok0)) {
-                        cp_async16(dst, (hi ? base1 : base0) + (r & (T - 1)) * T + piece_off, true);
-                    } else {
-                        const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
-                        st4(dst, inf4);
-                    }
+            for (int t = 0; t < (GK * 9 + 31) / 32; ++t) {
+                const uint32_t e = t * 32 + lane;
+                if (e >= uint32_t(GK * 9)) break;
+                const uint32_t kk = e / 9, u = e - kk * 9;
+                const uint32_t I = I0 + ((r0 + kk) >> 7);
+                const uint32_t col = A0 + 4 * u, J = col >> 7;
+                V* dst = sb + kk * GB_STRIDE + 4 * u;
+                if (kk < rows && I <= J && J < nb) {
+                    const V* src = q.bg + tidx(I, J, nb) * TT + uint64_t((r0 + kk) & (T - 1)) * T +
+                                   (col & (T - 1));
+                    cp_async16(dst, src, true);
+                } else {
+                    const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
+                    st4(dst, inf4);
                 }
             }
         } else {  // diagonal block (c1 == c2, 1/k of the pairs): generic lookup
@@ -410,6 +394,7 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
         }
         cp_async_commit();
     };
+    (void)Jlo;
 
     V acc[4 * NQ4];
 #pragma unroll
