@@ -340,3 +340,32 @@ def test_import_oracle_from_reference_tables(golden_small, name):
         assert np.array_equal(o.boundary_rows(c), case[f"bt{c}"])
     d, ops = o.batch_query(case["q_v1"], case["q_v2"], with_ops=True)
     assert np.array_equal(d, case["q_dist"]) and np.array_equal(ops, case["q_ops"])
+
+
+def test_edge_shapes():
+    # a single vertex, k = 1
+    o = P.build_oracle(P.Graph(1, [], [], []), 1, 1, 0)
+    assert o.query(0, 0) == (0.0, 0) and o.b == 0
+    # k = n: every vertex its own component (tests/test_partition.cpp:94-99)
+    g = P.generate_grid(4, 5, (1, 9), 2)
+    o = P.build_oracle(g, g.n, 2, 0)
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    v1, v2 = np.divmod(np.arange(g.n * g.n), g.n)
+    assert np.array_equal(o.batch_query(v1, v2), truth[v1, v2])
+    # caller-supplied partition with an empty component (make_partition
+    # allows it): component 1 owns nothing
+    g = P.generate_grid(6, 6, (1, 9), 5)
+    assign = np.where(np.arange(g.n) % 6 < 3, 0, 2).astype(np.uint32)
+    o = P.build_partitioned(g, 3, assign)
+    assert o.component_size(1) == 0
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    v1, v2 = np.divmod(np.arange(g.n * g.n), g.n)
+    for kernel in ("grouped", "warp"):
+        import os
+        os.environ["PSP_QUERY_KERNEL"] = kernel
+        try:
+            assert np.array_equal(o.batch_query(v1, v2), truth[v1, v2])
+        finally:
+            os.environ.pop("PSP_QUERY_KERNEL")
+    # empty batch
+    assert o.batch_query([], []).shape == (0,)
