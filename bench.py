@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 # banner off stdout unless the caller asked for NCCL logging
 os.environ.setdefault("NCCL_DEBUG", "WARN")
 
+FAMILY = {"grid": "grid", "delaunay": "Delaunay", "road": "road-like grid (f32 weights)"}
 METRIC = "distance queries/sec + preprocessing s (1M-vertex planar) at 1/2/4/8 B200 vs CPU"
 CONFIG = "delaunay262k_k256"
 BATCH = 1_000_000
@@ -323,6 +324,7 @@ def run_ours(args, rank, world, local):
     achieved_gbs = (tb / args.steps) / (per_launch_ms / 1e3) / 1e9
     peak_u32, clock_mhz = ctx.minplus_peak(P.VALUE_U32)
     k2_rate = st["k2_relaxations"] / (k2_ms / 1e3) if k2_ms else 0.0  # max over ranks
+    bg_gb = o.b * (o.b + 128) * 2 / 1e9
     line = {
         "metric": METRIC,
         "value": round(qps, 1),
@@ -335,11 +337,13 @@ def run_ours(args, rank, world, local):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u32" if o.value_kind == P.VALUE_U32 else "f32",
-        "data": "synthetic (seeded Delaunay + mt19937_64 pairs)",
-        "config": {"workload": f"{args.config}: Delaunay n={g.n} m={g.m} k={cfg['k']} b={o.b}, "
+        "data": f"synthetic (seeded {FAMILY[cfg['family']]} graph + mt19937_64 pairs)",
+        "config": {"workload": f"{args.config}: {FAMILY[cfg['family']]} n={g.n} m={g.m} k={cfg['k']} b={o.b}, "
                                f"{batch} random pairs per step per GPU",
-                   "batch_per_gpu": batch, "l2_policy": "inputs >> L2 (BG table "
-                   f"{o.b * (o.b + 128) * 2 / 1e9:.1f} GB symmetric u32), fresh pairs each step",
+                   "batch_per_gpu": batch, "l2_policy": (f"inputs >> L2 (boundary table {bg_gb:.1f} GB symmetric "
+                                 f"{'u32' if o.value_kind == P.VALUE_U32 else 'f32'}), fresh "
+                                 "pairs each step" if bg_gb > 0.126 else
+                                 f"small config: boundary table {bg_gb * 1e3:.1f} MB fits in L2"),
                    "parallelism": (f"boundary-graph FW row-sharded over {world} GPUs (NCCL "
                                    f"panel min-allreduce), queries sharded by rank, tables "
                                    f"replicated" if world > 1 else "1 GPU")},
@@ -420,8 +424,8 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Delaunay + mt19937_64 pairs)",
-        "config": {"workload": f"{args.config}: Delaunay n={g.n} k={cfg['k']} b={ro.b}, "
+        "data": f"synthetic (seeded {FAMILY[cfg['family']]} graph + mt19937_64 pairs)",
+        "config": {"workload": f"{args.config}: {FAMILY[cfg['family']]} n={g.n} k={cfg['k']} b={ro.b}, "
                                f"{sample} random pairs per step (bounded sample)"},
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": cores,
                          "kind": "reference",

@@ -15,22 +15,38 @@
 // (restart, round).
 //
 // What differs (speed only):
-//  * the 8 restarts are independent once their seed sets are drawn, so the
-//    seed draws run first (sequentially, they share the rng and the id
-//    shuffle); then the 8 grow/recenter chains run in parallel and all
-//    8 x 13 finalize calls (the expensive part, independent of each other
-//    because recentering reads the un-finalized growth) run as separate
-//    tasks on every host thread; the winner is the first minimum in
-//    (restart, round) order exactly as the reference's strict `<` scan
-//    picks it.
+//  * the 8 restarts are independent once their seed sets are drawn, and
+//    finalize() never feeds back into a chain (recentering reads the
+//    un-finalized growth), so the work runs as a dataflow on a task pool:
+//    the seed draws stay sequential (they share the rng and the id
+//    shuffle), each restart's grow/recenter chain starts as soon as its
+//    seeds exist, and each of the 8 x 13 grown states spawns its
+//    finalize() (the expensive part) on any free host thread; the winner
+//    is the first minimum in (restart, round) order exactly as the
+//    reference's strict `<` scan picks it.
+//  * all per-vertex state lives in a BFS-ordered relabelling of the graph
+//    (struct Local), so neighbourhoods are compact in memory; rules that
+//    depend on id order compare original ids, loops whose order matters
+//    still run in original id order, and grow/recenter evaluate their
+//    order-free closed forms (smallest-id claimant, smallest-id deepest
+//    vertex) instead of replaying the reference's sorted frontiers.
+//  * the seed draws' argmax keeps per-block maxima; refine keeps per-vertex
+//    foreign-neighbour counts (O(deg) per candidate move instead of
+//    O(deg^2)), walks the flagged vertices through a bitset and prefetches
+//    ahead of its random-order sweep.
 //  * rebalance collects each oversized component's members from per-
 //    component buckets instead of rescanning all n vertices; the member
 //    order is fixed by the reference's total (hop desc, id asc) sort anyway.
+// tools/part_bench.cpp times it without Python; tests/test_host.py checks
+// the assignments against the reference build, including scrambled ids.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <cstdint>
 #include <exception>
 #include <limits>
@@ -52,129 +68,300 @@ constexpr int kMaxRefineSweeps = 10;      // (:15)
 constexpr int kRecenterRounds = 12;       // (:16)
 constexpr int kRestarts = 8;              // (:17)
 constexpr uint64_t kSeedCandidates = 8;   // (:18)
+constexpr int kAhead = 16;                // refine's prefetch distance, in flagged vertices
 
 // balance_cap (:191-194): ceil(1.1 n / k) in integers
 uint64_t cap_of(uint64_t n, uint32_t k) { return (11 * n + 10 * uint64_t(k) - 1) / (10 * uint64_t(k)); }
 
-// Run fn(i) for i in [0, count) on up to `workers` threads; the first
-// exception is rethrown after all threads join (cf. psp::parallel_for,
-// include/psp/parallel.hpp:15-47).
-template <typename Fn>
-void parallel_tasks(size_t count, unsigned workers, Fn&& fn) {
-    workers = std::max(1u, std::min<unsigned>(workers, unsigned(count)));
-    if (workers == 1) {
-        for (size_t i = 0; i < count; ++i) fn(i);
-        return;
+// A small work pool for the partition dataflow (cf. psp::parallel_for,
+// include/psp/parallel.hpp:15-47, which the reference runs per phase):
+// `threads - 1` workers plus the thread that calls join(). High-priority
+// tasks run first. Tasks may push further tasks. The first exception stops
+// the pool (queued tasks are dropped) and is rethrown by join().
+class TaskPool {
+public:
+    explicit TaskPool(unsigned threads) {
+        for (unsigned t = 1; t < threads; ++t) pool_.emplace_back([this] { work(); });
     }
-    std::atomic<size_t> next{0};
-    std::exception_ptr err;
-    std::mutex mu;
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < workers; ++t)
-        pool.emplace_back([&] {
-            for (;;) {
-                const size_t i = next.fetch_add(1);
-                if (i >= count) return;
-                try {
-                    fn(i);
-                } catch (...) {
-                    std::lock_guard<std::mutex> lock(mu);
-                    if (!err) err = std::current_exception();
-                    return;
-                }
+    ~TaskPool() {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            closed_ = stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : pool_) t.join();
+    }
+    void push(bool high, std::function<void()> fn) {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            (high ? hi_ : lo_).push_back(std::move(fn));
+            ++pending_;
+        }
+        cv_.notify_one();
+    }
+    void join() {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            closed_ = true;
+        }
+        cv_.notify_all();
+        work();
+        for (auto& t : pool_) t.join();
+        pool_.clear();
+        if (err_) std::rethrow_exception(err_);
+    }
+
+private:
+    void work() {
+        std::unique_lock<std::mutex> lock(mu_);
+        for (;;) {
+            cv_.wait(lock, [&] { return stop_ || !hi_.empty() || !lo_.empty() || (closed_ && pending_ == 0); });
+            if (stop_ || (hi_.empty() && lo_.empty())) return;
+            auto& q = hi_.empty() ? lo_ : hi_;
+            std::function<void()> fn = std::move(q.front());
+            q.pop_front();
+            lock.unlock();
+            try {
+                fn();
+            } catch (...) {
+                lock.lock();
+                if (!err_) err_ = std::current_exception();
+                stop_ = true;
+                pending_ -= 1 + hi_.size() + lo_.size();
+                hi_.clear();
+                lo_.clear();
+                cv_.notify_all();
+                return;
             }
-        });
-    for (auto& t : pool) t.join();
-    if (err) std::rethrow_exception(err);
+            lock.lock();
+            if (--pending_ == 0) cv_.notify_all();
+        }
+    }
+
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> hi_, lo_;
+    size_t pending_ = 0;
+    bool closed_ = false, stop_ = false;
+    std::exception_ptr err_;
+    std::vector<std::thread> pool_;
+};
+
+// The graph relabelled in BFS order (every connected piece, pieces in id
+// order of their first vertex). Vertex ids in the reference's inputs need
+// carry no locality -- a Delaunay mesh of random points scatters every
+// neighbourhood over the whole id range -- so every pass below is bound by
+// cache misses on the original numbering. All per-vertex state lives at
+// `pos[v]`; every comparison the reference makes on vertex ids is made on
+// `id[u]`, the original id, and every loop whose order matters still runs
+// in original id order (u = pos[v] for v = 0, 1, ...).
+struct Local {
+    uint64_t n = 0;
+    std::vector<uint32_t> pos, id;  // original -> local, local -> original
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> to;
+
+    explicit Local(const Csr& g) : n(g.n), pos(g.n), id(g.n), off(g.n + 1), to(g.to.size()) {
+        std::vector<uint8_t> seen(n, 0);
+        uint64_t tail = 0;
+        for (uint64_t r = 0; r < n; ++r) {
+            if (seen[r]) continue;
+            seen[r] = 1;
+            uint64_t head = tail;
+            id[tail++] = static_cast<uint32_t>(r);
+            for (; head < tail; ++head) {
+                const uint32_t u = id[head];
+                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e)
+                    if (!seen[g.to[e]]) {
+                        seen[g.to[e]] = 1;
+                        id[tail++] = g.to[e];
+                    }
+            }
+        }
+        for (uint64_t i = 0; i < n; ++i) pos[id[i]] = static_cast<uint32_t>(i);
+        off[0] = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t u = id[i];
+            uint64_t o = off[i];
+            for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) to[o++] = pos[g.to[e]];
+            off[i + 1] = o;
+        }
+    }
+    uint64_t begin(uint32_t u) const { return off[u]; }
+    uint64_t end(uint32_t u) const { return off[u + 1]; }
+};
+
+// compute_boundary (:196-212) on local storage
+std::vector<uint8_t> local_boundary(const Local& g, const std::vector<uint32_t>& a) {
+    std::vector<uint8_t> flags(g.n, 0);
+    for (uint64_t u = 0; u < g.n; ++u)
+        for (uint64_t e = g.begin(u); e < g.end(u); ++e)
+            if (a[g.to[e]] != a[u]) {
+                flags[u] = 1;
+                break;
+            }
+    return flags;
 }
 
+// The seed draws' hop-count distances (relax_seed_dist, :272-284). After
+// relax_from(s) every vertex holds min(old, hop(s, v)) whatever order the
+// FIFO visits neighbours in (a vertex improves only if every vertex on a
+// shortest path from s to it does), so the relabelling cannot change them.
+// farthest_seeds' argmax (the first maximum in id order, :320-324) comes
+// from per-block maxima that a relax only dirties where it changed one.
+class SeedSpace {
+public:
+    explicit SeedSpace(const Local& g) : g_(g), dist_(g.n) {
+        nblk_ = (g.n + kBlock - 1) / kBlock;
+        barg_.resize(nblk_);
+        dirty_.assign(nblk_, 0);
+    }
+    void reset() {
+        std::fill(dist_.begin(), dist_.end(), kNone);
+        std::fill(dirty_.begin(), dirty_.end(), 1);
+        dirty_list_.resize(nblk_);
+        std::iota(dirty_list_.begin(), dirty_list_.end(), 0u);
+    }
+    uint32_t dist_of(uint32_t v) const { return dist_[g_.pos[v]]; }
+    void relax_from(uint32_t v) {
+        const uint32_t s = g_.pos[v];
+        set(s, 0);
+        q_.assign(1, s);
+        for (size_t head = 0; head < q_.size(); ++head) {
+            const uint32_t u = q_[head];
+            const uint32_t du = dist_[u] + 1;
+            for (uint64_t e = g_.begin(u); e < g_.end(u); ++e) {
+                const uint32_t x = g_.to[e];
+                if (dist_[x] > du) {
+                    set(x, du);
+                    q_.push_back(x);
+                }
+            }
+        }
+    }
+    uint32_t farthest() {
+        for (uint32_t b : dirty_list_) {
+            const uint64_t lo = uint64_t(b) * kBlock, hi = std::min<uint64_t>(lo + kBlock, g_.n);
+            uint32_t best = static_cast<uint32_t>(lo);
+            for (uint64_t i = lo + 1; i < hi; ++i)
+                if (better(static_cast<uint32_t>(i), best)) best = static_cast<uint32_t>(i);
+            barg_[b] = best;
+            dirty_[b] = 0;
+        }
+        dirty_list_.clear();
+        uint32_t best = barg_[0];
+        for (uint64_t b = 1; b < nblk_; ++b)
+            if (better(barg_[b], best)) best = barg_[b];
+        return g_.id[best];
+    }
+
+private:
+    static constexpr uint64_t kBlock = 256;
+    bool better(uint32_t a, uint32_t b) const {
+        return dist_[a] > dist_[b] || (dist_[a] == dist_[b] && g_.id[a] < g_.id[b]);
+    }
+    void set(uint32_t x, uint32_t d) {
+        dist_[x] = d;
+        const uint32_t b = static_cast<uint32_t>(x / kBlock);
+        if (!dirty_[b]) {
+            dirty_[b] = 1;
+            dirty_list_.push_back(b);
+        }
+    }
+    const Local& g_;
+    uint64_t nblk_ = 0;
+    std::vector<uint32_t> dist_, q_, barg_, dirty_list_;
+    std::vector<uint8_t> dirty_;
+};
+
+// The restart chain and finalize on local storage: `assign` and `hop` are
+// indexed by local position, seeds are original ids.
 struct Part {
-    const Csr& g;
+    const Local& g;
     uint32_t k;
     uint64_t cap;
 
-    // is_boundary_with_move (:22-31): u's boundary status with `moved`
-    // placed in component `to`.
-    bool boundary_if(const std::vector<uint32_t>& a, uint32_t u, uint32_t moved, uint32_t to) const {
-        const uint32_t cu = (u == moved) ? to : a[u];
-        for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
-            const uint32_t x = g.to[e];
-            if (((x == moved) ? to : a[x]) != cu) return true;
-        }
-        return false;
-    }
-
-    // voronoi_grow (:40-72)
+    // voronoi_grow (:40-72). The reference visits the frontier in id order
+    // and lets the first visitor claim, so x goes to the component of its
+    // smallest-id frontier neighbour; that rule is order-free and is what
+    // is evaluated here, in local order.
     void grow(const std::vector<uint32_t>& seeds, std::vector<uint32_t>& assign,
               std::vector<uint32_t>& hop) const {
         const uint64_t n = g.n;
         assign.assign(n, kNone);
         hop.assign(n, kNone);
-        std::vector<uint32_t> frontier, next, claimed(n, kNone);
+        std::vector<uint32_t> frontier, next, claim(n, kNone);
         for (uint32_t c = 0; c < seeds.size(); ++c) {
-            assign[seeds[c]] = c;
-            hop[seeds[c]] = 0;
-            frontier.push_back(seeds[c]);
+            const uint32_t u = g.pos[seeds[c]];
+            assign[u] = c;  // a repeated seed keeps its last component, as in the reference
+            hop[u] = 0;
+            frontier.push_back(u);
         }
-        std::sort(frontier.begin(), frontier.end());
         uint32_t round = 0;
         while (!frontier.empty()) {
             ++round;
             next.clear();
             for (uint32_t u : frontier)
-                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
                     const uint32_t x = g.to[e];
-                    if (assign[x] != kNone || claimed[x] != kNone) continue;
-                    claimed[x] = assign[u];
-                    next.push_back(x);
+                    if (assign[x] != kNone) continue;
+                    if (claim[x] == kNone) {
+                        claim[x] = u;
+                        next.push_back(x);
+                    } else if (g.id[u] < g.id[claim[x]]) {
+                        claim[x] = u;
+                    }
                 }
-            for (uint32_t v : next) {
-                assign[v] = claimed[v];
-                hop[v] = round;
+            for (uint32_t x : next) {
+                assign[x] = assign[claim[x]];
+                hop[x] = round;
             }
-            std::sort(next.begin(), next.end());
             frontier.swap(next);
         }
     }
 
-    // recenter (:77-119)
+    // recenter (:77-119): per component, the smallest-id vertex of the
+    // deepest BFS round from the component's boundary (round 0 = the
+    // smallest-id boundary vertex), again an order-free rule.
     std::vector<uint32_t> recenter(const std::vector<uint32_t>& a,
                                    const std::vector<uint32_t>& old) const {
         const uint64_t n = g.n;
         std::vector<uint32_t> seeds(old);
-        const std::vector<uint8_t> flags = compute_boundary(g, a);
+        const std::vector<uint8_t> flags = local_boundary(g, a);
         std::vector<uint32_t> best_hop(seeds.size(), 0), best(seeds.size(), kNone);
         std::vector<uint8_t> visited(n, 0);
         std::vector<uint32_t> frontier, next;
-        for (uint64_t v = 0; v < n; ++v)
-            if (flags[v]) {
-                visited[v] = 1;
-                frontier.push_back(static_cast<uint32_t>(v));
-                if (best[a[v]] == kNone) best[a[v]] = static_cast<uint32_t>(v);
+        for (uint64_t u = 0; u < n; ++u)
+            if (flags[u]) {
+                visited[u] = 1;
+                frontier.push_back(static_cast<uint32_t>(u));
+                const uint32_t c = a[u];
+                if (best[c] == kNone || g.id[u] < g.id[best[c]]) best[c] = static_cast<uint32_t>(u);
             }
         uint32_t round = 0;
         while (!frontier.empty()) {
             ++round;
             next.clear();
             for (uint32_t u : frontier)
-                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
                     const uint32_t x = g.to[e];
                     if (visited[x] || a[x] != a[u]) continue;
                     visited[x] = 1;
                     next.push_back(x);
                 }
-            std::sort(next.begin(), next.end());
-            for (uint32_t v : next) {
-                const uint32_t c = a[v];
+            for (uint32_t x : next) {
+                const uint32_t c = a[x];
                 if (round > best_hop[c]) {
                     best_hop[c] = round;
-                    best[c] = v;
+                    best[c] = x;
+                } else if (g.id[x] < g.id[best[c]]) {
+                    best[c] = x;
                 }
             }
             frontier.swap(next);
         }
         for (uint32_t c = 0; c < seeds.size(); ++c)
-            if (best[c] != kNone) seeds[c] = best[c];
+            if (best[c] != kNone) seeds[c] = g.id[best[c]];
         return seeds;
     }
 
@@ -196,23 +383,23 @@ struct Part {
         // members of c when c is processed = its vertices at entry plus
         // those moved into it while earlier components were trimmed
         std::vector<std::vector<uint32_t>> bucket(k);
-        for (uint64_t v = 0; v < n; ++v)
-            if (size[a[v]] > cap) bucket[a[v]].push_back(static_cast<uint32_t>(v));
+        for (uint64_t u = 0; u < n; ++u)
+            if (size[a[u]] > cap) bucket[a[u]].push_back(static_cast<uint32_t>(u));
         std::vector<std::vector<uint32_t>> moved_in(k);
         std::vector<uint32_t> members;
         for (uint32_t c = 0; c < k; ++c) {
             if (size[c] <= cap) continue;
             members.clear();
-            for (uint32_t v : bucket[c]) if (a[v] == c) members.push_back(v);
-            for (uint32_t v : moved_in[c]) if (a[v] == c) members.push_back(v);
+            for (uint32_t u : bucket[c]) if (a[u] == c) members.push_back(u);
+            for (uint32_t u : moved_in[c]) if (a[u] == c) members.push_back(u);
             std::sort(members.begin(), members.end(), [&](uint32_t x, uint32_t y) {
                 if (hop[x] != hop[y]) return hop[x] > hop[y];
-                return x < y;
+                return g.id[x] < g.id[y];
             });
-            for (uint32_t v : members) {
+            for (uint32_t u : members) {
                 if (size[c] <= cap) break;
                 uint32_t target = kNone;
-                for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
                     const uint32_t t = a[g.to[e]];
                     if (t == c || t == kNone || size[t] + 1 > cap) continue;
                     if (target == kNone || size[t] < size[target] ||
@@ -220,42 +407,129 @@ struct Part {
                         target = t;
                 }
                 if (target == kNone) target = smallest_with_room(c);
-                a[v] = target;
+                a[u] = target;
                 --size[c];
                 ++size[target];
-                if (target > c) moved_in[target].push_back(v);
+                if (target > c) moved_in[target].push_back(u);
             }
         }
     }
 
-    // the refine lambda (:334-387)
+    // the refine lambda (:334-387), sweeping in original id order. The
+    // reference re-derives every boundary flag it needs from scratch
+    // (is_boundary_with_move, O(deg) per vertex, so O(deg^2) per candidate
+    // move). Here each vertex keeps the number of its neighbours in other
+    // components, `foreign`, with flags[x] == (foreign[x] > 0) at all times.
+    // On a simple graph (build_csr rejects loops and duplicates) moving v
+    // from `from` to `to` changes a neighbour x's count by
+    // [a[x] != to] - [a[x] != from], and v's own count becomes
+    // deg(v) - #(neighbours in `to`), so a candidate's delta costs O(deg)
+    // and the decisions -- same sweep order, same target order, same strict
+    // `<` -- are the reference's.
     void refine(std::vector<uint32_t>& a, std::vector<uint64_t>& size,
                 std::vector<uint8_t>& flags) const {
         const uint64_t n = g.n;
+        std::vector<uint32_t> foreign(n, 0);
+        for (uint64_t u = 0; u < n; ++u) {
+            if (!flags[u]) continue;
+            uint32_t f = 0;
+            for (uint64_t e = g.begin(u); e < g.end(u); ++e) f += a[g.to[e]] != a[u];
+            foreign[u] = f;
+        }
+        // flags mirrored as a bitset in original id order, so a sweep skips
+        // interior vertices 64 at a time instead of touching each one
+        const uint64_t nw = (n + 63) / 64;
+        std::vector<uint64_t> bits(nw, 0);
+        for (uint64_t u = 0; u < n; ++u)
+            if (flags[u]) bits[g.id[u] >> 6] |= uint64_t(1) << (g.id[u] & 63);
+        auto set_flag = [&](uint32_t x, bool on) {
+            flags[x] = on ? 1 : 0;
+            const uint64_t bit = uint64_t(1) << (g.id[x] & 63);
+            if (on) bits[g.id[x] >> 6] |= bit;
+            else bits[g.id[x] >> 6] &= ~bit;
+        };
+        // next flagged original id >= v (forward) / <= v (backward), or n;
+        // re-read every time: a move may flag or clear vertices ahead
+        auto next_fwd = [&](uint64_t v) -> uint64_t {
+            if (v >= n) return n;
+            uint64_t w = v >> 6, word = bits[w] & (~uint64_t(0) << (v & 63));
+            while (!word) {
+                if (++w == nw) return n;
+                word = bits[w];
+            }
+            return (w << 6) + __builtin_ctzll(word);
+        };
+        auto next_bwd = [&](uint64_t v) -> uint64_t {  // v < n, or n for "none"
+            if (v >= n) return n;
+            uint64_t w = v >> 6, word = bits[w] & (~uint64_t(0) >> (63 - (v & 63)));
+            while (!word) {
+                if (w-- == 0) return n;
+                word = bits[w];
+            }
+            return (w << 6) + 63 - __builtin_clzll(word);
+        };
         std::vector<uint32_t> targets;
         for (int sweep = 0; sweep < kMaxRefineSweeps; ++sweep) {
             bool improved = false;
-            for (uint64_t step = 0; step < n; ++step) {
-                const uint32_t v = static_cast<uint32_t>((sweep % 2 == 0) ? step : n - 1 - step);
-                if (!flags[v]) continue;
+            const bool fwd = sweep % 2 == 0;
+            auto advance = [&](uint64_t ov) {  // next flagged id after ov in sweep order
+                return fwd ? next_fwd(ov + 1) : (ov == 0 ? n : next_bwd(ov - 1));
+            };
+            const uint64_t first = fwd ? next_fwd(0) : next_bwd(n - 1);
+            // Software prefetch: the sweep visits vertices in id order, which
+            // is random in memory, so it is latency-bound. Three cursors run
+            // ahead through the current flags (a hint only: flags may change
+            // before the sweep gets there) and pull in, in dependency order,
+            // a vertex's state, its adjacency slice and its neighbours' state.
+            uint64_t p1 = first, p2 = first, p3 = first;
+            for (int i = 0; i < kAhead && p1 < n; ++i) p1 = advance(p1);
+            for (int i = 0; i < kAhead / 2 && p2 < n; ++i) p2 = advance(p2);
+            for (int i = 0; i < kAhead / 4 && p3 < n; ++i) p3 = advance(p3);
+            for (uint64_t ov = first; ov < n; ov = advance(ov)) {
+                if (p1 < n) {
+                    const uint32_t u = g.pos[p1];
+                    __builtin_prefetch(&g.off[u]);
+                    __builtin_prefetch(&a[u]);
+                    __builtin_prefetch(&foreign[u]);
+                    p1 = advance(p1);
+                }
+                if (p2 < n) {
+                    __builtin_prefetch(&g.to[g.off[g.pos[p2]]]);
+                    p2 = advance(p2);
+                }
+                if (p3 < n) {
+                    const uint32_t u = g.pos[p3];
+                    for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
+                        __builtin_prefetch(&a[g.to[e]]);
+                        __builtin_prefetch(&foreign[g.to[e]]);
+                    }
+                    p3 = advance(p3);
+                }
+                const uint32_t v = g.pos[ov];
                 const uint32_t from = a[v];
                 if (size[from] <= 1) continue;
                 targets.clear();
-                for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                for (uint64_t e = g.begin(v); e < g.end(v); ++e) {
                     const uint32_t c = a[g.to[e]];
                     if (c != from && std::find(targets.begin(), targets.end(), c) == targets.end())
                         targets.push_back(c);
                 }
                 std::sort(targets.begin(), targets.end());
+                const uint32_t deg = static_cast<uint32_t>(g.end(v) - g.begin(v));
                 int best_delta = 0;
                 uint32_t best_to = kNone;
                 for (uint32_t to : targets) {
                     if (size[to] + 1 > cap) continue;
-                    int delta = (boundary_if(a, v, v, to) ? 1 : 0) - (flags[v] ? 1 : 0);
-                    for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                    uint32_t same = 0;  // neighbours of v already in `to`
+                    int delta = -1;     // flags[v] is set
+                    for (uint64_t e = g.begin(v); e < g.end(v); ++e) {
                         const uint32_t x = g.to[e];
-                        delta += (boundary_if(a, x, v, to) ? 1 : 0) - (flags[x] ? 1 : 0);
+                        const uint32_t ax = a[x];
+                        same += ax == to;
+                        const uint32_t after = foreign[x] + (ax != to) - (ax != from);
+                        delta += (after > 0 ? 1 : 0) - (foreign[x] > 0 ? 1 : 0);
                     }
+                    delta += same != deg ? 1 : 0;
                     if (delta < best_delta) {
                         best_delta = delta;
                         best_to = to;
@@ -265,11 +539,16 @@ struct Part {
                     a[v] = best_to;
                     --size[from];
                     ++size[best_to];
-                    flags[v] = boundary_if(a, v, v, best_to) ? 1 : 0;
-                    for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) {
+                    uint32_t f = 0;
+                    for (uint64_t e = g.begin(v); e < g.end(v); ++e) {
                         const uint32_t x = g.to[e];
-                        flags[x] = boundary_if(a, x, v, best_to) ? 1 : 0;
+                        const uint32_t ax = a[x];
+                        f += ax != best_to;
+                        foreign[x] = foreign[x] + (ax != best_to) - (ax != from);
+                        set_flag(x, foreign[x] > 0);
                     }
+                    foreign[v] = f;
+                    set_flag(v, f > 0);
                     improved = true;
                 }
             }
@@ -277,30 +556,35 @@ struct Part {
         }
     }
 
-    // the finalize lambda (:393-420); returns the candidate's cost
+    // the finalize lambda (:393-420); returns the candidate's cost and,
+    // when `out` is given, the assignment in original id order
     uint64_t finalize(std::vector<uint32_t> assign, const std::vector<uint32_t>& hop,
-                      std::vector<uint32_t>& out) const {
+                      std::vector<uint32_t>* out) const {
         const uint64_t n = g.n;
         std::vector<uint64_t> sz(k, 0);
-        for (uint64_t v = 0; v < n; ++v)
-            if (assign[v] != kNone) ++sz[assign[v]];
+        for (uint64_t u = 0; u < n; ++u)
+            if (assign[u] != kNone) ++sz[assign[u]];
         for (uint64_t v = 0; v < n; ++v) {
-            if (assign[v] != kNone) continue;
+            const uint32_t u = g.pos[v];
+            if (assign[u] != kNone) continue;
             uint32_t best = kNone;
             for (uint32_t c = 0; c < k; ++c)
                 if (sz[c] < cap && (best == kNone || sz[c] < sz[best])) best = c;
-            assign[v] = best;
+            assign[u] = best;
             ++sz[best];
         }
         rebalance(assign, hop, sz);
-        std::vector<uint8_t> flags = compute_boundary(g, assign);
+        std::vector<uint8_t> flags = local_boundary(g, assign);
         refine(assign, sz, flags);
         std::vector<uint64_t> bsz(k, 0);
-        for (uint64_t v = 0; v < n; ++v)
-            if (flags[v]) ++bsz[assign[v]];
+        for (uint64_t u = 0; u < n; ++u)
+            if (flags[u]) ++bsz[assign[u]];
         uint64_t cost = 0;
         for (uint32_t c = 0; c < k; ++c) cost += bsz[c] * bsz[c];
-        out = std::move(assign);
+        if (out) {
+            out->resize(n);
+            for (uint64_t v = 0; v < n; ++v) (*out)[v] = assign[g.pos[v]];
+        }
         return cost;
     }
 };
@@ -311,46 +595,73 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     const uint64_t n = g.n;
     if (k < 1) throw ArgError("partition_graph: k must be at least 1");
     if (k > n) throw ArgError("partition_graph: k exceeds vertex count");
-    Part P{g, k, cap_of(n, k)};
-
     const auto t_start = std::chrono::steady_clock::now();
+    const Local L(g);
+    Part P{L, k, cap_of(n, k)};
+
     // --- seed sets for all restarts, in the reference's rng order (:268-329)
     std::mt19937_64 rng(seed);
     std::vector<uint32_t> ids(n);
     std::iota(ids.begin(), ids.end(), 0u);
-    std::vector<uint32_t> dist(n);
-    std::vector<uint32_t> q;
-    auto relax_from = [&](uint32_t s) {  // relax_seed_dist (:272-284)
-        dist[s] = 0;
-        q.assign(1, s);
-        for (size_t head = 0; head < q.size(); ++head) {
-            const uint32_t u = q[head];
-            for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
-                const uint32_t x = g.to[e];
-                if (dist[x] > dist[u] + 1) {
-                    dist[x] = dist[u] + 1;
-                    q.push_back(x);
-                }
-            }
-        }
+    SeedSpace S(L);
+    if (std::getenv("PSP_PART_PROFILE"))
+        std::fprintf(stderr, "[partition] relabelled graph %.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
+    // --- restart chains (:430-444) as a dataflow. finalize() never feeds
+    // back into the chain (recenter reads the un-finalized growth), and
+    // the seed draws only feed their own restart, so
+    //   * restart r's grow/recenter chain starts as soon as its seed set is
+    //     drawn (the draws stay sequential on this thread: they share the
+    //     rng and the id shuffle);
+    //   * every grown (restart, round) state immediately spawns its
+    //     finalize(), costs only, on whichever pool thread is free (chain
+    //     steps first: they are the critical path);
+    // then the reference's winner -- the first strict minimum in (restart,
+    // round) order -- is finalized once more to materialise its assignment.
+    constexpr int kRounds = kRecenterRounds + 1;
+    struct Grown {
+        std::vector<uint32_t> assign, hop;
     };
     std::vector<std::vector<uint32_t>> seed_sets(kRestarts, std::vector<uint32_t>(k));
+    std::vector<std::vector<Grown>> grown(kRestarts, std::vector<Grown>(kRounds));
+    std::vector<uint64_t> cost(size_t(kRestarts) * kRounds);
+    const bool prof = std::getenv("PSP_PART_PROFILE") != nullptr;
+    auto lap = [&](const char* what) {
+        if (prof)
+            std::fprintf(stderr, "[partition] %s %.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start)
+                             .count());
+    };
+    std::function<void(int, int)> chain_step;  // outlives the pool (running tasks call it)
+    TaskPool tasks(std::max(1u, threads));
+    chain_step = [&](int r, int round) {
+        if (round == 0) {
+            P.grow(seed_sets[r], grown[r][0].assign, grown[r][0].hop);
+        } else {
+            seed_sets[r] = P.recenter(grown[r][round - 1].assign, seed_sets[r]);
+            P.grow(seed_sets[r], grown[r][round].assign, grown[r][round].hop);
+        }
+        tasks.push(false, [&, r, round] {
+            const Grown& gr = grown[r][round];
+            cost[size_t(r) * kRounds + round] = P.finalize(gr.assign, gr.hop, nullptr);
+        });
+        if (round + 1 < kRounds) tasks.push(true, [&, r, round] { chain_step(r, round + 1); });
+    };
     {  // farthest_seeds (:315-329)
         auto& s = seed_sets[0];
-        std::fill(dist.begin(), dist.end(), kNone);
+        S.reset();
         s[0] = static_cast<uint32_t>(rng() % n);
-        relax_from(s[0]);
+        S.relax_from(s[0]);
         for (uint32_t c = 1; c < k; ++c) {
-            uint32_t pick = 0;
-            for (uint32_t v = 1; v < n; ++v)
-                if (dist[v] > dist[pick]) pick = v;
-            s[c] = pick;
-            relax_from(pick);
+            s[c] = S.farthest();
+            S.relax_from(s[c]);
         }
     }
+    lap("farthest seeds");
+    tasks.push(true, [&] { chain_step(0, 0); });
     for (int r = 1; r < kRestarts; ++r) {  // draw_seeds (:285-306)
-        auto& s = seed_sets[r];
-        std::fill(dist.begin(), dist.end(), kNone);
+        std::vector<uint32_t> s(k);
+        S.reset();
         for (uint32_t c = 0; c < k; ++c) {
             const uint64_t m = std::min<uint64_t>(kSeedCandidates, n - c);
             for (uint64_t t = 0; t < m; ++t) {
@@ -360,63 +671,26 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
             uint64_t best = c;
             for (uint64_t t = 1; t < m; ++t) {
                 const uint32_t cand = ids[c + t], cur = ids[best];
-                if (dist[cand] > dist[cur] || (dist[cand] == dist[cur] && cand < cur)) best = c + t;
+                const uint32_t dc = S.dist_of(cand), du = S.dist_of(cur);
+                if (dc > du || (dc == du && cand < cur)) best = c + t;
             }
             std::swap(ids[c], ids[best]);
             s[c] = ids[c];
-            relax_from(s[c]);
+            S.relax_from(s[c]);
         }
+        seed_sets[r] = std::move(s);
+        tasks.push(true, [&, r] { chain_step(r, 0); });
     }
-
-    // --- restart chains (:430-444), two parallel stages. finalize() never
-    // feeds back into the chain (recenter reads the un-finalized growth), so
-    //   stage 1: per restart, the cheap grow/recenter chain, keeping every
-    //            round's grown state (8 restarts in parallel);
-    //   stage 2: all 8 x 13 finalize() calls, independent tasks on every
-    //            host thread, costs only;
-    // then the reference's winner -- the first strict minimum in (restart,
-    // round) order -- is finalized once more to materialise its assignment.
-    if (std::getenv("PSP_PART_PROFILE"))
-        std::fprintf(stderr, "[partition] seeds %.3f s\n",
-                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
-    constexpr int kRounds = kRecenterRounds + 1;
-    struct Grown {
-        std::vector<uint32_t> assign, hop;
-    };
-    std::vector<std::vector<Grown>> grown(kRestarts, std::vector<Grown>(kRounds));
-    const unsigned pool = std::max(1u, threads);
-    const bool prof = std::getenv("PSP_PART_PROFILE") != nullptr;
-    auto t_mark = std::chrono::steady_clock::now();
-    auto lap = [&](const char* what) {
-        if (!prof) return;
-        const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[partition] %s %.3f s\n", what,
-                     std::chrono::duration<double>(now - t_mark).count());
-        t_mark = now;
-    };
-    parallel_tasks(kRestarts, std::min<unsigned>(pool, kRestarts), [&](size_t r) {
-        std::vector<uint32_t> seeds = seed_sets[r];
-        P.grow(seeds, grown[r][0].assign, grown[r][0].hop);
-        for (int round = 1; round < kRounds; ++round) {
-            seeds = P.recenter(grown[r][round - 1].assign, seeds);
-            P.grow(seeds, grown[r][round].assign, grown[r][round].hop);
-        }
-    });
-    lap("grow/recenter chains");
-    std::vector<uint64_t> cost(size_t(kRestarts) * kRounds);
-    parallel_tasks(cost.size(), pool, [&](size_t t) {
-        std::vector<uint32_t> cand;
-        const Grown& gr = grown[t / kRounds][t % kRounds];
-        cost[t] = P.finalize(gr.assign, gr.hop, cand);
-    });
-    lap("finalize tasks");
+    lap("seeds drawn");
+    tasks.join();  // this thread helps until every chain and finalize is done
+    lap("chains + finalize");
     size_t win = 0;
     for (size_t t = 1; t < cost.size(); ++t)
         if (cost[t] < cost[win]) win = t;
     std::vector<uint32_t> assignment;
     const Grown& gw = grown[win / kRounds][win % kRounds];
-    P.finalize(gw.assign, gw.hop, assignment);
-    lap("winner");
+    P.finalize(gw.assign, gw.hop, &assignment);
+    lap("winner finalized");
     std::vector<uint64_t> sz(k, 0);
     for (uint32_t c : assignment) ++sz[c];
     for (uint32_t c = 0; c < k; ++c)

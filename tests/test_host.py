@@ -102,6 +102,31 @@ def test_partition_matches_live_reference(ref, kind, rows, cols, w, gseed, k, se
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("case", ["permuted_grid", "permuted_tri", "delaunay", "delaunay_pieces"])
+def test_partition_scrambled_ids_match_reference(ref, case):
+    """Ids with no locality (the partitioner relabels internally in BFS
+    order; every id-order rule must still be the reference's)."""
+    rng = np.random.default_rng(11)
+    if case.startswith("permuted"):
+        rg = ref.generate("grid" if case == "permuted_grid" else "tri", 30, 37, (1.0, 9.0), 4)
+        eu, ev, ew = rg.edges()
+        n = rg.n
+        perm = rng.permutation(n).astype(np.uint32)
+        eu, ev = perm[eu], perm[ev]
+    else:
+        from paper_1503_07192_b200 import graphs
+        g = graphs.delaunay(3000, 5)
+        n, eu, ev, ew = g.n, g.eu, g.ev, g.ew
+        if case == "delaunay_pieces":  # cut into pieces + isolated vertices
+            keep = (rng.random(len(eu)) < 0.55)
+            eu, ev, ew = eu[keep], ev[keep], ew[keep]
+    rgx = ref.graph(n, eu, ev, ew)
+    for k, seed in ((37, 2), (150, 7)):
+        want, _ = rgx.partition(k, seed)
+        got = P.partition_graph(P.Graph(n, eu, ev, ew), k, seed, threads=5)
+        assert np.array_equal(got, want), (case, k, seed)
+
+
 def test_partition_disconnected_matches_reference(ref):
     # unreached vertices + isolated vertices exercise finalize's fill step
     eu = np.array([0, 1, 2, 5, 6, 8], np.uint32)
