@@ -544,12 +544,19 @@ __global__ void unpack_window(MatSet<V> ms, uint32_t m, uint32_t row0, uint32_t 
 // thread, operands rotated through the accumulators so nothing folds.
 template <class V>
 __global__ void __launch_bounds__(NTHREADS) minplus_peak_kernel(V* out, uint32_t iters, V seed) {
+    // the FW / query inner loop's mix: 8x8 accumulators, k taken in pairs
+    // through addmin2 (2 x VIADDMNMX for u32; FADD, FADD, FMNMX3 for f32),
+    // 128 relaxations per thread per iteration. The operand rotation is
+    // tools/minplus_probe.cu's, whose register allocation reaches the
+    // highest f32 rate found (profiles/r1_minplus_peak.json).
     V acc[8][8];
-    V a[8], b[8];
+    V a0[8], b0[8], a1[8], b1[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        a[i] = seed + V(threadIdx.x & 7) + V(i);
-        b[i] = seed + V(i * 3);
+        a0[i] = seed + V(threadIdx.x & 7) + V(i);
+        b0[i] = seed + V(i * 3);
+        a1[i] = seed + V(i + 1);
+        b1[i] = seed + V(2 * i);
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = seed + V(1000 + i * 8 + j);
     }
@@ -557,11 +564,14 @@ __global__ void __launch_bounds__(NTHREADS) minplus_peak_kernel(V* out, uint32_t
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::addmin(a[i], b[j], acc[i][j]);
+            for (int j = 0; j < 8; ++j)
+                acc[i][j] = Ops<V>::addmin2(a0[i], b0[j], a1[i], b1[j], acc[i][j]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            a[i] = acc[i][(i + 1) & 7];
-            b[i] = acc[(i + 3) & 7][i];
+            a0[i] = acc[i][(i + 1) & 7];
+            b0[i] = acc[(i + 3) & 7][i];
+            a1[i] = acc[(i + 5) & 7][(i + 2) & 7];
+            b1[i] = acc[(i + 6) & 7][(i + 7) & 7];
         }
     }
     V s = acc[0][0];

@@ -52,9 +52,7 @@ template <> struct Ops<float> {
     // (1.5 instructions per relaxation instead of 2)
     static __device__ __forceinline__ float addmin2(float a0, float b0, float a1, float b1,
                                                     float c) {
-        float d;
-        asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(c), "f"(a0 + b0), "f"(a1 + b1));
-        return d;
+        return fminf(fminf(c, a0 + b0), a1 + b1);  // ptxas fuses to FMNMX3
     }
     static __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
     static __device__ __forceinline__ float from_bits(uint32_t u) { return __uint_as_float(u); }

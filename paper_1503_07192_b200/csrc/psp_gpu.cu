@@ -521,7 +521,7 @@ psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_
         cudaStream_t s = ctx->stream;
         DBuf out(ctx->sms * 64 * sizeof(uint32_t));
         const int blocks = ctx->sms * 4;
-        const uint32_t iters = 1 << 14;
+        const uint32_t iters = 1 << 13;
         EventTimer t;
         for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
             t.start(s);
@@ -533,7 +533,7 @@ psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_
             t.stop(s);
         }
         const double ms = t.ms();
-        *relax_per_s = double(blocks) * NTHREADS * 64.0 * iters / (ms * 1e-3);
+        *relax_per_s = double(blocks) * NTHREADS * 128.0 * iters / (ms * 1e-3);
         if (sm_clock_mhz) {
             int khz = 0;
             CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device));
