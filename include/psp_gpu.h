@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PSP_GPU_ABI_VERSION 1
+#define PSP_GPU_ABI_VERSION 2
 
 typedef enum psp_status {
     PSP_OK = 0,
@@ -182,6 +182,58 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
 psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       const uint32_t* v1, const uint32_t* v2, double* dist,
                                       void* stream);
+
+/* -------------------------------------------------- routed (sharded) -- */
+/* The paper's distributed query mode on real GPUs: psp::routed_query and
+ * psp::ClusterSim (include/psp/cluster.hpp:58-109, src/cluster.cpp) with
+ * psp::Placement (include/psp/placement.hpp:8-31) mapping components to
+ * the ranks of a multi-GPU context. */
+enum psp_placement_policy {
+    PSP_PLACE_ROUND_ROBIN = 0,  /* owner(c) = c mod p                         */
+    PSP_PLACE_PAIRS_PER_GPU = 1 /* contiguous blocks, sizes differ by <= 1    */
+};
+
+typedef struct psp_gpu_shard psp_gpu_shard;
+
+typedef struct psp_routed_stats {
+    uint64_t queries;          /* pairs this rank submitted                    */
+    uint64_t executed_here;    /* pairs this rank executed (owner(C1) == rank) */
+    uint64_t sent_to_peers;    /* submitted pairs executed on another rank     */
+    uint64_t transfer_queries; /* submitted pairs with owner(C1) != owner(C2)  */
+    uint64_t transfer_entries; /* their col2 entries (B2 each)                 */
+    uint64_t transfer_bytes;   /* 8 * entries (the reference's f64 ledger)     */
+    double route_ms;           /* device time of the pair exchange             */
+    double exec_ms;            /* device time of the executed batch            */
+} psp_routed_stats;
+
+/* psp::place_components (src/placement.cpp:7-33): owner[k]. p < 1 or
+ * p > k -> PSP_EINVAL. */
+psp_status psp_place_components(uint32_t k, uint32_t p, int policy, uint32_t* owner);
+
+/* COLLECTIVE over the oracle's context (every rank calls it with the same
+ * owner[k], each owner < world): keeps on this rank only the tables of the
+ * components it owns -- their full boundary rows, to-boundary rows and
+ * component tables -- and maps every peer's to-boundary rows through CUDA
+ * IPC. The oracle may be freed afterwards. */
+psp_status psp_gpu_shard_create(const psp_gpu_oracle* o, const uint32_t* owner,
+                                psp_gpu_shard** out);
+/* COLLECTIVE: barrier (peers may still read this rank's tables), then free. */
+psp_status psp_gpu_shard_free(psp_gpu_shard* sh);
+/* Device bytes this rank holds for the shard. */
+psp_status psp_gpu_shard_bytes(const psp_gpu_shard* sh, uint64_t* bytes);
+
+/* COLLECTIVE routed batch: every rank passes its own pairs (count may be
+ * 0); each executes at owner(C1) (NCCL send/recv of the ids), col2 comes
+ * from owner(C2)'s memory over NVLink, and dist[] returns in this rank's
+ * order, equal to psp_gpu_query_batch on the replicated oracle (bit-exact
+ * for u32). Optional per-query outputs (NULL to skip): executed_on,
+ * column_owner, transfer_entries (B2 when the owners differ, else 0;
+ * src/cluster.cpp:77-85). Host pointers. An id >= n on any rank fails the
+ * batch on every rank with PSP_EINVAL. */
+psp_status psp_gpu_routed_query_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1,
+                                      const uint32_t* v2, double* dist, uint32_t* executed_on,
+                                      uint32_t* column_owner, uint32_t* transfer_entries,
+                                      psp_routed_stats* stats);
 
 /* ---------------------------------------------------------- primitives -- */
 /* psp::apsp_dense (include/psp/shortest_paths.hpp:43): dense APSP of one

@@ -93,6 +93,14 @@ class RefLib:
             lib.ref_random_pairs.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]
             lib.ref_save_oracle.argtypes = [vp, C.c_char_p]
             lib.ref_load_oracle.argtypes = [C.c_char_p, C.POINTER(vp)]
+            lib.ref_place_components.argtypes = [C.c_uint32, C.c_uint32, C.c_int, _u32p]
+            lib.ref_routed_query.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                                             C.c_uint64, _f64p]
+            lib.ref_cluster_run_batch.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint64, _u32p,
+                                                  _u32p, _f64p, _u64p, C.POINTER(C.c_uint64)]
+            lib.ref_simulate_build_schedule.argtypes = [C.c_uint32, C.c_uint32, _f64p, C.c_int,
+                                                        _f64p, C.POINTER(C.c_double),
+                                                        C.POINTER(C.c_double)]
             RefLib._lib = lib
         self.lib = RefLib._lib
 
@@ -106,6 +114,20 @@ class RefLib:
         v2 = np.empty(count, np.uint32)
         self.lib.ref_random_pairs(n, count, seed, v1, v2)
         return v1, v2
+
+    # cluster layer (include/psp/placement.hpp, include/psp/cluster.hpp) ---
+    def place_components(self, k: int, p: int, policy: int = 0) -> np.ndarray:
+        owner = np.empty(max(k, 1), np.uint32)
+        self._check(self.lib.ref_place_components(k, p, policy, owner))
+        return owner[:k]
+
+    def simulate_build_schedule(self, k: int, p: int, costs, policy: int = 0):
+        costs = np.ascontiguousarray(costs, np.float64)
+        wc = np.empty(max(p, 1), np.float64)
+        mk, ml = C.c_double(), C.c_double()
+        self._check(self.lib.ref_simulate_build_schedule(k, p, costs, policy, wc, C.byref(mk),
+                                                         C.byref(ml)))
+        return wc[:p].tolist(), mk.value, ml.value
 
     def load_oracle(self, path: str) -> "RefOracle":
         """psp::load_oracle on the reference."""
@@ -231,6 +253,27 @@ class RefOracle:
         out = np.empty(max(r * self.b, 1), np.float64)
         self.ref.lib.ref_oracle_boundary_rows(self.h, c, out)
         return out[: r * self.b].reshape(r, self.b)
+
+    def routed_query(self, p: int, v1: int, v2: int, query_id: int = 0, policy: int = 0) -> dict:
+        """psp::routed_query (src/cluster.cpp:49-74) under place_components(k, p)."""
+        out = np.empty(15, np.float64)
+        self.ref._check(self.ref.lib.ref_routed_query(self.h, p, policy, v1, v2, query_id, out))
+        keys = ("distance", "minplus_ops", "b1", "b2", "same_component", "transfer_entries",
+                "executed_on", "column_owner", "has_transfer", "src_worker", "dst_worker",
+                "entries", "bytes", "overlap_cost", "serial_cost")
+        return dict(zip(keys, out.tolist()))
+
+    def cluster_run_batch(self, p: int, v1, v2, policy: int = 0):
+        """psp::ClusterSim::run_batch (src/cluster.cpp:225-231): distances and
+        the ledger rows (query_id, src_worker, dst_worker, entries, bytes)."""
+        v1 = np.ascontiguousarray(v1, np.uint32)
+        v2 = np.ascontiguousarray(v2, np.uint32)
+        dist = np.empty(len(v1), np.float64)
+        rec = np.empty(max(5 * len(v1), 5), np.uint64)
+        nrec = C.c_uint64()
+        self.ref._check(self.ref.lib.ref_cluster_run_batch(self.h, p, policy, len(v1), v1, v2,
+                                                           dist, rec, C.byref(nrec)))
+        return dist, rec[: 5 * nrec.value].reshape(-1, 5)
 
     def batch_query(self, v1, v2, workers: int = 1, with_ops: bool = False):
         v1 = np.ascontiguousarray(v1, np.uint32)

@@ -26,11 +26,13 @@
 #include <utility>
 #include <vector>
 
+#include "psp/cluster.hpp"
 #include "psp/generators.hpp"
 #include "psp/graph.hpp"
 #include "psp/oracle.hpp"
 #include "psp/oracle_io.hpp"
 #include "psp/partition.hpp"
+#include "psp/placement.hpp"
 #include "psp/query.hpp"
 #include "psp/shortest_paths.hpp"
 #include "support/reference.hpp"  // ref::random_pairs (tests/support/reference.hpp:80-91)
@@ -289,6 +291,74 @@ int ref_load_oracle(const char* path, void** out) {
             throw;
         }
         *out = ro;
+    });
+}
+
+// --- cluster layer (include/psp/placement.hpp, include/psp/cluster.hpp) ---
+static psp::PlacementPolicy policy_of(int p) {
+    return p == 1 ? psp::PlacementPolicy::PairsPerGpu : psp::PlacementPolicy::RoundRobin;
+}
+
+int ref_place_components(uint32_t k, uint32_t p, int policy, uint32_t* owner) {
+    return guarded([&] {
+        const psp::Placement pl = psp::place_components(k, p, policy_of(policy));
+        std::copy(pl.owner.begin(), pl.owner.end(), owner);
+    });
+}
+
+// out: distance, minplus_ops, b1, b2, same, transfer_entries, executed_on,
+// column_owner, has_transfer, rec.src, rec.dst, rec.entries, rec.bytes,
+// overlap_cost, serial_cost
+int ref_routed_query(const void* o, uint32_t p, int policy, uint32_t v1, uint32_t v2,
+                     uint64_t qid, double* out) {
+    return guarded([&] {
+        const psp::Oracle& orc = static_cast<const RefOracle*>(o)->o;
+        const psp::Placement pl = psp::place_components(orc.k, p, policy_of(policy));
+        const psp::RoutedQueryResult r = psp::routed_query(orc, pl, v1, v2, qid);
+        const auto& st = r.result.stats;
+        double v[15] = {r.result.distance, double(st.minplus_ops), double(st.boundary_size_1),
+                        double(st.boundary_size_2), st.same_component ? 1.0 : 0.0,
+                        double(st.transfer_entries), double(r.executed_on), double(r.column_owner),
+                        r.transfer ? 1.0 : 0.0, r.transfer ? double(r.transfer->src_worker) : 0.0,
+                        r.transfer ? double(r.transfer->dst_worker) : 0.0,
+                        r.transfer ? double(r.transfer->entries) : 0.0,
+                        r.transfer ? double(r.transfer->bytes) : 0.0, r.overlap_cost, r.serial_cost};
+        std::memcpy(out, v, sizeof(v));
+    });
+}
+
+// ClusterSim::run_batch; ledger rows (query_id, src, dst, entries, bytes)
+// into rec (count * 5 u64 max), their number into *nrec.
+int ref_cluster_run_batch(const void* o, uint32_t p, int policy, uint64_t count,
+                          const uint32_t* v1, const uint32_t* v2, double* dist, uint64_t* rec,
+                          uint64_t* nrec) {
+    return guarded([&] {
+        const psp::Oracle& orc = static_cast<const RefOracle*>(o)->o;
+        psp::ClusterSim sim(orc, psp::place_components(orc.k, p, policy_of(policy)));
+        std::vector<std::pair<psp::VertexId, psp::VertexId>> pairs(count);
+        for (uint64_t i = 0; i < count; ++i) pairs[i] = {v1[i], v2[i]};
+        const auto res = sim.run_batch(pairs);
+        for (uint64_t i = 0; i < count; ++i) dist[i] = res[i].distance;
+        const auto recs = sim.ledger().records();
+        *nrec = recs.size();
+        for (size_t i = 0; i < recs.size(); ++i) {
+            rec[5 * i + 0] = recs[i].query_id;
+            rec[5 * i + 1] = recs[i].src_worker;
+            rec[5 * i + 2] = recs[i].dst_worker;
+            rec[5 * i + 3] = recs[i].entries;
+            rec[5 * i + 4] = recs[i].bytes;
+        }
+    });
+}
+
+int ref_simulate_build_schedule(uint32_t k, uint32_t p, const double* costs, int policy,
+                                double* worker_cost, double* makespan, double* mean_load) {
+    return guarded([&] {
+        const psp::ScheduleProfile prof = psp::simulate_build_schedule(
+            k, p, std::span<const double>(costs, k), policy_of(policy));
+        std::copy(prof.worker_cost.begin(), prof.worker_cost.end(), worker_cost);
+        *makespan = prof.makespan;
+        *mean_load = prof.mean_load;
     });
 }
 

@@ -23,7 +23,14 @@ from . import _lib
 from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, ChecksumError,
                    FormatVersionError, GraphInvariantError, OracleIoError, PspError, PspValueError)
 
-__all__ = ["Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
+from . import cluster  # noqa: E402  (placement + routed queries, cluster.hpp)
+from .cluster import (PAIRS_PER_GPU, ROUND_ROBIN, Placement, RoutedOracle,  # noqa: E402
+                      TransferLedger, TransferRecord, place_components, routed_query,
+                      simulate_build_schedule)
+
+__all__ = ["cluster", "Placement", "RoutedOracle", "TransferLedger", "TransferRecord",
+           "place_components", "routed_query", "simulate_build_schedule", "ROUND_ROBIN",
+           "PAIRS_PER_GPU", "Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
            "random_pairs", "VALUE_AUTO", "VALUE_U32", "VALUE_F32", "PspError", "PspValueError",
            "GraphInvariantError", "OracleIoError", "FormatVersionError", "ChecksumError",

@@ -84,6 +84,24 @@ class OracleInfo(C.Structure):
     ]
 
 
+class RoutedStats(C.Structure):
+    _fields_ = [
+        ("queries", C.c_uint64),
+        ("executed_here", C.c_uint64),
+        ("sent_to_peers", C.c_uint64),
+        ("transfer_queries", C.c_uint64),
+        ("transfer_entries", C.c_uint64),
+        ("transfer_bytes", C.c_uint64),
+        ("route_ms", C.c_double),
+        ("exec_ms", C.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+PLACE_ROUND_ROBIN, PLACE_PAIRS_PER_GPU = 0, 1
+
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
@@ -116,6 +134,12 @@ SIGNATURES = {
     "psp_gpu_export_boundary_rows": (C.c_int, [_vp, C.c_uint32, _f64p]),
     "psp_gpu_query_batch": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp]),
     "psp_gpu_query_batch_device": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp]),
+    "psp_place_components": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int, _u32p]),
+    "psp_gpu_shard_create": (C.c_int, [_vp, _u32p, C.POINTER(_vp)]),
+    "psp_gpu_shard_free": (C.c_int, [_vp]),
+    "psp_gpu_shard_bytes": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
+    "psp_gpu_routed_query_batch": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                             C.POINTER(RoutedStats)]),
     "psp_gpu_apsp_dense": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
                                      C.c_uint64, C.c_int, _f64p]),
     "psp_gpu_boundary_apsp": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,

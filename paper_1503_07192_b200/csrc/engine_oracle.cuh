@@ -4,6 +4,21 @@
 #pragma once
 
 // ------------------------------------------------------------ oracle ----
+// Grow-only workspace of the grouped query kernel, and the event that
+// serialises its reuse across caller streams.
+struct GroupWorkspace {
+    DBuf buf, bins, temp, tasks;
+    uint64_t count = 0;
+    size_t temp_bytes = 0;
+    cudaEvent_t done = nullptr;
+    GroupWorkspace() = default;
+    GroupWorkspace(const GroupWorkspace&) = delete;
+    GroupWorkspace& operator=(const GroupWorkspace&) = delete;
+    ~GroupWorkspace() {
+        if (done) cudaEventDestroy(done);
+    }
+};
+
 struct psp_gpu_oracle {
     psp_gpu_ctx* ctx = nullptr;
     Kind kind{PSP_VALUE_U32, 0};
@@ -16,15 +31,7 @@ struct psp_gpu_oracle {
     // the tables themselves are read-only, src/query.cpp is re-entrant too)
     std::mutex query_mu;
     DBuf query_stage;
-    // grouped-query workspace (grow-only) and the event that serialises its
-    // reuse across caller streams
-    DBuf gw_buf, gw_bins, gw_temp, gw_tasks;
-    uint64_t gw_count = 0;
-    size_t gw_temp_bytes = 0;
-    cudaEvent_t gw_done = nullptr;
-    ~psp_gpu_oracle() {
-        if (gw_done) cudaEventDestroy(gw_done);
-    }
+    GroupWorkspace gw;
 };
 
 namespace {
@@ -367,38 +374,42 @@ void export_window(const psp_gpu_oracle* o, const MatArena& a, uint32_t m, uint3
     to_f64(h, dst, o->scale);
 }
 
-template <class V>
-void launch_grouped(psp_gpu_oracle* o, const QueryView<V>& q, uint64_t count, const uint32_t* v1,
-                    const uint32_t* v2, double* dist, cudaStream_t s) {
-    const uint32_t nbins = o->R.k * o->R.k;
-    if (!o->gw_done) CK(cudaEventCreateWithFlags(&o->gw_done, cudaEventDisableTiming));
+// Counting sort by component pair, task records, query_grouped, finish.
+// `bnd_off` is the host copy of the boundary offsets (task-count bound).
+template <class V, bool ROUTED>
+void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, int sms,
+                    const QueryView<V>& q, uint64_t count, const uint32_t* v1, const uint32_t* v2,
+                    double* dist, cudaStream_t s) {
+    const uint32_t k = q.k;
+    const uint32_t nbins = k * k;
+    if (!gw.done) CK(cudaEventCreateWithFlags(&gw.done, cudaEventDisableTiming));
     // the workspace is shared by all calls on this oracle: order after the
     // previous user, whatever stream it ran on
-    CK(cudaStreamWaitEvent(s, o->gw_done, 0));
-    if (o->gw_count < count) {
+    CK(cudaStreamWaitEvent(s, gw.done, 0));
+    if (gw.count < count) {
         CK(cudaStreamSynchronize(s));
-        o->gw_buf.alloc(count * 7 * sizeof(uint32_t));
-        o->gw_count = count;
+        gw.buf.alloc(count * 7 * sizeof(uint32_t));
+        gw.count = count;
     }
-    if (o->gw_bins.bytes < size_t(nbins + 1) * 4 * sizeof(uint32_t)) {
+    if (gw.bins.bytes < size_t(nbins + 1) * 4 * sizeof(uint32_t)) {
         CK(cudaStreamSynchronize(s));
-        o->gw_bins.alloc(size_t(nbins + 1) * 4 * sizeof(uint32_t));
+        gw.bins.alloc(size_t(nbins + 1) * 4 * sizeof(uint32_t));
         size_t t1 = 0;
         CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                          int(nbins + 1), s));
-        o->gw_temp.alloc(t1);
-        o->gw_temp_bytes = t1;
+        gw.temp.alloc(t1);
+        gw.temp_bytes = t1;
     }
     GroupWork w;
-    uint32_t* base = o->gw_buf.as<uint32_t>();
+    uint32_t* base = gw.buf.as<uint32_t>();
     w.key = base;
-    w.l1 = base + o->gw_count;
-    w.l2 = base + 2 * o->gw_count;
-    w.best = base + 3 * o->gw_count;
-    w.sorted = base + 4 * o->gw_count;
-    w.s_l1 = base + 5 * o->gw_count;
-    w.s_l2 = base + 6 * o->gw_count;
-    uint32_t* bins = o->gw_bins.as<uint32_t>();
+    w.l1 = base + gw.count;
+    w.l2 = base + 2 * gw.count;
+    w.best = base + 3 * gw.count;
+    w.sorted = base + 4 * gw.count;
+    w.s_l1 = base + 5 * gw.count;
+    w.s_l2 = base + 6 * gw.count;
+    uint32_t* bins = gw.bins.as<uint32_t>();
     w.bin_cnt = bins;
     w.bin_start = bins + (nbins + 1);
     w.task_cnt = bins + 2 * size_t(nbins + 1);
@@ -406,42 +417,43 @@ void launch_grouped(psp_gpu_oracle* o, const QueryView<V>& q, uint64_t count, co
     w.nbins = nbins;
     CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins + 1) * sizeof(uint32_t), s));
     const unsigned qb = unsigned((count + 255) / 256);
-    group_prep<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w);
+    group_prep<V, ROUTED><<<qb, 256, 0, s>>>(q, v1, v2, count, w);
     CK_LAUNCH();
     group_tasks<<<(nbins + 1 + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k);
     CK_LAUNCH();
-    size_t tb = o->gw_temp_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(o->gw_temp.p, tb, w.bin_cnt, w.bin_start, int(nbins + 1), s));
-    tb = o->gw_temp_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(o->gw_temp.p, tb, w.task_cnt, w.task_start, int(nbins + 1), s));
+    size_t tb = gw.temp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(gw.temp.p, tb, w.bin_cnt, w.bin_start, int(nbins + 1), s));
+    tb = gw.temp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(gw.temp.p, tb, w.task_cnt, w.task_start, int(nbins + 1), s));
     // task records: upper bound on the task count without a host round trip
     {
         uint64_t max_tasks = 0;
-        for (uint32_t c = 0; c < o->R.k; ++c)
-            max_tasks = std::max<uint64_t>(max_tasks, (o->R.bnd_off[c + 1] - o->R.bnd_off[c] + 31) / 32);
+        for (uint32_t c = 0; c < k; ++c)
+            max_tasks = std::max<uint64_t>(max_tasks, (bnd_off[c + 1] - bnd_off[c] + 31) / 32);
         max_tasks *= (count + GQ - 1) / GQ + std::min<uint64_t>(count, nbins);
-        if (o->gw_tasks.bytes < max_tasks * sizeof(uint4) + 16) {
+        if (gw.tasks.bytes < max_tasks * sizeof(uint4) + 16) {
             CK(cudaStreamSynchronize(s));
-            o->gw_tasks.alloc(max_tasks * sizeof(uint4) + 16);
+            gw.tasks.alloc(max_tasks * sizeof(uint4) + 16);
         }
     }
-    w.tasks = o->gw_tasks.as<uint4>();
+    w.tasks = gw.tasks.as<uint4>();
     group_emit<<<(nbins + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k);
     CK_LAUNCH();
     CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins) * sizeof(uint32_t), s));
     group_scatter<<<qb, 256, 0, s>>>(count, w);
     CK_LAUNCH();
     const int gsmem = GWARPS * sizeof(WarpStage<V>);
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[sizeof(V) == 4 && std::is_same<V, float>::value]) {
-        CK(cudaFuncSetAttribute(query_grouped<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
-        attr_set[std::is_same<V, float>::value] = true;
+    static bool attr_set = false;  // one flag per <V, ROUTED> instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(query_grouped<V, ROUTED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                gsmem));
+        attr_set = true;
     }
-    query_grouped<V><<<o->ctx->sms * 2, GTHREADS, gsmem, s>>>(q, w);
+    query_grouped<V, ROUTED><<<sms * 2, GTHREADS, gsmem, s>>>(q, w);
     CK_LAUNCH();
     group_finish<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w, dist);
     CK_LAUNCH();
-    CK(cudaEventRecord(o->gw_done, s));
+    CK(cudaEventRecord(gw.done, s));
 }
 
 // Every batch goes through the pair-grouped kernel: measured on cfg2/cfg3 it
@@ -477,7 +489,8 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     if (force && std::strcmp(force, "warp") == 0) grouped = false;
     if (force && std::strcmp(force, "grouped") == 0) grouped = true;
     if (grouped && k * k < (1ull << 31) && count < (1ull << 31)) {
-        launch_grouped<V>(const_cast<psp_gpu_oracle*>(o), q, count, v1, v2, dist, s);
+        launch_grouped<V, false>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off, o->ctx->sms, q, count,
+                                 v1, v2, dist, s);
         return;
     }
     const uint64_t warps_per_block = 8;

@@ -18,6 +18,7 @@
 //   engine_fw.cuh        contexts, FW drivers (1 GPU / row-sharded NCCL)
 //   engine_oracle.cuh    device oracle: build, import, export, query launch
 //   engine_file.cuh      PSP1 files from/to device tables
+//   engine_shard.cuh     routed (sharded) queries over NVLink
 //   psp_gpu.cu           this file: the extern "C" entry points
 //   host_graph.cpp, partition.cpp   host graph plumbing and partitioner
 #include <cub/device/device_scan.cuh>
@@ -51,6 +52,7 @@ using namespace pspg;
 #include "engine_fw.cuh"
 #include "engine_oracle.cuh"
 #include "engine_file.cuh"
+#include "engine_shard.cuh"
 
 // ================================================================ C-ABI ==
 extern "C" {
@@ -511,6 +513,86 @@ psp_status psp_gpu_boundary_apsp(psp_gpu_ctx* ctx, uint64_t b, uint64_t m, const
     // The boundary graph's all-pairs table is exactly the dense APSP of the
     // boundary graph; rows are already in boundary-id (component) order.
     return psp_gpu_apsp_dense(ctx, b, m, eu, ev, ew, 64, value_kind, out);
+}
+
+// ------------------------------------------------------ routed queries --
+psp_status psp_place_components(uint32_t k, uint32_t p, int policy, uint32_t* owner) {
+    return guarded([&] {
+        if (!owner) throw ArgError("place_components: NULL owner");
+        const std::vector<uint32_t> o = place(k, p, policy);
+        std::copy(o.begin(), o.end(), owner);
+    });
+}
+
+psp_status psp_gpu_shard_create(const psp_gpu_oracle* o, const uint32_t* owner,
+                                psp_gpu_shard** out) {
+    return guarded([&] {
+        if (!o || !owner || !out) throw ArgError("shard_create: NULL argument");
+        *out = nullptr;
+        psp_gpu_ctx* ctx = o->ctx;
+        if (ctx->world > 1 && !ctx->comm) throw ArgError("shard_create: context has no communicator");
+        CK(cudaSetDevice(ctx->device));
+        auto sh = std::make_unique<psp_gpu_shard>();
+        sh->ctx = ctx;
+        sh->kind = o->kind;
+        sh->scale = o->scale;
+        sh->n = o->R.n;
+        sh->k = o->R.k;
+        sh->b = o->R.b();
+        sh->bnd_off = o->R.bnd_off;
+        sh->owner.assign(owner, owner + o->R.k);
+        for (uint32_t w : sh->owner)
+            if (w >= uint32_t(ctx->world)) throw ArgError("shard_create: owner >= world size");
+        if (o->R.k * uint64_t(o->R.k) >= (1ull << 31))
+            throw ArgError("shard_create: k * k must fit the grouped kernel's 31-bit pair keys");
+        if (o->kind.kind == PSP_VALUE_U32) shard_build<uint32_t>(sh.get(), o);
+        else shard_build<float>(sh.get(), o);
+        *out = sh.release();
+    });
+}
+
+psp_status psp_gpu_shard_free(psp_gpu_shard* sh) {
+    return guarded([&] {
+        if (!sh) return;
+        std::unique_ptr<psp_gpu_shard> own(sh);
+        psp_gpu_ctx* ctx = sh->ctx;
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->world > 1) {  // nobody may still be reading our arena
+            DBuf one(4);
+            CK(cudaMemsetAsync(one.p, 0, 4, ctx->stream));
+            nccl_check(pspg::nccl().AllReduce(one.p, one.p, 1, ncclUint32, ncclMax, ctx->comm,
+                                              ctx->stream),
+                       "ncclAllReduce(shard barrier)");
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
+psp_status psp_gpu_shard_bytes(const psp_gpu_shard* sh, uint64_t* bytes) {
+    return guarded([&] {
+        if (!sh || !bytes) throw ArgError("shard_bytes: NULL argument");
+        *bytes = sh->device_bytes;
+    });
+}
+
+psp_status psp_gpu_routed_query_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1,
+                                      const uint32_t* v2, double* dist, uint32_t* executed_on,
+                                      uint32_t* column_owner, uint32_t* transfer_entries,
+                                      psp_routed_stats* stats) {
+    return guarded([&] {
+        if (!sh) throw ArgError("routed_query_batch: NULL shard");
+        if (count && (!v1 || !v2 || !dist)) throw ArgError("routed_query_batch: NULL array");
+        if (count >= (1ull << 31)) throw ArgError("routed_query_batch: count must be < 2^31");
+        CK(cudaSetDevice(sh->ctx->device));
+        std::lock_guard<std::mutex> lock(sh->mu);
+        if (sh->kind.kind == PSP_VALUE_U32)
+            routed_batch<uint32_t>(sh, count, v1, v2, dist, executed_on, column_owner,
+                                   transfer_entries, stats);
+        else
+            routed_batch<float>(sh, count, v1, v2, dist, executed_on, column_owner,
+                                transfer_entries, stats);
+    });
 }
 
 psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_per_s,

@@ -41,6 +41,15 @@ template <class V> struct QueryView {
     uint32_t n;                 // vertex count: ids >= n are rejected
     uint32_t* bad_id;           // set to 1 when a query id is out of range
     double scale;               // 2^-q (u32 fixed point) or 1
+    // routed (sharded) mode only, see engine_shard.cuh: this rank holds the
+    // full boundary rows of the components it owns, dense row-major; `cb`
+    // is its own compact to-boundary arena and cb_peer[r] rank r's, mapped
+    // over NVLink; cb_off[c] is c's offset in its owner's arena
+    const V* bt;                // [owned boundary rows][bt_stride]
+    uint64_t bt_stride;         // >= b, multiple of 4
+    const uint32_t* bt_row0;    // k: first local BT row of an owned component
+    const uint32_t* owner;      // k: rank owning component c
+    const V* const* cb_peer;    // world: every rank's compact CB arena
 };
 
 template <class V>
@@ -62,8 +71,9 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
     return q.comps.tiles[q.comps.tile_base[c] + sym_off(l1, l2, q.comps.nb[c])];
 }
 
-// Resolve a query to (c1 <= c2, l1, l2).
-template <class V>
+// Resolve a query to (c1 <= c2, l1, l2); routed mode keeps the caller's
+// orientation (the query executes at owner(C1), src/cluster.cpp:88-90).
+template <class V, bool ROUTED = false>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
                                         uint32_t& c1, uint32_t& c2, uint32_t& l1, uint32_t& l2) {
     // src/query.cpp:30: out-of-range ids invalidate the batch (the host API
@@ -75,7 +85,7 @@ __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint
     uint32_t r1 = q.perm[v1], r2 = q.perm[v2];
     c1 = q.assign[r1];
     c2 = q.assign[r2];
-    if (c1 > c2) {
+    if (!ROUTED && c1 > c2) {
         uint32_t t = r1; r1 = r2; r2 = t;
         t = c1; c1 = c2; c2 = t;
     }
@@ -205,13 +215,13 @@ struct GroupWork {
     uint32_t nbins;
 };
 
-template <class V>
+template <class V, bool ROUTED>
 __global__ void group_prep(QueryView<V> q, const uint32_t* __restrict__ v1,
                            const uint32_t* __restrict__ v2, uint64_t count, GroupWork w) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= count) return;
     uint32_t c1, c2, l1, l2;
-    resolve(q, v1[i], v2[i], c1, c2, l1, l2);
+    resolve<V, ROUTED>(q, v1[i], v2[i], c1, c2, l1, l2);
     const uint32_t key = c1 * q.k + c2;
     w.key[i] = key;
     w.l1[i] = l1;
@@ -325,7 +335,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
                  : "memory");
 }
 
-template <class V, int NQ4>
+template <class V, int NQ4, bool ROUTED>
 __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWork& w,
                                            WarpStage<V>* st, uint32_t c1, uint32_t c2,
                                            uint32_t q0, uint32_t m, uint32_t cg) {
@@ -335,7 +345,9 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
     const uint32_t Bp1 = cb_stride(B1), Bp2 = cb_stride(B2);
     const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
-    const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
+    // routed: col2 comes from owner(C2)'s arena, a peer GPU's memory when
+    // the owners differ (the paper's Alg. 2 line 8 transfer)
+    const V* __restrict__ cb2 = (ROUTED ? q.cb_peer[q.owner[c2]] : q.cb) + q.cb_off[c2];
     const uint32_t j = cg * 32 + lane;
     const bool col_ok = j < B2;
     // 16-byte-aligned column superset of this task's 32 columns
@@ -363,7 +375,23 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
             for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
         }
         V* sb = st->b[buf];
-        if (c1 != c2) {
+        if (ROUTED) {  // dense full rows of c1 (owned): any column block
+            const V* rows0 = q.bt + uint64_t(q.bt_row0[c1] + k0) * q.bt_stride;
+#pragma unroll
+            for (int t = 0; t < (GK * 9 + 31) / 32; ++t) {
+                const uint32_t e = t * 32 + lane;
+                if (e >= uint32_t(GK * 9)) break;
+                const uint32_t kk = e / 9, u = e - kk * 9;
+                const uint32_t col = A0 + 4 * u;
+                V* dst = sb + kk * GB_STRIDE + 4 * u;
+                if (kk < rows && col < q.bt_stride) {
+                    cp_async16(dst, rows0 + uint64_t(kk) * q.bt_stride + col, true);
+                } else {
+                    const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
+                    st4(dst, inf4);
+                }
+            }
+        } else if (c1 != c2) {
             const uint32_t gi0 = g1 + k0;
             const uint32_t I0 = gi0 >> 7, r0 = gi0 & (T - 1);
 #pragma unroll
@@ -440,7 +468,7 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     }
 }
 
-template <class V>
+template <class V, bool ROUTED>
 __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, GroupWork w) {
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
@@ -452,9 +480,9 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // three query-count variants (32/16/8 slots): finer variants cut the
         // padding (82% vs 77% utilisation) but grow the kernel past the
         // instruction cache and measured slower (321M vs 390M queries/s)
-        if (m > 16) group_task<V, 8>(q, w, st, c1, c2, q0, m, cg);
-        else if (m > 8) group_task<V, 4>(q, w, st, c1, c2, q0, m, cg);
-        else group_task<V, 2>(q, w, st, c1, c2, q0, m, cg);
+        if (m > 16) group_task<V, 8, ROUTED>(q, w, st, c1, c2, q0, m, cg);
+        else if (m > 8) group_task<V, 4, ROUTED>(q, w, st, c1, c2, q0, m, cg);
+        else group_task<V, 2, ROUTED>(q, w, st, c1, c2, q0, m, cg);
     }
 }
 

@@ -112,5 +112,29 @@ def main():
     np.savez(os.path.join(HERE, "random_pairs_n1000_s123.npz"), v1=v1, v2=v2)
 
 
+def cluster_fixture(R=None):
+    """ClusterSim::run_batch (src/cluster.cpp:225-231) on BASELINE configs[0]
+    with p = 2 and 4 workers, both placement policies: distances and ledger
+    rows, for the multi-GPU routed-query check (tools/routed_check.py)."""
+    R = R or oracle.RefLib()
+    rg = R.generate("grid", 64, 64, (1, 1025), 1)
+    ro = rg.build_oracle(16, 4, 0)
+    z = np.load(os.path.join(HERE, "ref_cfg1.npz"))
+    v1, v2 = z["q_v1"][:4000], z["q_v2"][:4000]
+    out = {"v1": v1, "v2": v2}
+    for p in (2, 4):
+        for pol in (0, 1):
+            dist, rec = ro.cluster_run_batch(p, v1, v2, pol)
+            out[f"p{p}_pol{pol}_dist"] = dist
+            out[f"p{p}_pol{pol}_ledger"] = rec
+            print(f"cluster p={p} policy={pol}: {len(rec)} transfers, {int(rec[:, 4].sum())} bytes")
+    np.savez_compressed(os.path.join(HERE, "ref_cluster_cfg1.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    import sys
+    if sys.argv[1:] == ["cluster"]:
+        cluster_fixture()
+    else:
+        main()
+        cluster_fixture()
