@@ -63,43 +63,85 @@ class TransferRecord:
 
 
 class TransferLedger:
-    """psp::TransferLedger (cluster.hpp:35-50): thread-safe append-only log."""
+    """psp::TransferLedger (cluster.hpp:35-50): thread-safe append-only log.
+
+    Stored columnar (rows of query_id, src_worker, dst_worker, entries,
+    bytes as uint64) because a routed batch appends up to one record per
+    query; records() materialises TransferRecord objects on demand."""
+
+    _EMPTY = np.empty((0, 5), np.uint64)
 
     def __init__(self):
         self._mu = threading.Lock()
-        self._records: list[TransferRecord] = []
+        self._chunks: list = []  # (N, 5) arrays, or routed batches still to expand
+
+    @staticmethod
+    def _rows(chunk) -> np.ndarray:
+        if isinstance(chunk, np.ndarray):
+            return chunk
+        base, ex, co, ent = chunk  # a routed batch: a record iff owner(C1) != owner(C2)
+        cross = np.flatnonzero(ex != co)
+        rows = np.empty((len(cross), 5), np.uint64)
+        rows[:, 0] = base + cross
+        rows[:, 1] = co[cross]
+        rows[:, 2] = ex[cross]
+        rows[:, 3] = ent[cross]  # B2 (src/cluster.cpp:83)
+        rows[:, 4] = 8 * rows[:, 3]
+        return rows
+
+    def _extend_routed(self, base: int, ex, co, ent) -> None:
+        """Append a routed batch's records without expanding them yet (a
+        batch can carry one record per query; expansion is deferred to the
+        first read)."""
+        with self._mu:
+            self._chunks.append((base, ex, co, ent))
 
     def record(self, rec: TransferRecord) -> None:
+        row = np.array([[rec.query_id, rec.src_worker, rec.dst_worker, rec.entries, rec.bytes]],
+                       np.uint64)
         with self._mu:
-            self._records.append(rec)
+            self._chunks.append(row)
 
-    def extend(self, recs) -> None:
+    def extend_rows(self, rows: np.ndarray) -> None:
+        """Append an (N, 5) array of records."""
+        rows = np.ascontiguousarray(rows, np.uint64).reshape(-1, 5)
+        if len(rows):
+            with self._mu:
+                self._chunks.append(rows)
+
+    def as_array(self) -> np.ndarray:
         with self._mu:
-            self._records.extend(recs)
+            return self._flat().copy()
+
+    def _flat(self) -> np.ndarray:  # caller holds the lock
+        if not self._chunks:
+            return self._EMPTY
+        if len(self._chunks) > 1 or not isinstance(self._chunks[0], np.ndarray):
+            self._chunks = [np.concatenate([self._rows(c) for c in self._chunks])]
+        return self._chunks[0]
 
     def records(self) -> list[TransferRecord]:
-        with self._mu:
-            return list(self._records)
+        return [TransferRecord(*map(int, r)) for r in self.as_array()]
 
     def size(self) -> int:
         with self._mu:
-            return len(self._records)
+            return len(self._flat())
 
     def total_entries(self) -> int:
         with self._mu:
-            return sum(r.entries for r in self._records)
+            return int(self._flat()[:, 3].sum())
 
     def total_bytes(self) -> int:
         with self._mu:
-            return sum(r.bytes for r in self._records)
+            return int(self._flat()[:, 4].sum())
 
     def write_csv(self, out) -> None:
         """"query_id,src_worker,dst_worker,entries,bytes", one row each
         (cluster.cpp:40-47)."""
-        with self._mu:
-            out.write("query_id,src_worker,dst_worker,entries,bytes\n")
-            for r in self._records:
-                out.write(f"{r.query_id},{r.src_worker},{r.dst_worker},{r.entries},{r.bytes}\n")
+        rows = self.as_array()
+        out.write("query_id,src_worker,dst_worker,entries,bytes\n")
+        if len(rows):
+            out.write("\n".join(",".join(map(str, r)) for r in rows.tolist()) + "\n")
 
 
 @dataclasses.dataclass
@@ -208,13 +250,7 @@ class RoutedOracle:
         _lib.check(_lib.lib().psp_gpu_routed_query_batch(self.h, n, p(v1), p(v2), p(dist), p(ex),
                                                         p(co), p(ent), C.byref(st)))
         self.last_stats = st.as_dict()
-        cross = np.nonzero(ex != co)[0]
-        c2 = self.assignment[self.permutation[v2[cross].astype(np.int64)]]
-        b2 = (self.boundary_offset[c2.astype(np.int64) + 1] -
-              self.boundary_offset[c2.astype(np.int64)]).astype(np.int64)
-        base = self._next_query_id
-        self._ledger.extend(TransferRecord(base + int(i), int(co[i]), int(ex[i]), int(b), 8 * int(b))
-                            for i, b in zip(cross.tolist(), b2.tolist()))
+        self._ledger._extend_routed(self._next_query_id, ex, co, ent)
         self._next_query_id += n
         return (dist, ex, co, ent) if with_routing else dist
 

@@ -34,7 +34,7 @@ struct psp_gpu_shard {
     MatArena comps;  // owned components only (the others have size 0)
     std::vector<void*> opened;  // peer arenas mapped through CUDA IPC
     GroupWorkspace gw;
-    DBuf stage;      // per-call routing buffers (grow-only)
+    DBuf stage, recv, out, gath;  // routing buffers (grow-only, reused per batch)
     std::mutex mu;   // one routed batch at a time (the batch is collective)
     uint64_t device_bytes = 0;
     ~psp_gpu_shard() {
@@ -286,7 +286,10 @@ void routed_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1, const u
     // x count), counts[world + 1] + cursor[world] + send_off[world], totals
     const uint64_t cnt = std::max<uint64_t>(count, 1);
     const size_t need = cnt * (9 * 4 + 8) + (4 * world + 8) * 4 + 64;
-    if (sh->stage.bytes < need) sh->stage.alloc(need);
+    if (sh->stage.bytes < need) {
+        CK(cudaStreamSynchronize(s));
+        sh->stage.alloc(need);
+    }
     uint32_t* d1 = sh->stage.as<uint32_t>();
     uint32_t* d2 = d1 + cnt;
     uint32_t* dexec = d2 + cnt;
@@ -318,10 +321,10 @@ void routed_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1, const u
     // so an invalid id fails the batch on every rank together
     std::vector<uint32_t> all(size_t(world) * (world + 1), 0);
     if (world > 1) {
-        DBuf g(all.size() * 4);
-        nccl_check(api.AllGather(counts, g.p, world + 1, ncclUint32, ctx->comm, s),
+        if (sh->gath.bytes < all.size() * 4) sh->gath.alloc(all.size() * 4);
+        nccl_check(api.AllGather(counts, sh->gath.p, world + 1, ncclUint32, ctx->comm, s),
                    "ncclAllGather(route counts)");
-        CK(cudaMemcpyAsync(all.data(), g.p, all.size() * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(all.data(), sh->gath.p, all.size() * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     } else {
         CK(cudaMemcpyAsync(all.data(), counts, (world + 1) * 4, cudaMemcpyDeviceToHost, s));
@@ -347,16 +350,19 @@ void routed_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1, const u
     }
     // receive side: R pairs to execute here, their answers, all in
     // (origin rank, arrival) order
-    DBuf recv;
     uint32_t *r1 = s1, *r2 = s2;
     double *rd = back, *sd = back;
     EventTimer t_route, t_exec;
     t_route.start(s);
     if (world > 1) {
-        recv.alloc(std::max<uint64_t>(R, 1) * 16);
-        r1 = recv.as<uint32_t>();
-        r2 = r1 + std::max<uint64_t>(R, 1);
-        rd = reinterpret_cast<double*>(r2 + std::max<uint64_t>(R, 1));
+        const uint64_t rc = std::max<uint64_t>(R, 1) + (R & 1);  // keeps rd 8-byte aligned
+        if (sh->recv.bytes < rc * 16) {
+            CK(cudaStreamSynchronize(s));
+            sh->recv.alloc(rc * 16);
+        }
+        r1 = sh->recv.as<uint32_t>();
+        r2 = r1 + rc;
+        rd = reinterpret_cast<double*>(r2 + rc);
         nccl_check(api.GroupStart(), "ncclGroupStart");
         for (uint32_t r = 0; r < world; ++r) {
             if (scnt[r]) {
@@ -390,10 +396,14 @@ void routed_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1, const u
     unsigned long long tot[2] = {0, 0};
     if (count) {
         // sd holds this rank's answers in send order
-        DBuf dout(count * 8);
-        route_gather<<<unsigned((count + 255) / 256), 256, 0, s>>>(sd, dslot, count, dout.as<double>());
+        if (sh->out.bytes < count * 8) {
+            CK(cudaStreamSynchronize(s));
+            sh->out.alloc(count * 8);
+        }
+        route_gather<<<unsigned((count + 255) / 256), 256, 0, s>>>(sd, dslot, count,
+                                                                    sh->out.as<double>());
         CK_LAUNCH();
-        CK(cudaMemcpyAsync(dist, dout.p, count * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(dist, sh->out.p, count * 8, cudaMemcpyDeviceToHost, s));
         if (exec_on) CK(cudaMemcpyAsync(exec_on, oE, count * 4, cudaMemcpyDeviceToHost, s));
         if (col_owner) CK(cudaMemcpyAsync(col_owner, oC, count * 4, cudaMemcpyDeviceToHost, s));
         if (entries) CK(cudaMemcpyAsync(entries, oN, count * 4, cudaMemcpyDeviceToHost, s));
