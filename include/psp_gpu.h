@@ -43,7 +43,8 @@ typedef enum psp_status {
     PSP_EGRAPH = 6,     /* graph invariant violated (psp::GraphInvariantError)   */
     PSP_EIO = 7,        /* file unreadable / truncated / inconsistent (psp::IoError) */
     PSP_EFORMAT = 8,    /* not a PSP1 file or wrong version (psp::FormatVersionError) */
-    PSP_ECHECKSUM = 9   /* CRC-64 mismatch (psp::ChecksumError)                  */
+    PSP_ECHECKSUM = 9,  /* CRC-64 mismatch (psp::ChecksumError)                  */
+    PSP_EPARSE = 10     /* malformed graph text (psp::ParseError); line: psp_gpu_last_parse_line */
 } psp_status;
 
 enum {
@@ -234,6 +235,42 @@ psp_status psp_gpu_routed_query_batch(psp_gpu_shard* sh, uint64_t count, const u
                                       const uint32_t* v2, double* dist, uint32_t* executed_on,
                                       uint32_t* column_owner, uint32_t* transfer_entries,
                                       psp_routed_stats* stats);
+
+/* ------------------------------------------------------ graph ingestion -- */
+/* psp::load_graph / read_graph / save_graph / write_graph / format_weight
+ * (include/psp/graph_io.hpp:10-25). The text is parsed on the GPU; graphs,
+ * values and ParseError messages ("<name>:<line>: <msg>") are the
+ * reference's. Edge lists are strict; DIMACS arcs are normalised (min weight
+ * per unordered pair, symmetrised, self-loops dropped, (u, v) order). */
+enum psp_graph_format {
+    PSP_FORMAT_EDGE_LIST = 0, /* "n m" header, one "u v w" line per edge   */
+    PSP_FORMAT_DIMACS = 1     /* "p sp n m", "a u v w" arcs, 1-based ids  */
+};
+typedef struct psp_graph psp_graph;
+
+/* File -> graph (PSP_EIO if unreadable, PSP_EPARSE / PSP_EGRAPH as the
+ * reference throws ParseError / GraphInvariantError). */
+psp_status psp_gpu_load_graph(psp_gpu_ctx* ctx, const char* path, int format, psp_graph** out);
+/* In-memory text -> graph; `name` prefixes parse errors (reference: "<stream>"). */
+psp_status psp_gpu_read_graph(psp_gpu_ctx* ctx, const char* text, uint64_t len, int format,
+                              const char* name, psp_graph** out);
+psp_status psp_graph_size(const psp_graph* g, uint64_t* n, uint64_t* m);
+/* Edges as parsed (edge list: file order; DIMACS: normalised order). */
+psp_status psp_graph_edges(const psp_graph* g, uint32_t* eu, uint32_t* ev, double* ew);
+void psp_graph_free(psp_graph* g);
+/* Line of the last PSP_EPARSE on this thread (psp::ParseError::line()). */
+uint64_t psp_gpu_last_parse_line(void);
+
+/* write_graph: text of the graph (edges validated as psp::Graph does, then
+ * written from its sorted edge list) into buf; call with buf == NULL for
+ * the length. save_graph writes it to a file. */
+psp_status psp_write_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                           const double* ew, int format, char* buf, uint64_t cap, uint64_t* len);
+psp_status psp_save_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                          const double* ew, const char* path, int format);
+/* Shortest decimal that parses back to w (std::to_chars); buf >= 32 bytes;
+ * returns the length. */
+uint32_t psp_format_weight(double w, char* buf);
 
 /* ---------------------------------------------------------- primitives -- */
 /* psp::apsp_dense (include/psp/shortest_paths.hpp:43): dense APSP of one

@@ -93,6 +93,11 @@ class RefLib:
             lib.ref_random_pairs.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]
             lib.ref_save_oracle.argtypes = [vp, C.c_char_p]
             lib.ref_load_oracle.argtypes = [C.c_char_p, C.POINTER(vp)]
+            lib.ref_read_graph.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_char_p,
+                                           C.POINTER(vp), C.POINTER(C.c_int),
+                                           C.POINTER(C.c_uint64)]
+            lib.ref_write_graph.argtypes = [vp, C.c_int, C.c_char_p, C.c_uint64,
+                                            C.POINTER(C.c_uint64)]
             lib.ref_place_components.argtypes = [C.c_uint32, C.c_uint32, C.c_int, _u32p]
             lib.ref_routed_query.argtypes = [vp, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
                                              C.c_uint64, _f64p]
@@ -114,6 +119,26 @@ class RefLib:
         v2 = np.empty(count, np.uint32)
         self.lib.ref_random_pairs(n, count, seed, v1, v2)
         return v1, v2
+
+    # graph text (include/psp/graph_io.hpp) -----------------------------
+    def read_graph(self, text, fmt: int = 0, name: str = "<stream>"):
+        """psp::read_graph: returns ("ok", RefGraph) or (kind, message, line)
+        with kind "parse" | "graph" | "io" | "other"."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h, kind, line = C.c_void_p(), C.c_int(), C.c_uint64()
+        rc = self.lib.ref_read_graph(data, len(data), fmt, name.encode(), C.byref(h),
+                                     C.byref(kind), C.byref(line))
+        if rc == 0:
+            return "ok", RefGraph(self, h)
+        kinds = {1: "parse", 2: "graph", 3: "io", 4: "other"}
+        return kinds[kind.value], self.lib.ref_last_error().decode(), int(line.value)
+
+    def write_graph(self, g: "RefGraph", fmt: int = 0) -> str:
+        n = C.c_uint64()
+        self._check(self.lib.ref_write_graph(g.h, fmt, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self._check(self.lib.ref_write_graph(g.h, fmt, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value].decode()
 
     # cluster layer (include/psp/placement.hpp, include/psp/cluster.hpp) ---
     def place_components(self, k: int, p: int, policy: int = 0) -> np.ndarray:

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <exception>
 #include <random>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <utility>
@@ -29,6 +30,8 @@
 #include "psp/cluster.hpp"
 #include "psp/generators.hpp"
 #include "psp/graph.hpp"
+#include "psp/errors.hpp"
+#include "psp/graph_io.hpp"
 #include "psp/oracle.hpp"
 #include "psp/oracle_io.hpp"
 #include "psp/partition.hpp"
@@ -291,6 +294,47 @@ int ref_load_oracle(const char* path, void** out) {
             throw;
         }
         *out = ro;
+    });
+}
+
+// --- graph text (include/psp/graph_io.hpp) ---
+// kind: 0 ok, 1 ParseError (line set), 2 GraphInvariantError, 3 IoError, 4 other
+int ref_read_graph(const char* text, uint64_t len, int format, const char* name, void** out,
+                   int* kind, uint64_t* line) {
+    *kind = 0;
+    *line = 0;
+    try {
+        std::istringstream in(std::string(text, len));
+        auto* rg = new RefGraph{psp::read_graph(
+            in, format == 1 ? psp::FileFormat::DimacsGr : psp::FileFormat::EdgeList, name)};
+        *out = rg;
+        return 0;
+    } catch (const psp::ParseError& e) {
+        g_err = e.what();
+        *kind = 1;
+        *line = e.line();
+    } catch (const psp::GraphInvariantError& e) {
+        g_err = e.what();
+        *kind = 2;
+    } catch (const psp::IoError& e) {
+        g_err = e.what();
+        *kind = 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        *kind = 4;
+    }
+    return 1;
+}
+
+// write_graph into buf (cap bytes); *len = full length
+int ref_write_graph(const void* g, int format, char* buf, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        std::ostringstream out;
+        psp::write_graph(static_cast<const RefGraph*>(g)->g, out,
+                         format == 1 ? psp::FileFormat::DimacsGr : psp::FileFormat::EdgeList);
+        const std::string t = out.str();
+        *len = t.size();
+        if (buf) std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
     });
 }
 

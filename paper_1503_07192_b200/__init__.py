@@ -21,14 +21,16 @@ import numpy as np
 
 from . import _lib
 from ._lib import (VALUE_AUTO, VALUE_F32, VALUE_U32, BuildStats, ChecksumError,
-                   FormatVersionError, GraphInvariantError, OracleIoError, PspError, PspValueError)
+                   FormatVersionError, GraphInvariantError, OracleIoError, ParseError, PspError,
+                   PspValueError)
 
 from . import cluster  # noqa: E402  (placement + routed queries, cluster.hpp)
 from .cluster import (PAIRS_PER_GPU, ROUND_ROBIN, Placement, RoutedOracle,  # noqa: E402
                       TransferLedger, TransferRecord, place_components, routed_query,
                       simulate_build_schedule)
 
-__all__ = ["cluster", "Placement", "RoutedOracle", "TransferLedger", "TransferRecord",
+__all__ = ["load_graph", "read_graph", "save_graph", "write_graph", "format_weight",
+           "ParseError", "EDGE_LIST", "DIMACS", "cluster", "Placement", "RoutedOracle", "TransferLedger", "TransferRecord",
            "place_components", "routed_query", "simulate_build_schedule", "ROUND_ROBIN",
            "PAIRS_PER_GPU", "Graph", "Context", "nccl_unique_id", "import_oracle", "GpuOracle", "build_oracle", "build_partitioned", "apsp_dense",
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
@@ -308,6 +310,90 @@ def generate_grid(rows: int, cols: int, weights=None, seed: int = 0) -> Graph:
 def generate_triangulated_grid(rows: int, cols: int, weights=None, seed: int = 0) -> Graph:
     """psp::generate_triangulated_grid."""
     return _grid(1, rows, cols, weights, seed)
+
+
+# ------------------------------------------------------- graph ingestion --
+# psp::FileFormat (include/psp/graph_io.hpp:10-13)
+EDGE_LIST, DIMACS = "edge_list", "dimacs"
+_FORMATS = {EDGE_LIST: _lib.FORMAT_EDGE_LIST, DIMACS: _lib.FORMAT_DIMACS}
+
+
+def _format(fmt: str) -> int:
+    if fmt not in _FORMATS:
+        raise ValueError(f"unknown graph format {fmt!r} (edge_list | dimacs)")
+    return _FORMATS[fmt]
+
+
+def _take_graph(h) -> Graph:
+    L = _lib.lib()
+    n, m = C.c_uint64(), C.c_uint64()
+    try:
+        _lib.check(L.psp_graph_size(h, C.byref(n), C.byref(m)))
+        eu = np.empty(max(m.value, 1), np.uint32)
+        ev = np.empty(max(m.value, 1), np.uint32)
+        ew = np.empty(max(m.value, 1), np.float64)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        _lib.check(L.psp_graph_edges(h, p(eu), p(ev), p(ew)))
+    finally:
+        L.psp_graph_free(h)
+    k = m.value
+    return Graph(int(n.value), eu[:k], ev[:k], ew[:k])
+
+
+def load_graph(path: str, fmt: str = EDGE_LIST, ctx: Context | None = None) -> Graph:
+    """psp::load_graph (graph_io.hpp:18): the file is parsed on the GPU.
+    Raises ParseError / GraphInvariantError / OracleIoError as the reference
+    throws ParseError / GraphInvariantError / IoError."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _lib.check(_lib.lib().psp_gpu_load_graph(ctx.h, os.fsencode(path), _format(fmt), C.byref(h)))
+    return _take_graph(h)
+
+
+def read_graph(text, fmt: str = EDGE_LIST, name: str = "<stream>",
+               ctx: Context | None = None) -> Graph:
+    """psp::read_graph (graph_io.hpp:19) over in-memory text (str or bytes)."""
+    ctx = ctx or default_context()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    _lib.check(_lib.lib().psp_gpu_read_graph(ctx.h, data, len(data), _format(fmt),
+                                             name.encode(), C.byref(h)))
+    return _take_graph(h)
+
+
+def _edges(g: Graph):
+    eu = np.ascontiguousarray(g.eu, np.uint32)
+    ev = np.ascontiguousarray(g.ev, np.uint32)
+    ew = np.ascontiguousarray(g.ew, np.float64)
+    return eu, ev, ew, (lambda a: a.ctypes.data_as(C.c_void_p))
+
+
+def write_graph(g: Graph, fmt: str = EDGE_LIST) -> str:
+    """psp::write_graph (graph_io.hpp:22): the graph's sorted edge list as
+    text, byte-identical to the reference's."""
+    eu, ev, ew, p = _edges(g)
+    L = _lib.lib()
+    n = C.c_uint64()
+    _lib.check(L.psp_write_graph(g.n, len(eu), p(eu), p(ev), p(ew), _format(fmt), None, 0,
+                                 C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    _lib.check(L.psp_write_graph(g.n, len(eu), p(eu), p(ev), p(ew), _format(fmt), buf, n.value,
+                                 C.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def save_graph(g: Graph, path: str, fmt: str = EDGE_LIST) -> None:
+    """psp::save_graph (graph_io.hpp:21)."""
+    eu, ev, ew, p = _edges(g)
+    _lib.check(_lib.lib().psp_save_graph(g.n, len(eu), p(eu), p(ev), p(ew), os.fsencode(path),
+                                         _format(fmt)))
+
+
+def format_weight(w: float) -> str:
+    """psp::format_weight (graph_io.hpp:25): shortest exact decimal."""
+    buf = C.create_string_buffer(32)
+    k = _lib.lib().psp_format_weight(float(w), buf)
+    return buf.raw[:k].decode()
 
 
 def random_pairs(n: int, count: int, seed: int, order: str = "cli"):

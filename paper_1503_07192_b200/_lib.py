@@ -15,7 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpsp_gpu.so")
 
 (PSP_OK, PSP_EINVAL, PSP_ENOMEM, PSP_ECUDA, PSP_ENCCL, PSP_EOVERFLOW, PSP_EGRAPH, PSP_EIO,
- PSP_EFORMAT, PSP_ECHECKSUM) = range(10)
+ PSP_EFORMAT, PSP_ECHECKSUM, PSP_EPARSE) = range(11)
+FORMAT_EDGE_LIST, FORMAT_DIMACS = 0, 1
 VALUE_AUTO, VALUE_U32, VALUE_F32 = 0, 1, 2
 VALUE_NAMES = {VALUE_U32: "u32", VALUE_F32: "f32"}
 
@@ -47,6 +48,15 @@ class FormatVersionError(OracleIoError):
 
 class ChecksumError(OracleIoError):
     """psp::ChecksumError (include/psp/errors.hpp:40-43)."""
+
+
+class ParseError(PspError):
+    """psp::ParseError (include/psp/errors.hpp:10-19): malformed graph text;
+    the message is "<name>:<line>: <what>", `line` the 1-based line."""
+
+    def __init__(self, status: int, msg: str, line: int):
+        super().__init__(status, msg)
+        self.line = line
 
 
 class BuildStats(C.Structure):
@@ -140,6 +150,17 @@ SIGNATURES = {
     "psp_gpu_shard_bytes": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
     "psp_gpu_routed_query_batch": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp, _vp,
                                              C.POINTER(RoutedStats)]),
+    "psp_gpu_load_graph": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
+    "psp_gpu_read_graph": (C.c_int, [_vp, C.c_char_p, C.c_uint64, C.c_int, C.c_char_p,
+                                     C.POINTER(_vp)]),
+    "psp_graph_size": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "psp_graph_edges": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "psp_graph_free": (None, [_vp]),
+    "psp_gpu_last_parse_line": (C.c_uint64, []),
+    "psp_write_graph": (C.c_int, [C.c_uint64, C.c_uint64, _vp, _vp, _vp, C.c_int, _vp, C.c_uint64,
+                                  C.POINTER(C.c_uint64)]),
+    "psp_save_graph": (C.c_int, [C.c_uint64, C.c_uint64, _vp, _vp, _vp, C.c_char_p, C.c_int]),
+    "psp_format_weight": (C.c_uint32, [C.c_double, C.c_char_p]),
     "psp_gpu_apsp_dense": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
                                      C.c_uint64, C.c_int, _f64p]),
     "psp_gpu_boundary_apsp": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
@@ -187,4 +208,6 @@ def check(status: int) -> None:
         raise FormatVersionError(status, msg)
     if status == PSP_EIO:
         raise OracleIoError(status, msg)
+    if status == PSP_EPARSE:
+        raise ParseError(status, msg, int(lib().psp_gpu_last_parse_line()))
     raise PspError(status, msg)

@@ -1,0 +1,690 @@
+// engine_graphio.cuh — graph ingestion at GB scale: psp::load_graph /
+// read_graph (src/graph_io.cpp:53-170) with the text parsed on the GPU.
+//
+// The reference reads line by line (getline + from_chars) and merges DIMACS
+// arcs in a std::map. Here the whole file goes to HBM once and is parsed in
+// parallel, with results identical to the reference's, errors included:
+//   L1  newline index: per-256-byte chunk counts, a scan, the positions;
+//   L2  one thread per line: trim, classify (blank / comment / header /
+//       edge or arc / other), tokenize, parse the ids (exact u64 with
+//       overflow) and the weight. Weights of the form digits[.digits] with
+//       <= 19 significant digits, mantissa < 2^53 and <= 22 fraction
+//       digits are converted exactly on the device (Clinger's fast path: one
+//       correctly rounded division of two exact doubles). Anything else
+//       ("1e5", "inf", "-0", long mantissas) marks the line HARD;
+//   host the earliest line that fails, or is HARD, is re-parsed by a
+//       line-for-line restatement of the reference's loop body with
+//       std::from_chars -- the same function the reference calls -- so
+//       values and ParseError messages are the reference's. Header lines,
+//       "more edges than declared" and the end-of-file checks follow the
+//       reference's order;
+//   DIMACS normalisation on the device: arcs keyed (min, max) << 32, radix
+//       sorted (stable, so file order survives among equal keys) and reduced
+//       by key with min -- the std::map's first-inserted-wins on equal
+//       weights and its (u, v) iteration order.
+// The Graph itself (CSR + invariant checks) is build_csr, whose messages
+// are the reference Graph constructor's.
+#pragma once
+
+#include <charconv>
+#include <thread>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+
+struct psp_graph {  // a parsed, validated graph (psp::Graph's edge input)
+    uint64_t n = 0;
+    std::vector<uint32_t> eu, ev;
+    std::vector<double> ew;
+};
+
+namespace {
+
+constexpr int PARSE_CHUNK = 256;
+
+// min that keeps the earlier value on ties (std::map's first insert wins
+// unless a later weight is strictly smaller, src/graph_io.cpp:129-130)
+struct KeepFirstMin {
+    __device__ __forceinline__ double operator()(double a, double b) const { return b < a ? b : a; }
+};
+
+__global__ void nl_count(const char* __restrict__ buf, uint64_t len, uint32_t* __restrict__ cnt,
+                         uint64_t nchunks) {
+    const uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const uint64_t a = c * PARSE_CHUNK, b = min(len, a + PARSE_CHUNK);
+    uint32_t k = 0;
+    for (uint64_t i = a; i < b; ++i) k += buf[i] == '\n';
+    cnt[c] = k;
+}
+
+__global__ void nl_write(const char* __restrict__ buf, uint64_t len,
+                         const uint32_t* __restrict__ off, uint64_t nchunks,
+                         uint64_t* __restrict__ nl) {
+    const uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const uint64_t a = c * PARSE_CHUNK, b = min(len, a + PARSE_CHUNK);
+    uint64_t at = off[c];
+    for (uint64_t i = a; i < b; ++i)
+        if (buf[i] == '\n') nl[at++] = i;
+}
+
+// line status
+enum : uint8_t { LN_SKIP = 0, LN_HEADER = 1, LN_EDGE = 2, LN_ERR = 3, LN_HARD = 4 };
+// line classes (first pass)
+enum : uint8_t { CL_SKIP = 0, CL_SIG = 1, CL_P = 2, CL_A = 3, CL_OTHER = 4 };
+
+struct LineSpan {
+    uint64_t a, b;  // trimmed body [a, b)
+};
+
+__device__ __forceinline__ LineSpan line_body(const char* buf, uint64_t len, const uint64_t* nl,
+                                              uint64_t nnl, uint64_t i) {
+    uint64_t a = i == 0 ? 0 : nl[i - 1] + 1;
+    uint64_t b = i < nnl ? nl[i] : len;
+    // trim " \t\r" both ends (src/graph_io.cpp:19-23)
+    while (a < b && (buf[a] == ' ' || buf[a] == '\t' || buf[a] == '\r')) ++a;
+    while (b > a && (buf[b - 1] == ' ' || buf[b - 1] == '\t' || buf[b - 1] == '\r')) --b;
+    return {a, b};
+}
+
+__global__ void classify_lines(const char* __restrict__ buf, uint64_t len,
+                               const uint64_t* __restrict__ nl, uint64_t nnl, uint64_t nlines,
+                               int dimacs, uint8_t* __restrict__ cls,
+                               unsigned long long* __restrict__ firsts) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines) return;
+    const LineSpan s = line_body(buf, len, nl, nnl, i);
+    uint8_t c = CL_SKIP;
+    if (s.a < s.b) {
+        const char f = buf[s.a];
+        if (!dimacs) c = f == '#' ? CL_SKIP : CL_SIG;
+        else c = f == 'c' ? CL_SKIP : f == 'p' ? CL_P : f == 'a' ? CL_A : CL_OTHER;
+    }
+    cls[i] = c;
+    // firsts[0] = first significant / 'p' line; firsts[1] = first 'a' or
+    // other line (DIMACS: an error if it precedes the problem line)
+    if (c == CL_SIG || c == CL_P) atomicMin(&firsts[0], (unsigned long long)i);
+    if (c == CL_A || c == CL_OTHER) atomicMin(&firsts[1], (unsigned long long)i);
+}
+
+// Splits [a, b) on runs of ' '/'\t' (src/graph_io.cpp:26-37); up to 5 tokens.
+__device__ __forceinline__ int split_tokens(const char* buf, uint64_t a, uint64_t b,
+                                            uint64_t (&ta)[5], uint64_t (&tb)[5]) {
+    int n = 0;
+    uint64_t i = a;
+    while (i < b) {
+        while (i < b && (buf[i] == ' ' || buf[i] == '\t')) ++i;
+        uint64_t j = i;
+        while (j < b && buf[j] != ' ' && buf[j] != '\t') ++j;
+        if (j > i) {
+            if (n < 5) {
+                ta[n] = i;
+                tb[n] = j;
+            }
+            ++n;
+        }
+        i = j;
+    }
+    return n;
+}
+
+// from_chars<uint64_t> on a whole token: digits only, no overflow
+__device__ __forceinline__ bool parse_u64(const char* buf, uint64_t a, uint64_t b, uint64_t& v) {
+    if (a >= b) return false;
+    uint64_t x = 0;
+    for (uint64_t i = a; i < b; ++i) {
+        const unsigned d = static_cast<unsigned char>(buf[i]) - '0';
+        if (d > 9) return false;
+        if (x > (~0ull - d) / 10) return false;  // overflow -> result_out_of_range
+        x = x * 10 + d;
+    }
+    v = x;
+    return true;
+}
+
+// Clinger's exact fast path; false = leave it to the host's from_chars
+__device__ __forceinline__ bool parse_weight_fast(const char* buf, uint64_t a, uint64_t b,
+                                                  double& w) {
+    uint64_t mant = 0;
+    int digits = 0, frac = 0;
+    bool dot = false, any = false;
+    for (uint64_t i = a; i < b; ++i) {
+        const char ch = buf[i];
+        if (ch == '.') {
+            if (dot) return false;
+            dot = true;
+            continue;
+        }
+        const unsigned d = static_cast<unsigned char>(ch) - '0';
+        if (d > 9) return false;
+        any = true;
+        if (mant != 0 || d != 0) ++digits;
+        if (digits > 19) return false;
+        mant = mant * 10 + d;
+        if (dot) ++frac;
+    }
+    if (!any || mant >= (1ull << 53) || frac > 22) return false;
+    const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                            1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+    w = double(mant) / p10[frac];
+    return true;
+}
+
+// Second pass, one thread per line: status + (u, v, w) of edge / arc lines.
+// Edge list: header = line `first`, every later significant line an edge.
+// DIMACS: arcs after the problem line (ids 1-based, checked against n).
+__global__ void parse_lines(const char* __restrict__ buf, uint64_t len,
+                            const uint64_t* __restrict__ nl, uint64_t nnl, uint64_t nlines,
+                            int dimacs, const uint8_t* __restrict__ cls, uint64_t first,
+                            uint64_t n, uint8_t* __restrict__ st, uint64_t* __restrict__ uu,
+                            uint64_t* __restrict__ vv, double* __restrict__ ww) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines) return;
+    const uint8_t c = cls[i];
+    uint8_t s = LN_SKIP;
+    if (i == first) {
+        s = LN_HEADER;
+    } else if (!dimacs && c == CL_SIG && i > first) {
+        s = LN_EDGE;
+    } else if (dimacs && i > first && (c == CL_P || c == CL_OTHER)) {
+        s = LN_ERR;  // duplicate problem line / unrecognized line type
+    } else if (dimacs && c == CL_A && i > first) {
+        s = LN_EDGE;
+    }
+    if (s == LN_EDGE) {
+        const LineSpan sp = line_body(buf, len, nl, nnl, i);
+        uint64_t ta[5], tb[5];
+        const int nt = split_tokens(buf, sp.a, sp.b, ta, tb);
+        const int t0 = dimacs ? 1 : 0;
+        uint64_t u = 0, v = 0;
+        double w = 0;
+        if (nt != 3 + t0 || !parse_u64(buf, ta[t0], tb[t0], u) ||
+            !parse_u64(buf, ta[t0 + 1], tb[t0 + 1], v)) {
+            s = LN_ERR;
+        } else if (!parse_weight_fast(buf, ta[t0 + 2], tb[t0 + 2], w)) {
+            s = LN_HARD;  // exact value (or its error) from the host
+        } else if (dimacs ? (u < 1 || u > n || v < 1 || v > n) : (u >= n || v >= n)) {
+            s = LN_ERR;
+        } else {
+            uu[i] = u;
+            vv[i] = v;
+            ww[i] = w;
+        }
+    }
+    st[i] = s;
+}
+
+// DIMACS normalisation keys: (min, max) 0-based, self-loop arcs dropped
+__global__ void arc_keys(const uint8_t* __restrict__ st, const uint64_t* __restrict__ uu,
+                         const uint64_t* __restrict__ vv, const double* __restrict__ ww,
+                         const uint32_t* __restrict__ pos, uint64_t nlines,
+                         uint64_t* __restrict__ key, double* __restrict__ w) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines || st[i] != LN_EDGE) return;
+    uint64_t a = uu[i] - 1, b = vv[i] - 1;
+    if (a == b) return;
+    if (a > b) {
+        const uint64_t t = a; a = b; b = t;
+    }
+    key[pos[i]] = (a << 32) | b;
+    w[pos[i]] = ww[i];
+}
+
+__global__ void edge_compact(const uint8_t* __restrict__ st, const uint64_t* __restrict__ uu,
+                             const uint64_t* __restrict__ vv, const double* __restrict__ ww,
+                             const uint32_t* __restrict__ pos, uint64_t nlines,
+                             uint32_t* __restrict__ eu, uint32_t* __restrict__ ev,
+                             double* __restrict__ ew) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines || st[i] != LN_EDGE) return;
+    eu[pos[i]] = static_cast<uint32_t>(uu[i]);
+    ev[pos[i]] = static_cast<uint32_t>(vv[i]);
+    ew[pos[i]] = ww[i];
+}
+
+// mode 0: edge / arc lines; 1: arcs without self-loops (DIMACS keys);
+// 2: every line after the header that is not skipped (edge, error, hard)
+__global__ void flag_to_u32(const uint8_t* __restrict__ st, uint64_t nlines, int mode,
+                            uint32_t* __restrict__ f, const uint64_t* __restrict__ uu,
+                            const uint64_t* __restrict__ vv) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines) return;
+    const uint8_t s = st[i];
+    bool on;
+    if (mode == 2) on = s == LN_EDGE || s == LN_ERR || s == LN_HARD;
+    else on = s == LN_EDGE && !(mode == 1 && uu[i] == vv[i]);
+    f[i] = on ? 1u : 0u;
+}
+
+__global__ void first_status(const uint8_t* __restrict__ st, uint64_t nlines,
+                             unsigned long long* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nlines) return;  // nlines doubles as the search bound
+    if (st[i] == LN_ERR || st[i] == LN_HARD) atomicMin(&out[0], (unsigned long long)i);
+}
+
+// ------------------------------------------------------------- host side --
+std::string_view host_trim(std::string_view s) {
+    while (!s.empty() && (s.front() == ' ' || s.front() == '\t' || s.front() == '\r')) s.remove_prefix(1);
+    while (!s.empty() && (s.back() == ' ' || s.back() == '\t' || s.back() == '\r')) s.remove_suffix(1);
+    return s;
+}
+
+std::vector<std::string_view> host_tokens(std::string_view s) {
+    std::vector<std::string_view> out;
+    size_t i = 0;
+    while (i < s.size()) {
+        while (i < s.size() && (s[i] == ' ' || s[i] == '\t')) ++i;
+        size_t j = i;
+        while (j < s.size() && s[j] != ' ' && s[j] != '\t') ++j;
+        if (j > i) out.push_back(s.substr(i, j - i));
+        i = j;
+    }
+    return out;
+}
+
+template <typename T>
+T host_number(std::string_view tok, const std::string& name, uint64_t line, const char* what) {
+    T value{};
+    auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), value);
+    if (ec != std::errc{} || ptr != tok.data() + tok.size())
+        throw ParseFail{name + ":" + std::to_string(line) + ": expected " + what + ", got '" +
+                            std::string(tok) + "'",
+                        line};
+    return value;
+}
+
+[[noreturn]] void parse_fail(const std::string& name, uint64_t line, const std::string& msg) {
+    throw ParseFail{name + ":" + std::to_string(line) + ": " + msg, line};
+}
+
+struct HostEdge {
+    uint64_t u, v;
+    double w;
+};
+
+// The reference's per-line bodies (src/graph_io.cpp:67-80 edge list,
+// :112-127 DIMACS arcs). Throws ParseFail; returns the parsed edge.
+HostEdge host_edge_line(std::string_view body, bool dimacs, uint64_t n, const std::string& name,
+                        uint64_t line) {
+    auto toks = host_tokens(body);
+    const size_t t0 = dimacs ? 1 : 0;
+    if (toks.size() != 3 + t0)
+        parse_fail(name, line, dimacs ? "arc line must be 'a u v w'" : "edge line must be 'u v w'");
+    const auto u = host_number<uint64_t>(toks[t0], name, line, "vertex id");
+    const auto v = host_number<uint64_t>(toks[t0 + 1], name, line, "vertex id");
+    const auto w = host_number<double>(toks[t0 + 2], name, line, "weight");
+    if (dimacs) {
+        if (u < 1 || u > n || v < 1 || v > n)
+            parse_fail(name, line, "vertex id out of range (ids are 1-based)");
+    } else if (u >= n || v >= n) {
+        parse_fail(name, line, "vertex id out of range");
+    }
+    if (w < 0.0) parse_fail(name, line, "negative weight");
+    if (std::isnan(w) || std::isinf(w)) parse_fail(name, line, "non-finite weight");
+    return {u, v, w};
+}
+
+struct ParsedGraph {
+    uint64_t n = 0;
+    std::vector<uint32_t> eu, ev;
+    std::vector<double> ew;
+};
+
+struct DevText {
+    DBuf buf;
+    uint64_t len = 0;
+};
+
+// Reads a file into device memory (pinned bounce buffer, chunked).
+DevText read_to_device(const std::string& path, cudaStream_t s) {
+    const int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw Fail{PSP_EIO, "cannot open '" + path + "' for reading"};
+    struct stat sb;
+    if (fstat(fd, &sb) != 0) {
+        ::close(fd);
+        throw Fail{PSP_EIO, "cannot open '" + path + "' for reading"};
+    }
+    DevText t;
+    t.len = static_cast<uint64_t>(sb.st_size);
+    t.buf.alloc(t.len + 1);
+    constexpr size_t CH = 64ull << 20;
+    std::vector<char*> pin(2, nullptr);
+    for (auto& p : pin) CK(cudaMallocHost(&p, CH));
+    cudaEvent_t ev[2];
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    uint64_t off = 0;
+    int k = 0;
+    std::string err;
+    while (off < t.len && err.empty()) {
+        CK(cudaEventSynchronize(ev[k]));  // this bounce buffer's previous copy is done
+        const size_t want = std::min<uint64_t>(CH, t.len - off);
+        size_t got = 0;
+        while (got < want) {
+            const ssize_t r = ::pread(fd, pin[k] + got, want - got, off + got);
+            if (r <= 0) {
+                err = "read from '" + path + "' failed";
+                break;
+            }
+            got += size_t(r);
+        }
+        if (!err.empty()) break;
+        CK(cudaMemcpyAsync(t.buf.as<char>() + off, pin[k], want, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ev[k], s));
+        off += want;
+        k ^= 1;
+    }
+    ::close(fd);
+    CK(cudaStreamSynchronize(s));
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto p : pin) cudaFreeHost(p);
+    if (!err.empty()) throw Fail{PSP_EIO, err};
+    return t;
+}
+
+DevText text_to_device(const char* text, uint64_t len, cudaStream_t s) {
+    DevText t;
+    t.len = len;
+    t.buf.alloc(len + 1);
+    if (len) CK(cudaMemcpyAsync(t.buf.p, text, len, cudaMemcpyHostToDevice, s));
+    return t;
+}
+
+std::string host_line(const DevText& t, const std::vector<uint64_t>& nl_host_pair, cudaStream_t s) {
+    // nl_host_pair = {a, b} byte range of the line
+    const uint64_t a = nl_host_pair[0], b = nl_host_pair[1];
+    std::string line(b - a, '\0');
+    if (b > a) CK(cudaMemcpyAsync(line.data(), t.buf.as<char>() + a, b - a, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return line;
+}
+
+ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string& name,
+                               cudaStream_t s, int sms) {
+    const char* buf = t.buf.as<char>();
+    const uint64_t len = t.len;
+    const uint64_t nchunks = (len + PARSE_CHUNK - 1) / PARSE_CHUNK;
+    // L1: newline positions
+    DBuf cnt((nchunks + 1) * 4), off((nchunks + 1) * 4);
+    CK(cudaMemsetAsync(cnt.p, 0, (nchunks + 1) * 4, s));
+    if (nchunks) {
+        nl_count<<<unsigned((nchunks + 255) / 256), 256, 0, s>>>(buf, len, cnt.as<uint32_t>(), nchunks);
+        CK_LAUNCH();
+    }
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), off.as<uint32_t>(),
+                                     int(nchunks + 1), s));
+    DBuf tmp(tb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<uint32_t>(), off.as<uint32_t>(),
+                                     int(nchunks + 1), s));
+    uint32_t nnl32 = 0;
+    CK(cudaMemcpyAsync(&nnl32, off.as<uint32_t>() + nchunks, 4, cudaMemcpyDeviceToHost, s));
+    char last = '\n';
+    if (len) CK(cudaMemcpyAsync(&last, buf + len - 1, 1, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t nnl = nnl32;
+    // getline: a final line without '\n' still counts
+    const uint64_t nlines = nnl + (len > 0 && last != '\n' ? 1 : 0);
+    DBuf nl(std::max<uint64_t>(nnl, 1) * 8);
+    if (nchunks) {
+        nl_write<<<unsigned((nchunks + 255) / 256), 256, 0, s>>>(buf, len, off.as<uint32_t>(), nchunks,
+                                                                 nl.as<uint64_t>());
+        CK_LAUNCH();
+    }
+    const uint64_t* d_nl = nl.as<uint64_t>();
+    auto line_range = [&](uint64_t i) {
+        std::vector<uint64_t> r(2);
+        uint64_t prev = 0, cur = len;
+        if (i > 0) CK(cudaMemcpyAsync(&prev, d_nl + i - 1, 8, cudaMemcpyDeviceToHost, s));
+        if (i < nnl) CK(cudaMemcpyAsync(&cur, d_nl + i, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        r[0] = i > 0 ? prev + 1 : 0;
+        r[1] = cur;
+        return r;
+    };
+    auto body_of = [&](uint64_t i) { return host_line(t, line_range(i), s); };
+    const unsigned lb = unsigned((std::max<uint64_t>(nlines, 1) + 255) / 256);
+    const uint64_t lineno_end = nlines ? nlines : 1;  // "lineno ? lineno : 1"
+
+    // L2a: classes and the first header line
+    DBuf cls(std::max<uint64_t>(nlines, 1)), firsts(16);
+    std::vector<unsigned long long> hf = {~0ull, ~0ull};
+    CK(cudaMemcpyAsync(firsts.p, hf.data(), 16, cudaMemcpyHostToDevice, s));
+    if (nlines) {
+        classify_lines<<<lb, 256, 0, s>>>(buf, len, d_nl, nnl, nlines, dimacs ? 1 : 0,
+                                          cls.as<uint8_t>(), firsts.as<unsigned long long>());
+        CK_LAUNCH();
+    }
+    CK(cudaMemcpyAsync(hf.data(), firsts.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t first = hf[0];
+    // DIMACS lines before the problem line: 'a' or unknown -> error there
+    if (dimacs && hf[1] != ~0ull && hf[1] < first) {
+        const std::string line = body_of(hf[1]);
+        const std::string_view body = host_trim(line);
+        if (body.front() == 'a') parse_fail(name, hf[1] + 1, "arc line before problem line");
+        parse_fail(name, hf[1] + 1, "unrecognized line type '" + std::string(1, body.front()) + "'");
+    }
+    if (first == ~0ull)
+        parse_fail(name, lineno_end, dimacs ? "missing 'p sp n m' line" : "missing 'n m' header");
+    // the header (src/graph_io.cpp:58-66, :103-110)
+    uint64_t n = 0, m = 0;
+    {
+        const std::string line = body_of(first);
+        const auto toks = host_tokens(host_trim(line));
+        const uint64_t ln = first + 1;
+        if (dimacs) {
+            if (toks.size() != 4 || toks[1] != "sp") parse_fail(name, ln, "problem line must be 'p sp n m'");
+            n = host_number<size_t>(toks[2], name, ln, "vertex count");
+            m = host_number<size_t>(toks[3], name, ln, "arc count");
+        } else {
+            if (toks.size() != 2) parse_fail(name, ln, "header must be 'n m'");
+            n = host_number<size_t>(toks[0], name, ln, "vertex count");
+            m = host_number<size_t>(toks[1], name, ln, "edge count");
+        }
+    }
+    // L2b: every later line
+    DBuf st(std::max<uint64_t>(nlines, 1)), uu(std::max<uint64_t>(nlines, 1) * 8),
+        vv(std::max<uint64_t>(nlines, 1) * 8), ww(std::max<uint64_t>(nlines, 1) * 8);
+    parse_lines<<<lb, 256, 0, s>>>(buf, len, d_nl, nnl, nlines, dimacs ? 1 : 0, cls.as<uint8_t>(),
+                                   first, n, st.as<uint8_t>(), uu.as<uint64_t>(), vv.as<uint64_t>(),
+                                   ww.as<double>());
+    CK_LAUNCH();
+    // positions of the edge / arc lines in file order
+    DBuf flag(std::max<uint64_t>(nlines, 1) * 4 + 4), pos(std::max<uint64_t>(nlines, 1) * 4 + 4);
+    auto positions = [&](int mode) -> uint64_t {
+        CK(cudaMemsetAsync(flag.p, 0, flag.bytes, s));
+        if (nlines) {
+            flag_to_u32<<<lb, 256, 0, s>>>(st.as<uint8_t>(), nlines, mode, flag.as<uint32_t>(),
+                                           uu.as<uint64_t>(), vv.as<uint64_t>());
+            CK_LAUNCH();
+        }
+        size_t b2 = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, flag.as<uint32_t>(), pos.as<uint32_t>(),
+                                         int(nlines + 1), s));
+        DBuf t2(b2);
+        CK(cub::DeviceScan::ExclusiveSum(t2.p, b2, flag.as<uint32_t>(), pos.as<uint32_t>(),
+                                         int(nlines + 1), s));
+        uint32_t total = 0;
+        CK(cudaMemcpyAsync(&total, pos.as<uint32_t>() + nlines, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return total;
+    };
+    // Edge list: the (m+1)-th line after the header stops the reference with
+    // "more edges than declared" (:80) unless it, or an earlier line, fails
+    // first -- so errors are only searched up to and including that line.
+    uint64_t cut = nlines;  // search bound (exclusive)
+    if (!dimacs) {
+        const uint64_t nsig = positions(2);
+        if (nsig > m) {
+            std::vector<uint32_t> hpos(nlines + 1);
+            CK(cudaMemcpyAsync(hpos.data(), pos.p, (nlines + 1) * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            cut = std::upper_bound(hpos.begin(), hpos.end(), uint32_t(m)) - hpos.begin();
+        }
+    }
+    // resolve lines in file order until the first real error: HARD lines
+    // are re-parsed on the host (their values written back), ERR lines give
+    // the reference's message
+    DBuf fe(8);
+    for (;;) {
+        unsigned long long f = ~0ull;
+        CK(cudaMemcpyAsync(fe.p, &f, 8, cudaMemcpyHostToDevice, s));
+        first_status<<<lb, 256, 0, s>>>(st.as<uint8_t>(), cut, fe.as<unsigned long long>());
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(&f, fe.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (f == ~0ull) break;  // no error up to the bound
+        const std::string line = body_of(f);
+        const std::string_view body = host_trim(line);
+        const uint64_t ln = f + 1;
+        if (dimacs && body.front() == 'p') parse_fail(name, ln, "duplicate problem line");
+        if (dimacs && body.front() != 'a')
+            parse_fail(name, ln, "unrecognized line type '" + std::string(1, body.front()) + "'");
+        const HostEdge e = host_edge_line(body, dimacs, n, name, ln);  // throws for ERR lines
+        const uint8_t ok = LN_EDGE;
+        CK(cudaMemcpyAsync(uu.as<uint64_t>() + f, &e.u, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(vv.as<uint64_t>() + f, &e.v, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ww.as<double>() + f, &e.w, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(st.as<uint8_t>() + f, &ok, 1, cudaMemcpyHostToDevice, s));
+    }
+    if (cut < nlines) parse_fail(name, cut, "more edges than declared in header");
+    const uint64_t nedge_lines = positions(0);
+    ParsedGraph G;
+    G.n = n;
+    if (!dimacs) {
+        if (nedge_lines != m)
+            parse_fail(name, lineno_end,
+                       "declared " + std::to_string(m) + " edges, found " + std::to_string(nedge_lines));
+        G.eu.resize(m);
+        G.ev.resize(m);
+        G.ew.resize(m);
+        DBuf du(m * 4 + 4), dv(m * 4 + 4), dw(m * 8 + 8);
+        if (nlines) {
+            edge_compact<<<lb, 256, 0, s>>>(st.as<uint8_t>(), uu.as<uint64_t>(), vv.as<uint64_t>(),
+                                            ww.as<double>(), pos.as<uint32_t>(), nlines,
+                                            du.as<uint32_t>(), dv.as<uint32_t>(), dw.as<double>());
+            CK_LAUNCH();
+        }
+        if (m) {
+            CK(cudaMemcpyAsync(G.eu.data(), du.p, m * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(G.ev.data(), dv.p, m * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(G.ew.data(), dw.p, m * 8, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        return G;
+    }
+    // DIMACS: arcs_seen counts self-loop arcs too (src/graph_io.cpp:123-124)
+    if (nedge_lines != m)
+        parse_fail(name, lineno_end,
+                   "declared " + std::to_string(m) + " arcs, found " + std::to_string(nedge_lines));
+    const uint64_t na = positions(1);  // keyed arcs: self-loops dropped
+    DBuf k1(na * 8 + 8), k2(na * 8 + 8), w1(na * 8 + 8), w2(na * 8 + 8), uk(na * 8 + 8),
+        uw(na * 8 + 8), nrun(8);
+    if (nlines) {
+        arc_keys<<<lb, 256, 0, s>>>(st.as<uint8_t>(), uu.as<uint64_t>(), vv.as<uint64_t>(),
+                                    ww.as<double>(), pos.as<uint32_t>(), nlines, k1.as<uint64_t>(),
+                                    w1.as<double>());
+        CK_LAUNCH();
+    }
+    uint64_t runs = 0;
+    if (na) {
+        size_t b3 = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, b3, k1.as<uint64_t>(), k2.as<uint64_t>(),
+                                           w1.as<double>(), w2.as<double>(), int(na), 0, 64, s));
+        DBuf t3(b3);
+        CK(cub::DeviceRadixSort::SortPairs(t3.p, b3, k1.as<uint64_t>(), k2.as<uint64_t>(),
+                                           w1.as<double>(), w2.as<double>(), int(na), 0, 64, s));
+        size_t b4 = 0;
+        CK(cub::DeviceReduce::ReduceByKey(nullptr, b4, k2.as<uint64_t>(), uk.as<uint64_t>(),
+                                          w2.as<double>(), uw.as<double>(), nrun.as<int>(),
+                                          KeepFirstMin{}, int(na), s));
+        DBuf t4(b4);
+        CK(cub::DeviceReduce::ReduceByKey(t4.p, b4, k2.as<uint64_t>(), uk.as<uint64_t>(),
+                                          w2.as<double>(), uw.as<double>(), nrun.as<int>(),
+                                          KeepFirstMin{}, int(na), s));
+        int r = 0;
+        CK(cudaMemcpyAsync(&r, nrun.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        runs = uint64_t(r);
+    }
+    std::vector<uint64_t> keys(runs);
+    G.ew.resize(runs);
+    if (runs) {
+        CK(cudaMemcpyAsync(keys.data(), uk.p, runs * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(G.ew.data(), uw.p, runs * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    G.eu.resize(runs);
+    G.ev.resize(runs);
+    for (uint64_t i = 0; i < runs; ++i) {
+        G.eu[i] = static_cast<uint32_t>(keys[i] >> 32);
+        G.ev[i] = static_cast<uint32_t>(keys[i] & 0xffffffffu);
+    }
+    (void)sms;
+    return G;
+}
+
+// ------------------------------------------------------------- writer --
+// format_weight (src/graph_io.cpp:147-151): shortest round-trip decimal.
+uint32_t format_weight_into(double w, char* buf) {
+    auto r = std::to_chars(buf, buf + 32, w);
+    return static_cast<uint32_t>(r.ptr - buf);
+}
+
+// write_graph (src/graph_io.cpp:160-176) of the CSR's edge list (u < v,
+// lexicographic, Graph::edge_list), formatted on all host threads.
+std::string write_graph_text(const Csr& g, bool dimacs, unsigned threads) {
+    std::vector<uint64_t> ecount(g.n + 1, 0);  // edges with u < v per vertex, prefix
+    for (uint64_t u = 0; u < g.n; ++u) {
+        uint64_t c = 0;
+        for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) c += g.to[e] > u;
+        ecount[u + 1] = ecount[u] + c;
+    }
+    const uint64_t m = ecount[g.n];
+    std::string head = dimacs ? "p sp " + std::to_string(g.n) + " " + std::to_string(2 * m) + "\n"
+                              : std::to_string(g.n) + " " + std::to_string(m) + "\n";
+    threads = std::max(1u, std::min<unsigned>(threads, unsigned(std::max<uint64_t>(1, g.n / 4096))));
+    std::vector<std::string> part(threads);
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            const uint64_t u0 = g.n * t / threads, u1 = g.n * (t + 1) / threads;
+            std::string& out = part[t];
+            out.reserve((ecount[u1] - ecount[u0]) * (dimacs ? 48 : 24));
+            char wb[32], ib[24];
+            for (uint64_t u = u0; u < u1; ++u)
+                for (uint64_t e = g.off[u]; e < g.off[u + 1]; ++e) {
+                    const uint64_t v = g.to[e];
+                    if (v <= u) continue;
+                    const uint32_t wl = format_weight_into(g.w[e], wb);
+                    auto put = [&](uint64_t x) {
+                        auto r = std::to_chars(ib, ib + sizeof ib, x);
+                        out.append(ib, r.ptr);
+                    };
+                    if (!dimacs) {
+                        put(u); out.push_back(' '); put(v); out.push_back(' ');
+                        out.append(wb, wl); out.push_back('\n');
+                    } else {  // both arc directions, 1-based
+                        out.append("a "); put(u + 1); out.push_back(' '); put(v + 1); out.push_back(' ');
+                        out.append(wb, wl); out.push_back('\n');
+                        out.append("a "); put(v + 1); out.push_back(' '); put(u + 1); out.push_back(' ');
+                        out.append(wb, wl); out.push_back('\n');
+                    }
+                }
+        });
+    for (auto& th : pool) th.join();
+    size_t total = head.size();
+    for (auto& p : part) total += p.size();
+    std::string out;
+    out.reserve(total);
+    out += head;
+    for (auto& p : part) out += p;
+    return out;
+}
+
+}  // namespace

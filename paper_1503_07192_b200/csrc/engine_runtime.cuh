@@ -6,10 +6,16 @@
 namespace {
 
 thread_local std::string g_err;
+thread_local uint64_t g_parse_line = 0;  // psp::ParseError::line() of the last PSP_EPARSE
 
 struct Fail {
     psp_status st;
     std::string msg;
+};
+
+struct ParseFail {  // psp::ParseError: "<name>:<line>: <msg>"
+    std::string msg;
+    uint64_t line;
 };
 
 #define CK(x)                                                                          \
@@ -29,6 +35,10 @@ psp_status guarded(F&& f) {
     } catch (const Fail& e) {
         g_err = e.msg;
         return e.st;
+    } catch (const ParseFail& e) {
+        g_err = e.msg;
+        g_parse_line = e.line;
+        return PSP_EPARSE;
     } catch (const GraphError& e) {
         g_err = e.what();
         return PSP_EGRAPH;

@@ -19,6 +19,7 @@
 //   engine_oracle.cuh    device oracle: build, import, export, query launch
 //   engine_file.cuh      PSP1 files from/to device tables
 //   engine_shard.cuh     routed (sharded) queries over NVLink
+//   engine_graphio.cuh   graph text parsed on the GPU (load_graph), writer
 //   psp_gpu.cu           this file: the extern "C" entry points
 //   host_graph.cpp, partition.cpp   host graph plumbing and partitioner
 #include <cub/device/device_scan.cuh>
@@ -53,6 +54,7 @@ using namespace pspg;
 #include "engine_oracle.cuh"
 #include "engine_file.cuh"
 #include "engine_shard.cuh"
+#include "engine_graphio.cuh"
 
 // ================================================================ C-ABI ==
 extern "C" {
@@ -594,6 +596,132 @@ psp_status psp_gpu_routed_query_batch(psp_gpu_shard* sh, uint64_t count, const u
                                 transfer_entries, stats);
     });
 }
+
+// ----------------------------------------------------- graph ingestion --
+namespace {
+psp_graph* finish_graph(ParsedGraph&& G, bool dimacs, const std::string& name, uint64_t lineno_end) {
+    // psp::Graph(n, edges): edge-list files wrap its GraphInvariantError in
+    // a ParseError at the last line (src/graph_io.cpp:88-93); DIMACS input
+    // is normalised and lets it through unchanged
+    try {
+        (void)build_csr(G.n, G.eu.size(), G.eu.data(), G.ev.data(), G.ew.data());
+    } catch (const GraphError& e) {
+        if (dimacs) throw;
+        throw ParseFail{name + ":" + std::to_string(lineno_end) + ": " + e.what(), lineno_end};
+    }
+    auto g = std::make_unique<psp_graph>();
+    g->n = G.n;
+    g->eu = std::move(G.eu);
+    g->ev = std::move(G.ev);
+    g->ew = std::move(G.ew);
+    return g.release();
+}
+
+uint64_t count_lines(const DevText& t, cudaStream_t s) {
+    // getline's line count, for the wrapped Graph error's line number
+    if (t.len == 0) return 1;
+    const uint64_t nch = (t.len + PARSE_CHUNK - 1) / PARSE_CHUNK;
+    DBuf cnt(nch * 4);
+    nl_count<<<unsigned((nch + 255) / 256), 256, 0, s>>>(t.buf.as<char>(), t.len, cnt.as<uint32_t>(), nch);
+    CK_LAUNCH();
+    std::vector<uint32_t> h(nch);
+    CK(cudaMemcpyAsync(h.data(), cnt.p, nch * 4, cudaMemcpyDeviceToHost, s));
+    char last = 0;
+    CK(cudaMemcpyAsync(&last, t.buf.as<char>() + t.len - 1, 1, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t nl = 0;
+    for (uint32_t x : h) nl += x;
+    const uint64_t lines = nl + (last != '\n' ? 1 : 0);
+    return lines ? lines : 1;
+}
+
+psp_graph* parse_text(psp_gpu_ctx* ctx, const DevText& t, int format, const std::string& name) {
+    if (format != PSP_FORMAT_EDGE_LIST && format != PSP_FORMAT_DIMACS)
+        throw ArgError("graph format must be PSP_FORMAT_EDGE_LIST or PSP_FORMAT_DIMACS");
+    const bool dimacs = format == PSP_FORMAT_DIMACS;
+    ParsedGraph G = parse_graph_device(t, dimacs, name, ctx->stream, ctx->sms);
+    return finish_graph(std::move(G), dimacs, name, dimacs ? 0 : count_lines(t, ctx->stream));
+}
+}  // namespace
+
+psp_status psp_gpu_load_graph(psp_gpu_ctx* ctx, const char* path, int format, psp_graph** out) {
+    return guarded([&] {
+        if (!ctx || !path || !out) throw ArgError("load_graph: NULL argument");
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        const DevText t = read_to_device(path, ctx->stream);
+        *out = parse_text(ctx, t, format, path);
+    });
+}
+
+psp_status psp_gpu_read_graph(psp_gpu_ctx* ctx, const char* text, uint64_t len, int format,
+                              const char* name, psp_graph** out) {
+    return guarded([&] {
+        if (!ctx || (!text && len) || !out) throw ArgError("read_graph: NULL argument");
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        const DevText t = text_to_device(text, len, ctx->stream);
+        *out = parse_text(ctx, t, format, name ? name : "<stream>");
+    });
+}
+
+psp_status psp_graph_size(const psp_graph* g, uint64_t* n, uint64_t* m) {
+    return guarded([&] {
+        if (!g) throw ArgError("graph_size: NULL graph");
+        if (n) *n = g->n;
+        if (m) *m = g->eu.size();
+    });
+}
+
+psp_status psp_graph_edges(const psp_graph* g, uint32_t* eu, uint32_t* ev, double* ew) {
+    return guarded([&] {
+        if (!g) throw ArgError("graph_edges: NULL graph");
+        if (eu) std::copy(g->eu.begin(), g->eu.end(), eu);
+        if (ev) std::copy(g->ev.begin(), g->ev.end(), ev);
+        if (ew) std::copy(g->ew.begin(), g->ew.end(), ew);
+    });
+}
+
+void psp_graph_free(psp_graph* g) { delete g; }
+
+uint64_t psp_gpu_last_parse_line(void) { return g_parse_line; }
+
+psp_status psp_write_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                           const double* ew, int format, char* buf, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        if (m && (!eu || !ev || !ew)) throw ArgError("write_graph: NULL edge array");
+        if (format != PSP_FORMAT_EDGE_LIST && format != PSP_FORMAT_DIMACS)
+            throw ArgError("graph format must be PSP_FORMAT_EDGE_LIST or PSP_FORMAT_DIMACS");
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        const std::string text = write_graph_text(g, format == PSP_FORMAT_DIMACS,
+                                                  std::max(1u, std::thread::hardware_concurrency()));
+        if (len) *len = text.size();
+        if (buf) {
+            if (cap < text.size()) throw ArgError("write_graph: buffer too small");
+            std::memcpy(buf, text.data(), text.size());
+        }
+    });
+}
+
+psp_status psp_save_graph(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                          const double* ew, const char* path, int format) {
+    return guarded([&] {
+        if (!path) throw ArgError("save_graph: NULL path");
+        if (m && (!eu || !ev || !ew)) throw ArgError("save_graph: NULL edge array");
+        if (format != PSP_FORMAT_EDGE_LIST && format != PSP_FORMAT_DIMACS)
+            throw ArgError("graph format must be PSP_FORMAT_EDGE_LIST or PSP_FORMAT_DIMACS");
+        const Csr g = build_csr(n, m, eu, ev, ew);
+        const std::string text = write_graph_text(g, format == PSP_FORMAT_DIMACS,
+                                                  std::max(1u, std::thread::hardware_concurrency()));
+        std::ofstream f(path, std::ios::binary);
+        if (!f) throw Fail{PSP_EIO, std::string("cannot open '") + path + "' for writing"};
+        f.write(text.data(), std::streamsize(text.size()));
+        f.flush();
+        if (!f) throw Fail{PSP_EIO, std::string("write to '") + path + "' failed"};
+    });
+}
+
+uint32_t psp_format_weight(double w, char* buf) { return buf ? format_weight_into(w, buf) : 0; }
 
 psp_status psp_gpu_minplus_peak(psp_gpu_ctx* ctx, int value_kind, double* relax_per_s,
                                 double* sm_clock_mhz) {
