@@ -7,17 +7,17 @@
 //   L1  newline index: per-256-byte chunk counts, a scan, the positions;
 //   L2  one thread per line: trim, classify (blank / comment / header /
 //       edge or arc / other), tokenize, parse the ids (exact u64 with
-//       overflow) and the weight. Weights of the form digits[.digits] with
-//       <= 19 significant digits, mantissa < 2^53 and <= 22 fraction
-//       digits are converted exactly on the device (Clinger's fast path: one
-//       correctly rounded division of two exact doubles). Anything else
-//       ("1e5", "inf", "-0", long mantissas) marks the line HARD;
-//   host the earliest line that fails, or is HARD, is re-parsed by a
-//       line-for-line restatement of the reference's loop body with
-//       std::from_chars -- the same function the reference calls -- so
-//       values and ParseError messages are the reference's. Header lines,
-//       "more edges than declared" and the end-of-file checks follow the
-//       reference's order;
+//       overflow) and the weight, correctly rounded on the device by
+//       Eisel-Lemire (decimal_parse.cuh: digits[.digits][e[+-]digits],
+//       <= 19 significant digits, normal results). Anything else (signs,
+//       "inf", subnormal or overflowing values, malformed tokens, ids out
+//       of range) marks the line HARD or ERR;
+//   host the HARD / ERR lines, in file order up to the first real error,
+//       are re-parsed by a line-for-line restatement of the reference's
+//       loop body with std::from_chars -- the function the reference calls
+//       -- in one batch, so values and ParseError messages are the
+//       reference's. Header lines, "more edges than declared" and the
+//       end-of-file checks follow the reference's order;
 //   DIMACS normalisation on the device: arcs keyed (min, max) << 32, radix
 //       sorted (stable, so file order survives among equal keys) and reduced
 //       by key with min -- the std::map's first-inserted-wins on equal
@@ -31,6 +31,8 @@
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
+
+#include "decimal_parse.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -146,34 +148,6 @@ __device__ __forceinline__ bool parse_u64(const char* buf, uint64_t a, uint64_t 
     return true;
 }
 
-// Clinger's exact fast path; false = leave it to the host's from_chars
-__device__ __forceinline__ bool parse_weight_fast(const char* buf, uint64_t a, uint64_t b,
-                                                  double& w) {
-    uint64_t mant = 0;
-    int digits = 0, frac = 0;
-    bool dot = false, any = false;
-    for (uint64_t i = a; i < b; ++i) {
-        const char ch = buf[i];
-        if (ch == '.') {
-            if (dot) return false;
-            dot = true;
-            continue;
-        }
-        const unsigned d = static_cast<unsigned char>(ch) - '0';
-        if (d > 9) return false;
-        any = true;
-        if (mant != 0 || d != 0) ++digits;
-        if (digits > 19) return false;
-        mant = mant * 10 + d;
-        if (dot) ++frac;
-    }
-    if (!any || mant >= (1ull << 53) || frac > 22) return false;
-    const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
-                            1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
-    w = double(mant) / p10[frac];
-    return true;
-}
-
 // Second pass, one thread per line: status + (u, v, w) of edge / arc lines.
 // Edge list: header = line `first`, every later significant line an edge.
 // DIMACS: arcs after the problem line (ids 1-based, checked against n).
@@ -205,7 +179,7 @@ __global__ void parse_lines(const char* __restrict__ buf, uint64_t len,
         if (nt != 3 + t0 || !parse_u64(buf, ta[t0], tb[t0], u) ||
             !parse_u64(buf, ta[t0 + 1], tb[t0 + 1], v)) {
             s = LN_ERR;
-        } else if (!parse_weight_fast(buf, ta[t0 + 2], tb[t0 + 2], w)) {
+        } else if (!parse_decimal(buf + ta[t0 + 2], tb[t0 + 2] - ta[t0 + 2], w)) {
             s = LN_HARD;  // exact value (or its error) from the host
         } else if (dimacs ? (u < 1 || u > n || v < 1 || v > n) : (u >= n || v >= n)) {
             s = LN_ERR;
@@ -256,15 +230,55 @@ __global__ void flag_to_u32(const uint8_t* __restrict__ st, uint64_t nlines, int
     const uint8_t s = st[i];
     bool on;
     if (mode == 2) on = s == LN_EDGE || s == LN_ERR || s == LN_HARD;
+    else if (mode == 3) on = s == LN_ERR || s == LN_HARD;
     else on = s == LN_EDGE && !(mode == 1 && uu[i] == vv[i]);
     f[i] = on ? 1u : 0u;
 }
 
-__global__ void first_status(const uint8_t* __restrict__ st, uint64_t nlines,
-                             unsigned long long* __restrict__ out) {
+// compacted (line, body begin, body end) of the ERR / HARD lines < bound
+__global__ void collect_lines(const char* __restrict__ buf, uint64_t len,
+                              const uint64_t* __restrict__ nl, uint64_t nnl,
+                              const uint8_t* __restrict__ st, const uint32_t* __restrict__ pos,
+                              uint64_t bound, uint64_t* __restrict__ out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= nlines) return;  // nlines doubles as the search bound
-    if (st[i] == LN_ERR || st[i] == LN_HARD) atomicMin(&out[0], (unsigned long long)i);
+    if (i >= bound || (st[i] != LN_ERR && st[i] != LN_HARD)) return;
+    const LineSpan sp = line_body(buf, len, nl, nnl, i);
+    out[3 * uint64_t(pos[i]) + 0] = i;
+    out[3 * uint64_t(pos[i]) + 1] = sp.a;
+    out[3 * uint64_t(pos[i]) + 2] = sp.b;
+}
+
+// host-resolved HARD lines: (line, u, v, w bits) -> edge
+__global__ void apply_lines(const uint64_t* __restrict__ rec, uint64_t count,
+                            uint8_t* __restrict__ st, uint64_t* __restrict__ uu,
+                            uint64_t* __restrict__ vv, double* __restrict__ ww) {
+    const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= count) return;
+    const uint64_t i = rec[4 * j];
+    uu[i] = rec[4 * j + 1];
+    vv[i] = rec[4 * j + 2];
+    ww[i] = __longlong_as_double(static_cast<long long>(rec[4 * j + 3]));
+    st[i] = LN_EDGE;
+}
+
+// psp::Graph(n, edges) checks for a parsed edge list (src/graph.cpp:22-56):
+// ids, weights are already valid, so the first self-loop in edge order,
+// then the lexicographically smallest duplicated pair (the first the
+// constructor's sorted-adjacency scan meets).
+__global__ void edge_checks(const uint32_t* __restrict__ eu, const uint32_t* __restrict__ ev,
+                            uint64_t m, uint64_t* __restrict__ key,
+                            unsigned long long* __restrict__ first_loop) {
+    const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const uint32_t a = eu[e], b = ev[e];
+    if (a == b) atomicMin(first_loop, (unsigned long long)e);
+    key[e] = (uint64_t(min(a, b)) << 32) | max(a, b);
+}
+
+__global__ void first_duplicate(const uint64_t* __restrict__ key, uint64_t m,
+                                unsigned long long* __restrict__ dup) {
+    const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e + 1 < m && key[e] == key[e + 1]) atomicMin(dup, (unsigned long long)key[e]);
 }
 
 // ------------------------------------------------------------- host side --
@@ -336,71 +350,65 @@ struct ParsedGraph {
 };
 
 struct DevText {
-    DBuf buf;
+    DBuf buf;            // the text in HBM
+    const char* host = nullptr;  // the same bytes on the host
     uint64_t len = 0;
+    char* pinned = nullptr;      // owned host copy (files)
+    DevText() = default;
+    DevText(const DevText&) = delete;
+    DevText& operator=(const DevText&) = delete;
+    ~DevText() {
+        if (pinned) cudaFreeHost(pinned);
+    }
 };
 
-// Reads a file into device memory (pinned bounce buffer, chunked).
-DevText read_to_device(const std::string& path, cudaStream_t s) {
+// Reads a file into pinned host memory (parallel preads) and HBM.
+void read_to_device(const std::string& path, cudaStream_t s, DevText& t) {
     const int fd = ::open(path.c_str(), O_RDONLY);
     if (fd < 0) throw Fail{PSP_EIO, "cannot open '" + path + "' for reading"};
     struct stat sb;
-    if (fstat(fd, &sb) != 0) {
+    if (fstat(fd, &sb) != 0 || !S_ISREG(sb.st_mode)) {
         ::close(fd);
         throw Fail{PSP_EIO, "cannot open '" + path + "' for reading"};
     }
-    DevText t;
     t.len = static_cast<uint64_t>(sb.st_size);
     t.buf.alloc(t.len + 1);
-    constexpr size_t CH = 64ull << 20;
-    std::vector<char*> pin(2, nullptr);
-    for (auto& p : pin) CK(cudaMallocHost(&p, CH));
-    cudaEvent_t ev[2];
-    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    uint64_t off = 0;
-    int k = 0;
-    std::string err;
-    while (off < t.len && err.empty()) {
-        CK(cudaEventSynchronize(ev[k]));  // this bounce buffer's previous copy is done
-        const size_t want = std::min<uint64_t>(CH, t.len - off);
-        size_t got = 0;
-        while (got < want) {
-            const ssize_t r = ::pread(fd, pin[k] + got, want - got, off + got);
-            if (r <= 0) {
-                err = "read from '" + path + "' failed";
-                break;
-            }
-            got += size_t(r);
-        }
-        if (!err.empty()) break;
-        CK(cudaMemcpyAsync(t.buf.as<char>() + off, pin[k], want, cudaMemcpyHostToDevice, s));
-        CK(cudaEventRecord(ev[k], s));
-        off += want;
-        k ^= 1;
+    if (cudaMallocHost(&t.pinned, t.len + 1) != cudaSuccess) {
+        ::close(fd);
+        throw Fail{PSP_ENOMEM, "pinned host buffer for '" + path + "'"};
     }
+    t.host = t.pinned;
+    const unsigned nt = std::max(1u, std::min(16u, unsigned(t.len >> 24) + 1));
+    std::vector<std::thread> pool;
+    std::atomic<bool> failed{false};
+    for (unsigned k = 0; k < nt; ++k)
+        pool.emplace_back([&, k] {
+            uint64_t off = t.len * k / nt;
+            const uint64_t end = t.len * (k + 1) / nt;
+            while (off < end) {
+                const ssize_t r = ::pread(fd, t.pinned + off, std::min<uint64_t>(end - off, 1ull << 30), off);
+                if (r <= 0) {
+                    failed = true;
+                    return;
+                }
+                off += uint64_t(r);
+            }
+        });
+    for (auto& th : pool) th.join();
     ::close(fd);
-    CK(cudaStreamSynchronize(s));
-    for (auto& e : ev) cudaEventDestroy(e);
-    for (auto p : pin) cudaFreeHost(p);
-    if (!err.empty()) throw Fail{PSP_EIO, err};
-    return t;
+    if (failed) throw Fail{PSP_EIO, "read from '" + path + "' failed"};
+    if (t.len) CK(cudaMemcpyAsync(t.buf.p, t.pinned, t.len, cudaMemcpyHostToDevice, s));
 }
 
-DevText text_to_device(const char* text, uint64_t len, cudaStream_t s) {
-    DevText t;
+void text_to_device(const char* text, uint64_t len, cudaStream_t s, DevText& t) {
     t.len = len;
+    t.host = text;
     t.buf.alloc(len + 1);
     if (len) CK(cudaMemcpyAsync(t.buf.p, text, len, cudaMemcpyHostToDevice, s));
-    return t;
 }
 
-std::string host_line(const DevText& t, const std::vector<uint64_t>& nl_host_pair, cudaStream_t s) {
-    // nl_host_pair = {a, b} byte range of the line
-    const uint64_t a = nl_host_pair[0], b = nl_host_pair[1];
-    std::string line(b - a, '\0');
-    if (b > a) CK(cudaMemcpyAsync(line.data(), t.buf.as<char>() + a, b - a, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return line;
+std::string host_line(const DevText& t, const std::vector<uint64_t>& r) {
+    return std::string(t.host + r[0], t.host + r[1]);  // r = {begin, end} of the line
 }
 
 ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string& name,
@@ -446,7 +454,7 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
         r[1] = cur;
         return r;
     };
-    auto body_of = [&](uint64_t i) { return host_line(t, line_range(i), s); };
+    auto body_of = [&](uint64_t i) { return host_line(t, line_range(i)); };
     const unsigned lb = unsigned((std::max<uint64_t>(nlines, 1) + 255) / 256);
     const uint64_t lineno_end = nlines ? nlines : 1;  // "lineno ? lineno : 1"
 
@@ -518,41 +526,60 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
     // "more edges than declared" (:80) unless it, or an earlier line, fails
     // first -- so errors are only searched up to and including that line.
     uint64_t cut = nlines;  // search bound (exclusive)
+    bool more = false;
     if (!dimacs) {
         const uint64_t nsig = positions(2);
         if (nsig > m) {
+            more = true;
             std::vector<uint32_t> hpos(nlines + 1);
             CK(cudaMemcpyAsync(hpos.data(), pos.p, (nlines + 1) * 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             cut = std::upper_bound(hpos.begin(), hpos.end(), uint32_t(m)) - hpos.begin();
         }
     }
-    // resolve lines in file order until the first real error: HARD lines
-    // are re-parsed on the host (their values written back), ERR lines give
-    // the reference's message
-    DBuf fe(8);
-    for (;;) {
-        unsigned long long f = ~0ull;
-        CK(cudaMemcpyAsync(fe.p, &f, 8, cudaMemcpyHostToDevice, s));
-        first_status<<<lb, 256, 0, s>>>(st.as<uint8_t>(), cut, fe.as<unsigned long long>());
-        CK_LAUNCH();
-        CK(cudaMemcpyAsync(&f, fe.p, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (f == ~0ull) break;  // no error up to the bound
-        const std::string line = body_of(f);
-        const std::string_view body = host_trim(line);
-        const uint64_t ln = f + 1;
-        if (dimacs && body.front() == 'p') parse_fail(name, ln, "duplicate problem line");
-        if (dimacs && body.front() != 'a')
-            parse_fail(name, ln, "unrecognized line type '" + std::string(1, body.front()) + "'");
-        const HostEdge e = host_edge_line(body, dimacs, n, name, ln);  // throws for ERR lines
-        const uint8_t ok = LN_EDGE;
-        CK(cudaMemcpyAsync(uu.as<uint64_t>() + f, &e.u, 8, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(vv.as<uint64_t>() + f, &e.v, 8, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ww.as<double>() + f, &e.w, 8, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(st.as<uint8_t>() + f, &ok, 1, cudaMemcpyHostToDevice, s));
+    // resolve the HARD / ERR lines before the bound in file order, in one
+    // batch: the first real error throws the reference's ParseError; the
+    // HARD lines that parse are written back as edges
+    {
+        const uint64_t nflag = positions(3);
+        uint64_t nres = 0;
+        if (nflag) {
+            DBuf recs(nflag * 24);
+            collect_lines<<<lb, 256, 0, s>>>(buf, len, d_nl, nnl, st.as<uint8_t>(), pos.as<uint32_t>(),
+                                             cut, recs.as<uint64_t>());
+            CK_LAUNCH();
+            uint32_t nb = 0;  // flagged lines below the bound
+            CK(cudaMemcpyAsync(&nb, pos.as<uint32_t>() + cut, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<uint64_t> h(uint64_t(nb) * 3);
+            if (nb) CK(cudaMemcpyAsync(h.data(), recs.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<uint64_t> ok;
+            ok.reserve(uint64_t(nb) * 4);
+            for (uint64_t j = 0; j < nb; ++j) {
+                const uint64_t f = h[3 * j], ln = f + 1;
+                const std::string_view body(t.host + h[3 * j + 1], h[3 * j + 2] - h[3 * j + 1]);
+                if (dimacs && body.front() == 'p') parse_fail(name, ln, "duplicate problem line");
+                if (dimacs && body.front() != 'a')
+                    parse_fail(name, ln, "unrecognized line type '" + std::string(1, body.front()) + "'");
+                const HostEdge e = host_edge_line(body, dimacs, n, name, ln);  // ERR lines throw
+                uint64_t wb;
+                std::memcpy(&wb, &e.w, 8);
+                ok.insert(ok.end(), {f, e.u, e.v, wb});
+            }
+            nres = ok.size() / 4;
+            if (nres) {
+                DBuf d(ok.size() * 8);
+                CK(cudaMemcpyAsync(d.p, ok.data(), ok.size() * 8, cudaMemcpyHostToDevice, s));
+                apply_lines<<<unsigned((nres + 255) / 256), 256, 0, s>>>(
+                    d.as<uint64_t>(), nres, st.as<uint8_t>(), uu.as<uint64_t>(), vv.as<uint64_t>(),
+                    ww.as<double>());
+                CK_LAUNCH();
+                CK(cudaStreamSynchronize(s));
+            }
+        }
     }
-    if (cut < nlines) parse_fail(name, cut, "more edges than declared in header");
+    if (more) parse_fail(name, cut, "more edges than declared in header");
     const uint64_t nedge_lines = positions(0);
     ParsedGraph G;
     G.n = n;
@@ -574,6 +601,30 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
             CK(cudaMemcpyAsync(G.eu.data(), du.p, m * 4, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(G.ev.data(), dv.p, m * 4, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(G.ew.data(), dw.p, m * 8, cudaMemcpyDeviceToHost, s));
+            // the Graph constructor's remaining checks, on the device
+            DBuf keys(m * 8), sorted(m * 8), flags(16);
+            std::vector<unsigned long long> hf = {~0ull, ~0ull};
+            CK(cudaMemcpyAsync(flags.p, hf.data(), 16, cudaMemcpyHostToDevice, s));
+            const unsigned eb = unsigned((m + 255) / 256);
+            edge_checks<<<eb, 256, 0, s>>>(du.as<uint32_t>(), dv.as<uint32_t>(), m, keys.as<uint64_t>(),
+                                           flags.as<unsigned long long>());
+            CK_LAUNCH();
+            size_t b5 = 0;
+            CK(cub::DeviceRadixSort::SortKeys(nullptr, b5, keys.as<uint64_t>(), sorted.as<uint64_t>(),
+                                              int(m), 0, 64, s));
+            DBuf t5(b5);
+            CK(cub::DeviceRadixSort::SortKeys(t5.p, b5, keys.as<uint64_t>(), sorted.as<uint64_t>(),
+                                              int(m), 0, 64, s));
+            first_duplicate<<<eb, 256, 0, s>>>(sorted.as<uint64_t>(), m,
+                                               flags.as<unsigned long long>() + 1);
+            CK_LAUNCH();
+            CK(cudaMemcpyAsync(hf.data(), flags.p, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (hf[0] != ~0ull)
+                throw GraphError("self-loop at vertex " + std::to_string(G.eu[hf[0]]));
+            if (hf[1] != ~0ull)
+                throw GraphError("duplicate edge (" + std::to_string(hf[1] >> 32) + "," +
+                                 std::to_string(hf[1] & 0xffffffffu) + ")");
         }
         CK(cudaStreamSynchronize(s));
         return G;

@@ -599,16 +599,7 @@ psp_status psp_gpu_routed_query_batch(psp_gpu_shard* sh, uint64_t count, const u
 
 // ----------------------------------------------------- graph ingestion --
 namespace {
-psp_graph* finish_graph(ParsedGraph&& G, bool dimacs, const std::string& name, uint64_t lineno_end) {
-    // psp::Graph(n, edges): edge-list files wrap its GraphInvariantError in
-    // a ParseError at the last line (src/graph_io.cpp:88-93); DIMACS input
-    // is normalised and lets it through unchanged
-    try {
-        (void)build_csr(G.n, G.eu.size(), G.eu.data(), G.ev.data(), G.ew.data());
-    } catch (const GraphError& e) {
-        if (dimacs) throw;
-        throw ParseFail{name + ":" + std::to_string(lineno_end) + ": " + e.what(), lineno_end};
-    }
+psp_graph* finish_graph(ParsedGraph&& G) {
     auto g = std::make_unique<psp_graph>();
     g->n = G.n;
     g->eu = std::move(G.eu);
@@ -617,21 +608,11 @@ psp_graph* finish_graph(ParsedGraph&& G, bool dimacs, const std::string& name, u
     return g.release();
 }
 
-uint64_t count_lines(const DevText& t, cudaStream_t s) {
-    // getline's line count, for the wrapped Graph error's line number
-    if (t.len == 0) return 1;
-    const uint64_t nch = (t.len + PARSE_CHUNK - 1) / PARSE_CHUNK;
-    DBuf cnt(nch * 4);
-    nl_count<<<unsigned((nch + 255) / 256), 256, 0, s>>>(t.buf.as<char>(), t.len, cnt.as<uint32_t>(), nch);
-    CK_LAUNCH();
-    std::vector<uint32_t> h(nch);
-    CK(cudaMemcpyAsync(h.data(), cnt.p, nch * 4, cudaMemcpyDeviceToHost, s));
-    char last = 0;
-    CK(cudaMemcpyAsync(&last, t.buf.as<char>() + t.len - 1, 1, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+uint64_t count_lines(const DevText& t) {
+    // getline's line count (the wrapped Graph error's line number)
     uint64_t nl = 0;
-    for (uint32_t x : h) nl += x;
-    const uint64_t lines = nl + (last != '\n' ? 1 : 0);
+    for (uint64_t i = 0; i < t.len; ++i) nl += t.host[i] == '\n';
+    const uint64_t lines = nl + (t.len && t.host[t.len - 1] != '\n' ? 1 : 0);
     return lines ? lines : 1;
 }
 
@@ -639,8 +620,16 @@ psp_graph* parse_text(psp_gpu_ctx* ctx, const DevText& t, int format, const std:
     if (format != PSP_FORMAT_EDGE_LIST && format != PSP_FORMAT_DIMACS)
         throw ArgError("graph format must be PSP_FORMAT_EDGE_LIST or PSP_FORMAT_DIMACS");
     const bool dimacs = format == PSP_FORMAT_DIMACS;
-    ParsedGraph G = parse_graph_device(t, dimacs, name, ctx->stream, ctx->sms);
-    return finish_graph(std::move(G), dimacs, name, dimacs ? 0 : count_lines(t, ctx->stream));
+    try {
+        return finish_graph(parse_graph_device(t, dimacs, name, ctx->stream, ctx->sms));
+    } catch (const GraphError& e) {
+        // psp::Graph(n, edges) failing on an edge list surfaces as a
+        // ParseError at the last line (src/graph_io.cpp:88-93); normalised
+        // DIMACS input cannot fail it
+        if (dimacs) throw;
+        const uint64_t ln = count_lines(t);
+        throw ParseFail{name + ":" + std::to_string(ln) + ": " + e.what(), ln};
+    }
 }
 }  // namespace
 
@@ -649,8 +638,15 @@ psp_status psp_gpu_load_graph(psp_gpu_ctx* ctx, const char* path, int format, ps
         if (!ctx || !path || !out) throw ArgError("load_graph: NULL argument");
         *out = nullptr;
         CK(cudaSetDevice(ctx->device));
-        const DevText t = read_to_device(path, ctx->stream);
+        const auto t0 = Clock::now();
+        DevText t;
+        read_to_device(path, ctx->stream, t);
+        CK(cudaStreamSynchronize(ctx->stream));
+        const double read_ms = ms_since(t0);
         *out = parse_text(ctx, t, format, path);
+        if (std::getenv("PSP_IO_PROFILE"))
+            std::fprintf(stderr, "[load_graph] read+H2D %.1f ms, parse+validate %.1f ms\n", read_ms,
+                         ms_since(t0) - read_ms);
     });
 }
 
@@ -660,7 +656,8 @@ psp_status psp_gpu_read_graph(psp_gpu_ctx* ctx, const char* text, uint64_t len, 
         if (!ctx || (!text && len) || !out) throw ArgError("read_graph: NULL argument");
         *out = nullptr;
         CK(cudaSetDevice(ctx->device));
-        const DevText t = text_to_device(text, len, ctx->stream);
+        DevText t;
+        text_to_device(text, len, ctx->stream, t);
         *out = parse_text(ctx, t, format, name ? name : "<stream>");
     });
 }
