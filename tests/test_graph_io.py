@@ -207,3 +207,32 @@ def test_load_graph_file_round_trip(ref, ctx, tmp_path):
     with pytest.raises(P.ParseError) as e:
         P.load_graph(str(bad), ctx=ctx)
     assert str(e.value) == f"{bad}:3: more edges than declared in header"
+
+
+# ---- the device weight conversion, checked on the host ----------------------
+def test_decimal_parse_matches_from_chars(tmp_path):
+    """decimal_parse.cuh (Eisel-Lemire, __host__ __device__) against
+    std::from_chars -- the reference's weight parser -- on random strings."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "decimal_check"
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    subprocess.run([cxx, "-O2", "-std=c++20", "-I", os.path.join(root, "paper_1503_07192_b200", "csrc"),
+                    os.path.join(root, "tools", "decimal_check.cpp"), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), "1000000"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout
+    assert " 0 mismatches" in r.stdout
+
+
+def test_pow5_table_is_generated():
+    """pow5_table.cuh is exactly what tools/gen_pow5.py produces."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen_pow5", os.path.join(root, "tools", "gen_pow5.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    vals = list(mod.entries())
+    text = open(mod.OUT).read()
+    for q, v in ((-342, vals[0]), (0, vals[342]), (308, vals[650]), (-1, vals[341])):
+        assert f"0x{v >> 64:016x}ull, 0x{v & ((1 << 64) - 1):016x}ull," in text, q
+    assert text.count("ull, 0x") == 2 * 651
