@@ -32,6 +32,9 @@ struct psp_gpu_oracle {
     std::mutex query_mu;
     DBuf query_stage;
     GroupWorkspace gw;
+    // block query layout of the boundary table (optional, see
+    // build_query_blocks): BQ blocks and their offsets
+    DBuf bq, d_bq_off;
 };
 
 namespace {
@@ -132,6 +135,62 @@ void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
     CK_LAUNCH();
 }
 
+// Block query layout: every component pair block (c1 <= c2) of the
+// boundary table stored contiguously as [column group][B1p rows][32
+// columns], B1p = B1 rounded up to GK, INF in the padding. A 16-row chunk of
+// one column group is then one 2 KB bulk copy for query_grouped instead of
+// 144 address-computed 16-byte copies out of the tile arena. About 1.2x the
+// symmetric arena; built only when it fits beside it with headroom.
+template <class V>
+__global__ void pack_query_blocks(const V* __restrict__ bg, uint32_t nb,
+                                  const uint32_t* __restrict__ bnd_off, uint32_t k,
+                                  const uint64_t* __restrict__ blk_off, V* __restrict__ bq) {
+    const uint32_t c1 = blockIdx.x / k, c2 = blockIdx.x % k;
+    if (c2 < c1) return;
+    const uint32_t g1 = bnd_off[c1], B1 = bnd_off[c1 + 1] - g1;
+    const uint32_t g2 = bnd_off[c2], B2 = bnd_off[c2 + 1] - g2;
+    const uint64_t B1p = (B1 + GK - 1) / GK * GK, ncg = (B2 + 31) / 32;
+    const uint64_t total = ncg * B1p * 32;
+    V* out = bq + blk_off[blockIdx.x];
+    for (uint64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const uint64_t cg = idx / (B1p * 32), rem = idx - cg * B1p * 32;
+        const uint32_t r = static_cast<uint32_t>(rem >> 5), col = static_cast<uint32_t>(cg * 32 + (rem & 31));
+        out[idx] = (r < B1 && col < B2) ? bg[sym_off(g1 + r, g2 + col, nb)] : Ops<V>::inf();
+    }
+}
+
+template <class V>
+void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
+    const Reordered& R = o->R;
+    const uint64_t k = R.k;
+    o->bq.reset();
+    o->d_bq_off.reset();
+    const char* lay = std::getenv("PSP_QUERY_LAYOUT");
+    if (lay && std::strcmp(lay, "tiles") == 0) return;
+    if (!o->bg.nmat || k * k >= (1ull << 31)) return;
+    std::vector<uint64_t> off(k * k, 0);
+    uint64_t acc = 0;
+    for (uint64_t c1 = 0; c1 < k; ++c1) {
+        const uint64_t B1 = R.bnd_off[c1 + 1] - R.bnd_off[c1], B1p = (B1 + GK - 1) / GK * GK;
+        for (uint64_t c2 = c1; c2 < k; ++c2) {
+            const uint64_t B2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
+            off[c1 * k + c2] = acc;
+            acc += (B2 + 31) / 32 * 32 * B1p;
+        }
+    }
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t need = acc * sizeof(V) + off.size() * 8;
+    if (need + (8ull << 30) > free_b) return;  // keep 8 GB for query workspaces
+    o->bq.alloc(acc * sizeof(V));
+    o->d_bq_off = upload(off, s);
+    pack_query_blocks<V><<<unsigned(k * k), 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0],
+                                                         o->d_bnd_off.as<uint32_t>(), uint32_t(k),
+                                                         o->d_bq_off.as<uint64_t>(), o->bq.as<V>());
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+}
+
 template <class V>
 void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     psp_gpu_ctx* ctx = o->ctx;
@@ -196,11 +255,12 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     // panels are build-time scratch
     o->comps.panel.reset();
     o->bg.panel.reset();
+    build_query_blocks<V>(o, s);
     const double boundary_ms = ms_since(t0);
 
     o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->d_cb_off.bytes +
                       o->d_comp_off.bytes + o->d_bnd_off.bytes + o->d_perm.bytes +
-                      o->d_assign.bytes;
+                      o->d_assign.bytes + o->bq.bytes + o->d_bq_off.bytes;
     if (st) {
         st->component_apsp_ms = component_ms;
         st->boundary_ms = boundary_ms;
@@ -288,7 +348,8 @@ void import_tables(psp_gpu_oracle* o, const double* const* ct, const double* con
     }
     finish_query_tables<V>(o, upload(R.bnd_off, s), s);
     CK(cudaStreamSynchronize(s));
-    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes;
+    build_query_blocks<V>(o, s);
+    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->bq.bytes;
 }
 
 void set_peak_entries(const Reordered& R, unsigned workers, psp_build_stats* st) {
@@ -376,7 +437,7 @@ void export_window(const psp_gpu_oracle* o, const MatArena& a, uint32_t m, uint3
 
 // Counting sort by component pair, task records, query_grouped, finish.
 // `bnd_off` is the host copy of the boundary offsets (task-count bound).
-template <class V, bool ROUTED>
+template <class V, int MODE>
 void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, int sms,
                     const QueryView<V>& q, uint64_t count, const uint32_t* v1, const uint32_t* v2,
                     double* dist, cudaStream_t s) {
@@ -417,7 +478,7 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     w.nbins = nbins;
     CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins + 1) * sizeof(uint32_t), s));
     const unsigned qb = unsigned((count + 255) / 256);
-    group_prep<V, ROUTED><<<qb, 256, 0, s>>>(q, v1, v2, count, w);
+    group_prep<V, MODE == QM_ROUTED><<<qb, 256, 0, s>>>(q, v1, v2, count, w);
     CK_LAUNCH();
     group_tasks<<<(nbins + 1 + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k);
     CK_LAUNCH();
@@ -443,13 +504,13 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     group_scatter<<<qb, 256, 0, s>>>(count, w);
     CK_LAUNCH();
     const int gsmem = GWARPS * sizeof(WarpStage<V>);
-    static bool attr_set = false;  // one flag per <V, ROUTED> instantiation
+    static bool attr_set = false;  // one flag per <V, MODE> instantiation
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(query_grouped<V, ROUTED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(query_grouped<V, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 gsmem));
         attr_set = true;
     }
-    query_grouped<V, ROUTED><<<sms * 2, GTHREADS, gsmem, s>>>(q, w);
+    query_grouped<V, MODE><<<sms * 2, GTHREADS, gsmem, s>>>(q, w);
     CK_LAUNCH();
     group_finish<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w, dist);
     CK_LAUNCH();
@@ -466,7 +527,7 @@ template <class V>
 void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
                     const uint32_t* v2, double* dist, cudaStream_t s, uint32_t* bad_id) {
     if (count == 0) return;
-    QueryView<V> q;
+    QueryView<V> q{};
     q.n = static_cast<uint32_t>(o->R.n);
     q.bad_id = bad_id;
     q.perm = o->d_perm.as<uint32_t>();
@@ -480,6 +541,8 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     q.bg_nb = o->bg.nmat ? o->bg.nb[0] : 0;
     q.k = o->R.k;
     q.scale = o->scale;
+    q.bq = o->bq.p ? o->bq.as<V>() : nullptr;
+    q.bq_off = o->bq.p ? o->d_bq_off.as<uint64_t>() : nullptr;
     const uint64_t k = o->R.k;
     const double pairs = double(k) * double(k + 1) / 2.0;
     // PSP_QUERY_KERNEL=warp|grouped overrides the density heuristic (tests,
@@ -489,8 +552,15 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     if (force && std::strcmp(force, "warp") == 0) grouped = false;
     if (force && std::strcmp(force, "grouped") == 0) grouped = true;
     if (grouped && k * k < (1ull << 31) && count < (1ull << 31)) {
-        launch_grouped<V, false>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off, o->ctx->sms, q, count,
-                                 v1, v2, dist, s);
+        // the block query layout when it was built (PSP_QUERY_LAYOUT=tiles
+        // forces the tile-packed path; both give identical distances)
+        const char* lay = std::getenv("PSP_QUERY_LAYOUT");
+        if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0))
+            launch_grouped<V, QM_BLOCKS>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+                                         o->ctx->sms, q, count, v1, v2, dist, s);
+        else
+            launch_grouped<V, QM_TILES>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+                                        o->ctx->sms, q, count, v1, v2, dist, s);
         return;
     }
     const uint64_t warps_per_block = 8;

@@ -380,7 +380,7 @@ void routed_batch(psp_gpu_shard* sh, uint64_t count, const uint32_t* v1, const u
     t_exec.start(s);
     if (R) {
         const QueryView<V> q = shard_view<V>(sh);
-        launch_grouped<V, true>(sh->gw, sh->bnd_off, ctx->sms, q, R, r1, r2, rd, s);
+        launch_grouped<V, QM_ROUTED>(sh->gw, sh->bnd_off, ctx->sms, q, R, r1, r2, rd, s);
     }
     t_exec.stop(s);
     if (world > 1) {

@@ -23,6 +23,7 @@
 //    lanes own target columns, every row segment of the block is fetched by
 //    the whole warp at once so DRAM sees full contiguous segments.
 #pragma once
+#include "fw_kernels.cuh"  // mbarrier / bulk-copy helpers
 #include "minplus.cuh"
 
 namespace pspg {
@@ -50,6 +51,11 @@ template <class V> struct QueryView {
     const uint32_t* bt_row0;    // k: first local BT row of an owned component
     const uint32_t* owner;      // k: rank owning component c
     const V* const* cb_peer;    // world: every rank's compact CB arena
+    // block query layout (optional, engine_oracle.cuh build_query_blocks):
+    // block (c1 <= c2) at bq + bq_off[c1 * k + c2], stored [cg][B1p][32]
+    // with B1p = B1 rounded up to GK, INF padding rows and columns
+    const V* bq;
+    const uint64_t* bq_off;
 };
 
 template <class V>
@@ -73,6 +79,12 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
 
 // Resolve a query to (c1 <= c2, l1, l2); routed mode keeps the caller's
 // orientation (the query executes at owner(C1), src/cluster.cpp:88-90).
+// Where a task's B1 x B2 block comes from (template parameter of the
+// grouped kernel): the FW's tile-packed symmetric arena, the dense owned
+// rows of a routed shard, or the block query layout (one contiguous 2 KB
+// bulk copy per 16-row chunk).
+enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2 };
+
 template <class V, bool ROUTED = false>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
                                         uint32_t& c1, uint32_t& c2, uint32_t& l1, uint32_t& l2) {
@@ -299,7 +311,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int GA_STRIDE = GK + 4;  // 16-byte aligned rows, <= 4-way conflicted fill
 constexpr int GB_STRIDE = 36;  // the 9 staged 4-column chunks, conflict-free reads
 
-template <class V, int NQ4>
+template <class V, int NQ4, int BSTRIDE>
 __device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* __restrict__ sB,
                                             V (&acc)[4 * NQ4], uint32_t rows4, uint32_t shift,
                                             int lane) {
@@ -307,7 +319,7 @@ __device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* _
     for (uint32_t k4 = 0; k4 < rows4; k4 += 4) {
         V b[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) b[r] = bcol[(k4 + r) * GB_STRIDE];
+        for (int r = 0; r < 4; ++r) b[r] = bcol[(k4 + r) * BSTRIDE];
 #pragma unroll
         for (int qq = 0; qq < 4 * NQ4; ++qq) {
             const uint4 u = *reinterpret_cast<const uint4*>(sA + qq * GA_STRIDE + k4);
@@ -326,6 +338,7 @@ template <class V> struct WarpStage {
     V b[2][GK * GB_STRIDE];
     V c2[GQ * 32];  // col2_q[j] per (query, lane), fetched at task start
     uint32_t id[GQ], c2off[GQ];
+    uint64_t bar[2];  // QM_BLOCKS: completion of the B bulk copies
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -335,10 +348,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
                  : "memory");
 }
 
-template <class V, int NQ4, bool ROUTED>
+template <class V, int NQ4, int MODE>
 __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWork& w,
                                            WarpStage<V>* st, uint32_t c1, uint32_t c2,
-                                           uint32_t q0, uint32_t m, uint32_t cg) {
+                                           uint32_t q0, uint32_t m, uint32_t cg,
+                                           uint32_t& phase) {
+    constexpr bool ROUTED = MODE == QM_ROUTED;
     const int lane = threadIdx.x & 31;
     const uint32_t nb = q.bg_nb;
     const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
@@ -353,6 +368,9 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     // 16-byte-aligned column superset of this task's 32 columns
     const uint32_t G0 = g2 + cg * 32, A0 = G0 & ~3u, shift = G0 - A0;
     const uint32_t Jlo = A0 >> 7;
+    const V* bq_task = nullptr;  // QM_BLOCKS: this column group's [B1p][32] slab
+    if (MODE == QM_BLOCKS)
+        bq_task = q.bq + q.bq_off[c1 * q.k + c2] + uint64_t(cg) * ((B1 + GK - 1) / GK * GK) * 32;
     // this lane's staging slots for B: e = t*32 + lane -> (row kk, chunk u)
     // over the 32 x 9 chunks of 4 columns
     __syncwarp();
@@ -375,7 +393,13 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
             for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
         }
         V* sb = st->b[buf];
-        if (ROUTED) {  // dense full rows of c1 (owned): any column block
+        if (MODE == QM_BLOCKS) {  // one contiguous 16 x 32 chunk of the block
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&st->bar[buf], GK * 32 * sizeof(V));
+                bulk_g2s(sb, bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(V), &st->bar[buf]);
+            }
+        } else if (ROUTED) {  // dense full rows of c1 (owned): any column block
             const V* rows0 = q.bt + uint64_t(q.bt_row0[c1] + k0) * q.bt_stride;
 #pragma unroll
             for (int t = 0; t < (GK * 9 + 31) / 32; ++t) {
@@ -441,9 +465,17 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
         const bool more = k0 + GK < B1;
         if (more) issue(k0 + GK, buf ^ 1);
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+        if (MODE == QM_BLOCKS) {
+            mbar_wait(&st->bar[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
+        }
         __syncwarp();
-        group_chunk<V, NQ4>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u,
-                            shift, lane);
+        if (MODE == QM_BLOCKS)
+            group_chunk<V, NQ4, 32>(st->a[buf], st->b[buf], acc,
+                                    (min(uint32_t(GK), B1 - k0) + 3) & ~3u, 0, lane);
+        else
+            group_chunk<V, NQ4, GB_STRIDE>(st->a[buf], st->b[buf], acc,
+                                           (min(uint32_t(GK), B1 - k0) + 3) & ~3u, shift, lane);
         __syncwarp();  // buffer `buf` is refilled two chunks later
         buf ^= 1;
     }
@@ -468,10 +500,18 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     }
 }
 
-template <class V, bool ROUTED>
+template <class V, int MODE>
 __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, GroupWork w) {
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
+    uint32_t phase = 0;  // QM_BLOCKS: parity of each B buffer's barrier
+    if (MODE == QM_BLOCKS) {
+        if ((threadIdx.x & 31) == 0) {
+            mbar_init(&st->bar[0], 1);
+            mbar_init(&st->bar[1], 1);
+        }
+        __syncwarp();
+    }
     const uint32_t total = w.task_start[w.nbins];
     const uint32_t nwarps = gridDim.x * GWARPS;
     for (uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5); task < total; task += nwarps) {
@@ -480,9 +520,9 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // three query-count variants (32/16/8 slots): finer variants cut the
         // padding (82% vs 77% utilisation) but grow the kernel past the
         // instruction cache and measured slower (321M vs 390M queries/s)
-        if (m > 16) group_task<V, 8, ROUTED>(q, w, st, c1, c2, q0, m, cg);
-        else if (m > 8) group_task<V, 4, ROUTED>(q, w, st, c1, c2, q0, m, cg);
-        else group_task<V, 2, ROUTED>(q, w, st, c1, c2, q0, m, cg);
+        if (m > 16) group_task<V, 8, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
+        else if (m > 8) group_task<V, 4, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
+        else group_task<V, 2, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
     }
 }
 
