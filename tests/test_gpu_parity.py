@@ -369,3 +369,22 @@ def test_edge_shapes():
             os.environ.pop("PSP_QUERY_KERNEL")
     # empty batch
     assert o.batch_query([], []).shape == (0,)
+
+
+@pytest.mark.gpu
+def test_block_query_layout_matches_tile_arena(monkeypatch, golden_cfg1):
+    """The block query layout (default) and the tile-arena fallback give the
+    same distances, and both match the reference fixture."""
+    from paper_1503_07192_b200 import graphs
+    z = golden_cfg1
+    cases = [(P.Graph(int(z["n"]), z["eu"], z["ev"], z["ew"]), 16), (graphs.delaunay(20_000, 4), 97)]
+    for g, k in cases:
+        monkeypatch.setenv("PSP_QUERY_LAYOUT", "tiles")
+        ot = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_QUERY_LAYOUT")
+        ob = P.build_oracle(g, k, 4, 0)
+        v1, v2 = P.random_pairs(g.n, 300_000, 7)
+        assert np.array_equal(ob.batch_query(v1, v2), ot.batch_query(v1, v2))
+    assert np.array_equal(ob.batch_query(v1[:10], v2[:10]), ot.batch_query(v1[:10], v2[:10]))
+    o = P.build_oracle(cases[0][0], 16, 4, 0)
+    assert np.array_equal(o.batch_query(z["q_v1"], z["q_v2"]), z["q_dist"])
