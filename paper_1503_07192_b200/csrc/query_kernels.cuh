@@ -520,7 +520,11 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // three query-count variants (32/16/8 slots): finer variants cut the
         // padding (82% vs 77% utilisation) but grow the kernel past the
         // instruction cache and measured slower (321M vs 390M queries/s)
-        if (m > 16) group_task<V, 8, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
+        // the block-layout kernel has a fourth, 24-slot variant: its code is
+        // small enough (no per-element staging) to stay in the instruction
+        // cache, and it lifts useful/padded relaxations 0.76 -> 0.80 (cfg2)
+        if (m > 24 || (MODE != QM_BLOCKS && m > 16)) group_task<V, 8, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
+        else if (MODE == QM_BLOCKS && m > 16) group_task<V, 6, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
         else if (m > 8) group_task<V, 4, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
         else group_task<V, 2, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
     }
