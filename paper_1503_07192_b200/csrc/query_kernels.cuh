@@ -83,7 +83,9 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
 // grouped kernel): the FW's tile-packed symmetric arena, the dense owned
 // rows of a routed shard, or the block query layout (one contiguous 2 KB
 // bulk copy per 16-row chunk).
-enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2 };
+// QM_BLOCKS_LANE is the block layout with the earlier lane-per-column
+// product (PSP_QUERY_PRODUCT=lane, kept for A/B measurement).
+enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2, QM_BLOCKS_LANE = 3 };
 
 template <class V, bool ROUTED = false>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
@@ -500,12 +502,140 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
     }
 }
 
+// ------------------------- block layout: register-blocked warp task --
+// Same task and staging as group_task<QM_BLOCKS> (one 2 KB bulk copy per
+// 16-row chunk of the column group, row1 by 16-byte cp.async into
+// [query][row]), but the product is register-blocked: lane = (query group
+// qg = lane & 7, column octet cq = lane >> 3) owns queries qg + 8i
+// (i < QPT) x columns cq*8 .. cq*8+7, i.e. QPT x 8 accumulators. Per 4 rows
+// a lane issues QPT LDS.128 of row1 (8 distinct conflict-free addresses per
+// warp, GA_STRIDE = 20), 8 LDS.128 of block rows and 32*QPT relaxations:
+// 91% of the issued instructions are VIADDMNMX at QPT = 4, against 78% for
+// the lane-per-column product, and every accumulator is independent.
+// col2 is staged [query][32] with its 16-byte chunks XOR-swizzled by the
+// query (chunk u of query q at u ^ (q & 7)), so the epilogue's LDS.128s
+// are conflict-free; the 4 column-octet lanes of a query meet by SHFL.
+template <class V, int QPT>
+__device__ __forceinline__ void rb_chunk(const V* __restrict__ sA, const V* __restrict__ sB,
+                                         V (&acc)[QPT][8], uint32_t rows4, int qg, int cq) {
+    const V* a0 = sA + qg * GA_STRIDE;
+    const V* b0 = sB + cq * 8;
+#pragma unroll
+    for (uint32_t k4 = 0; k4 < uint32_t(GK); k4 += 4) {
+        if (k4 >= rows4) break;
+        uint4 a[QPT];
+#pragma unroll
+        for (int i = 0; i < QPT; ++i)
+            a[i] = *reinterpret_cast<const uint4*>(a0 + 8 * i * GA_STRIDE + k4);
+#pragma unroll
+        for (int r = 0; r < 4; r += 2) {
+            const uint4 x0 = *reinterpret_cast<const uint4*>(b0 + (k4 + r) * 32);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(b0 + (k4 + r) * 32 + 4);
+            const uint4 y0 = *reinterpret_cast<const uint4*>(b0 + (k4 + r + 1) * 32);
+            const uint4 y1 = *reinterpret_cast<const uint4*>(b0 + (k4 + r + 1) * 32 + 4);
+            const uint32_t bx[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const uint32_t by[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+            for (int i = 0; i < QPT; ++i) {
+                const V ar0 = Ops<V>::from_bits(r == 0 ? a[i].x : a[i].z);
+                const V ar1 = Ops<V>::from_bits(r == 0 ? a[i].y : a[i].w);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    acc[i][c] = Ops<V>::addmin2(ar0, Ops<V>::from_bits(bx[c]), ar1,
+                                                Ops<V>::from_bits(by[c]), acc[i][c]);
+            }
+        }
+    }
+}
+
+template <class V, int QPT>
+__device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const GroupWork& w,
+                                              WarpStage<V>* st, uint32_t c1, uint32_t c2,
+                                              uint32_t q0, uint32_t m, uint32_t cg,
+                                              uint32_t& phase) {
+    const int lane = threadIdx.x & 31, qg = lane & 7, cq = lane >> 3;
+    const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
+    const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
+    const uint32_t Bp1 = cb_stride(B1), Bp2 = cb_stride(B2);
+    const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
+    const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
+    const V* bq_task = q.bq + q.bq_off[c1 * q.k + c2] + uint64_t(cg) * ((B1 + GK - 1) / GK * GK) * 32;
+    __syncwarp();
+    const V* my_row1 = cb1;
+    if (uint32_t(lane) < m) {
+        st->id[lane] = w.sorted[q0 + lane];
+        st->c2off[lane] = w.s_l2[q0 + lane] * Bp2 + cg * 32;
+        my_row1 = cb1 + uint64_t(w.s_l1[q0 + lane]) * Bp1;
+    }
+    __syncwarp();
+    // col2: chunk u (4 columns) of query qq -> st->c2[qq * 32 + 4 * (u ^ (qq & 7))];
+    // chunks past the row's padded end zero-fill (their block columns are
+    // INF, so those sums never win)
+#pragma unroll
+    for (int t = 0; t < QPT * 2; ++t) {
+        const uint32_t e = t * 32 + lane, qq = e >> 3, u = e & 7;
+        const bool ok = qq < m && cg * 32 + 4 * u < Bp2;
+        cp_async16(st->c2 + qq * 32 + 4 * (u ^ (qq & 7)), cb2 + (ok ? st->c2off[qq] + 4 * u : 0), ok);
+    }
+    cp_async_commit();
+
+    auto issue = [&](uint32_t k0, int buf) {
+        V* sa = st->a[buf] + lane * GA_STRIDE;
+        if (uint32_t(lane) < m) {
+#pragma unroll
+            for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
+        }
+        cp_async_commit();
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&st->bar[buf], GK * 32 * sizeof(V));
+            bulk_g2s(st->b[buf], bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(V), &st->bar[buf]);
+        }
+    };
+
+    V acc[QPT][8];
+#pragma unroll
+    for (int i = 0; i < QPT; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[i][c] = Ops<V>::inf();
+    if (B1 > 0) issue(0, 0);
+    int buf = 0;
+    for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
+        const bool more = k0 + GK < B1;
+        if (more) issue(k0 + GK, buf ^ 1);
+        if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+        mbar_wait(&st->bar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        __syncwarp();
+        rb_chunk<V, QPT>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, qg, cq);
+        __syncwarp();  // buffer `buf` is refilled by the next issue
+        buf ^= 1;
+    }
+    cp_async_wait<0>();  // col2 (also covers B1 == 0)
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+        const uint32_t qq = qg + 8 * i;
+        const V* crow = st->c2 + qq * 32;
+        const uint4 c0 = *reinterpret_cast<const uint4*>(crow + 4 * ((2 * cq) ^ qg));
+        const uint4 c1v = *reinterpret_cast<const uint4*>(crow + 4 * ((2 * cq + 1) ^ qg));
+        const uint32_t cv[8] = {c0.x, c0.y, c0.z, c0.w, c1v.x, c1v.y, c1v.z, c1v.w};
+        V d = Ops<V>::inf();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) d = Ops<V>::addmin(acc[i][c], Ops<V>::from_bits(cv[c]), d);
+        d = Ops<V>::vmin(d, __shfl_xor_sync(0xffffffffu, d, 8));
+        d = Ops<V>::vmin(d, __shfl_xor_sync(0xffffffffu, d, 16));
+        // the 4 lanes of query qq now agree; lane cq == i reports it
+        if (cq == (i & 3) && qq < m) atomic_min_bits<V>(&w.best[st->id[qq]], d);
+    }
+}
+
 template <class V, int MODE>
 __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, GroupWork w) {
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
-    uint32_t phase = 0;  // QM_BLOCKS: parity of each B buffer's barrier
-    if (MODE == QM_BLOCKS) {
+    uint32_t phase = 0;  // QM_BLOCKS*: parity of each B buffer's barrier
+    if (MODE == QM_BLOCKS || MODE == QM_BLOCKS_LANE) {
         if ((threadIdx.x & 31) == 0) {
             mbar_init(&st->bar[0], 1);
             mbar_init(&st->bar[1], 1);
@@ -523,10 +653,18 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // the block-layout kernel has a fourth, 24-slot variant: its code is
         // small enough (no per-element staging) to stay in the instruction
         // cache, and it lifts useful/padded relaxations 0.76 -> 0.80 (cfg2)
-        if (m > 24 || (MODE != QM_BLOCKS && m > 16)) group_task<V, 8, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
-        else if (MODE == QM_BLOCKS && m > 16) group_task<V, 6, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
-        else if (m > 8) group_task<V, 4, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
-        else group_task<V, 2, MODE>(q, w, st, c1, c2, q0, m, cg, phase);
+        if (MODE == QM_BLOCKS) {  // register-blocked product, 8-query steps
+            if (m > 24) group_task_rb<V, 4>(q, w, st, c1, c2, q0, m, cg, phase);
+            else if (m > 16) group_task_rb<V, 3>(q, w, st, c1, c2, q0, m, cg, phase);
+            else if (m > 8) group_task_rb<V, 2>(q, w, st, c1, c2, q0, m, cg, phase);
+            else group_task_rb<V, 1>(q, w, st, c1, c2, q0, m, cg, phase);
+            continue;
+        }
+        constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
+        if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+        else if (TM == QM_BLOCKS && m > 16) group_task<V, 6, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+        else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+        else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
     }
 }
 
