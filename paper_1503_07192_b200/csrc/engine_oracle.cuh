@@ -557,9 +557,13 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
         const char* lay = std::getenv("PSP_QUERY_LAYOUT");
         const char* prod = std::getenv("PSP_QUERY_PRODUCT");
         const bool lane_product = prod && std::strcmp(prod, "lane") == 0;
+        const bool p8x8 = prod && std::strcmp(prod, "8x8") == 0;
         if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0) && lane_product)
             launch_grouped<V, QM_BLOCKS_LANE>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
                                               o->ctx->sms, q, count, v1, v2, dist, s);
+        else if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0) && p8x8)
+            launch_grouped<V, QM_BLOCKS_8X8>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+                                             o->ctx->sms, q, count, v1, v2, dist, s);
         else if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0))
             launch_grouped<V, QM_BLOCKS>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
                                          o->ctx->sms, q, count, v1, v2, dist, s);

@@ -83,9 +83,9 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
 // grouped kernel): the FW's tile-packed symmetric arena, the dense owned
 // rows of a routed shard, or the block query layout (one contiguous 2 KB
 // bulk copy per 16-row chunk).
-// QM_BLOCKS_LANE is the block layout with the earlier lane-per-column
-// product (PSP_QUERY_PRODUCT=lane, kept for A/B measurement).
-enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2, QM_BLOCKS_LANE = 3 };
+// QM_BLOCKS_LANE / QM_BLOCKS_8X8 are the block layout with earlier products
+// (PSP_QUERY_PRODUCT=lane|8x8, kept for A/B measurement).
+enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2, QM_BLOCKS_LANE = 3, QM_BLOCKS_8X8 = 4 };
 
 template <class V, bool ROUTED = false>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
@@ -263,14 +263,17 @@ __global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, ui
     const uint32_t n = w.task_cnt[b];
     if (n == 0) return;
     const uint32_t c1 = b / k, c2 = b % k;
-    const uint32_t ncg = (bnd_off[c2 + 1] - bnd_off[c2] + 31) / 32;
+    const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2], ncg = (B2 + 31) / 32;
     const uint32_t start = w.bin_start[b], end = w.bin_start[b + 1];
     uint4* out = w.tasks + w.task_start[b];
     for (uint32_t t = 0; t < n; ++t) {
         const uint32_t item = t / ncg, cg = t % ncg;
         const uint32_t q0 = start + item * GQ;
         const uint32_t m = min(uint32_t(GQ), end - q0);
-        out[t] = make_uint4(c1, c2, q0, m | (cg << 8));
+        // bit 6: the pair's last column group holds <= 16 columns (the
+        // register-blocked block-layout kernel then runs a 16-column task)
+        const uint32_t half = (cg + 1 == ncg && B2 - cg * 32 <= 16) ? 1u : 0u;
+        out[t] = make_uint4(c1, c2, q0, m | (half << 6) | (cg << 8));
     }
 }
 
@@ -505,55 +508,160 @@ __device__ __forceinline__ void group_task(const QueryView<V>& q, const GroupWor
 // ------------------------- block layout: register-blocked warp task --
 // Same task and staging as group_task<QM_BLOCKS> (one 2 KB bulk copy per
 // 16-row chunk of the column group, row1 by 16-byte cp.async into
-// [query][row]), but the product is register-blocked: lane = (query group
-// qg = lane & 7, column octet cq = lane >> 3) owns queries qg + 8i
-// (i < QPT) x columns cq*8 .. cq*8+7, i.e. QPT x 8 accumulators. Per 4 rows
-// a lane issues QPT LDS.128 of row1 (8 distinct conflict-free addresses per
-// warp, GA_STRIDE = 20), 8 LDS.128 of block rows and 32*QPT relaxations:
-// 91% of the issued instructions are VIADDMNMX at QPT = 4, against 78% for
-// the lane-per-column product, and every accumulator is independent.
+// [query][row]), but the product is register-blocked. Lane layout
+// <NQG, CPL>: query group qg = lane % NQG, column slot cq = lane / NQG; the
+// lane owns queries qg + NQG*i (i < QPT) x columns cq*CPL .. cq*CPL+CPL-1,
+// i.e. QPT x CPL independent accumulators. Per 4 rows a lane issues QPT
+// LDS.128 of row1 (NQG distinct conflict-free addresses per warp,
+// GA_STRIDE = 20), 2*CPL/4 ... CPL LDS.128 of block rows and 4*CPL*QPT
+// relaxations (~90% of the issued instructions are VIADDMNMX).
+//   <4, 4>: 32 columns, queries in steps of 4 (QPT 1..8)
+//   <8, 4>: 16 columns, the last column group of a pair when <= 16 of its
+//           columns exist (task flag), queries in steps of 8 (QPT 1..4)
+//   <8, 8>: 32 columns, steps of 8 (PSP_QUERY_PRODUCT=8x8, A/B only)
+// On cfg2 the finer steps lift useful / issued relaxations from 0.80 to
+// 0.90 (query padding to 4 instead of 8, column padding to 16 instead of 32).
 // col2 is staged [query][32] with its 16-byte chunks XOR-swizzled by the
 // query (chunk u of query q at u ^ (q & 7)), so the epilogue's LDS.128s
-// are conflict-free; the 4 column-octet lanes of a query meet by SHFL.
-template <class V, int QPT>
+// are conflict-free; the column-slot lanes of a query meet by SHFL.
+template <class V, int NQG, int CPL, int QPT>
 __device__ __forceinline__ void rb_chunk(const V* __restrict__ sA, const V* __restrict__ sB,
-                                         V (&acc)[QPT][8], uint32_t rows4, int qg, int cq) {
+                                         V (&acc)[32], uint32_t rows4, int lane) {
+    const int qg = lane % NQG, cq = lane / NQG;
     const V* a0 = sA + qg * GA_STRIDE;
-    const V* b0 = sB + cq * 8;
-#pragma unroll
-    for (uint32_t k4 = 0; k4 < uint32_t(GK); k4 += 4) {
-        if (k4 >= rows4) break;
+    const V* b0 = sB + cq * CPL;
+    // not unrolled: one 4-row step is 4 * CPL * QPT relaxations, and four
+    // unrolled copies per variant overflow the instruction cache
+#pragma unroll 1
+    for (uint32_t k4 = 0; k4 < rows4; k4 += 4) {
         uint4 a[QPT];
 #pragma unroll
         for (int i = 0; i < QPT; ++i)
-            a[i] = *reinterpret_cast<const uint4*>(a0 + 8 * i * GA_STRIDE + k4);
+            a[i] = *reinterpret_cast<const uint4*>(a0 + NQG * i * GA_STRIDE + k4);
 #pragma unroll
         for (int r = 0; r < 4; r += 2) {
-            const uint4 x0 = *reinterpret_cast<const uint4*>(b0 + (k4 + r) * 32);
-            const uint4 x1 = *reinterpret_cast<const uint4*>(b0 + (k4 + r) * 32 + 4);
-            const uint4 y0 = *reinterpret_cast<const uint4*>(b0 + (k4 + r + 1) * 32);
-            const uint4 y1 = *reinterpret_cast<const uint4*>(b0 + (k4 + r + 1) * 32 + 4);
-            const uint32_t bx[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            const uint32_t by[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+            uint32_t bx[CPL], by[CPL];
+#pragma unroll
+            for (int h = 0; h < CPL / 4; ++h) {
+                const uint4 x = *reinterpret_cast<const uint4*>(b0 + (k4 + r) * 32 + 4 * h);
+                const uint4 y = *reinterpret_cast<const uint4*>(b0 + (k4 + r + 1) * 32 + 4 * h);
+                bx[4 * h] = x.x; bx[4 * h + 1] = x.y; bx[4 * h + 2] = x.z; bx[4 * h + 3] = x.w;
+                by[4 * h] = y.x; by[4 * h + 1] = y.y; by[4 * h + 2] = y.z; by[4 * h + 3] = y.w;
+            }
 #pragma unroll
             for (int i = 0; i < QPT; ++i) {
                 const V ar0 = Ops<V>::from_bits(r == 0 ? a[i].x : a[i].z);
                 const V ar1 = Ops<V>::from_bits(r == 0 ? a[i].y : a[i].w);
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    acc[i][c] = Ops<V>::addmin2(ar0, Ops<V>::from_bits(bx[c]), ar1,
-                                                Ops<V>::from_bits(by[c]), acc[i][c]);
+                for (int c = 0; c < CPL; ++c)
+                    acc[i * CPL + c] = Ops<V>::addmin2(ar0, Ops<V>::from_bits(bx[c]), ar1,
+                                                       Ops<V>::from_bits(by[c]), acc[i * CPL + c]);
             }
         }
     }
 }
 
-template <class V, int QPT>
+// Epilogue of one variant: t = min over the lane's columns of acc + col2 per
+// query slot, written to red[query][column slot] for the generic reduction.
+template <class V, int NQG, int CPL, int QPT>
+__device__ __forceinline__ void rb_combine(const V (&acc)[32], const V* __restrict__ c2s,
+                                           V* __restrict__ red, int lane) {
+    constexpr int NCS = 32 / NQG;
+    const int qg = lane % NQG, cq = lane / NQG;
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+        const uint32_t qq = qg + NQG * i;
+        const V* crow = c2s + qq * 32;
+        V d = Ops<V>::inf();
+#pragma unroll
+        for (int h = 0; h < CPL / 4; ++h) {
+            const uint4 cv = *reinterpret_cast<const uint4*>(
+                crow + 4 * ((cq * (CPL / 4) + h) ^ (qq & 7)));
+            d = Ops<V>::addmin(acc[i * CPL + 4 * h], Ops<V>::from_bits(cv.x), d);
+            d = Ops<V>::addmin(acc[i * CPL + 4 * h + 1], Ops<V>::from_bits(cv.y), d);
+            d = Ops<V>::addmin(acc[i * CPL + 4 * h + 2], Ops<V>::from_bits(cv.z), d);
+            d = Ops<V>::addmin(acc[i * CPL + 4 * h + 3], Ops<V>::from_bits(cv.w), d);
+        }
+        red[qq * 9 + cq] = d;  // 9-word rows: conflict-free over qg
+        (void)NCS;
+    }
+}
+
+// Variant table (the task's lane layout and query slots), one switch per
+// chunk over a flat 32-register accumulator array so all variants share the
+// staging, pipeline and reduction code (the kernel stays inside the
+// instruction cache):
+//   0..7   <4, 4, QPT = v + 1>   32 columns, 4 .. 32 queries in steps of 4
+//   8..11  <8, 4, QPT = v - 7>   16 columns (last column group of a pair
+//                                 with <= 16 columns), steps of 8
+//   ALT:   <8, 8, QPT = v + 1>   32 columns, steps of 8 (PSP_QUERY_PRODUCT=8x8)
+template <class V, bool ALT>
+__device__ __forceinline__ void rb_chunk_v(int v, const V* sA, const V* sB, V (&acc)[32],
+                                           uint32_t rows4, int lane) {
+    if constexpr (ALT) {
+        switch (v) {
+            case 0: rb_chunk<V, 8, 8, 1>(sA, sB, acc, rows4, lane); break;
+            case 1: rb_chunk<V, 8, 8, 2>(sA, sB, acc, rows4, lane); break;
+            case 2: rb_chunk<V, 8, 8, 3>(sA, sB, acc, rows4, lane); break;
+            default: rb_chunk<V, 8, 8, 4>(sA, sB, acc, rows4, lane); break;
+        }
+    } else {
+        switch (v) {
+            case 0: rb_chunk<V, 4, 4, 1>(sA, sB, acc, rows4, lane); break;
+            case 1: rb_chunk<V, 4, 4, 2>(sA, sB, acc, rows4, lane); break;
+            case 2: rb_chunk<V, 4, 4, 3>(sA, sB, acc, rows4, lane); break;
+            case 3: rb_chunk<V, 4, 4, 4>(sA, sB, acc, rows4, lane); break;
+            case 4: rb_chunk<V, 4, 4, 5>(sA, sB, acc, rows4, lane); break;
+            case 5: rb_chunk<V, 4, 4, 6>(sA, sB, acc, rows4, lane); break;
+            case 6: rb_chunk<V, 4, 4, 7>(sA, sB, acc, rows4, lane); break;
+            case 7: rb_chunk<V, 4, 4, 8>(sA, sB, acc, rows4, lane); break;
+            case 8: rb_chunk<V, 8, 4, 1>(sA, sB, acc, rows4, lane); break;
+            case 9: rb_chunk<V, 8, 4, 2>(sA, sB, acc, rows4, lane); break;
+            case 10: rb_chunk<V, 8, 4, 3>(sA, sB, acc, rows4, lane); break;
+            default: rb_chunk<V, 8, 4, 4>(sA, sB, acc, rows4, lane); break;
+        }
+    }
+}
+template <class V, bool ALT>
+__device__ __forceinline__ void rb_combine_v(int v, const V (&acc)[32], const V* c2s, V* red,
+                                             int lane) {
+    if constexpr (ALT) {
+        switch (v) {
+            case 0: rb_combine<V, 8, 8, 1>(acc, c2s, red, lane); break;
+            case 1: rb_combine<V, 8, 8, 2>(acc, c2s, red, lane); break;
+            case 2: rb_combine<V, 8, 8, 3>(acc, c2s, red, lane); break;
+            default: rb_combine<V, 8, 8, 4>(acc, c2s, red, lane); break;
+        }
+    } else {
+        switch (v) {
+            case 0: rb_combine<V, 4, 4, 1>(acc, c2s, red, lane); break;
+            case 1: rb_combine<V, 4, 4, 2>(acc, c2s, red, lane); break;
+            case 2: rb_combine<V, 4, 4, 3>(acc, c2s, red, lane); break;
+            case 3: rb_combine<V, 4, 4, 4>(acc, c2s, red, lane); break;
+            case 4: rb_combine<V, 4, 4, 5>(acc, c2s, red, lane); break;
+            case 5: rb_combine<V, 4, 4, 6>(acc, c2s, red, lane); break;
+            case 6: rb_combine<V, 4, 4, 7>(acc, c2s, red, lane); break;
+            case 7: rb_combine<V, 4, 4, 8>(acc, c2s, red, lane); break;
+            case 8: rb_combine<V, 8, 4, 1>(acc, c2s, red, lane); break;
+            case 9: rb_combine<V, 8, 4, 2>(acc, c2s, red, lane); break;
+            case 10: rb_combine<V, 8, 4, 3>(acc, c2s, red, lane); break;
+            default: rb_combine<V, 8, 4, 4>(acc, c2s, red, lane); break;
+        }
+    }
+}
+
+template <class V, bool ALT>
 __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const GroupWork& w,
                                               WarpStage<V>* st, uint32_t c1, uint32_t c2,
-                                              uint32_t q0, uint32_t m, uint32_t cg,
+                                              uint32_t q0, uint32_t m, uint32_t cg, bool half,
                                               uint32_t& phase) {
-    const int lane = threadIdx.x & 31, qg = lane & 7, cq = lane >> 3;
+    const int lane = threadIdx.x & 31;
+    // variant and its column-slot count (NCS lanes share a query)
+    int v, ncs;
+    if (ALT) { v = int((m + 7) / 8) - 1; ncs = 4; }
+    else if (half) { v = 7 + int((m + 7) / 8); ncs = 4; }
+    else { v = int((m + 3) / 4) - 1; ncs = 8; }
+    const uint32_t cch = half ? 4u : 8u;  // 4-column chunks of col2 the task uses
     const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
     const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
     const uint32_t Bp1 = cb_stride(B1), Bp2 = cb_stride(B2);
@@ -570,11 +678,10 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
     __syncwarp();
     // col2: chunk u (4 columns) of query qq -> st->c2[qq * 32 + 4 * (u ^ (qq & 7))];
     // chunks past the row's padded end zero-fill (their block columns are
-    // INF, so those sums never win)
-#pragma unroll
-    for (int t = 0; t < QPT * 2; ++t) {
-        const uint32_t e = t * 32 + lane, qq = e >> 3, u = e & 7;
-        const bool ok = qq < m && cg * 32 + 4 * u < Bp2;
+    // INF, so those sums never win). Slots >= m are never reported.
+    for (uint32_t e = lane; e < m * cch; e += 32) {
+        const uint32_t qq = e / cch, u = e % cch;
+        const bool ok = cg * 32 + 4 * u < Bp2;
         cp_async16(st->c2 + qq * 32 + 4 * (u ^ (qq & 7)), cb2 + (ok ? st->c2off[qq] + 4 * u : 0), ok);
     }
     cp_async_commit();
@@ -593,11 +700,9 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
         }
     };
 
-    V acc[QPT][8];
+    V acc[32];
 #pragma unroll
-    for (int i = 0; i < QPT; ++i)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[i][c] = Ops<V>::inf();
+    for (int i = 0; i < 32; ++i) acc[i] = Ops<V>::inf();
     if (B1 > 0) issue(0, 0);
     int buf = 0;
     for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
@@ -607,26 +712,20 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
         mbar_wait(&st->bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
         __syncwarp();
-        rb_chunk<V, QPT>(st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, qg, cq);
+        rb_chunk_v<V, ALT>(v, st->a[buf], st->b[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, lane);
         __syncwarp();  // buffer `buf` is refilled by the next issue
         buf ^= 1;
     }
     cp_async_wait<0>();  // col2 (also covers B1 == 0)
     __syncwarp();
-#pragma unroll
-    for (int i = 0; i < QPT; ++i) {
-        const uint32_t qq = qg + 8 * i;
-        const V* crow = st->c2 + qq * 32;
-        const uint4 c0 = *reinterpret_cast<const uint4*>(crow + 4 * ((2 * cq) ^ qg));
-        const uint4 c1v = *reinterpret_cast<const uint4*>(crow + 4 * ((2 * cq + 1) ^ qg));
-        const uint32_t cv[8] = {c0.x, c0.y, c0.z, c0.w, c1v.x, c1v.y, c1v.z, c1v.w};
-        V d = Ops<V>::inf();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) d = Ops<V>::addmin(acc[i][c], Ops<V>::from_bits(cv[c]), d);
-        d = Ops<V>::vmin(d, __shfl_xor_sync(0xffffffffu, d, 8));
-        d = Ops<V>::vmin(d, __shfl_xor_sync(0xffffffffu, d, 16));
-        // the 4 lanes of query qq now agree; lane cq == i reports it
-        if (cq == (i & 3) && qq < m) atomic_min_bits<V>(&w.best[st->id[qq]], d);
+    static_assert(GQ * 9 <= GQ * GA_STRIDE, "reduction scratch fits a[0]");
+    V* red = st->a[0];  // [query][9]: free after the last chunk
+    rb_combine_v<V, ALT>(v, acc, st->c2, red, lane);
+    __syncwarp();
+    if (uint32_t(lane) < m) {
+        V d = red[lane * 9];
+        for (int c = 1; c < ncs; ++c) d = Ops<V>::vmin(d, red[lane * 9 + c]);
+        atomic_min_bits<V>(&w.best[st->id[lane]], d);
     }
 }
 
@@ -635,7 +734,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
     uint32_t phase = 0;  // QM_BLOCKS*: parity of each B buffer's barrier
-    if (MODE == QM_BLOCKS || MODE == QM_BLOCKS_LANE) {
+    if (MODE == QM_BLOCKS || MODE == QM_BLOCKS_LANE || MODE == QM_BLOCKS_8X8) {
         if ((threadIdx.x & 31) == 0) {
             mbar_init(&st->bar[0], 1);
             mbar_init(&st->bar[1], 1);
@@ -646,25 +745,23 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
     const uint32_t nwarps = gridDim.x * GWARPS;
     for (uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5); task < total; task += nwarps) {
         const uint4 rec = w.tasks[task];
-        const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0xffu, cg = rec.w >> 8;
+        const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0x3fu, cg = rec.w >> 8;
+        const bool half = (rec.w >> 6) & 1u;  // last column group, <= 16 columns
         // three query-count variants (32/16/8 slots): finer variants cut the
         // padding (82% vs 77% utilisation) but grow the kernel past the
         // instruction cache and measured slower (321M vs 390M queries/s)
         // the block-layout kernel has a fourth, 24-slot variant: its code is
         // small enough (no per-element staging) to stay in the instruction
         // cache, and it lifts useful/padded relaxations 0.76 -> 0.80 (cfg2)
-        if (MODE == QM_BLOCKS) {  // register-blocked product, 8-query steps
-            if (m > 24) group_task_rb<V, 4>(q, w, st, c1, c2, q0, m, cg, phase);
-            else if (m > 16) group_task_rb<V, 3>(q, w, st, c1, c2, q0, m, cg, phase);
-            else if (m > 8) group_task_rb<V, 2>(q, w, st, c1, c2, q0, m, cg, phase);
-            else group_task_rb<V, 1>(q, w, st, c1, c2, q0, m, cg, phase);
-            continue;
+        if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {  // register-blocked product
+            group_task_rb<V, MODE == QM_BLOCKS_8X8>(q, w, st, c1, c2, q0, m, cg, half, phase);
+        } else {
+            constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
+            if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+            else if (TM == QM_BLOCKS && m > 16) group_task<V, 6, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+            else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+            else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
         }
-        constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
-        if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-        else if (TM == QM_BLOCKS && m > 16) group_task<V, 6, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-        else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-        else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
     }
 }
 
