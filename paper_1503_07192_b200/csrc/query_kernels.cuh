@@ -743,16 +743,24 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
     }
     const uint32_t total = w.task_start[w.nbins];
     const uint32_t nwarps = gridDim.x * GWARPS;
-    for (uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5); task < total; task += nwarps) {
+    // dynamic task queue: a warp's first task is its global warp id, later
+    // ones come from a counter (task_cnt[nbins], zeroed by group_tasks and
+    // free after the scans) fetched one task ahead so the atomic's latency
+    // hides behind the current task. Static striding left the last warps
+    // running ~20% past the mean (tasks differ in B1 and query count).
+    uint32_t* const queue = w.task_cnt + w.nbins;
+    const bool lead = (threadIdx.x & 31) == 0;
+    uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5);
+    while (task < total) {
+        uint32_t next = 0;
+        if (lead) next = atomicAdd(queue, 1u) + nwarps;
         const uint4 rec = w.tasks[task];
         const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0x3fu, cg = rec.w >> 8;
         const bool half = (rec.w >> 6) & 1u;  // last column group, <= 16 columns
-        // three query-count variants (32/16/8 slots): finer variants cut the
-        // padding (82% vs 77% utilisation) but grow the kernel past the
-        // instruction cache and measured slower (321M vs 390M queries/s)
-        // the block-layout kernel has a fourth, 24-slot variant: its code is
-        // small enough (no per-element staging) to stay in the instruction
-        // cache, and it lifts useful/padded relaxations 0.76 -> 0.80 (cfg2)
+        // block layout: the register-blocked product (12 variants behind one
+        // switch, see group_task_rb). Tile arena / routed / lane product:
+        // three query-count variants (32/16/8 slots; finer ones grew that
+        // kernel past the instruction cache), 24 slots for the lane product
         if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {  // register-blocked product
             group_task_rb<V, MODE == QM_BLOCKS_8X8>(q, w, st, c1, c2, q0, m, cg, half, phase);
         } else {
@@ -762,6 +770,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
             else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
             else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
         }
+        task = __shfl_sync(0xffffffffu, next, 0);
     }
 }
 
