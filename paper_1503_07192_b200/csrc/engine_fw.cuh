@@ -39,7 +39,15 @@ void fill_arena(MatArena& a, cudaStream_t s, int sms) {
     }
 }
 
-// The blocked FW driver: 3 launches per k-block on one stream.
+void read_p3_tiles(MatArena& a, cudaStream_t s) {
+    unsigned long long t = 0;
+    CK(cudaMemcpyAsync(&t, a.act_work_ptr(), sizeof(t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    a.p3_tiles = t;
+}
+
+// The blocked FW driver: 3 launches per k-block on one stream (4 with the
+// sparse phase-3 work list of a single matrix).
 template <class V>
 void run_fw(const MatArena& a, cudaStream_t s, int sms) {
     if (a.nmat == 0 || a.nb_max == 0) return;
@@ -48,16 +56,22 @@ void run_fw(const MatArena& a, cudaStream_t s, int sms) {
     const int smem = 2 * TT * sizeof(V);
     const uint64_t work = a.work_prefix[a.nmat];
     const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
+    if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
     for (uint32_t kb = 0; kb < a.nb_max; ++kb) {
         fw_phase1<V><<<a.nmat, NTHREADS, 0, s>>>(v, kb);
         CK_LAUNCH();
         if (a.nb_max > 1) {
             fw_phase2<V><<<dim3(a.nmat, a.nb_max), NTHREADS, smem, s>>>(v, kb);
             CK_LAUNCH();
+            if (v.act_flag) {
+                fw_active_list<V><<<1, 1024, 0, s>>>(v, kb);
+                CK_LAUNCH();
+            }
             fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
             CK_LAUNCH();
         }
     }
+    if (v.act_flag) read_p3_tiles(const_cast<MatArena&>(a), s);
 }
 
 #define NCK(x)                                                                         \
@@ -98,6 +112,7 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     double acc_ms[4] = {0, 0, 0, 0};
     if (prof)
         for (auto& e : ev) CK(cudaEventCreate(&e));
+    if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
     for (uint32_t kb = 0; kb < nb; ++kb) {
         const int owner = int(kb % ctx->world);
         V* diag = tiles + tidx(kb, kb, nb) * TT;
@@ -118,9 +133,16 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
             fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(v, kb);
             CK_LAUNCH();
             if (prof) CK(cudaEventRecord(ev[2], s));
-            NCK(nccl().AllReduce(a.panel.p, a.panel.p, uint64_t(nb) * TT, dt, ncclMin, ctx->comm, s));
+            // sparse: the activity flags follow the panel slots in the same buffer
+            NCK(nccl().AllReduce(a.panel.p, a.panel.p, uint64_t(nb) * TT + (v.act_flag ? nb : 0), dt,
+                                 ncclMin, ctx->comm, s));
             if (prof) CK(cudaEventRecord(ev[3], s));
-            if (a.nrows) {
+            if (v.act_flag) {
+                fw_active_list<V><<<1, 1024, 0, s>>>(v, kb);
+                CK_LAUNCH();
+                fw_phase3<V><<<ctx->sms, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
+                CK_LAUNCH();
+            } else if (a.nrows) {
                 fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
                 CK_LAUNCH();
             }
@@ -141,6 +163,10 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
                      "allreduce %.1f ms, phase3 %.1f ms\n",
                      ctx->rank, nb, acc_ms[0], acc_ms[1], acc_ms[2], acc_ms[3]);
         for (auto& e : ev) cudaEventDestroy(e);
+    }
+    if (v.act_flag) {  // total phase-3 tiles over all ranks
+        NCK(nccl().AllReduce(v.act_work, v.act_work, 1, ncclUint64, ncclSum, ctx->comm, s));
+        read_p3_tiles(a, s);
     }
     // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
     const uint32_t batch = 64;

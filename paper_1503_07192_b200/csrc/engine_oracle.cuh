@@ -191,6 +191,44 @@ void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
 }
 
+// K2 elimination order (bg_order.hpp) when the FW walks sparse tiles, the
+// order beats the reference numbering, k is small enough for the host
+// simulation, and a second table fits for the permutation back
+// (PSP_BG_ORDER=natural keeps the reference numbering). Fills pos_off.
+template <class V>
+bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& pos_off) {
+    const Reordered& R = o->R;
+    const uint32_t k = R.k;
+    const char* env = std::getenv("PSP_BG_ORDER");
+    if (!o->bg.sparse || k < 3 || k > 4096 || (env && std::strcmp(env, "natural") == 0)) return false;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (o->bg.tiles.bytes + (2ull << 30) > free_b) return false;
+    std::vector<uint64_t> bsize(k);
+    for (uint32_t c = 0; c < k; ++c) bsize[c] = R.bnd_off[c + 1] - R.bnd_off[c];
+    std::vector<std::pair<uint32_t, uint32_t>> adj;
+    adj.reserve(L.bi.size());
+    auto comp_of = [&](uint32_t id) {
+        return uint32_t(std::upper_bound(R.bnd_off.begin(), R.bnd_off.end(), id) - R.bnd_off.begin() - 1);
+    };
+    for (size_t e = 0; e < L.bi.size(); ++e) adj.emplace_back(comp_of(L.bi[e]), comp_of(L.bj[e]));
+    std::sort(adj.begin(), adj.end());
+    adj.erase(std::unique(adj.begin(), adj.end()), adj.end());
+    const BgOrder ord = bg_component_order(k, bsize, adj);
+    bool ident = true;
+    for (uint32_t i = 0; i < k && ident; ++i) ident = ord.order[i] == i;
+    if (std::getenv("PSP_FW_PROFILE"))
+        std::fprintf(stderr, "[psp] K2 order: simulated work %.3e (reference numbering %.3e)%s\n",
+                     ord.work, ord.natural, ident ? ", kept" : "");
+    if (ident) return false;
+    uint64_t acc = 0;
+    for (uint32_t c : ord.order) {
+        pos_off[c] = static_cast<uint32_t>(acc);
+        acc += bsize[c];
+    }
+    return true;
+}
+
 template <class V>
 void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     psp_gpu_ctx* ctx = o->ctx;
@@ -224,17 +262,37 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     DBuf d_bnd = upload(R.bnd_off, s);
     unsigned long long clique = 0;
     double k2_ms = 0.0;
+    uint64_t k2_relax = 0;
     if (b > 0) {
         t_post.start(s);
         o->bg.create({b}, sizeof(V), true, s);
+        // K2 elimination order (bg_order.hpp): component c's boundary block
+        // sits at pos_off[c] during the FW; P -> reference ids afterwards
+        std::vector<uint32_t> pos_off(R.bnd_off.begin(), R.bnd_off.end() - 1);
+        const bool permuted = choose_bg_order<V>(o, L, pos_off);
         fill_arena<V>(o->bg, s, ctx->sms);
+        DBuf d_pos_off = upload(pos_off, s);
         DBuf d_clique(sizeof(unsigned long long));
         CK(cudaMemsetAsync(d_clique.p, 0, sizeof(unsigned long long), s));
         copy_boundary_blocks<V><<<k, 256, 0, s>>>(o->comps.view<V>(), d_bnd.as<uint32_t>(),
-                                                  o->bg.view<V>(),
+                                                  d_pos_off.as<uint32_t>(), o->bg.view<V>(),
                                                   d_clique.as<unsigned long long>());
         CK_LAUNCH();
-        scatter<V>(o->bg, nullptr, L.bi, L.bj, L.bw, q, s);
+        std::vector<uint32_t> posmap;  // boundary id -> K2 position
+        if (permuted) {
+            posmap.resize(b);
+            for (uint32_t c = 0; c < k; ++c)
+                for (uint32_t i = R.bnd_off[c]; i < R.bnd_off[c + 1]; ++i)
+                    posmap[i] = pos_off[c] + (i - R.bnd_off[c]);
+            std::vector<uint32_t> pi(L.bi.size()), pj(L.bj.size());
+            for (size_t e = 0; e < pi.size(); ++e) {
+                pi[e] = posmap[L.bi[e]];
+                pj[e] = posmap[L.bj[e]];
+            }
+            scatter<V>(o->bg, nullptr, pi, pj, L.bw, q, s);
+        } else {
+            scatter<V>(o->bg, nullptr, L.bi, L.bj, L.bw, q, s);
+        }
         CK(cudaMemcpyAsync(&clique, d_clique.p, sizeof(clique), cudaMemcpyDeviceToHost, s));
         t_post.stop(s);
         CK(cudaStreamSynchronize(s));
@@ -242,6 +300,19 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
+        k2_relax = o->bg.relaxations();
+        if (permuted) {
+            o->bg.panel.reset();
+            MatArena ref;
+            ref.create({b}, sizeof(V), false, s);
+            DBuf d_pos = upload(posmap, s);
+            const uint32_t nb = ref.nb[0];
+            permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), ref.tiles.as<V>(), nb,
+                                                        uint32_t(b), d_pos.as<uint32_t>());
+            CK_LAUNCH();
+            CK(cudaStreamSynchronize(s));
+            o->bg = std::move(ref);
+        }
         t_k2.stop(s);
         CK(cudaStreamSynchronize(s));
         k2_ms = t_k2.ms();
@@ -268,7 +339,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         st->k2_device_ms = k2_ms;
         st->init_device_ms = init_ms;
         st->k1_relaxations = o->comps.relaxations();
-        st->k2_relaxations = b ? o->bg.relaxations() : 0;
+        st->k2_relaxations = k2_relax;
         st->boundary_total = b;
         st->bg_edges = L.bi.size() + clique;
         uint64_t stored = 0;

@@ -111,6 +111,13 @@ struct MatArena {
     // row ownership for the multi-GPU boundary graph (nmat == 1)
     uint32_t rank = 0, world = 1, nrows = 0;
     DBuf d_rows, d_row_prefix;
+    // sparse phase 3 (single matrix, see MatSet::act_*): flags ride at the
+    // end of the panel buffer, the work lists in d_act; p3_tiles = phase-3
+    // tiles actually walked (all ranks), read back after the FW.
+    // PSP_FW_DENSE=1 walks every tile (A/B measurement).
+    bool sparse = false;
+    DBuf d_act;
+    uint64_t p3_tiles = 0;
 
     void shard_rows(uint32_t r, uint32_t g, cudaStream_t s) {
         rank = r;
@@ -146,7 +153,9 @@ struct MatArena {
             work_prefix[m + 1] = work_prefix[m] + ntiles_upper(nb[m]);
         }
         tiles.alloc(tile_elems * vbytes);
-        if (with_panel) panel.alloc(panel_elems * vbytes);
+        sparse = with_panel && nmat == 1 && nb[0] > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
+        if (with_panel) panel.alloc((panel_elems + (sparse ? nb[0] : 0)) * vbytes);
+        if (sparse) d_act.alloc(act_bytes());
         d_tile_base = upload(tile_base, s);
         d_panel_base = upload(panel_base, s);
         d_work_prefix = upload(work_prefix, s);
@@ -167,11 +176,26 @@ struct MatArena {
         v.nrows = world > 1 ? nrows : 0;
         v.rank = rank;
         v.world = world;
+        const bool sp = sparse && panel.p && d_act.p;
+        v.act_flag = sp ? panel.as<V>() + panel_elems : nullptr;
+        unsigned char* ab = sp ? d_act.as<unsigned char>() : nullptr;
+        const uint64_t n = nmat ? nb[0] : 0;
+        v.act_prefix = sp ? reinterpret_cast<uint64_t*>(ab) : nullptr;
+        v.act_work = sp ? reinterpret_cast<unsigned long long*>(ab + 8 * (n + 1)) : nullptr;
+        v.act_list = sp ? reinterpret_cast<uint32_t*>(ab + 8 * (n + 2)) : nullptr;
+        v.act_rows = sp ? v.act_list + n : nullptr;
+        v.act_meta = sp ? v.act_rows + n : nullptr;
         return v;
+    }
+    size_t act_bytes() const { return 8 * (uint64_t(nb[0]) + 2) + 4 * (2 * uint64_t(nb[0]) + 2); }
+    unsigned long long* act_work_ptr() const {
+        return reinterpret_cast<unsigned long long*>(d_act.as<unsigned char>() + 8 * (uint64_t(nb[0]) + 1));
     }
     // relaxations the FW executes on the padded matrices: per k-block the
     // diagonal tile, the nb-1 panel tiles and the upper tiles off row/col kb
     uint64_t relaxations() const {
+        if (sparse && nmat == 1)  // diagonal + panel tiles per k-block, walked phase-3 tiles
+            return (p3_tiles + uint64_t(nb[0]) * nb[0]) * uint64_t(T) * T * T;
         uint64_t r = 0;
         for (uint32_t m = 0; m < nmat; ++m) r += ntiles_upper(nb[m]) * nb[m];
         return r * uint64_t(T) * T * T;

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
                 const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
                 st4(panel + e, inf4);
             }
+            if (ms.act_flag && threadIdx.x == 0) ms.act_flag[J] = V(1);  // min-allreduce neutral
             return;
         }
     }
@@ -272,6 +273,90 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
         store_block(home, acc, ty, tx);
         store_block_t(panel, acc, ty, tx);
     }
+    if (ms.act_flag) {
+        bool fin = false;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fin |= acc[i][j] < Ops<V>::inf();
+        fin = __syncthreads_or(fin);
+        if (tid == 0) ms.act_flag[J] = fin ? V(0) : V(1);
+    }
+}
+
+// Sparse phase 3 work list for k-block kb (one CTA of 1024 threads): the
+// active panel slots J != kb in ascending order, the rows this rank walks
+// (all of them, or I mod world == rank) as positions in that list, and the
+// prefix of their tile counts (row at position p walks J = list[p..m)).
+template <class V>
+__global__ void __launch_bounds__(1024) fw_active_list(MatSet<V> ms, uint32_t kb) {
+    __shared__ uint32_t warp_sum[32];
+    __shared__ uint32_t carry;
+    const uint32_t nb = ms.nb[0];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    // pass 1: compact the active slots
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t J = base + tid;
+        const bool act = J < nb && J != kb && ms.act_flag[J] == V(0);
+        const uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (lane == 0) warp_sum[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t before = carry;
+        for (int w = 0; w < wid; ++w) before += warp_sum[w];
+        before += __popc(bal & ((1u << lane) - 1u));
+        if (act) ms.act_list[before] = J;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < 32; ++w) t += warp_sum[w];
+            carry += t;
+        }
+        __syncthreads();
+    }
+    const uint32_t m = carry;
+    __syncthreads();
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    // pass 2: rows of this rank (positions p) and the exclusive prefix of
+    // their tile counts (m - p), one block-wide scan per 1024 positions
+    __shared__ unsigned long long wsum64[32];
+    __shared__ unsigned long long carry64;
+    if (tid == 0) carry64 = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < m; base += 1024) {
+        const uint32_t p = base + tid;
+        const bool own = p < m && (ms.world <= 1 || ms.act_list[p] % ms.world == ms.rank);
+        const uint32_t bal = __ballot_sync(0xffffffffu, own);
+        unsigned long long v = own ? (unsigned long long)(m - p) : 0ull, incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) { warp_sum[wid] = __popc(bal); wsum64[wid] = incl; }
+        __syncthreads();
+        uint32_t before = carry;
+        unsigned long long pre = carry64;
+        for (int w = 0; w < wid; ++w) { before += warp_sum[w]; pre += wsum64[w]; }
+        before += __popc(bal & ((1u << lane) - 1u));
+        if (own) {
+            ms.act_rows[before] = p;
+            ms.act_prefix[before] = pre + incl - v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 0; w < 32; ++w) { carry += warp_sum[w]; carry64 += wsum64[w]; }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ms.act_prefix[carry] = carry64;
+        ms.act_meta[0] = m;
+        ms.act_meta[1] = carry;
+        atomicAdd(ms.act_work, carry64);
+    }
 }
 
 // ---------------------------------------------------------------- phase 3 --
@@ -291,12 +376,22 @@ __device__ __forceinline__ uint32_t row_start(uint32_t I, uint32_t nb) {
 struct P3Cursor {
     uint64_t w;
     uint32_t m, ri, nb, I, J;
+    uint32_t p, q, am, anr;  // sparse mode: positions of I and J in act_list, |list|, rows
 };
 
 template <class V>
 __device__ __forceinline__ void p3_advance(const MatSet<V>& ms, P3Cursor& c) {
     ++c.w;
-    if (ms.rows != nullptr) {
+    if (ms.act_flag != nullptr) {
+        if (++c.q == c.am && ++c.ri < c.anr) {
+            c.p = ms.act_rows[c.ri];
+            c.q = c.p;
+        }
+        if (c.ri < c.anr) {
+            c.I = ms.act_list[c.p];
+            c.J = ms.act_list[c.q];
+        }
+    } else if (ms.rows != nullptr) {
         if (++c.J == c.nb && ++c.ri < ms.nrows) {
             c.I = ms.rows[c.ri];
             c.J = c.I;
@@ -326,8 +421,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
     __shared__ uint64_t bars[2];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 
-    const bool rowlist = ms.rows != nullptr;
-    const uint64_t total = rowlist ? ms.row_prefix[ms.nrows] : ms.work_prefix[ms.nmat];
+    const bool sparse = ms.act_flag != nullptr;
+    const bool rowlist = !sparse && ms.rows != nullptr;
+    const uint32_t anr = sparse ? ms.act_meta[1] : 0u;
+    const uint64_t total = sparse ? ms.act_prefix[anr]
+                                  : rowlist ? ms.row_prefix[ms.nrows] : ms.work_prefix[ms.nmat];
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t w0 = uint64_t(blockIdx.x) * per;
     const uint64_t w1 = min(total, w0 + per);
@@ -337,7 +435,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
     cur.w = w0;
     cur.m = 0;
     cur.ri = 0;
-    if (rowlist) {
+    if (sparse) {
+        uint32_t lo = 0, hi = anr;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (ms.act_prefix[mid] <= w0) lo = mid; else hi = mid;
+        }
+        cur.ri = lo;
+        cur.nb = ms.nb[0];
+        cur.am = ms.act_meta[0];
+        cur.anr = anr;
+        cur.p = ms.act_rows[lo];
+        cur.q = cur.p + static_cast<uint32_t>(w0 - ms.act_prefix[lo]);
+        cur.I = ms.act_list[cur.p];
+        cur.J = ms.act_list[cur.q];
+    } else if (rowlist) {
         // owned rows only (multi-GPU boundary graph): binary search the row
         uint32_t lo = 0, hi = ms.nrows;
         while (hi - lo > 1) {
@@ -471,12 +583,15 @@ __global__ void scatter_pairs(MatSet<V> ms, const uint32_t* __restrict__ mat,
 // boundary prefix of every component table lands on the BG block diagonal;
 // counts finite pairs i < j for BuildStats::bg_edges.
 // grid: k CTAs, one component each (block-stride over its B x B block)
+// dst_off[c] = where component c's boundary block sits in the BG matrix
+// (bnd_off itself, or the K2 elimination order's positions, bg_order.hpp).
 template <class V>
 __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict__ bnd_off,
-                                     MatSet<V> bg, unsigned long long* clique_edges) {
+                                     const uint32_t* __restrict__ dst_off, MatSet<V> bg,
+                                     unsigned long long* clique_edges) {
     const uint32_t c = blockIdx.x;
-    const uint32_t g = bnd_off[c];
-    const uint32_t B = bnd_off[c + 1] - g;
+    const uint32_t g = dst_off[c];
+    const uint32_t B = bnd_off[c + 1] - bnd_off[c];
     const uint64_t total = uint64_t(B) * B;
     uint32_t finite = 0;
     for (uint64_t base = 0; base < total; base += blockDim.x) {
@@ -492,6 +607,25 @@ __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict
     }
     const uint32_t warp_total = __reduce_add_sync(0xffffffffu, finite);
     if ((threadIdx.x & 31) == 0 && warp_total) atomicAdd(clique_edges, warp_total);
+}
+
+// R <- P with boundary ids restored: element (i, j) of R's upper tiles is
+// P(pos[i], pos[j]) (pos = boundary id -> K2 position, bg_order.hpp);
+// padding vertices are isolated (INF, 0 on the diagonal).
+// grid: (nb, nb) CTAs, tile (I = y, J = x), lower ones exit.
+template <class V>
+__global__ void permute_sym(const V* __restrict__ P, V* __restrict__ R, uint32_t nb, uint32_t b,
+                            const uint32_t* __restrict__ pos) {
+    const uint32_t I = blockIdx.y, J = blockIdx.x;
+    if (I > J) return;
+    V* out = R + tidx(I, J, nb) * TT;
+    for (uint32_t e = threadIdx.x; e < uint32_t(TT); e += blockDim.x) {
+        const uint32_t i = I * T + e / T, j = J * T + e % T;
+        V v;
+        if (i < b && j < b) v = P[sym_off(pos[i], pos[j], nb)];
+        else v = i == j ? V(0) : Ops<V>::inf();
+        out[e] = v;
+    }
 }
 
 // Query side table CB[c] = rows 0..|C| of component c restricted to its

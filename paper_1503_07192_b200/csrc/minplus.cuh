@@ -105,6 +105,20 @@ template <class V> struct MatSet {
     const uint64_t* row_prefix; // prefix of their upper-tile counts (nrows + 1)
     uint32_t nrows;
     uint32_t rank, world;
+    // sparse phase 3 (nmat == 1; null: dense). Per k-block phase 2 writes
+    // act_flag[J] (V-typed so the sharded build min-allreduces it with the
+    // panel: 0 = panel slot J holds a finite entry, 1 = all INF);
+    // fw_active_list compacts the active slots into act_list and the rows
+    // this rank processes into act_rows (positions in act_list) with the
+    // prefix of their upper-tile counts; act_meta = {m, nrows}. A phase-3
+    // tile (I, J) whose panel slot I or J is all INF cannot change (INF + x
+    // >= INF), so only active x active tiles are walked.
+    V* act_flag;
+    uint32_t* act_list;
+    uint32_t* act_rows;
+    uint64_t* act_prefix;
+    uint32_t* act_meta;
+    unsigned long long* act_work;  // running count of phase-3 tiles walked
 };
 
 }  // namespace pspg

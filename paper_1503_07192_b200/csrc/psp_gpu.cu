@@ -39,6 +39,7 @@
 #include <string>
 #include <vector>
 
+#include "bg_order.hpp"
 #include "fw_kernels.cuh"
 #include "host_graph.hpp"
 #include "minplus.cuh"
