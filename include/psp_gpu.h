@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PSP_GPU_ABI_VERSION 2
+#define PSP_GPU_ABI_VERSION 3
 
 typedef enum psp_status {
     PSP_OK = 0,
@@ -183,6 +183,25 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
 psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       const uint32_t* v1, const uint32_t* v2, double* dist,
                                       void* stream);
+
+/* Pipelined host batches: the same answers as psp_gpu_query_batch, with up
+ * to `depth` batches in flight. A submit enqueues the host->device copy of
+ * its pairs on an input copy stream, the query kernels on the pipe's compute
+ * stream and the distance copy back on an output copy stream (ordered by
+ * events) and returns at once, so the copies of neighbouring batches overlap
+ * the kernels of this one (the serving loop of src/query.cpp:106-114 run as
+ * a stream). Host arrays must stay valid until psp_gpu_query_pipe_wait, and
+ * be pinned for the copies to be asynchronous. A submit blocks only while
+ * all `depth` slots are busy. wait() drains every submitted batch and
+ * returns PSP_EINVAL if any held an id >= n (src/query.cpp:30); the dist
+ * array of such a batch is then unspecified. One thread per pipe. */
+typedef struct psp_gpu_query_pipe psp_gpu_query_pipe;
+psp_status psp_gpu_query_pipe_create(const psp_gpu_oracle* o, int depth,
+                                     psp_gpu_query_pipe** out);
+psp_status psp_gpu_query_pipe_submit(psp_gpu_query_pipe* p, uint64_t count, const uint32_t* v1,
+                                     const uint32_t* v2, double* dist);
+psp_status psp_gpu_query_pipe_wait(psp_gpu_query_pipe* p);
+void psp_gpu_query_pipe_destroy(psp_gpu_query_pipe* p);
 
 /* -------------------------------------------------- routed (sharded) -- */
 /* The paper's distributed query mode on real GPUs: psp::routed_query and

@@ -197,11 +197,61 @@ class GpuOracle:
         from the device tables, byte-identical to the reference's image."""
         _lib.check(_lib.lib().psp_gpu_oracle_save(self.h, os.fsencode(path)))
 
+    def query_pipe(self, depth: int = 2) -> "QueryPipe":
+        """Pipelined host batches (psp_gpu_query_pipe_*): copies of
+        neighbouring batches overlap the kernels of the current one."""
+        return QueryPipe(self, depth)
+
     def batch_query_device(self, v1_ptr: int, v2_ptr: int, dist_ptr: int, count: int,
                            stream: int | None = None) -> None:
         """Device-resident queries: raw device pointers, enqueued on `stream`."""
         _lib.check(_lib.lib().psp_gpu_query_batch_device(self.h, count, v1_ptr, v2_ptr, dist_ptr,
                                                          stream))
+
+
+class QueryPipe:
+    """Up to `depth` host batches in flight on one oracle. submit() returns at
+    once; the arrays passed to it are kept alive until wait(), which drains
+    the pipe and raises ValueError if a batch held an id >= n (that batch's
+    distances are then unspecified). Arrays may be numpy (copied to
+    contiguous u32 / written in place as f64) or raw host pointers."""
+
+    def __init__(self, oracle: "GpuOracle", depth: int = 2):
+        self.oracle = oracle
+        self.h = C.c_void_p()
+        _lib.check(_lib.lib().psp_gpu_query_pipe_create(oracle.h, depth, C.byref(self.h)))
+        self._live = []
+
+    def submit(self, v1, v2, dist, count: int | None = None) -> None:
+        if isinstance(v1, int):  # raw pointers
+            _lib.check(_lib.lib().psp_gpu_query_pipe_submit(self.h, count, v1, v2, dist))
+            return
+        v1 = np.ascontiguousarray(v1, np.uint32)
+        v2 = np.ascontiguousarray(v2, np.uint32)
+        if v1.shape != v2.shape or dist.shape != v1.shape or dist.dtype != np.float64:
+            raise ValueError("QueryPipe.submit: v1, v2, dist must have equal length (dist f64)")
+        if not dist.flags.c_contiguous:
+            raise ValueError("QueryPipe.submit: dist must be contiguous")
+        self._live.append((v1, v2, dist))
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        _lib.check(_lib.lib().psp_gpu_query_pipe_submit(self.h, len(v1), p(v1), p(v2), p(dist)))
+
+    def wait(self) -> None:
+        try:
+            _lib.check(_lib.lib().psp_gpu_query_pipe_wait(self.h))
+        finally:
+            self._live.clear()
+
+    def close(self) -> None:
+        if self.h:
+            _lib.lib().psp_gpu_query_pipe_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def build_oracle(g: Graph, k: int, workers: int = 1, seed: int = 0,

@@ -144,6 +144,10 @@ SIGNATURES = {
     "psp_gpu_export_boundary_rows": (C.c_int, [_vp, C.c_uint32, _f64p]),
     "psp_gpu_query_batch": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp]),
     "psp_gpu_query_batch_device": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp, _vp]),
+    "psp_gpu_query_pipe_create": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
+    "psp_gpu_query_pipe_submit": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+    "psp_gpu_query_pipe_wait": (C.c_int, [_vp]),
+    "psp_gpu_query_pipe_destroy": (None, [_vp]),
     "psp_place_components": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int, _u32p]),
     "psp_gpu_shard_create": (C.c_int, [_vp, _u32p, C.POINTER(_vp)]),
     "psp_gpu_shard_free": (C.c_int, [_vp]),

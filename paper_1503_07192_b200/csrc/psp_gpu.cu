@@ -484,6 +484,110 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
     });
 }
 
+// ------------------------------------------------ pipelined host batches --
+struct psp_gpu_query_pipe {
+    const psp_gpu_oracle* o = nullptr;
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    struct Slot {
+        DBuf buf;  // dist (f64) | v1 | v2 | bad flag
+        cudaEvent_t in_done{}, cmp_done{}, out_done{};
+        uint32_t* h_bad = nullptr;  // pinned: the batch's bad-id flag
+        bool busy = false;
+    };
+    std::vector<Slot> slots;
+    uint64_t next = 0;
+    bool bad = false;
+    ~psp_gpu_query_pipe() {
+        for (auto& sl : slots) {
+            if (sl.busy) cudaEventSynchronize(sl.out_done);
+            cudaEventDestroy(sl.in_done);
+            cudaEventDestroy(sl.cmp_done);
+            cudaEventDestroy(sl.out_done);
+            if (sl.h_bad) cudaFreeHost(sl.h_bad);
+        }
+        for (cudaStream_t s : {s_in, s_cmp, s_out})
+            if (s) cudaStreamDestroy(s);
+    }
+    void retire(Slot& sl) {
+        if (!sl.busy) return;
+        CK(cudaEventSynchronize(sl.out_done));
+        if (*sl.h_bad) bad = true;
+        sl.busy = false;
+    }
+};
+
+psp_status psp_gpu_query_pipe_create(const psp_gpu_oracle* o, int depth, psp_gpu_query_pipe** out) {
+    return guarded([&] {
+        if (!o || !out) throw ArgError("query_pipe_create: NULL argument");
+        if (depth < 1 || depth > 64) throw ArgError("query_pipe_create: depth must be in 1..64");
+        CK(cudaSetDevice(o->ctx->device));
+        auto p = std::make_unique<psp_gpu_query_pipe>();
+        p->o = o;
+        for (cudaStream_t* s : {&p->s_in, &p->s_cmp, &p->s_out})
+            CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+        p->slots.resize(depth);
+        for (auto& sl : p->slots) {
+            CK(cudaEventCreateWithFlags(&sl.in_done, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sl.cmp_done, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming));
+            CK(cudaMallocHost(&sl.h_bad, sizeof(uint32_t)));
+            *sl.h_bad = 0;
+        }
+        *out = p.release();
+    });
+}
+
+psp_status psp_gpu_query_pipe_submit(psp_gpu_query_pipe* p, uint64_t count, const uint32_t* v1,
+                                     const uint32_t* v2, double* dist) {
+    return guarded([&] {
+        if (!p) throw ArgError("query_pipe_submit: NULL pipe");
+        if (count == 0) return;
+        if (!v1 || !v2 || !dist) throw ArgError("query_pipe_submit: NULL array");
+        const psp_gpu_oracle* o = p->o;
+        CK(cudaSetDevice(o->ctx->device));
+        auto& sl = p->slots[p->next++ % p->slots.size()];
+        p->retire(sl);  // its previous batch (buffers are reused)
+        const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t)) + 16;
+        if (sl.buf.bytes < need) sl.buf.alloc(need);
+        double* dd = sl.buf.as<double>();
+        uint32_t* d1 = reinterpret_cast<uint32_t*>(dd + count);
+        uint32_t* d2 = d1 + count;
+        uint32_t* dbad = d2 + count;
+        CK(cudaMemsetAsync(dbad, 0, sizeof(uint32_t), p->s_in));
+        CK(cudaMemcpyAsync(d1, v1, count * 4, cudaMemcpyHostToDevice, p->s_in));
+        CK(cudaMemcpyAsync(d2, v2, count * 4, cudaMemcpyHostToDevice, p->s_in));
+        CK(cudaEventRecord(sl.in_done, p->s_in));
+        CK(cudaStreamWaitEvent(p->s_cmp, sl.in_done, 0));
+        {
+            // the oracle's group workspace is shared with the other query
+            // entry points (its host-side growth is guarded here)
+            psp_gpu_oracle* mo = const_cast<psp_gpu_oracle*>(o);
+            std::lock_guard<std::mutex> lock(mo->query_mu);
+            if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, d1, d2, dd, p->s_cmp, dbad);
+            else launch_queries<float>(o, count, d1, d2, dd, p->s_cmp, dbad);
+        }
+        CK(cudaEventRecord(sl.cmp_done, p->s_cmp));
+        CK(cudaStreamWaitEvent(p->s_out, sl.cmp_done, 0));
+        CK(cudaMemcpyAsync(dist, dd, count * 8, cudaMemcpyDeviceToHost, p->s_out));
+        CK(cudaMemcpyAsync(sl.h_bad, dbad, sizeof(uint32_t), cudaMemcpyDeviceToHost, p->s_out));
+        CK(cudaEventRecord(sl.out_done, p->s_out));
+        sl.busy = true;
+    });
+}
+
+psp_status psp_gpu_query_pipe_wait(psp_gpu_query_pipe* p) {
+    return guarded([&] {
+        if (!p) throw ArgError("query_pipe_wait: NULL pipe");
+        CK(cudaSetDevice(p->o->ctx->device));
+        for (auto& sl : p->slots) p->retire(sl);
+        const bool bad = p->bad;
+        p->bad = false;
+        if (bad) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
+    });
+}
+
+void psp_gpu_query_pipe_destroy(psp_gpu_query_pipe* p) { delete p; }
+
 psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       const uint32_t* v1, const uint32_t* v2, double* dist,
                                       void* stream) {

@@ -388,3 +388,65 @@ def test_block_query_layout_matches_tile_arena(monkeypatch, golden_cfg1):
     assert np.array_equal(ob.batch_query(v1[:10], v2[:10]), ot.batch_query(v1[:10], v2[:10]))
     o = P.build_oracle(cases[0][0], 16, 4, 0)
     assert np.array_equal(o.batch_query(z["q_v1"], z["q_v2"]), z["q_dist"])
+
+
+@pytest.mark.gpu
+def test_query_pipe_matches_batch_query(golden_cfg1):
+    """psp_gpu_query_pipe_*: pipelined host batches give batch_query's answers;
+    a bad id fails wait() and the pipe stays usable."""
+    z = golden_cfg1
+    o = P.build_oracle(graph_of(z), 16, 4, 0)
+    for depth in (1, 2, 3):
+        pipe = o.query_pipe(depth)
+        sizes = [1, 10_000, 77, 250_000, 3, 100_000, 5_000]
+        batches = []
+        for i, m in enumerate(sizes):
+            v1, v2 = P.random_pairs(o.n, m, 100 + i)
+            out = np.empty(m, np.float64)
+            pipe.submit(v1, v2, out)
+            batches.append((v1, v2, out))
+        pipe.wait()
+        for v1, v2, out in batches:
+            assert np.array_equal(out, o.batch_query(v1, v2))
+        fixture = np.empty(len(z["q_v1"]), np.float64)
+        pipe.submit(z["q_v1"], z["q_v2"], fixture)
+        pipe.wait()
+        assert np.array_equal(fixture, z["q_dist"])
+        bad1 = np.array([0, o.n], np.uint32)
+        pipe.submit(z["q_v1"][:2], z["q_v2"][:2], np.empty(2))
+        pipe.submit(bad1, bad1[::-1].copy(), np.empty(2))
+        with pytest.raises(ValueError):
+            pipe.wait()
+        again = np.empty(len(z["q_v1"]), np.float64)
+        pipe.submit(z["q_v1"], z["q_v2"], again)
+        pipe.wait()
+        assert np.array_equal(again, z["q_dist"])
+        pipe.close()
+
+
+@pytest.mark.gpu
+def test_k2_order_and_sparse_walk_do_not_change_the_tables(monkeypatch, golden_cfg1):
+    """The K2 elimination order (bg_order.hpp, permuted back to reference
+    ids) and the sparse phase-3 walk give the same boundary tables and
+    answers as the dense FW in the reference numbering."""
+    from paper_1503_07192_b200 import graphs
+    z = golden_cfg1
+    cases = [(graph_of(z), 16), (graphs.delaunay(20_000, 4), 97),
+             (P.generate_grid(40, 60, (1, 9), 3), 24)]
+    for g, k in cases:
+        monkeypatch.setenv("PSP_FW_DENSE", "1")
+        monkeypatch.setenv("PSP_BG_ORDER", "natural")
+        od = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_FW_DENSE")
+        on = P.build_oracle(g, k, 4, 0)  # sparse walk, reference numbering
+        monkeypatch.delenv("PSP_BG_ORDER")
+        oo = P.build_oracle(g, k, 4, 0)  # sparse walk, elimination order
+        for c in range(k):
+            ref = od.boundary_rows(c)
+            assert np.array_equal(on.boundary_rows(c), ref)
+            assert np.array_equal(oo.boundary_rows(c), ref)
+        assert oo.stats["k2_relaxations"] <= od.stats["k2_relaxations"]
+        v1, v2 = P.random_pairs(g.n, 200_000, 9)
+        d = od.batch_query(v1, v2)
+        assert np.array_equal(on.batch_query(v1, v2), d)
+        assert np.array_equal(oo.batch_query(v1, v2), d)

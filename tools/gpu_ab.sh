@@ -1,6 +1,4 @@
 # A/B driver for gpurun: GPU tests, then bench variants (JSON in gpurun_out/)
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
-PSP_FW_PROFILE=1 timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
-PSP_BG_ORDER=natural timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench_natural.json 2> gpurun_out/bench_natural.err
-PSP_FW_DENSE=1 timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench_dense.json 2> gpurun_out/bench_dense.err
-PSP_FW_PROFILE=1 timeout 900 python bench.py --no-cpu-baseline --config delaunay1m_k1024 > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+timeout 900 python bench.py --no-cpu-baseline --config delaunay1m_k1024 > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
