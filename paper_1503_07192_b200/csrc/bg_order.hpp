@@ -1,4 +1,4 @@
-// bg_order.hpp — elimination order of the components for the boundary-graph FW.
+// bg_order.hpp — elimination order of the boundary-graph FW.
 //
 // The FW result does not depend on the pivot order, but its work does once
 // phase 3 skips tiles whose panel slot is all INF (fw_active_list): when
@@ -8,13 +8,19 @@
 // numbers components by the partitioner (src/partition.cpp), which after
 // ~30% of the pivots makes every row finite (cfg2: 71% of the dense work).
 // A greedy minimum-reach order, the minimum-degree heuristic of sparse
-// elimination restated at component granularity (every boundary clique is
-// one block, src/oracle.cpp:110-122), keeps the reach small far longer:
-// simulated 40% (cfg2, k = 256) and 34% (cfg3, k = 1024) of the dense work.
+// elimination, keeps the reach small far longer. Its unit is a PIECE: the
+// boundary vertices of one connected part of a component. A component's
+// boundary clique (src/oracle.cpp:110-122) only joins vertices at finite
+// distance, and the partitioner leaves small fragments of a component
+// inside its neighbours (cfg2: 979 pieces in 256 components), so whole
+// components as units would tie unrelated regions together (component
+// graph degree ~15, piece graph ~5.4). Simulated work on cfg2: 2.4e12
+// relaxations for pieces, 8.5e12 for components, 1.5e13 for the reference
+// numbering, 2.1e13 dense.
 //
-// The order only relabels where each component's boundary block sits in the
-// device matrix during K2; the finished table is permuted back to the
-// reference's boundary ids (permute_sym) before anything reads it.
+// The order only relabels where each boundary vertex sits in the device
+// matrix during K2; the finished table is permuted back to the reference's
+// boundary ids (permute_sym) before anything reads it.
 #pragma once
 #include <algorithm>
 #include <cstdint>
@@ -24,12 +30,13 @@
 namespace pspg {
 
 struct BgOrder {
-    std::vector<uint32_t> order;    // components in elimination order
+    std::vector<uint32_t> order;    // units in elimination order
     double work = 0.0, natural = 0.0;  // simulated relaxations (order / identity)
 };
 
-// bsize[c] = |B(c)|; adj = component pairs joined by a cross edge.
-inline BgOrder bg_component_order(uint32_t k, const std::vector<uint64_t>& bsize,
+// bsize[u] = boundary vertices of unit u; adj = unit pairs joined by a
+// cross edge.
+inline BgOrder bg_unit_order(uint32_t k, const std::vector<uint64_t>& bsize,
                                   const std::vector<std::pair<uint32_t, uint32_t>>& adj) {
     BgOrder out;
     const uint32_t W = (k + 63) / 64;

@@ -192,40 +192,73 @@ void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
 }
 
 // K2 elimination order (bg_order.hpp) when the FW walks sparse tiles, the
-// order beats the reference numbering, k is small enough for the host
-// simulation, and a second table fits for the permutation back
-// (PSP_BG_ORDER=natural keeps the reference numbering). Fills pos_off.
+// order beats the reference numbering, the unit count is small enough for
+// the host simulation, and a second table fits for the permutation back
+// (PSP_BG_ORDER=natural keeps the reference numbering, =component orders
+// whole components). Fills posmap (boundary id -> K2 position).
 template <class V>
-bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& pos_off) {
+bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& posmap) {
     const Reordered& R = o->R;
     const uint32_t k = R.k;
+    const uint64_t b = R.b();
     const char* env = std::getenv("PSP_BG_ORDER");
-    if (!o->bg.sparse || k < 3 || k > 4096 || (env && std::strcmp(env, "natural") == 0)) return false;
+    if (!o->bg.sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     if (o->bg.tiles.bytes + (2ull << 30) > free_b) return false;
-    std::vector<uint64_t> bsize(k);
-    for (uint32_t c = 0; c < k; ++c) bsize[c] = R.bnd_off[c + 1] - R.bnd_off[c];
+    const bool by_component = env && std::strcmp(env, "component") == 0;
+    // unit of every boundary id: its component, or the connected part of
+    // the component it lies in (union-find over the intra-component edges)
+    std::vector<uint32_t> unit(b);
+    uint32_t nu = 0;
+    if (by_component) {
+        for (uint32_t c = 0; c < k; ++c)
+            for (uint64_t i = R.bnd_off[c]; i < R.bnd_off[c + 1]; ++i) unit[i] = c;
+        nu = k;
+    } else {
+        std::vector<uint32_t> up(R.n);
+        for (uint64_t v = 0; v < R.n; ++v) up[v] = static_cast<uint32_t>(v);
+        auto find = [&](uint32_t x) {
+            while (up[x] != x) x = up[x] = up[up[x]];
+            return x;
+        };
+        for (size_t e = 0; e < L.mat.size(); ++e) {
+            const uint32_t base = static_cast<uint32_t>(R.comp_off[L.mat[e]]);
+            const uint32_t x = find(base + L.ii[e]), y = find(base + L.jj[e]);
+            if (x != y) up[std::max(x, y)] = std::min(x, y);
+        }
+        std::vector<uint32_t> id_of_root(R.n, UINT32_MAX);
+        for (uint32_t c = 0; c < k; ++c)
+            for (uint64_t i = R.bnd_off[c]; i < R.bnd_off[c + 1]; ++i) {
+                // boundary vertices come first in their component (local id = i - bnd_off)
+                const uint32_t r = find(static_cast<uint32_t>(R.comp_off[c] + (i - R.bnd_off[c])));
+                if (id_of_root[r] == UINT32_MAX) id_of_root[r] = nu++;
+                unit[i] = id_of_root[r];
+            }
+    }
+    if (nu < 3 || nu > 16384) return false;
+    std::vector<uint64_t> bsize(nu, 0);
+    for (uint64_t i = 0; i < b; ++i) ++bsize[unit[i]];
     std::vector<std::pair<uint32_t, uint32_t>> adj;
     adj.reserve(L.bi.size());
-    auto comp_of = [&](uint32_t id) {
-        return uint32_t(std::upper_bound(R.bnd_off.begin(), R.bnd_off.end(), id) - R.bnd_off.begin() - 1);
-    };
-    for (size_t e = 0; e < L.bi.size(); ++e) adj.emplace_back(comp_of(L.bi[e]), comp_of(L.bj[e]));
+    for (size_t e = 0; e < L.bi.size(); ++e) adj.emplace_back(unit[L.bi[e]], unit[L.bj[e]]);
     std::sort(adj.begin(), adj.end());
     adj.erase(std::unique(adj.begin(), adj.end()), adj.end());
-    const BgOrder ord = bg_component_order(k, bsize, adj);
+    const BgOrder ord = bg_unit_order(nu, bsize, adj);
     bool ident = true;
-    for (uint32_t i = 0; i < k && ident; ++i) ident = ord.order[i] == i;
+    for (uint32_t i = 0; i < nu && ident; ++i) ident = ord.order[i] == i;
     if (std::getenv("PSP_FW_PROFILE"))
-        std::fprintf(stderr, "[psp] K2 order: simulated work %.3e (reference numbering %.3e)%s\n",
-                     ord.work, ord.natural, ident ? ", kept" : "");
+        std::fprintf(stderr, "[psp] K2 order over %u %s: simulated work %.3e (reference numbering %.3e)%s\n",
+                     nu, by_component ? "components" : "pieces", ord.work, ord.natural,
+                     ident ? ", kept" : "");
     if (ident) return false;
-    uint64_t acc = 0;
-    for (uint32_t c : ord.order) {
-        pos_off[c] = static_cast<uint32_t>(acc);
-        acc += bsize[c];
-    }
+    // positions: units in elimination order, each unit's ids ascending
+    std::vector<uint64_t> rank_of(nu), off(nu + 1, 0), start(nu);
+    for (uint32_t r = 0; r < nu; ++r) rank_of[ord.order[r]] = r;
+    for (uint32_t r = 0; r < nu; ++r) off[r + 1] = off[r] + bsize[ord.order[r]];
+    for (uint32_t u = 0; u < nu; ++u) start[u] = off[rank_of[u]];
+    posmap.resize(b);
+    for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(start[unit[i]]++);
     return true;
 }
 
@@ -266,24 +299,23 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     if (b > 0) {
         t_post.start(s);
         o->bg.create({b}, sizeof(V), true, s);
-        // K2 elimination order (bg_order.hpp): component c's boundary block
-        // sits at pos_off[c] during the FW; P -> reference ids afterwards
-        std::vector<uint32_t> pos_off(R.bnd_off.begin(), R.bnd_off.end() - 1);
-        const bool permuted = choose_bg_order<V>(o, L, pos_off);
+        // K2 elimination order (bg_order.hpp): boundary id i sits at
+        // posmap[i] during the FW; P -> reference ids afterwards
+        std::vector<uint32_t> posmap;
+        const bool permuted = choose_bg_order<V>(o, L, posmap);
+        if (!permuted) {
+            posmap.resize(b);
+            for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(i);
+        }
         fill_arena<V>(o->bg, s, ctx->sms);
-        DBuf d_pos_off = upload(pos_off, s);
+        DBuf d_pos = upload(posmap, s);
         DBuf d_clique(sizeof(unsigned long long));
         CK(cudaMemsetAsync(d_clique.p, 0, sizeof(unsigned long long), s));
         copy_boundary_blocks<V><<<k, 256, 0, s>>>(o->comps.view<V>(), d_bnd.as<uint32_t>(),
-                                                  d_pos_off.as<uint32_t>(), o->bg.view<V>(),
+                                                  d_pos.as<uint32_t>(), o->bg.view<V>(),
                                                   d_clique.as<unsigned long long>());
         CK_LAUNCH();
-        std::vector<uint32_t> posmap;  // boundary id -> K2 position
         if (permuted) {
-            posmap.resize(b);
-            for (uint32_t c = 0; c < k; ++c)
-                for (uint32_t i = R.bnd_off[c]; i < R.bnd_off[c + 1]; ++i)
-                    posmap[i] = pos_off[c] + (i - R.bnd_off[c]);
             std::vector<uint32_t> pi(L.bi.size()), pj(L.bj.size());
             for (size_t e = 0; e < pi.size(); ++e) {
                 pi[e] = posmap[L.bi[e]];
@@ -305,7 +337,6 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             o->bg.panel.reset();
             MatArena ref;
             ref.create({b}, sizeof(V), false, s);
-            DBuf d_pos = upload(posmap, s);
             const uint32_t nb = ref.nb[0];
             permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), ref.tiles.as<V>(), nb,
                                                         uint32_t(b), d_pos.as<uint32_t>());

@@ -583,14 +583,14 @@ __global__ void scatter_pairs(MatSet<V> ms, const uint32_t* __restrict__ mat,
 // boundary prefix of every component table lands on the BG block diagonal;
 // counts finite pairs i < j for BuildStats::bg_edges.
 // grid: k CTAs, one component each (block-stride over its B x B block)
-// dst_off[c] = where component c's boundary block sits in the BG matrix
-// (bnd_off itself, or the K2 elimination order's positions, bg_order.hpp).
+// pos[id] = where boundary id sits in the BG matrix (the id itself, or its
+// K2 elimination-order position, bg_order.hpp).
 template <class V>
 __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict__ bnd_off,
-                                     const uint32_t* __restrict__ dst_off, MatSet<V> bg,
+                                     const uint32_t* __restrict__ pos, MatSet<V> bg,
                                      unsigned long long* clique_edges) {
     const uint32_t c = blockIdx.x;
-    const uint32_t g = dst_off[c];
+    const uint32_t* p = pos + bnd_off[c];
     const uint32_t B = bnd_off[c + 1] - bnd_off[c];
     const uint64_t total = uint64_t(B) * B;
     uint32_t finite = 0;
@@ -599,7 +599,7 @@ __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict
         if (idx < total) {
             const uint32_t i = static_cast<uint32_t>(idx / B), j = static_cast<uint32_t>(idx % B);
             const V val = comps.tiles[comps.tile_base[c] + sym_off(i, j, comps.nb[c])];
-            const uint32_t gi = g + i, gj = g + j;
+            const uint32_t gi = p[i], gj = p[j];
             if (gi / T <= gj / T)
                 bg.tiles[tidx(gi / T, gj / T, bg.nb[0]) * TT + uint64_t(gi % T) * T + gj % T] = val;
             finite += (i < j && val < Ops<V>::inf()) ? 1u : 0u;

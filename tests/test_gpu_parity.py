@@ -439,14 +439,17 @@ def test_k2_order_and_sparse_walk_do_not_change_the_tables(monkeypatch, golden_c
         od = P.build_oracle(g, k, 4, 0)
         monkeypatch.delenv("PSP_FW_DENSE")
         on = P.build_oracle(g, k, 4, 0)  # sparse walk, reference numbering
+        monkeypatch.setenv("PSP_BG_ORDER", "component")
+        oc = P.build_oracle(g, k, 4, 0)  # sparse walk, component order
         monkeypatch.delenv("PSP_BG_ORDER")
-        oo = P.build_oracle(g, k, 4, 0)  # sparse walk, elimination order
+        oo = P.build_oracle(g, k, 4, 0)  # sparse walk, piece order (default)
         for c in range(k):
             ref = od.boundary_rows(c)
             assert np.array_equal(on.boundary_rows(c), ref)
+            assert np.array_equal(oc.boundary_rows(c), ref)
             assert np.array_equal(oo.boundary_rows(c), ref)
         assert oo.stats["k2_relaxations"] <= od.stats["k2_relaxations"]
         v1, v2 = P.random_pairs(g.n, 200_000, 9)
         d = od.batch_query(v1, v2)
-        assert np.array_equal(on.batch_query(v1, v2), d)
-        assert np.array_equal(oo.batch_query(v1, v2), d)
+        for o in (on, oc, oo):
+            assert np.array_equal(o.batch_query(v1, v2), d)
