@@ -196,16 +196,37 @@ void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
 // the host simulation, and a second table fits for the permutation back
 // (PSP_BG_ORDER=natural keeps the reference numbering, =component orders
 // whole components). Fills posmap (boundary id -> K2 position).
+// When the second table does not fit beside the component tables, those
+// (idle during K2) are parked in host memory for the FW and the permutation
+// (`spill`), if the host has room for them.
+uint64_t host_mem_available() {
+    std::ifstream f("/proc/meminfo");
+    std::string key;
+    uint64_t kb = 0;
+    while (f >> key >> kb) {
+        if (key == "MemAvailable:") return kb * 1024;
+        f.ignore(256, '\n');
+    }
+    return 0;
+}
+
 template <class V>
-bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& posmap) {
+bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& posmap,
+                     bool& spill) {
     const Reordered& R = o->R;
     const uint32_t k = R.k;
     const uint64_t b = R.b();
+    spill = false;
     const char* env = std::getenv("PSP_BG_ORDER");
     if (!o->bg.sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    if (o->bg.tiles.bytes + (2ull << 30) > free_b) return false;
+    const uint64_t need = o->bg.tiles.bytes + (2ull << 30);
+    if (need > free_b) {
+        const uint64_t parked = o->comps.tiles.bytes;
+        if (need > free_b + parked || host_mem_available() < parked + (8ull << 30)) return false;
+        spill = true;
+    }
     const bool by_component = env && std::strcmp(env, "component") == 0;
     // unit of every boundary id: its component, or the connected part of
     // the component it lies in (union-find over the intra-component edges)
@@ -285,6 +306,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     run_fw<V>(o->comps, s, ctx->sms);
     t_k1.stop(s);
     CK(cudaStreamSynchronize(s));
+    o->comps.panel.reset();  // K1 scratch
     const double k1_ms = t_k1.ms();
     double init_ms = t_init.ms();
     const double component_ms = ms_since(t0);
@@ -302,7 +324,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         // K2 elimination order (bg_order.hpp): boundary id i sits at
         // posmap[i] during the FW; P -> reference ids afterwards
         std::vector<uint32_t> posmap;
-        const bool permuted = choose_bg_order<V>(o, L, posmap);
+        bool spill = false;
+        const bool permuted = choose_bg_order<V>(o, L, posmap, spill);
         if (!permuted) {
             posmap.resize(b);
             for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(i);
@@ -329,10 +352,39 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         t_post.stop(s);
         CK(cudaStreamSynchronize(s));
         init_ms += t_post.ms();
+        // park the component tables on the host while K2 runs (copied on a
+        // side stream from a helper thread, overlapping the FW)
+        std::unique_ptr<unsigned char[]> parked;  // default-initialised: no 70 GB memset
+        size_t parked_bytes = 0;
+        std::thread parker;
+        struct Joiner {
+            std::thread& t;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+            }
+        } join_on_unwind{parker};
+        Fail park_fail{PSP_OK, ""};
+        if (spill) {
+            parked_bytes = o->comps.tiles.bytes;
+            parked.reset(new unsigned char[parked_bytes]);
+            parker = std::thread([&] {
+                try {
+                    staged_copy(parked.get(), o->comps.tiles.p, parked_bytes, true, ctx->device);
+                } catch (const Fail& f) {
+                    park_fail = f;
+                }
+            });
+        }
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
         k2_relax = o->bg.relaxations();
+        const double fw_done_ms = ms_since(t0);
+        if (spill) {
+            parker.join();
+            if (park_fail.st != PSP_OK) throw park_fail;
+            o->comps.tiles.reset();
+        }
         if (permuted) {
             o->bg.panel.reset();
             MatArena ref;
@@ -343,6 +395,17 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             CK_LAUNCH();
             CK(cudaStreamSynchronize(s));
             o->bg = std::move(ref);
+        }
+        if (spill) {  // the component tables come back
+            const double back0 = ms_since(t0);
+            o->comps.tiles.alloc(parked_bytes);
+            CK(cudaStreamSynchronize(s));
+            staged_copy(o->comps.tiles.p, parked.get(), parked_bytes, false, ctx->device);
+            if (std::getenv("PSP_FW_PROFILE"))
+                std::fprintf(stderr,
+                             "[psp] component tables parked on the host during K2 (%.1f GB): FW done "
+                             "at %.0f ms, copy back %.0f ms (boundary phase so far %.0f ms)\n",
+                             parked_bytes / 1e9, fw_done_ms, ms_since(t0) - back0, ms_since(t0));
         }
         t_k2.stop(s);
         CK(cudaStreamSynchronize(s));

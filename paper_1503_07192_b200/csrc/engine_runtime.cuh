@@ -100,6 +100,51 @@ DBuf upload(const std::vector<T>& h, cudaStream_t s) {
     return d;
 }
 
+// Bulk copy between device memory and PAGEABLE host memory at PCIe speed:
+// worker threads each stage 64 MB chunks through their own pinned buffer and
+// stream (pageable cudaMemcpy runs at a few GB/s; pinning tens of GB up
+// front costs more than the copy).
+inline void staged_copy(void* dst, const void* src, size_t bytes, bool to_host, int device) {
+    const size_t chunk = 64ull << 20;
+    const size_t nchunks = (bytes + chunk - 1) / chunk;
+    const unsigned nthreads =
+        static_cast<unsigned>(std::min<size_t>(nchunks, std::max(2u, std::min(8u, std::thread::hardware_concurrency()))));
+    std::vector<std::thread> pool;
+    std::vector<Fail> fails(nthreads, Fail{PSP_OK, ""});
+    for (unsigned t = 0; t < nthreads; ++t) {
+        pool.emplace_back([&, t] {
+            void* pin = nullptr;
+            cudaStream_t st = nullptr;
+            try {
+                CK(cudaSetDevice(device));
+                CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                CK(cudaMallocHost(&pin, chunk));
+                for (size_t c = t; c < nchunks; c += nthreads) {
+                    const size_t off = c * chunk, len = std::min(chunk, bytes - off);
+                    if (to_host) {
+                        CK(cudaMemcpyAsync(pin, static_cast<const char*>(src) + off, len,
+                                           cudaMemcpyDeviceToHost, st));
+                        CK(cudaStreamSynchronize(st));
+                        std::memcpy(static_cast<char*>(dst) + off, pin, len);
+                    } else {
+                        std::memcpy(pin, static_cast<const char*>(src) + off, len);
+                        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin, len,
+                                           cudaMemcpyHostToDevice, st));
+                        CK(cudaStreamSynchronize(st));
+                    }
+                }
+            } catch (const Fail& f) {
+                fails[t] = f;
+            }
+            if (pin) cudaFreeHost(pin);
+            if (st) cudaStreamDestroy(st);
+        });
+    }
+    for (auto& th : pool) th.join();
+    for (auto& f : fails)
+        if (f.st != PSP_OK) throw f;
+}
+
 // A batch of symmetric tile-packed matrices (see minplus.cuh).
 struct MatArena {
     uint32_t nmat = 0, nb_max = 0;

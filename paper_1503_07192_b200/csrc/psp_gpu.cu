@@ -35,6 +35,7 @@
 #include <memory>
 #include <mutex>
 #include <random>
+#include <thread>
 #include <type_traits>
 #include <string>
 #include <vector>
