@@ -39,39 +39,11 @@ void fill_arena(MatArena& a, cudaStream_t s, int sms) {
     }
 }
 
-void read_p3_tiles(MatArena& a, cudaStream_t s) {
+void read_walked_tiles(MatArena& a, cudaStream_t s) {
     unsigned long long t = 0;
     CK(cudaMemcpyAsync(&t, a.act_work_ptr(), sizeof(t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    a.p3_tiles = t;
-}
-
-// The blocked FW driver: 3 launches per k-block on one stream (4 with the
-// sparse phase-3 work list of a single matrix).
-template <class V>
-void run_fw(const MatArena& a, cudaStream_t s, int sms) {
-    if (a.nmat == 0 || a.nb_max == 0) return;
-    set_kernel_attrs<V>();
-    const MatSet<V> v = a.view<V>();
-    const int smem = 2 * TT * sizeof(V);
-    const uint64_t work = a.work_prefix[a.nmat];
-    const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
-    if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
-    for (uint32_t kb = 0; kb < a.nb_max; ++kb) {
-        fw_phase1<V><<<a.nmat, NTHREADS, 0, s>>>(v, kb);
-        CK_LAUNCH();
-        if (a.nb_max > 1) {
-            fw_phase2<V><<<dim3(a.nmat, a.nb_max), NTHREADS, smem, s>>>(v, kb);
-            CK_LAUNCH();
-            if (v.act_flag) {
-                fw_active_list<V><<<1, 1024, 0, s>>>(v, kb);
-                CK_LAUNCH();
-            }
-            fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
-            CK_LAUNCH();
-        }
-    }
-    if (v.act_flag) read_p3_tiles(const_cast<MatArena&>(a), s);
+    a.walked_tiles = t;
 }
 
 #define NCK(x)                                                                         \
@@ -84,6 +56,114 @@ void run_fw(const MatArena& a, cudaStream_t s, int sms) {
 template <class V> ncclDataType_t nccl_type();
 template <> ncclDataType_t nccl_type<uint32_t>() { return ncclUint32; }
 template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+
+// Sparse walk: per-matrix active lists, then the prefix over matrices.
+template <class V>
+void launch_active_list(const MatSet<V>& v, uint32_t kb, cudaStream_t s) {
+    fw_active_list<V><<<v.nmat, 1024, 0, s>>>(v, kb);
+    CK_LAUNCH();
+    fw_mat_prefix<V><<<1, 1024, 0, s>>>(v);
+    CK_LAUNCH();
+}
+
+// The blocked FW driver over a set of matrices: 3 launches per k-block on
+// one stream (5 with the sparse walk's work lists).
+template <class V>
+void run_fw_set(const MatSet<V>& v, uint32_t nb_max, uint64_t work, cudaStream_t s, int sms) {
+    if (v.nmat == 0 || nb_max == 0) return;
+    set_kernel_attrs<V>();
+    const int smem = 2 * TT * sizeof(V);
+    const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
+    if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
+    for (uint32_t kb = 0; kb < nb_max; ++kb) {
+        fw_phase1<V><<<v.nmat, NTHREADS, 0, s>>>(v, kb);
+        CK_LAUNCH();
+        if (nb_max > 1) {
+            fw_phase2<V><<<dim3(v.nmat, nb_max), NTHREADS, smem, s>>>(v, kb);
+            CK_LAUNCH();
+            if (v.act_flag) launch_active_list<V>(v, kb, s);
+            fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
+            CK_LAUNCH();
+        }
+    }
+}
+
+template <class V>
+void run_fw(const MatArena& a, cudaStream_t s, int sms) {
+    if (a.nmat == 0 || a.nb_max == 0) return;
+    const MatSet<V> v = a.view<V>();
+    run_fw_set<V>(v, a.nb_max, a.work_prefix[a.nmat], s, sms);
+    if (v.act_flag) read_walked_tiles(const_cast<MatArena&>(a), s);
+}
+
+// Component-sharded K1 (multi-GPU): the k component matrices are
+// independent, so rank r closes a contiguous range of them, balanced by FW
+// work (ntiles_upper(nb) * nb tiles per matrix), and the ranges are then
+// broadcast from their owners, so every GPU ends with the full arena (queries
+// stay replicated). Each range is one contiguous run of the tile arena.
+inline std::vector<uint32_t> k1_ranges(const MatArena& a, int world) {
+    std::vector<uint64_t> cost(a.nmat + 1, 0);
+    for (uint32_t m = 0; m < a.nmat; ++m) cost[m + 1] = cost[m] + ntiles_upper(a.nb[m]) * a.nb[m];
+    std::vector<uint32_t> cut(world + 1, a.nmat);
+    cut[0] = 0;
+    uint32_t m = 0;
+    for (int r = 1; r < world; ++r) {
+        const double goal = double(cost[a.nmat]) * r / world;
+        while (m < a.nmat && double(cost[m + 1]) <= goal) ++m;
+        cut[r] = std::max(m, cut[r - 1]);
+    }
+    return cut;
+}
+
+// Every rank's range of the component arena from its owner (component-
+// sharded K1, see k1_ranges).
+template <class V>
+void broadcast_component_ranges(const MatArena& a, const std::vector<uint32_t>& cut, psp_gpu_ctx* ctx) {
+    const ncclDataType_t dt = nccl_type<V>();
+    V* tiles = a.tiles.as<V>();
+    NCK(nccl().GroupStart());
+    for (int r = 0; r < ctx->world; ++r) {
+        const uint64_t e0 = cut[r] < a.nmat ? a.tile_base[cut[r]] : a.tile_elems;
+        const uint64_t e1 = cut[r + 1] < a.nmat ? a.tile_base[cut[r + 1]] : a.tile_elems;
+        if (e1 > e0) NCK(nccl().Broadcast(tiles + e0, tiles + e0, e1 - e0, dt, r, ctx->comm, ctx->stream));
+    }
+    NCK(nccl().GroupEnd());
+}
+
+template <class V>
+void run_fw_components_sharded(const MatArena& a, psp_gpu_ctx* ctx) {
+    if (a.nmat == 0 || a.nb_max == 0) return;
+    cudaStream_t s = ctx->stream;
+    const std::vector<uint32_t> cut = k1_ranges(a, ctx->world);
+    const uint32_t m0 = cut[ctx->rank], m1 = cut[ctx->rank + 1];
+    if (m1 > m0) {
+        // a view of matrices [m0, m1): their own index arrays (work prefix
+        // rebased to 0) over the shared tile and panel buffers
+        std::vector<uint64_t> tb(a.tile_base.begin() + m0, a.tile_base.begin() + m1);
+        std::vector<uint64_t> pb(a.panel_base.begin() + m0, a.panel_base.begin() + m1);
+        std::vector<uint32_t> nbv(a.nb.begin() + m0, a.nb.begin() + m1);
+        std::vector<uint64_t> wp(m1 - m0 + 1);
+        for (uint32_t m = m0; m <= m1; ++m) wp[m - m0] = a.work_prefix[m] - a.work_prefix[m0];
+        DBuf d_tb = upload(tb, s), d_pb = upload(pb, s), d_nb = upload(nbv, s), d_wp = upload(wp, s);
+        MatSet<V> v = a.view<V>();
+        v.tile_base = d_tb.as<uint64_t>();
+        v.panel_base = d_pb.as<uint64_t>();
+        v.nb = d_nb.as<uint32_t>();
+        v.work_prefix = d_wp.as<uint64_t>();
+        v.nmat = m1 - m0;
+        v.nb_max = *std::max_element(nbv.begin(), nbv.end());
+        v.rows = nullptr;
+        v.row_prefix = nullptr;
+        v.nrows = 0;
+        v.rank = 0;
+        v.world = 1;
+        v.act_flag = nullptr;
+        run_fw_set<V>(v, v.nb_max, wp.back(), s, ctx->sms);
+        CK(cudaStreamSynchronize(s));  // the index arrays die here
+    }
+    broadcast_component_ranges<V>(a, cut, ctx);
+}
+
 
 // Row-sharded blocked FW of the boundary graph over ctx->world GPUs
 // (SURVEY §8e): tile row I is owned by rank I mod world. Per k-block the
@@ -138,8 +218,7 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
                                  ncclMin, ctx->comm, s));
             if (prof) CK(cudaEventRecord(ev[3], s));
             if (v.act_flag) {
-                fw_active_list<V><<<1, 1024, 0, s>>>(v, kb);
-                CK_LAUNCH();
+                launch_active_list<V>(v, kb, s);
                 fw_phase3<V><<<ctx->sms, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
                 CK_LAUNCH();
             } else if (a.nrows) {
@@ -166,7 +245,7 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     }
     if (v.act_flag) {  // total phase-3 tiles over all ranks
         NCK(nccl().AllReduce(v.act_work, v.act_work, 1, ncclUint64, ncclSum, ctx->comm, s));
-        read_p3_tiles(a, s);
+        read_walked_tiles(a, s);
     }
     // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
     const uint32_t batch = 64;

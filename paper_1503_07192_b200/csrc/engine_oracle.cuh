@@ -283,6 +283,115 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
     return true;
 }
 
+// ---- K1 with the nested-dissection elimination order (k1_order.hpp)
+// Components [m0, m1) (this rank's range) are closed in groups sized to the
+// free device memory: per group a working arena in FW positions, walked
+// sparse, then permute_batch writes the tables in reference numbering into
+// the final arena (which therefore needs no fill). Returns false (nothing
+// done) when a single component's working arena does not fit.
+struct K1Result {
+    double init_ms = 0.0, k1_ms = 0.0, order_ms = 0.0;
+    uint64_t walked_tiles = 0;
+};
+
+template <class V>
+bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1, K1Result& res) {
+    psp_gpu_ctx* ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
+    const Reordered& R = o->R;
+    const MatArena& F = o->comps;
+    const int q = o->kind.shift;
+    auto need = [&](uint32_t c) {  // working bytes of component c (tiles, panel, flags, lists)
+        const uint64_t nb = F.nb[c];
+        return (ntiles_upper(nb) * TT + nb * TT + nb) * sizeof(V) + 16 * nb + 64;
+    };
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t margin = 1ull << 30;
+    if (free_b < margin) return false;
+    const uint64_t budget = free_b - margin;
+    for (uint32_t c = m0; c < m1; ++c)
+        if (need(c) > budget) return false;
+    const auto t0 = Clock::now();
+    // intra-component edges bucketed by component
+    std::vector<uint64_t> eoff(R.k + 1, 0);
+    for (uint32_t c : L.mat) ++eoff[c + 1];
+    for (uint32_t c = 0; c < R.k; ++c) eoff[c + 1] += eoff[c];
+    std::vector<uint64_t> eidx(L.mat.size());
+    {
+        std::vector<uint64_t> fill(eoff.begin(), eoff.end() - 1);
+        for (uint64_t e = 0; e < L.mat.size(); ++e) eidx[fill[L.mat[e]]++] = e;
+    }
+    // positions per component, on all host threads
+    std::vector<uint64_t> pos_off(m1 - m0 + 1, 0);
+    for (uint32_t c = m0; c < m1; ++c)
+        pos_off[c - m0 + 1] = pos_off[c - m0] + (R.comp_off[c + 1] - R.comp_off[c]);
+    std::vector<uint32_t> pos(pos_off.back());
+    {
+        std::atomic<uint32_t> next{m0};
+        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nt; ++t)
+            pool.emplace_back([&] {
+                NdOrder nd;
+                std::vector<std::pair<uint32_t, uint32_t>> edges;
+                for (uint32_t c; (c = next.fetch_add(1)) < m1;) {
+                    const uint32_t n = R.comp_off[c + 1] - R.comp_off[c];
+                    edges.clear();
+                    for (uint64_t x = eoff[c]; x < eoff[c + 1]; ++x)
+                        edges.emplace_back(L.ii[eidx[x]], L.jj[eidx[x]]);
+                    const std::vector<uint32_t> p = nd.positions(n, edges);
+                    std::copy(p.begin(), p.end(), pos.begin() + pos_off[c - m0]);
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    res.order_ms += ms_since(t0);
+    EventTimer t_init, t_fw;
+    for (uint32_t g0 = m0; g0 < m1;) {
+        uint32_t g1 = g0;
+        uint64_t bytes = 0;
+        while (g1 < m1 && bytes + need(g1) <= budget) bytes += need(g1++);
+        std::vector<uint64_t> gsizes(g1 - g0);
+        for (uint32_t c = g0; c < g1; ++c) gsizes[c - g0] = R.comp_off[c + 1] - R.comp_off[c];
+        std::vector<uint32_t> gm, gi, gj;
+        std::vector<double> gw;
+        for (uint32_t c = g0; c < g1; ++c) {
+            const uint32_t* pc = pos.data() + pos_off[c - m0];
+            for (uint64_t x = eoff[c]; x < eoff[c + 1]; ++x) {
+                const uint64_t e = eidx[x];
+                gm.push_back(c - g0);
+                gi.push_back(pc[L.ii[e]]);
+                gj.push_back(pc[L.jj[e]]);
+                gw.push_back(L.w[e]);
+            }
+        }
+        std::vector<uint64_t> goff(g1 - g0 + 1);
+        for (uint32_t c = g0; c <= g1; ++c) goff[c - g0] = pos_off[c - m0] - pos_off[g0 - m0];
+        std::vector<uint32_t> gpos(pos.begin() + pos_off[g0 - m0], pos.begin() + pos_off[g1 - m0]);
+        MatArena W;
+        t_init.start(s);
+        W.create(gsizes, sizeof(V), true, s, 1);
+        fill_arena<V>(W, s, ctx->sms);
+        scatter<V>(W, &gm, gi, gj, gw, q, s);
+        t_init.stop(s);
+        res.init_ms += t_init.ms();
+        DBuf d_pos = upload(gpos, s), d_off = upload(goff, s);
+        t_fw.start(s);
+        run_fw<V>(W, s, ctx->sms);
+        if (W.nb_max > 0) {
+            permute_batch<V><<<dim3(W.nb_max, W.nb_max, g1 - g0), 256, 0, s>>>(
+                W.view<V>(), F.view<V>(), g0, d_pos.as<uint32_t>(), d_off.as<uint64_t>());
+            CK_LAUNCH();
+        }
+        t_fw.stop(s);
+        res.k1_ms += t_fw.ms();
+        res.walked_tiles += W.sparse ? W.walked_tiles : W.relaxations() / (uint64_t(T) * T * T);
+        g0 = g1;
+    }
+    return true;
+}
+
 template <class V>
 void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     psp_gpu_ctx* ctx = o->ctx;
@@ -290,26 +399,73 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     const Reordered& R = o->R;
     const uint32_t k = R.k;
     const int q = o->kind.shift;
-    EventTimer t_init, t_k1, t_k2, t_post;
+    EventTimer t_k2, t_post;
 
     // ---- Phase 2: K0 + K1
     auto t0 = Clock::now();
     std::vector<uint64_t> sizes(k);
     for (uint32_t c = 0; c < k; ++c) sizes[c] = R.comp_off[c + 1] - R.comp_off[c];
     EdgeLists L = split_edges(R);
-    t_init.start(s);
-    o->comps.create(sizes, sizeof(V), true, s);
-    fill_arena<V>(o->comps, s, ctx->sms);
-    scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
-    t_init.stop(s);
-    t_k1.start(s);
-    run_fw<V>(o->comps, s, ctx->sms);
-    t_k1.stop(s);
-    CK(cudaStreamSynchronize(s));
-    o->comps.panel.reset();  // K1 scratch
-    const double k1_ms = t_k1.ms();
-    double init_ms = t_init.ms();
+    const double split_ms = ms_since(t0);
+    double init_ms = 0.0, k1_ms = 0.0, order_ms = 0.0;
+    uint64_t k1_relax = 0;
+    const char* k1env = std::getenv("PSP_K1_ORDER");
+    const bool want_order = !(k1env && std::strcmp(k1env, "natural") == 0);
+    // this rank's components (all of them on one GPU)
+    std::vector<uint32_t> cut{0, k};
+    bool ordered = false;
+    if (want_order) {
+        o->comps.create(sizes, sizeof(V), false, s);
+        if (ctx->world > 1) cut = k1_ranges(o->comps, ctx->world);
+        if (o->comps.nb_max > 2) {
+            K1Result res;
+            ordered = k1_ordered<V>(o, L, cut[ctx->rank], cut[ctx->rank + 1], res);
+            init_ms = res.init_ms;
+            k1_ms = res.k1_ms;
+            order_ms = res.order_ms;
+            k1_relax = res.walked_tiles;
+        }
+        if (ordered) {
+            if (ctx->world > 1) {
+                // k1_relax: this rank's share; total over ranks
+                DBuf d_w(sizeof(unsigned long long));
+                CK(cudaMemcpyAsync(d_w.p, &k1_relax, 8, cudaMemcpyHostToDevice, s));
+                NCK(nccl().AllReduce(d_w.p, d_w.p, 1, ncclUint64, ncclSum, ctx->comm, s));
+                EventTimer t_bc;
+                t_bc.start(s);
+                broadcast_component_ranges<V>(o->comps, cut, ctx);
+                t_bc.stop(s);
+                k1_ms += t_bc.ms();
+                CK(cudaMemcpyAsync(&k1_relax, d_w.p, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
+            k1_relax *= uint64_t(T) * T * T;
+        }
+    }
+    if (!ordered) {  // reference numbering, dense walk, in place
+        EventTimer t_init, t_k1;
+        t_init.start(s);
+        o->comps.create(sizes, sizeof(V), true, s);
+        fill_arena<V>(o->comps, s, ctx->sms);
+        scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
+        t_init.stop(s);
+        t_k1.start(s);
+        if (ctx->world > 1) run_fw_components_sharded<V>(o->comps, ctx);
+        else run_fw<V>(o->comps, s, ctx->sms);
+        t_k1.stop(s);
+        CK(cudaStreamSynchronize(s));
+        o->comps.panel.reset();  // K1 scratch
+        k1_ms = t_k1.ms();
+        init_ms = t_init.ms();
+        k1_relax = o->comps.relaxations();
+    }
     const double component_ms = ms_since(t0);
+    if (std::getenv("PSP_FW_PROFILE"))
+        std::fprintf(stderr,
+                     "[psp] component phase %.1f ms (%s): split %.1f, order %.1f, device init "
+                     "%.2f + K1 %.2f ms, %.3e relaxations\n",
+                     component_ms, ordered ? "nested-dissection order, sparse walk" : "dense walk",
+                     split_ms, order_ms, init_ms, k1_ms, double(k1_relax));
 
     // ---- Phase 3: BG init + K2 + query tables
     t0 = Clock::now();
@@ -326,6 +482,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         std::vector<uint32_t> posmap;
         bool spill = false;
         const bool permuted = choose_bg_order<V>(o, L, posmap, spill);
+        if (std::getenv("PSP_FW_PROFILE"))
+            std::fprintf(stderr, "[psp] boundary phase: order chosen at %.1f ms\n", ms_since(t0));
         if (!permuted) {
             posmap.resize(b);
             for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(i);
@@ -378,7 +536,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
-        k2_relax = o->bg.relaxations();
+        k2_relax = o->bg.relaxations();  // (reads the walked-tile count: syncs)
         const double fw_done_ms = ms_since(t0);
         if (spill) {
             parker.join();
@@ -386,15 +544,24 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             o->comps.tiles.reset();
         }
         if (permuted) {
+            const double p0 = ms_since(t0);
             o->bg.panel.reset();
+            const double p1 = ms_since(t0);
             MatArena ref;
             ref.create({b}, sizeof(V), false, s);
+            const double p2 = ms_since(t0);
             const uint32_t nb = ref.nb[0];
             permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), ref.tiles.as<V>(), nb,
                                                         uint32_t(b), d_pos.as<uint32_t>());
             CK_LAUNCH();
             CK(cudaStreamSynchronize(s));
+            const double p3 = ms_since(t0);
             o->bg = std::move(ref);
+            if (std::getenv("PSP_FW_PROFILE"))
+                std::fprintf(stderr,
+                             "[psp] K2 permutation: panel free %.1f ms, table alloc %.1f ms, "
+                             "permute_sym %.1f ms, old table free %.1f ms\n",
+                             p1 - p0, p2 - p1, p3 - p2, ms_since(t0) - p3);
         }
         if (spill) {  // the component tables come back
             const double back0 = ms_since(t0);
@@ -410,6 +577,11 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         t_k2.stop(s);
         CK(cudaStreamSynchronize(s));
         k2_ms = t_k2.ms();
+        if (std::getenv("PSP_FW_PROFILE"))
+            std::fprintf(stderr,
+                         "[psp] boundary phase: FW issued+done at %.1f ms, K2 (FW + permute) %.1f "
+                         "ms device, phase so far %.1f ms\n",
+                         fw_done_ms, k2_ms, ms_since(t0));
     }
     // query-side tables
     t_post.start(s);
@@ -432,7 +604,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         st->k1_device_ms = k1_ms;
         st->k2_device_ms = k2_ms;
         st->init_device_ms = init_ms;
-        st->k1_relaxations = o->comps.relaxations();
+        st->k1_relaxations = k1_relax;
         st->k2_relaxations = k2_relax;
         st->boundary_total = b;
         st->bg_edges = L.bi.size() + clique;

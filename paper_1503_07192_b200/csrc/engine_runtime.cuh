@@ -156,13 +156,14 @@ struct MatArena {
     // row ownership for the multi-GPU boundary graph (nmat == 1)
     uint32_t rank = 0, world = 1, nrows = 0;
     DBuf d_rows, d_row_prefix;
-    // sparse phase 3 (single matrix, see MatSet::act_*): flags ride at the
-    // end of the panel buffer, the work lists in d_act; p3_tiles = phase-3
-    // tiles actually walked (all ranks), read back after the FW.
-    // PSP_FW_DENSE=1 walks every tile (A/B measurement).
+    // sparse walk (see MatSet::act_*): flags ride at the end of the panel
+    // buffer (one per panel slot), the work lists in d_act; walked_tiles =
+    // tile products actually executed (all phases, all ranks), read back
+    // after the FW. PSP_FW_DENSE=1 walks every tile (A/B measurement).
     bool sparse = false;
     DBuf d_act;
-    uint64_t p3_tiles = 0;
+    uint64_t walked_tiles = 0;
+    uint64_t nslots = 0;  // sum of nb over the matrices (= panel slots)
 
     void shard_rows(uint32_t r, uint32_t g, cudaStream_t s) {
         rank = r;
@@ -178,8 +179,10 @@ struct MatArena {
         d_row_prefix = upload(prefix, s);
     }
 
+    // sparse_walk: -1 = the default (a single matrix, i.e. the boundary
+    // graph), 0 / 1 = off / on for a batch of matrices
     void create(const std::vector<uint64_t>& sizes, size_t value_bytes, bool with_panel,
-                cudaStream_t s) {
+                cudaStream_t s, int sparse_walk = -1) {
         vbytes = value_bytes;
         nmat = static_cast<uint32_t>(sizes.size());
         nb.resize(nmat);
@@ -197,9 +200,11 @@ struct MatArena {
             panel_elems += uint64_t(nb[m]) * TT;
             work_prefix[m + 1] = work_prefix[m] + ntiles_upper(nb[m]);
         }
+        nslots = panel_elems / TT;
         tiles.alloc(tile_elems * vbytes);
-        sparse = with_panel && nmat == 1 && nb[0] > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
-        if (with_panel) panel.alloc((panel_elems + (sparse ? nb[0] : 0)) * vbytes);
+        sparse = with_panel && nb_max > 1 && std::getenv("PSP_FW_DENSE") == nullptr &&
+                 (sparse_walk < 0 ? nmat == 1 : sparse_walk > 0);
+        if (with_panel) panel.alloc((panel_elems + (sparse ? nslots : 0)) * vbytes);
         if (sparse) d_act.alloc(act_bytes());
         d_tile_base = upload(tile_base, s);
         d_panel_base = upload(panel_base, s);
@@ -224,23 +229,23 @@ struct MatArena {
         const bool sp = sparse && panel.p && d_act.p;
         v.act_flag = sp ? panel.as<V>() + panel_elems : nullptr;
         unsigned char* ab = sp ? d_act.as<unsigned char>() : nullptr;
-        const uint64_t n = nmat ? nb[0] : 0;
-        v.act_prefix = sp ? reinterpret_cast<uint64_t*>(ab) : nullptr;
-        v.act_work = sp ? reinterpret_cast<unsigned long long*>(ab + 8 * (n + 1)) : nullptr;
-        v.act_list = sp ? reinterpret_cast<uint32_t*>(ab + 8 * (n + 2)) : nullptr;
-        v.act_rows = sp ? v.act_list + n : nullptr;
-        v.act_meta = sp ? v.act_rows + n : nullptr;
+        // d_act: act_work | act_prefix (nslots + nmat) | mat_prefix (nmat + 1)
+        //        | act_list (nslots) | act_rows (nslots) | act_meta (2 nmat)
+        v.act_work = sp ? reinterpret_cast<unsigned long long*>(ab) : nullptr;
+        v.act_prefix = sp ? reinterpret_cast<uint64_t*>(ab + 8) : nullptr;
+        v.mat_prefix = sp ? v.act_prefix + nslots + nmat : nullptr;
+        v.act_list = sp ? reinterpret_cast<uint32_t*>(v.mat_prefix + nmat + 1) : nullptr;
+        v.act_rows = sp ? v.act_list + nslots : nullptr;
+        v.act_meta = sp ? v.act_rows + nslots : nullptr;
         return v;
     }
-    size_t act_bytes() const { return 8 * (uint64_t(nb[0]) + 2) + 4 * (2 * uint64_t(nb[0]) + 2); }
-    unsigned long long* act_work_ptr() const {
-        return reinterpret_cast<unsigned long long*>(d_act.as<unsigned char>() + 8 * (uint64_t(nb[0]) + 1));
-    }
+    size_t act_bytes() const { return 8 * (1 + nslots + 2 * uint64_t(nmat) + 1) + 4 * (2 * nslots + 2 * uint64_t(nmat)); }
+    unsigned long long* act_work_ptr() const { return reinterpret_cast<unsigned long long*>(d_act.p); }
     // relaxations the FW executes on the padded matrices: per k-block the
     // diagonal tile, the nb-1 panel tiles and the upper tiles off row/col kb
     uint64_t relaxations() const {
-        if (sparse && nmat == 1)  // diagonal + panel tiles per k-block, walked phase-3 tiles
-            return (p3_tiles + uint64_t(nb[0]) * nb[0]) * uint64_t(T) * T * T;
+        if (sparse)  // diagonal, computed panel and walked phase-3 tiles
+            return walked_tiles * uint64_t(T) * T * T;
         uint64_t r = 0;
         for (uint32_t m = 0; m < nmat; ++m) r += ntiles_upper(nb[m]) * nb[m];
         return r * uint64_t(T) * T * T;

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
                 const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
                 st4(panel + e, inf4);
             }
-            if (ms.act_flag && threadIdx.x == 0) ms.act_flag[J] = V(1);  // min-allreduce neutral
+            if (ms.act_flag && threadIdx.x == 0) ms.act_flag[J] = V(1);  // min-allreduce neutral (nmat == 1)
             return;
         }
     }
@@ -261,6 +261,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = Ops<V>::inf();
     mbar_wait(&bar, 0);
+    if (ms.act_flag) {
+        // sparse walk: a panel tile that is all INF stays all INF (and its
+        // slot inactive); one that holds a finite entry stays finite (Dkk*
+        // has a zero diagonal), so the flag is known before the product
+        const V* in = upper ? sB : sA;
+        bool fin = false;
+        for (int e = tid * 4; e < TT; e += NTHREADS * 4) {
+            const uint4 u = *reinterpret_cast<const uint4*>(in + e);
+            fin |= (Ops<V>::from_bits(u.x) < Ops<V>::inf()) | (Ops<V>::from_bits(u.y) < Ops<V>::inf()) |
+                   (Ops<V>::from_bits(u.z) < Ops<V>::inf()) | (Ops<V>::from_bits(u.w) < Ops<V>::inf());
+        }
+        fin = __syncthreads_or(fin);
+        if (tid == 0) ms.act_flag[ms.panel_base[m] / TT + J] = fin ? V(0) : V(1);
+        if (!fin) return;
+    }
     if (upper) {
         // out[k][j] = min_k' Dkk[k][k'] + R_J[k'][j]
         minplus_tile<V, true>(sA, sB, acc, ty, tx);
@@ -273,40 +288,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
         store_block(home, acc, ty, tx);
         store_block_t(panel, acc, ty, tx);
     }
-    if (ms.act_flag) {
-        bool fin = false;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) fin |= acc[i][j] < Ops<V>::inf();
-        fin = __syncthreads_or(fin);
-        if (tid == 0) ms.act_flag[J] = fin ? V(0) : V(1);
-    }
 }
 
-// Sparse phase 3 work list for k-block kb (one CTA of 1024 threads): the
-// active panel slots J != kb in ascending order, the rows this rank walks
-// (all of them, or I mod world == rank) as positions in that list, and the
-// prefix of their tile counts (row at position p walks J = list[p..m)).
+// Sparse phase 3 work lists for k-block kb, one CTA of 1024 threads per
+// matrix m: its active panel slots J != kb in ascending order, the rows this
+// rank walks (all of them, or I mod world == rank) as positions in that
+// list, and the prefix of their tile counts (row at position p walks
+// J = list[p..na)). act_work counts the tile products of the k-block: the
+// walked phase-3 tiles plus the diagonal and the computed panel tiles
+// (counted once, on rank 0, in the sharded build).
 template <class V>
 __global__ void __launch_bounds__(1024) fw_active_list(MatSet<V> ms, uint32_t kb) {
     __shared__ uint32_t warp_sum[32];
     __shared__ uint32_t carry;
-    const uint32_t nb = ms.nb[0];
+    const uint32_t mi = blockIdx.x;
+    const uint32_t nb = ms.nb[mi];
+    const uint64_t sb = ms.panel_base[mi] / TT, ab = sb + mi;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (kb >= nb) {  // finished (or empty) matrix: no work
+        if (tid == 0) {
+            ms.act_meta[2 * mi] = 0;
+            ms.act_meta[2 * mi + 1] = 0;
+            ms.act_prefix[ab] = 0;
+        }
+        return;
+    }
+    const V* flag = ms.act_flag + sb;
+    uint32_t* list = ms.act_list + sb;
     if (tid == 0) carry = 0;
     __syncthreads();
     // pass 1: compact the active slots
     for (uint32_t base = 0; base < nb; base += 1024) {
         const uint32_t J = base + tid;
-        const bool act = J < nb && J != kb && ms.act_flag[J] == V(0);
+        const bool act = J < nb && J != kb && flag[J] == V(0);
         const uint32_t bal = __ballot_sync(0xffffffffu, act);
         if (lane == 0) warp_sum[wid] = __popc(bal);
         __syncthreads();
         uint32_t before = carry;
         for (int w = 0; w < wid; ++w) before += warp_sum[w];
         before += __popc(bal & ((1u << lane) - 1u));
-        if (act) ms.act_list[before] = J;
+        if (act) list[before] = J;
         __syncthreads();
         if (tid == 0) {
             uint32_t t = 0;
@@ -315,21 +336,21 @@ __global__ void __launch_bounds__(1024) fw_active_list(MatSet<V> ms, uint32_t kb
         }
         __syncthreads();
     }
-    const uint32_t m = carry;
+    const uint32_t na = carry;
     __syncthreads();
     if (tid == 0) carry = 0;
     __syncthreads();
     // pass 2: rows of this rank (positions p) and the exclusive prefix of
-    // their tile counts (m - p), one block-wide scan per 1024 positions
+    // their tile counts (na - p), one block-wide scan per 1024 positions
     __shared__ unsigned long long wsum64[32];
     __shared__ unsigned long long carry64;
     if (tid == 0) carry64 = 0;
     __syncthreads();
-    for (uint32_t base = 0; base < m; base += 1024) {
+    for (uint32_t base = 0; base < na; base += 1024) {
         const uint32_t p = base + tid;
-        const bool own = p < m && (ms.world <= 1 || ms.act_list[p] % ms.world == ms.rank);
+        const bool own = p < na && (ms.world <= 1 || list[p] % ms.world == ms.rank);
         const uint32_t bal = __ballot_sync(0xffffffffu, own);
-        unsigned long long v = own ? (unsigned long long)(m - p) : 0ull, incl = v;
+        unsigned long long v = own ? (unsigned long long)(na - p) : 0ull, incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -342,8 +363,8 @@ __global__ void __launch_bounds__(1024) fw_active_list(MatSet<V> ms, uint32_t kb
         for (int w = 0; w < wid; ++w) { before += warp_sum[w]; pre += wsum64[w]; }
         before += __popc(bal & ((1u << lane) - 1u));
         if (own) {
-            ms.act_rows[before] = p;
-            ms.act_prefix[before] = pre + incl - v;
+            ms.act_rows[sb + before] = p;
+            ms.act_prefix[ab + before] = pre + incl - v;
         }
         __syncthreads();
         if (tid == 0) {
@@ -352,10 +373,44 @@ __global__ void __launch_bounds__(1024) fw_active_list(MatSet<V> ms, uint32_t kb
         __syncthreads();
     }
     if (tid == 0) {
-        ms.act_prefix[carry] = carry64;
-        ms.act_meta[0] = m;
-        ms.act_meta[1] = carry;
-        atomicAdd(ms.act_work, carry64);
+        ms.act_prefix[ab + carry] = carry64;
+        ms.act_meta[2 * mi] = na;
+        ms.act_meta[2 * mi + 1] = carry;
+        atomicAdd(ms.act_work, carry64 + ((ms.world <= 1 || ms.rank == 0) ? na + 1ull : 0ull));
+    }
+}
+
+// mat_prefix = exclusive prefix over the matrices of their phase-3 work
+// (one CTA of 1024 threads).
+template <class V>
+__global__ void __launch_bounds__(1024) fw_mat_prefix(MatSet<V> ms) {
+    __shared__ unsigned long long wsum[32];
+    __shared__ unsigned long long carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        carry = 0;
+        ms.mat_prefix[0] = 0;
+    }
+    __syncthreads();
+    for (uint32_t base = 0; base < ms.nmat; base += 1024) {
+        const uint32_t mi = base + tid;
+        unsigned long long v = 0;
+        if (mi < ms.nmat) v = ms.act_prefix[ms.panel_base[mi] / TT + mi + ms.act_meta[2 * mi + 1]];
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        unsigned long long pre = carry;
+        for (int w = 0; w < wid; ++w) pre += wsum[w];
+        if (mi < ms.nmat) ms.mat_prefix[mi + 1] = pre + incl;
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 0; w < 32; ++w) carry += wsum[w];
+        __syncthreads();
     }
 }
 
@@ -377,20 +432,40 @@ struct P3Cursor {
     uint64_t w;
     uint32_t m, ri, nb, I, J;
     uint32_t p, q, am, anr;  // sparse mode: positions of I and J in act_list, |list|, rows
+    uint64_t sb;             // sparse mode: matrix m's first panel slot (its lists start there)
 };
+
+// sparse mode: enter matrix m at its first walked row
+template <class V>
+__device__ __forceinline__ void p3_enter(const MatSet<V>& ms, P3Cursor& c, uint32_t m) {
+    c.m = m;
+    c.nb = ms.nb[m];
+    c.sb = ms.panel_base[m] / TT;
+    c.am = ms.act_meta[2 * m];
+    c.anr = ms.act_meta[2 * m + 1];
+    c.ri = 0;
+}
 
 template <class V>
 __device__ __forceinline__ void p3_advance(const MatSet<V>& ms, P3Cursor& c) {
     ++c.w;
     if (ms.act_flag != nullptr) {
         if (++c.q == c.am && ++c.ri < c.anr) {
-            c.p = ms.act_rows[c.ri];
+            c.p = ms.act_rows[c.sb + c.ri];
             c.q = c.p;
         }
-        if (c.ri < c.anr) {
-            c.I = ms.act_list[c.p];
-            c.J = ms.act_list[c.q];
+        if (c.ri >= c.anr) {  // next matrix with work
+            uint32_t m = c.m;
+            do {
+                ++m;
+            } while (m < ms.nmat && ms.mat_prefix[m + 1] == ms.mat_prefix[m]);
+            if (m >= ms.nmat) return;  // past the end: c.w >= total
+            p3_enter(ms, c, m);
+            c.p = ms.act_rows[c.sb];
+            c.q = c.p;
         }
+        c.I = ms.act_list[c.sb + c.p];
+        c.J = ms.act_list[c.sb + c.q];
     } else if (ms.rows != nullptr) {
         if (++c.J == c.nb && ++c.ri < ms.nrows) {
             c.I = ms.rows[c.ri];
@@ -423,8 +498,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
 
     const bool sparse = ms.act_flag != nullptr;
     const bool rowlist = !sparse && ms.rows != nullptr;
-    const uint32_t anr = sparse ? ms.act_meta[1] : 0u;
-    const uint64_t total = sparse ? ms.act_prefix[anr]
+    const uint64_t total = sparse ? ms.mat_prefix[ms.nmat]
                                   : rowlist ? ms.row_prefix[ms.nrows] : ms.work_prefix[ms.nmat];
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t w0 = uint64_t(blockIdx.x) * per;
@@ -436,19 +510,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase3(MatSet<V> ms, uint32_t 
     cur.m = 0;
     cur.ri = 0;
     if (sparse) {
-        uint32_t lo = 0, hi = anr;
+        // matrix: the last m with mat_prefix[m] <= w0 (it has work, since
+        // w0 < mat_prefix[m + 1]); then its row by the row prefix
+        uint32_t lo = 0, hi = ms.nmat;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) / 2;
-            if (ms.act_prefix[mid] <= w0) lo = mid; else hi = mid;
+            if (ms.mat_prefix[mid] <= w0) lo = mid; else hi = mid;
         }
-        cur.ri = lo;
-        cur.nb = ms.nb[0];
-        cur.am = ms.act_meta[0];
-        cur.anr = anr;
-        cur.p = ms.act_rows[lo];
-        cur.q = cur.p + static_cast<uint32_t>(w0 - ms.act_prefix[lo]);
-        cur.I = ms.act_list[cur.p];
-        cur.J = ms.act_list[cur.q];
+        p3_enter(ms, cur, lo);
+        const uint64_t local = w0 - ms.mat_prefix[lo];
+        const uint64_t* pre = ms.act_prefix + cur.sb + lo;
+        uint32_t rlo = 0, rhi = cur.anr;
+        while (rhi - rlo > 1) {
+            const uint32_t mid = (rlo + rhi) / 2;
+            if (pre[mid] <= local) rlo = mid; else rhi = mid;
+        }
+        cur.ri = rlo;
+        cur.p = ms.act_rows[cur.sb + rlo];
+        cur.q = cur.p + static_cast<uint32_t>(local - pre[rlo]);
+        cur.I = ms.act_list[cur.sb + cur.p];
+        cur.J = ms.act_list[cur.sb + cur.q];
     } else if (rowlist) {
         // owned rows only (multi-GPU boundary graph): binary search the row
         uint32_t lo = 0, hi = ms.nrows;
@@ -624,6 +705,38 @@ __global__ void permute_sym(const V* __restrict__ P, V* __restrict__ R, uint32_t
         V v;
         if (i < b && j < b) v = P[sym_off(pos[i], pos[j], nb)];
         else v = i == j ? V(0) : Ops<V>::inf();
+        out[e] = v;
+    }
+}
+
+// K1 elimination order (k1_order.hpp), undone: matrix g0 + z of the final
+// component arena R gets element (i, j) = W_z(pos[i], pos[j]) of working
+// matrix z (pos = pos_all + pos_off[z], the local vertex -> FW position
+// map); padding vertices are isolated (INF, 0 on the diagonal).
+// grid: (nb_max, nb_max, matrices), tile (I = y, J = x), others exit.
+template <class V>
+__global__ void permute_batch(MatSet<V> W, MatSet<V> R, uint32_t g0,
+                              const uint32_t* __restrict__ pos_all,
+                              const uint64_t* __restrict__ pos_off) {
+    const uint32_t z = blockIdx.z, I = blockIdx.y, J = blockIdx.x;
+    const uint32_t nb = W.nb[z];
+    if (I > J || J >= nb) return;
+    const uint32_t* pos = pos_all + pos_off[z];
+    const uint32_t n = static_cast<uint32_t>(pos_off[z + 1] - pos_off[z]);
+    const V* P = W.tiles + W.tile_base[z];
+    V* out = R.tiles + R.tile_base[g0 + z] + tidx(I, J, nb) * TT;
+    __shared__ uint32_t prow[T], pcol[T];
+    for (uint32_t t = threadIdx.x; t < uint32_t(T); t += blockDim.x) {
+        prow[t] = I * T + t < n ? pos[I * T + t] : UINT32_MAX;
+        pcol[t] = J * T + t < n ? pos[J * T + t] : UINT32_MAX;
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < uint32_t(TT); e += blockDim.x) {
+        const uint32_t r = e / T, c = e % T;
+        const uint32_t pi = prow[r], pj = pcol[c];
+        V v;
+        if (pi != UINT32_MAX && pj != UINT32_MAX) v = P[sym_off(pi, pj, nb)];
+        else v = (I * T + r == J * T + c) ? V(0) : Ops<V>::inf();
         out[e] = v;
     }
 }

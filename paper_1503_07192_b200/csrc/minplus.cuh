@@ -105,20 +105,24 @@ template <class V> struct MatSet {
     const uint64_t* row_prefix; // prefix of their upper-tile counts (nrows + 1)
     uint32_t nrows;
     uint32_t rank, world;
-    // sparse phase 3 (nmat == 1; null: dense). Per k-block phase 2 writes
-    // act_flag[J] (V-typed so the sharded build min-allreduces it with the
-    // panel: 0 = panel slot J holds a finite entry, 1 = all INF);
-    // fw_active_list compacts the active slots into act_list and the rows
-    // this rank processes into act_rows (positions in act_list) with the
-    // prefix of their upper-tile counts; act_meta = {m, nrows}. A phase-3
-    // tile (I, J) whose panel slot I or J is all INF cannot change (INF + x
-    // >= INF), so only active x active tiles are walked.
+    // sparse walk (null: dense). Per k-block phase 2 writes act_flag[s + J]
+    // (s = panel_base[m] / TT, matrix m's first panel slot; V-typed so the
+    // sharded build min-allreduces it with the panel: 0 = panel slot J holds
+    // a finite entry, 1 = all INF; a panel tile that is all INF on input is
+    // not computed). fw_active_list compacts matrix m's active slots into
+    // act_list[s..] and the rows this rank processes into act_rows[s..]
+    // (positions in act_list) with the prefix of their upper-tile counts in
+    // act_prefix[s + m ..]; act_meta[2m..2m+1] = {active slots, rows};
+    // fw_mat_prefix scans the per-matrix totals into mat_prefix (nmat + 1).
+    // A phase-3 tile (I, J) whose panel slot I or J is all INF cannot change
+    // (INF + x >= INF), so only active x active tiles are walked.
     V* act_flag;
     uint32_t* act_list;
     uint32_t* act_rows;
     uint64_t* act_prefix;
     uint32_t* act_meta;
-    unsigned long long* act_work;  // running count of phase-3 tiles walked
+    uint64_t* mat_prefix;
+    unsigned long long* act_work;  // running count of tile products executed (all phases)
 };
 
 }  // namespace pspg

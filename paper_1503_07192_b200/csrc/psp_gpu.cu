@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -43,6 +44,7 @@
 #include "bg_order.hpp"
 #include "fw_kernels.cuh"
 #include "host_graph.hpp"
+#include "k1_order.hpp"
 #include "minplus.cuh"
 #include "nccl_api.hpp"
 #include "oracle_file.cuh"
