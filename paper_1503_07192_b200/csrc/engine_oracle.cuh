@@ -370,8 +370,8 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         for (uint32_t c = g0; c <= g1; ++c) goff[c - g0] = pos_off[c - m0] - pos_off[g0 - m0];
         std::vector<uint32_t> gpos(pos.begin() + pos_off[g0 - m0], pos.begin() + pos_off[g1 - m0]);
         MatArena W;
-        t_init.start(s);
         W.create(gsizes, sizeof(V), true, s, 1);
+        t_init.start(s);
         fill_arena<V>(W, s, ctx->sms);
         scatter<V>(W, &gm, gi, gj, gw, q, s);
         t_init.stop(s);
@@ -444,8 +444,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     }
     if (!ordered) {  // reference numbering, dense walk, in place
         EventTimer t_init, t_k1;
-        t_init.start(s);
         o->comps.create(sizes, sizeof(V), true, s);
+        t_init.start(s);
         fill_arena<V>(o->comps, s, ctx->sms);
         scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
         t_init.stop(s);
@@ -533,6 +533,11 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                 }
             });
         }
+        // the table in reference numbering: allocated up front (no host
+        // allocation stalls inside the K2 window) unless the component
+        // tables must leave the device first
+        MatArena ref;
+        if (permuted && !spill) ref.create({b}, sizeof(V), false, s);
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
@@ -545,23 +550,24 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         }
         if (permuted) {
             const double p0 = ms_since(t0);
-            o->bg.panel.reset();
+            if (spill) {
+                o->bg.panel.reset();
+                ref.create({b}, sizeof(V), false, s);
+            }
             const double p1 = ms_since(t0);
-            MatArena ref;
-            ref.create({b}, sizeof(V), false, s);
-            const double p2 = ms_since(t0);
             const uint32_t nb = ref.nb[0];
             permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), ref.tiles.as<V>(), nb,
                                                         uint32_t(b), d_pos.as<uint32_t>());
             CK_LAUNCH();
+            if (!spill) t_k2.stop(s);
             CK(cudaStreamSynchronize(s));
-            const double p3 = ms_since(t0);
+            const double p2 = ms_since(t0);
+            o->bg.panel.reset();
             o->bg = std::move(ref);
             if (std::getenv("PSP_FW_PROFILE"))
                 std::fprintf(stderr,
-                             "[psp] K2 permutation: panel free %.1f ms, table alloc %.1f ms, "
-                             "permute_sym %.1f ms, old table free %.1f ms\n",
-                             p1 - p0, p2 - p1, p3 - p2, ms_since(t0) - p3);
+                             "[psp] K2 permutation: alloc %.1f ms, permute_sym %.1f ms, frees %.1f ms\n",
+                             p1 - p0, p2 - p1, ms_since(t0) - p2);
         }
         if (spill) {  // the component tables come back
             const double back0 = ms_since(t0);
@@ -574,7 +580,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                              "at %.0f ms, copy back %.0f ms (boundary phase so far %.0f ms)\n",
                              parked_bytes / 1e9, fw_done_ms, ms_since(t0) - back0, ms_since(t0));
         }
-        t_k2.stop(s);
+        if (!permuted || spill) t_k2.stop(s);
         CK(cudaStreamSynchronize(s));
         k2_ms = t_k2.ms();
         if (std::getenv("PSP_FW_PROFILE"))

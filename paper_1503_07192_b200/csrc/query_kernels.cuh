@@ -265,11 +265,18 @@ __global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, ui
     const uint32_t c1 = b / k, c2 = b % k;
     const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2], ncg = (B2 + 31) / 32;
     const uint32_t start = w.bin_start[b], end = w.bin_start[b + 1];
+    // the bin's queries split into items of near-equal size in steps of 4
+    // (e.g. 36 -> 20 + 16 instead of 32 + 4): the same query slots, but no
+    // item is left with a 1-query-group remainder, whose register-blocked
+    // product has little instruction-level parallelism for the same block
+    // traffic (items <= GQ, so (items - 1) * mbig < queries)
+    const uint32_t nq = end - start, items = (nq + GQ - 1) / GQ;
+    const uint32_t mbig = min(uint32_t(GQ), ((nq + items - 1) / items + 3) & ~3u);
     uint4* out = w.tasks + w.task_start[b];
     for (uint32_t t = 0; t < n; ++t) {
         const uint32_t item = t / ncg, cg = t % ncg;
-        const uint32_t q0 = start + item * GQ;
-        const uint32_t m = min(uint32_t(GQ), end - q0);
+        const uint32_t q0 = start + item * mbig;
+        const uint32_t m = min(mbig, end - q0);
         // bit 6: the pair's last column group holds <= 16 columns (the
         // register-blocked block-layout kernel then runs a 16-column task)
         const uint32_t half = (cg + 1 == ncg && B2 - cg * 32 <= 16) ? 1u : 0u;
