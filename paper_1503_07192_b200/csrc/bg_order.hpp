@@ -18,6 +18,15 @@
 // relaxations for pieces, 8.5e12 for components, 1.5e13 for the reference
 // numbering, 2.1e13 dense.
 //
+// Tile packing (bg_pack): the device walks T-wide tiles, and a unit cut by a
+// tile boundary makes both tiles active for its whole reach. Units are laid
+// out in the greedy order, except that a unit which would straddle a tile
+// boundary is swapped for the first of the next LOOK units that fits the
+// room left, and the rest of the tile is padding when none does (isolated
+// positions: INF rows, zero diagonal). Tile-level simulation
+// (tools/k2_layout_sim.cpp): cfg2 3.49e12 -> 2.75e12 relaxations (nb 273 ->
+// 288), cfg3 1.17e14 -> 9.3e13 (nb 1055 -> 1120).
+//
 // The order only relabels where each boundary vertex sits in the device
 // matrix during K2; the finished table is permuted back to the reference's
 // boundary ids (permute_sym) before anything reads it.
@@ -98,6 +107,43 @@ inline BgOrder bg_unit_order(uint32_t k, const std::vector<uint64_t>& bsize,
         out.work = out.natural;
     }
     return out;
+}
+
+// start position of every unit (and the padded position count) for the
+// greedy order `order` packed into tiles of `tile` positions
+inline uint64_t bg_pack(const std::vector<uint32_t>& order, const std::vector<uint64_t>& bsize,
+                        uint32_t tile, uint32_t look, std::vector<uint64_t>& start) {
+    const size_t nu = order.size();
+    std::vector<char> used(nu, 0);
+    start.assign(bsize.size(), 0);
+    uint64_t p = 0;
+    size_t head = 0, placed = 0;
+    while (placed < nu) {
+        while (used[head]) ++head;
+        const uint64_t room = tile - p % tile;
+        size_t pick = head;
+        const uint64_t s0 = bsize[order[head]];
+        if (s0 <= tile && s0 > room) {
+            pick = nu;
+            for (size_t i = head + 1, seen = 0; i < nu && seen < look; ++i) {
+                if (used[i]) continue;
+                ++seen;
+                if (bsize[order[i]] <= room) {
+                    pick = i;
+                    break;
+                }
+            }
+            if (pick == nu) {
+                p = (p / tile + 1) * tile;
+                pick = head;
+            }
+        }
+        used[pick] = 1;
+        start[order[pick]] = p;
+        p += bsize[order[pick]];
+        ++placed;
+    }
+    return p;
 }
 
 }  // namespace pspg

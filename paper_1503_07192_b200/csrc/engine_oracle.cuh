@@ -210,23 +210,28 @@ uint64_t host_mem_available() {
     return 0;
 }
 
+// Chosen before the boundary-graph arena exists: `npos` is the working
+// matrix size (positions incl. the tile-packing padding, >= b). Device
+// memory must hold the working matrix with its panel plus the table in
+// reference numbering (2 GB spare).
 template <class V>
 bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& posmap,
-                     bool& spill) {
+                     uint64_t& npos, bool& spill) {
     const Reordered& R = o->R;
     const uint32_t k = R.k;
     const uint64_t b = R.b();
     spill = false;
+    npos = b;
     const char* env = std::getenv("PSP_BG_ORDER");
-    if (!o->bg.sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
+    const bool sparse = (b + T - 1) / T > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
+    if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t need = o->bg.tiles.bytes + (2ull << 30);
-    if (need > free_b) {
-        const uint64_t parked = o->comps.tiles.bytes;
-        if (need > free_b + parked || host_mem_available() < parked + (8ull << 30)) return false;
-        spill = true;
-    }
+    auto table_bytes = [](uint64_t n) {
+        const uint64_t nb = (n + T - 1) / T;
+        return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
+    };
+    auto need = [&](uint64_t n) { return table_bytes(n) + ((n + T - 1) / T + 1) * TT * sizeof(V) + table_bytes(b) + (2ull << 30); };
     const bool by_component = env && std::strcmp(env, "component") == 0;
     // unit of every boundary id: its component, or the connected part of
     // the component it lies in (union-find over the intra-component edges)
@@ -273,11 +278,24 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
                      nu, by_component ? "components" : "pieces", ord.work, ord.natural,
                      ident ? ", kept" : "");
     if (ident) return false;
-    // positions: units in elimination order, each unit's ids ascending
-    std::vector<uint64_t> rank_of(nu), off(nu + 1, 0), start(nu);
-    for (uint32_t r = 0; r < nu; ++r) rank_of[ord.order[r]] = r;
-    for (uint32_t r = 0; r < nu; ++r) off[r + 1] = off[r] + bsize[ord.order[r]];
-    for (uint32_t u = 0; u < nu; ++u) start[u] = off[rank_of[u]];
+    // positions: units in elimination order packed into tiles (bg_pack),
+    // each unit's ids ascending; without room for the padding, contiguous
+    std::vector<uint64_t> start;
+    const char* pk = std::getenv("PSP_BG_PACK");
+    const bool pack = !(pk && std::strcmp(pk, "0") == 0);
+    npos = pack ? bg_pack(ord.order, bsize, T, 16, start) : bg_pack(ord.order, bsize, 1, 0, start);
+    const uint64_t parked = o->comps.tiles.bytes;
+    const bool host_room = host_mem_available() >= parked + (8ull << 30);
+    if (need(npos) > free_b && (need(npos) > free_b + parked || !host_room)) {
+        npos = bg_pack(ord.order, bsize, 1, 0, start);  // contiguous
+    }
+    if (need(npos) > free_b) {
+        if (need(npos) > free_b + parked || !host_room) return false;
+        spill = true;
+    }
+    if (std::getenv("PSP_FW_PROFILE"))
+        std::fprintf(stderr, "[psp] K2 layout: %llu positions for %llu boundary vertices%s\n",
+                     (unsigned long long)npos, (unsigned long long)b, spill ? " (component tables parked)" : "");
     posmap.resize(b);
     for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(start[unit[i]]++);
     return true;
@@ -476,12 +494,14 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     uint64_t k2_relax = 0;
     if (b > 0) {
         t_post.start(s);
-        o->bg.create({b}, sizeof(V), true, s);
         // K2 elimination order (bg_order.hpp): boundary id i sits at
-        // posmap[i] during the FW; P -> reference ids afterwards
+        // posmap[i] of the npos-vertex working matrix during the FW; P ->
+        // reference ids afterwards
         std::vector<uint32_t> posmap;
         bool spill = false;
-        const bool permuted = choose_bg_order<V>(o, L, posmap, spill);
+        uint64_t npos = b;
+        const bool permuted = choose_bg_order<V>(o, L, posmap, npos, spill);
+        o->bg.create({permuted ? npos : b}, sizeof(V), true, s);
         if (std::getenv("PSP_FW_PROFILE"))
             std::fprintf(stderr, "[psp] boundary phase: order chosen at %.1f ms\n", ms_since(t0));
         if (!permuted) {
@@ -556,8 +576,9 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             }
             const double p1 = ms_since(t0);
             const uint32_t nb = ref.nb[0];
-            permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), ref.tiles.as<V>(), nb,
-                                                        uint32_t(b), d_pos.as<uint32_t>());
+            permute_sym<V><<<dim3(nb, nb), 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0],
+                                                        ref.tiles.as<V>(), nb, uint32_t(b),
+                                                        d_pos.as<uint32_t>());
             CK_LAUNCH();
             if (!spill) t_k2.stop(s);
             CK(cudaStreamSynchronize(s));

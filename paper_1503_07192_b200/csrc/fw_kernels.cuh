@@ -691,19 +691,20 @@ __global__ void copy_boundary_blocks(MatSet<V> comps, const uint32_t* __restrict
 }
 
 // R <- P with boundary ids restored: element (i, j) of R's upper tiles is
-// P(pos[i], pos[j]) (pos = boundary id -> K2 position, bg_order.hpp);
+// P(pos[i], pos[j]) (pos = boundary id -> K2 position, bg_order.hpp; P has
+// nbP >= nb tiles per side, the tile-packing padding);
 // padding vertices are isolated (INF, 0 on the diagonal).
 // grid: (nb, nb) CTAs, tile (I = y, J = x), lower ones exit.
 template <class V>
-__global__ void permute_sym(const V* __restrict__ P, V* __restrict__ R, uint32_t nb, uint32_t b,
-                            const uint32_t* __restrict__ pos) {
+__global__ void permute_sym(const V* __restrict__ P, uint32_t nbP, V* __restrict__ R, uint32_t nb,
+                            uint32_t b, const uint32_t* __restrict__ pos) {
     const uint32_t I = blockIdx.y, J = blockIdx.x;
     if (I > J) return;
     V* out = R + tidx(I, J, nb) * TT;
     for (uint32_t e = threadIdx.x; e < uint32_t(TT); e += blockDim.x) {
         const uint32_t i = I * T + e / T, j = J * T + e % T;
         V v;
-        if (i < b && j < b) v = P[sym_off(pos[i], pos[j], nb)];
+        if (i < b && j < b) v = P[sym_off(pos[i], pos[j], nbP)];
         else v = i == j ? V(0) : Ops<V>::inf();
         out[e] = v;
     }
