@@ -23,9 +23,12 @@
 // out in the greedy order, except that a unit which would straddle a tile
 // boundary is swapped for the first of the next LOOK units that fits the
 // room left, and the rest of the tile is padding when none does (isolated
-// positions: INF rows, zero diagonal). Tile-level simulation
-// (tools/k2_layout_sim.cpp): cfg2 3.49e12 -> 2.75e12 relaxations (nb 273 ->
-// 288), cfg3 1.17e14 -> 9.3e13 (nb 1055 -> 1120).
+// positions: INF rows, zero diagonal). The tile-level simulation
+// (tools/k2_layout_sim.cpp) predicts cfg3 1.17e14 -> 9.3e13 relaxations (nb
+// 1055 -> 1120); measured (PSP_K2_TRACE per k-block active slots), the
+// simulation tracks the device early on but underestimates the late reach,
+// and the walked work drops only 3% (K2 8.29 -> 8.05 s). Used from 128
+// tiles per side.
 //
 // The order only relabels where each boundary vertex sits in the device
 // matrix during K2; the finished table is permuted back to the reference's

@@ -75,6 +75,10 @@ void run_fw_set(const MatSet<V>& v, uint32_t nb_max, uint64_t work, cudaStream_t
     const int smem = 2 * TT * sizeof(V);
     const int g3 = int(std::max<uint64_t>(1, std::min<uint64_t>(work, uint64_t(sms))));
     if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
+    // PSP_K2_TRACE=file: per k-block active slots and phase-3 tiles of a
+    // single sparse matrix (diagnostic; synchronises every k-block)
+    const char* trace = v.nmat == 1 && v.act_flag ? std::getenv("PSP_K2_TRACE") : nullptr;
+    FILE* tf = trace ? std::fopen(trace, "w") : nullptr;
     for (uint32_t kb = 0; kb < nb_max; ++kb) {
         fw_phase1<V><<<v.nmat, NTHREADS, 0, s>>>(v, kb);
         CK_LAUNCH();
@@ -82,10 +86,19 @@ void run_fw_set(const MatSet<V>& v, uint32_t nb_max, uint64_t work, cudaStream_t
             fw_phase2<V><<<dim3(v.nmat, nb_max), NTHREADS, smem, s>>>(v, kb);
             CK_LAUNCH();
             if (v.act_flag) launch_active_list<V>(v, kb, s);
+            if (tf) {
+                uint32_t meta[2];
+                uint64_t tot = 0;
+                CK(cudaMemcpyAsync(meta, v.act_meta, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(&tot, v.mat_prefix + 1, 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                std::fprintf(tf, "%u %u %llu\n", kb, meta[0], (unsigned long long)tot);
+            }
             fw_phase3<V><<<g3, NTHREADS, P3_SMEM<V>, s>>>(v, kb);
             CK_LAUNCH();
         }
     }
+    if (tf) std::fclose(tf);
 }
 
 template <class V>

@@ -58,7 +58,9 @@ struct Fill {
 };
 
 // tile products of a layout
-double simulate(const Units& U, const std::vector<uint32_t>& order, const std::vector<uint64_t>& start, uint64_t npos) {
+double simulate(const Units& U, const std::vector<uint32_t>& order, const std::vector<uint64_t>& start, uint64_t npos,
+                const char* trace = nullptr) {
+    FILE* tf = trace ? std::fopen(trace, "w") : nullptr;
     Fill f(U);
     const uint32_t nb = uint32_t((npos + T - 1) / T);
     std::vector<uint64_t> reach(f.W);
@@ -85,7 +87,9 @@ double simulate(const Units& U, const std::vector<uint32_t>& order, const std::v
         double a = 0;
         for (char c : tileact) a += c;
         work += a * (a + 1) / 2;
+        if (tf) std::fprintf(tf, "%u %.0f\n", kb, a);
     }
+    if (tf) std::fclose(tf);
     return work;
 }
 
@@ -208,7 +212,7 @@ int main(int argc, char** argv) {
     contiguous(U, ident, false, st, np);
     std::printf("natural contiguous       : %.3e relax (nb %llu)\n", simulate(U, ident, st, np) * T3, (unsigned long long)((np + T - 1) / T));
     contiguous(U, g.order, false, st, np);
-    std::printf("greedy contiguous (now)  : %.3e relax (nb %llu)\n", simulate(U, g.order, st, np) * T3, (unsigned long long)((np + T - 1) / T));
+    std::printf("greedy contiguous (now)  : %.3e relax (nb %llu)\n", simulate(U, g.order, st, np, argc > 3 ? argv[3] : nullptr) * T3, (unsigned long long)((np + T - 1) / T));
     contiguous(U, g.order, true, st, np);
     std::printf("greedy, no straddle      : %.3e relax (nb %llu)\n", simulate(U, g.order, st, np) * T3, (unsigned long long)((np + T - 1) / T));
     std::vector<uint32_t> o2;
@@ -218,7 +222,8 @@ int main(int argc, char** argv) {
     std::printf("tile greedy, straddling  : %.3e relax (nb %llu)\n", simulate(U, o2, st, np) * T3, (unsigned long long)((np + T - 1) / T));
     for (uint32_t look : {4u, 16u, 64u, 256u}) {
         lookahead(U, g.order, look, o2, st, np);
-        std::printf("greedy, lookahead %4u   : %.3e relax (nb %llu)\n", look, simulate(U, o2, st, np) * T3, (unsigned long long)((np + T - 1) / T));
+        std::printf("greedy, lookahead %4u   : %.3e relax (nb %llu)\n", look,
+                    simulate(U, o2, st, np, look == 16 && argc > 2 ? argv[2] : nullptr) * T3, (unsigned long long)((np + T - 1) / T));
     }
     return 0;
 }
