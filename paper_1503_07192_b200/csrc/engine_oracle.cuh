@@ -864,7 +864,7 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
         }
     }
     w.tasks = gw.tasks.as<uint4>();
-    group_emit<<<(nbins + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k);
+    group_emit<<<(nbins + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k, MODE == QM_BLOCKS);
     CK_LAUNCH();
     CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins) * sizeof(uint32_t), s));
     group_scatter<<<qb, 256, 0, s>>>(count, w);

@@ -257,7 +257,7 @@ __global__ void group_tasks(GroupWork w, const uint32_t* __restrict__ bnd_off, u
 
 // one thread per bin writes the bin's complete (item, column group) task
 // records, so a warp starts a task with one 16-byte load
-__global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, uint32_t k) {
+__global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, uint32_t k, bool balanced) {
     const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= w.nbins) return;
     const uint32_t n = w.task_cnt[b];
@@ -265,13 +265,15 @@ __global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, ui
     const uint32_t c1 = b / k, c2 = b % k;
     const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2], ncg = (B2 + 31) / 32;
     const uint32_t start = w.bin_start[b], end = w.bin_start[b + 1];
-    // the bin's queries split into items of near-equal size in steps of 4
-    // (e.g. 36 -> 20 + 16 instead of 32 + 4): the same query slots, but no
-    // item is left with a 1-query-group remainder, whose register-blocked
-    // product has little instruction-level parallelism for the same block
-    // traffic (items <= GQ, so (items - 1) * mbig < queries)
+    // balanced (register-blocked block-layout product, queries in steps of
+    // 4): the bin's queries split into items of near-equal size (e.g. 36 ->
+    // 20 + 16 instead of 32 + 4), the same query slots, but no item is left
+    // with a 1-query-group remainder, whose product has little instruction-
+    // level parallelism for the same block traffic (items <= GQ, so
+    // (items - 1) * mbig < queries). The lane products (8/16/32 slots) keep
+    // full items.
     const uint32_t nq = end - start, items = (nq + GQ - 1) / GQ;
-    const uint32_t mbig = min(uint32_t(GQ), ((nq + items - 1) / items + 3) & ~3u);
+    const uint32_t mbig = balanced ? min(uint32_t(GQ), ((nq + items - 1) / items + 3) & ~3u) : uint32_t(GQ);
     uint4* out = w.tasks + w.task_start[b];
     for (uint32_t t = 0; t < n; ++t) {
         const uint32_t item = t / ncg, cg = t % ncg;
