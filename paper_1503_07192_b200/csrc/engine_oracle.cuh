@@ -287,7 +287,11 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
     const bool pack = !(pk && std::strcmp(pk, "0") == 0) && b >= 128ull * T;
     npos = pack ? bg_pack(ord.order, bsize, T, 16, start) : bg_pack(ord.order, bsize, 1, 0, start);
     const uint64_t parked = o->comps.tiles.bytes;
-    const bool host_room = host_mem_available() >= parked + (8ull << 30);
+    // room to park them: only PSP_K2_SPILL=host needs host memory (the
+    // default drops the component tables and recomputes them after K2)
+    const char* sp = std::getenv("PSP_K2_SPILL");
+    const bool host_room = !(sp && std::strcmp(sp, "host") == 0) ||
+                           host_mem_available() >= parked + (8ull << 30);
     if (need(npos) > free_b && (need(npos) > free_b + parked || !host_room)) {
         npos = bg_pack(ord.order, bsize, 1, 0, start);  // contiguous
     }
@@ -295,9 +299,11 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
         if (need(npos) > free_b + parked || !host_room) return false;
         spill = true;
     }
+    // PSP_K2_FORCE_SPILL=1 (tests): take the spill path on any size
+    if (std::getenv("PSP_K2_FORCE_SPILL")) spill = true;
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr, "[psp] K2 layout: %llu positions for %llu boundary vertices%s\n",
-                     (unsigned long long)npos, (unsigned long long)b, spill ? " (component tables parked)" : "");
+                     (unsigned long long)npos, (unsigned long long)b, spill ? " (component tables off the device during K2)" : "");
     posmap.resize(b);
     for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(start[unit[i]]++);
     return true;
@@ -431,54 +437,60 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     uint64_t k1_relax = 0;
     const char* k1env = std::getenv("PSP_K1_ORDER");
     const bool want_order = !(k1env && std::strcmp(k1env, "natural") == 0);
-    // this rank's components (all of them on one GPU)
-    std::vector<uint32_t> cut{0, k};
     bool ordered = false;
-    if (want_order) {
-        o->comps.create(sizes, sizeof(V), false, s);
-        if (ctx->world > 1) cut = k1_ranges(o->comps, ctx->world);
-        if (o->comps.nb_max > 2) {
-            K1Result res;
-            ordered = k1_ordered<V>(o, L, cut[ctx->rank], cut[ctx->rank + 1], res);
-            init_ms = res.init_ms;
-            k1_ms = res.k1_ms;
-            order_ms = res.order_ms;
-            k1_relax = res.walked_tiles;
-        }
-        if (ordered) {
-            if (ctx->world > 1) {
-                // k1_relax: this rank's share; total over ranks
-                DBuf d_w(sizeof(unsigned long long));
-                CK(cudaMemcpyAsync(d_w.p, &k1_relax, 8, cudaMemcpyHostToDevice, s));
-                NCK(nccl().AllReduce(d_w.p, d_w.p, 1, ncclUint64, ncclSum, ctx->comm, s));
-                EventTimer t_bc;
-                t_bc.start(s);
-                broadcast_component_ranges<V>(o->comps, cut, ctx);
-                t_bc.stop(s);
-                k1_ms += t_bc.ms();
-                CK(cudaMemcpyAsync(&k1_relax, d_w.p, 8, cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
+    // Phase 2 as a unit: also re-run after K2 when the component tables had
+    // to leave the device for the boundary-graph FW (`spill`, see below)
+    auto phase2 = [&] {
+        ordered = false;
+        // this rank's components (all of them on one GPU)
+        std::vector<uint32_t> cut{0, k};
+        if (want_order) {
+            o->comps.create(sizes, sizeof(V), false, s);
+            if (ctx->world > 1) cut = k1_ranges(o->comps, ctx->world);
+            if (o->comps.nb_max > 2) {
+                K1Result res;
+                ordered = k1_ordered<V>(o, L, cut[ctx->rank], cut[ctx->rank + 1], res);
+                init_ms = res.init_ms;
+                k1_ms = res.k1_ms;
+                order_ms = res.order_ms;
+                k1_relax = res.walked_tiles;
             }
-            k1_relax *= uint64_t(T) * T * T;
+            if (ordered) {
+                if (ctx->world > 1) {
+                    // k1_relax: this rank's share; total over ranks
+                    DBuf d_w(sizeof(unsigned long long));
+                    CK(cudaMemcpyAsync(d_w.p, &k1_relax, 8, cudaMemcpyHostToDevice, s));
+                    NCK(nccl().AllReduce(d_w.p, d_w.p, 1, ncclUint64, ncclSum, ctx->comm, s));
+                    EventTimer t_bc;
+                    t_bc.start(s);
+                    broadcast_component_ranges<V>(o->comps, cut, ctx);
+                    t_bc.stop(s);
+                    k1_ms += t_bc.ms();
+                    CK(cudaMemcpyAsync(&k1_relax, d_w.p, 8, cudaMemcpyDeviceToHost, s));
+                    CK(cudaStreamSynchronize(s));
+                }
+                k1_relax *= uint64_t(T) * T * T;
+            }
         }
-    }
-    if (!ordered) {  // reference numbering, dense walk, in place
-        EventTimer t_init, t_k1;
-        o->comps.create(sizes, sizeof(V), true, s);
-        t_init.start(s);
-        fill_arena<V>(o->comps, s, ctx->sms);
-        scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
-        t_init.stop(s);
-        t_k1.start(s);
-        if (ctx->world > 1) run_fw_components_sharded<V>(o->comps, ctx);
-        else run_fw<V>(o->comps, s, ctx->sms);
-        t_k1.stop(s);
-        CK(cudaStreamSynchronize(s));
-        o->comps.panel.reset();  // K1 scratch
-        k1_ms = t_k1.ms();
-        init_ms = t_init.ms();
-        k1_relax = o->comps.relaxations();
-    }
+        if (!ordered) {  // reference numbering, dense walk, in place
+            EventTimer t_init, t_k1;
+            o->comps.create(sizes, sizeof(V), true, s);
+            t_init.start(s);
+            fill_arena<V>(o->comps, s, ctx->sms);
+            scatter<V>(o->comps, &L.mat, L.ii, L.jj, L.w, q, s);
+            t_init.stop(s);
+            t_k1.start(s);
+            if (ctx->world > 1) run_fw_components_sharded<V>(o->comps, ctx);
+            else run_fw<V>(o->comps, s, ctx->sms);
+            t_k1.stop(s);
+            CK(cudaStreamSynchronize(s));
+            o->comps.panel.reset();  // K1 scratch
+            k1_ms = t_k1.ms();
+            init_ms = t_init.ms();
+            k1_relax = o->comps.relaxations();
+        }
+    };
+    phase2();
     const double component_ms = ms_since(t0);
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr,
@@ -532,8 +544,17 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         t_post.stop(s);
         CK(cudaStreamSynchronize(s));
         init_ms += t_post.ms();
-        // park the component tables on the host while K2 runs (copied on a
-        // side stream from a helper thread, overlapping the FW)
+        // `spill`: the component tables leave the device for K2. Default:
+        // dropped and recomputed afterwards (Phase 2 again: host order +
+        // init + K1, ~1 s on cfg4, NVLink broadcast of the ranges when
+        // sharded). PSP_K2_SPILL=host parks them in host memory instead
+        // (copied on side streams from a helper thread, overlapping the FW),
+        // which costs a PCIe round trip of the whole arena, shared by all
+        // ranks of a node.
+        const char* spill_env = std::getenv("PSP_K2_SPILL");
+        const bool park_host = spill && spill_env && std::strcmp(spill_env, "host") == 0;
+        const bool recompute = spill && !park_host;
+        if (recompute) o->comps = MatArena();
         std::unique_ptr<unsigned char[]> parked;  // default-initialised: no 70 GB memset
         size_t parked_bytes = 0;
         std::thread parker;
@@ -544,7 +565,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             }
         } join_on_unwind{parker};
         Fail park_fail{PSP_OK, ""};
-        if (spill) {
+        if (park_host) {
             parked_bytes = o->comps.tiles.bytes;
             parked.reset(new unsigned char[parked_bytes]);
             parker = std::thread([&] {
@@ -565,7 +586,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         else run_fw<V>(o->bg, s, ctx->sms);
         k2_relax = o->bg.relaxations();  // (reads the walked-tile count: syncs)
         const double fw_done_ms = ms_since(t0);
-        if (spill) {
+        if (park_host) {
             parker.join();
             if (park_fail.st != PSP_OK) throw park_fail;
             o->comps.tiles.reset();
@@ -592,7 +613,19 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                              "[psp] K2 permutation: alloc %.1f ms, permute_sym %.1f ms, frees %.1f ms\n",
                              p1 - p0, p2 - p1, ms_since(t0) - p2);
         }
-        if (spill) {  // the component tables come back
+        if (recompute) {  // the component tables come back: Phase 2 again
+            const double back0 = ms_since(t0);
+            const double si = init_ms, sk = k1_ms, so = order_ms;
+            const uint64_t sr = k1_relax;
+            phase2();
+            init_ms = si, k1_ms = sk, order_ms = so, k1_relax = sr;
+            if (std::getenv("PSP_FW_PROFILE"))
+                std::fprintf(stderr,
+                             "[psp] component tables dropped during K2: FW done at %.0f ms, "
+                             "recomputed in %.0f ms (boundary phase so far %.0f ms)\n",
+                             fw_done_ms, ms_since(t0) - back0, ms_since(t0));
+        }
+        if (park_host) {  // the component tables come back
             const double back0 = ms_since(t0);
             o->comps.tiles.alloc(parked_bytes);
             CK(cudaStreamSynchronize(s));

@@ -306,9 +306,12 @@ def test_large_boundaries_query_paths(monkeypatch):
             assert np.array_equal(d, dw)
 
 
-def test_multigpu_sharded_build():
+@pytest.mark.parametrize("spill", [False, True])
+def test_multigpu_sharded_build(spill):
     # BG Floyd-Warshall row-sharded over every visible GPU (NCCL), checked
-    # bitwise against the reference fixture and a single-GPU build
+    # bitwise against the reference fixture and a single-GPU build; `spill`
+    # forces the path where the component tables are dropped during K2 and
+    # recomputed (component-sharded K1 + NVLink broadcast) afterwards
     import subprocess
     import sys
     n = P._lib.lib().psp_gpu_device_count()
@@ -318,7 +321,8 @@ def test_multigpu_sharded_build():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
                         "--nproc-per-node", str(min(n, 4)), os.path.join(root, "tools", "mgpu_check.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, **({"PSP_K2_FORCE_SPILL": "1"} if spill else {})))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("bit-exact") == min(n, 4)
 
@@ -453,3 +457,29 @@ def test_k2_order_and_sparse_walk_do_not_change_the_tables(monkeypatch, golden_c
         d = od.batch_query(v1, v2)
         for o in (on, oc, oo):
             assert np.array_equal(o.batch_query(v1, v2), d)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["recompute", "host"])
+def test_k2_spill_paths_give_the_same_oracle(monkeypatch, golden_cfg1, mode):
+    """When the ordered K2 table does not fit beside the component tables
+    (cfg4), the component tables leave the device for the boundary-graph FW:
+    dropped and recomputed (default) or parked in host memory
+    (PSP_K2_SPILL=host). Forced here on small graphs, both must give the
+    same component tables, boundary tables and answers."""
+    from paper_1503_07192_b200 import graphs
+    z = golden_cfg1
+    cases = [(graph_of(z), 16), (graphs.delaunay(20_000, 4), 97)]
+    for g, k in cases:
+        base = P.build_oracle(g, k, 4, 0)
+        monkeypatch.setenv("PSP_K2_FORCE_SPILL", "1")
+        if mode == "host":
+            monkeypatch.setenv("PSP_K2_SPILL", "host")
+        o = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_K2_FORCE_SPILL")
+        monkeypatch.delenv("PSP_K2_SPILL", raising=False)
+        for c in range(k):
+            assert np.array_equal(o.component_table(c), base.component_table(c))
+            assert np.array_equal(o.boundary_rows(c), base.boundary_rows(c))
+        v1, v2 = P.random_pairs(g.n, 100_000, 5)
+        assert np.array_equal(o.batch_query(v1, v2), base.batch_query(v1, v2))
