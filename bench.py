@@ -233,6 +233,12 @@ def run_ours(args, rank, world, local):
     else:
         ctx = P.Context(local)
 
+    # process warm-up outside the timed build: one small oracle (64x64 grid,
+    # k = 16, f32 and u32) loads the kernel modules lazily and primes the
+    # allocator, as the warm-up steps do for the queries
+    wg = P.generate_grid(64, 64, (1, 1025), 1)
+    P.build_oracle(wg, 16, 1, 0, ctx=ctx)
+    P.build_oracle(wg, 16, 1, 0, value_kind=P.VALUE_F32, ctx=ctx)
     t0 = time.time()
     g, cfg = graphs.make(args.config)
     gen_s = time.time() - t0
@@ -418,6 +424,7 @@ def run_ours(args, rank, world, local):
             "k2_relax_per_s": k2_rate, "k2_alu_frac_per_gpu": round(k2_rate / (peak_u32 * world), 4),
             "minplus_peak_relax_per_s": peak_u32, "peak_source": "measured in-run "
             f"(minplus_peak_kernel, {peak_insn})", "host_threads": threads,
+            "warmup_build": "one 64x64-grid oracle (u32 and f32) built before the timed build",
             "b": o.b, "bg_edges": st["bg_edges"], "stored_entries": st["stored_entries"]},
         "clocks": clk.summary(),
     }
