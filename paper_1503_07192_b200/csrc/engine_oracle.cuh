@@ -318,6 +318,7 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
 struct K1Result {
     double init_ms = 0.0, k1_ms = 0.0, order_ms = 0.0;
     uint64_t walked_tiles = 0;
+    std::string laps;  // host wall-clock laps (PSP_FW_PROFILE)
 };
 
 template <class V>
@@ -331,8 +332,15 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         const uint64_t nb = F.nb[c];
         return (ntiles_upper(nb) * TT + nb * TT + nb) * sizeof(V) + 16 * nb + 64;
     };
+    const auto tl = Clock::now();
+    auto lap = [&](const char* what) {
+        char buf[64];
+        std::snprintf(buf, sizeof buf, " %s@%.1f", what, ms_since(tl));
+        res.laps += buf;
+    };
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
+    lap("meminfo");
     const uint64_t margin = 1ull << 30;
     if (free_b < margin) return false;
     const uint64_t budget = free_b - margin;
@@ -373,6 +381,7 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         for (auto& th : pool) th.join();
     }
     res.order_ms += ms_since(t0);
+    lap("ordered");
     EventTimer t_init, t_fw;
     for (uint32_t g0 = m0; g0 < m1;) {
         uint32_t g1 = g0;
@@ -395,13 +404,16 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         std::vector<uint64_t> goff(g1 - g0 + 1);
         for (uint32_t c = g0; c <= g1; ++c) goff[c - g0] = pos_off[c - m0] - pos_off[g0 - m0];
         std::vector<uint32_t> gpos(pos.begin() + pos_off[g0 - m0], pos.begin() + pos_off[g1 - m0]);
+        lap("host-lists");
         MatArena W;
         W.create(gsizes, sizeof(V), true, s, 1);
+        lap("W-alloc");
         t_init.start(s);
         fill_arena<V>(W, s, ctx->sms);
         scatter<V>(W, &gm, gi, gj, gw, q, s);
         t_init.stop(s);
         res.init_ms += t_init.ms();
+        lap("init");
         DBuf d_pos = upload(gpos, s), d_off = upload(goff, s);
         t_fw.start(s);
         run_fw<V>(W, s, ctx->sms);
@@ -412,9 +424,11 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         }
         t_fw.stop(s);
         res.k1_ms += t_fw.ms();
+        lap("fw");
         res.walked_tiles += W.sparse ? W.walked_tiles : W.relaxations() / (uint64_t(T) * T * T);
         g0 = g1;
     }
+    lap("W-freed");
     return true;
 }
 
@@ -435,6 +449,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     const double split_ms = ms_since(t0);
     double init_ms = 0.0, k1_ms = 0.0, order_ms = 0.0;
     uint64_t k1_relax = 0;
+    double create_ms = 0.0;
+    std::string k1_laps;
     const char* k1env = std::getenv("PSP_K1_ORDER");
     const bool want_order = !(k1env && std::strcmp(k1env, "natural") == 0);
     bool ordered = false;
@@ -445,7 +461,9 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         // this rank's components (all of them on one GPU)
         std::vector<uint32_t> cut{0, k};
         if (want_order) {
+            const auto tc = Clock::now();
             o->comps.create(sizes, sizeof(V), false, s);
+            create_ms = ms_since(tc);
             if (ctx->world > 1) cut = k1_ranges(o->comps, ctx->world);
             if (o->comps.nb_max > 2) {
                 K1Result res;
@@ -454,6 +472,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                 k1_ms = res.k1_ms;
                 order_ms = res.order_ms;
                 k1_relax = res.walked_tiles;
+                k1_laps = res.laps;
             }
             if (ordered) {
                 if (ctx->world > 1) {
@@ -495,9 +514,10 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr,
                      "[psp] component phase %.1f ms (%s): split %.1f, order %.1f, device init "
-                     "%.2f + K1 %.2f ms, %.3e relaxations\n",
+                     "%.2f + K1 %.2f ms, %.3e relaxations; table alloc %.1f ms, laps:%s\n",
                      component_ms, ordered ? "nested-dissection order, sparse walk" : "dense walk",
-                     split_ms, order_ms, init_ms, k1_ms, double(k1_relax));
+                     split_ms, order_ms, init_ms, k1_ms, double(k1_relax), create_ms,
+                     k1_laps.c_str());
 
     // ---- Phase 3: BG init + K2 + query tables
     t0 = Clock::now();
