@@ -179,7 +179,7 @@ void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
         }
     }
     size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    mem_info(&free_b, &total_b);
     const uint64_t need = acc * sizeof(V) + off.size() * 8;
     if (need + (8ull << 30) > free_b) return;  // keep 8 GB for query workspaces
     o->bq.alloc(acc * sizeof(V));
@@ -226,7 +226,7 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
     const bool sparse = (b + T - 1) / T > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
     if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
     size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    mem_info(&free_b, &total_b);
     auto table_bytes = [](uint64_t n) {
         const uint64_t nb = (n + T - 1) / T;
         return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
@@ -339,7 +339,7 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
         res.laps += buf;
     };
     size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    mem_info(&free_b, &total_b);
     lap("meminfo");
     const uint64_t margin = 1ull << 30;
     if (free_b < margin) return false;

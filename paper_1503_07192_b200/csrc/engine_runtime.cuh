@@ -60,6 +60,88 @@ double ms_since(Clock::time_point t) {
 }
 
 // ------------------------------------------------------ device buffers --
+// Freed buffers up to kMaxBuf bytes are kept for reuse (at most kMaxHeld
+// bytes per process). On these boxes a cudaMalloc/cudaFree pair costs 1-9 ms
+// and single calls have stalled for up to 0.85 s (profiles/r1s5_component_laps),
+// and a build makes hundreds of small ones (uploads, arena metadata, lists).
+// Semantics kept from cudaFree: the give-back synchronizes the device first,
+// so a cached block is idle when it is handed out again. Budgets count cached
+// bytes as free (mem_info), and an allocation that fails flushes and retries,
+// so budget decisions and OOM behaviour are what they were without it.
+class BufCache {
+public:
+    static constexpr size_t kMaxBuf = size_t(64) << 20, kMaxHeld = size_t(1) << 30;
+    static size_t rounded(size_t n) {
+        if (n <= (size_t(1) << 20)) {
+            size_t r = 256;
+            while (r < n) r <<= 1;
+            return r;
+        }
+        const size_t g = size_t(2) << 20;
+        return (n + g - 1) / g * g;
+    }
+    void* take(size_t n) {
+        if (n > kMaxBuf || off_) return nullptr;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = free_.find({dev, rounded(n)});
+        if (it == free_.end()) return nullptr;
+        void* p = it->second;
+        held_ -= it->first.second;
+        free_.erase(it);
+        return p;
+    }
+    bool give(void* p, size_t n) {
+        if (n > kMaxBuf || off_) return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const size_t r = rounded(n);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (held_ + r > kMaxHeld) return false;
+        }
+        if (cudaDeviceSynchronize() != cudaSuccess) return false;  // as cudaFree would
+        std::lock_guard<std::mutex> lk(mu_);
+        free_.emplace(std::make_pair(dev, r), p);
+        held_ += r;
+        return true;
+    }
+    size_t held() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return held_;
+    }
+    void flush() {
+        std::lock_guard<std::mutex> lk(mu_);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto& [key, p] : free_) {
+            if (key.first != cur) cudaSetDevice(key.first);
+            cudaFree(p);
+            if (key.first != cur) cudaSetDevice(cur);
+        }
+        free_.clear();
+        held_ = 0;
+    }
+
+private:
+    std::mutex mu_;
+    std::multimap<std::pair<int, size_t>, void*> free_;
+    size_t held_ = 0;
+    const bool off_ = std::getenv("PSP_NO_BUF_CACHE") != nullptr;
+};
+BufCache& buf_cache() {
+    static BufCache* c = new BufCache;  // never destroyed: frees after CUDA teardown are unsafe
+    return *c;
+}
+// free device memory as the budgets see it: cached blocks count as free
+// (flushing them here costs 0.4-0.7 s of cudaFree on these boxes); a large
+// allocation that then does not fit flushes the cache and retries (DBuf::alloc)
+void mem_info(size_t* free_b, size_t* total_b) {
+    CK(cudaMemGetInfo(free_b, total_b));
+    *free_b += buf_cache().held();
+}
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -82,11 +164,23 @@ struct DBuf {
     void alloc(size_t n) {
         reset();
         if (n == 0) n = 16;
-        CK(cudaMalloc(&p, n));
         bytes = n;
+        if ((p = buf_cache().take(n))) return;
+        const size_t r = n <= BufCache::kMaxBuf ? BufCache::rounded(n) : n;
+        cudaError_t e = cudaMalloc(&p, r);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            buf_cache().flush();
+            e = cudaMalloc(&p, r);
+        }
+        if (e != cudaSuccess) {
+            p = nullptr;
+            bytes = 0;
+            CK(e);
+        }
     }
     void reset() {
-        if (p) cudaFree(p);
+        if (p && !buf_cache().give(p, bytes)) cudaFree(p);
         p = nullptr;
         bytes = 0;
     }

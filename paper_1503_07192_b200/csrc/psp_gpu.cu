@@ -34,6 +34,7 @@
 #include <fstream>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <random>
 #include <thread>
@@ -117,6 +118,7 @@ psp_status psp_gpu_ctx_create(int device, int rank, int world, const void* nccl_
 void psp_gpu_ctx_destroy(psp_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    buf_cache().flush();
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
