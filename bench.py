@@ -1,25 +1,33 @@
 #!/usr/bin/env python
 """Benchmark: distance queries/s (+ preprocessing seconds) on B200.
 
-Contract (see DESIGN.md §Measurement):
+Contract (see DESIGN.md §5):
   python bench.py --gpus N --steps K --warmup W [--impl ours|reference]
 Under torchrun (N > 1) each rank drives one GPU; rank 0 prints ONE JSON line.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on that
-fits one GPU): Delaunay triangulation of 262,144 uniform points, integer
-weights 1..1024, k = 256 components, batches of 1,000,000 random pairs.
-A step = one batch of 1M queries through the hot path. Every rank builds
-the oracle (partition on the host, phases 2-3 on its GPU) and answers its
-own 1M-pair batches ("scaling": "weak", queries sharded by rank, no data-path
-collective: the query path does not need one when every GPU holds the
-tables — SURVEY §8e(i)).
+Workload: BASELINE.json configs[2], the configuration the metric is quoted on
+("1M-vertex planar"), which fits one B200: Delaunay triangulation of
+1,048,576 uniform points, integer weights 1..1024, k = 1024 components
+(b = 135,009), batches of 10,000,000 random pairs per step per GPU. Every
+rank builds the oracle (partition on the host, phases 2-3 on the GPUs, the
+boundary-graph FW row-sharded over the ranks) and answers its own batches
+("scaling": "weak", queries sharded by rank, no data-path collective: the
+query path needs none when every GPU holds the tables).
+`--config delaunay262k_k256` gives the configs[1] line.
 
 value  device-resident queries/s over all ranks (pairs already in HBM,
        CUDA events on the launching stream, max over ranks)
-e2e    the same batches through psp_gpu_query_batch with pinned host pairs:
-       H2D of 8 B/pair and D2H of 8 B/distance inside the timed region
-Inputs (the 4.9 GB boundary-graph table) are far larger than the 126 MB L2,
+e2e    the same batches through the pipelined host API with pinned host
+       pairs: H2D of 8 B/pair and D2H of 8 B/distance inside the timed region
+Inputs (the 36.5 GB boundary-graph table) are far larger than the 126 MB L2,
 so no flush is needed between steps; each step uses a fresh slice of pairs.
+
+--impl reference runs the UNMODIFIED reference (oracle/_ref/libpspref.so,
+built from /root/reference/proj/src by oracle/Makefile) on the host cores and
+never imports the product package (workloads.py draws the graph). Where the
+reference's f64 boundary tables exceed host RAM (cfg3: 145.8 GB) its Phase 3
+runs on a seeded sample of components (labelled
+"extrapolated") and its queries start in those components.
 """
 from __future__ import annotations
 
@@ -43,7 +51,13 @@ os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 FAMILY = {"grid": "grid", "delaunay": "Delaunay", "road": "road-like grid (f32 weights)"}
 METRIC = "distance queries/sec + preprocessing s (1M-vertex planar) at 1/2/4/8 B200 vs CPU"
-CONFIG = "delaunay262k_k256"
+CONFIG = "delaunay1m_k1024"
+# components whose boundary rows the reference computes where its full
+# f64 tables exceed host RAM
+REF_COMPONENTS = 16
+# the reference builds in full up to this many vertices (cfg2: 9.8 GB of f64
+# boundary tables), with a sampled Phase 3 beyond
+REF_FULL_MAX_N = 300_000
 BATCH = 1_000_000
 
 
@@ -397,15 +411,12 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "u32" if o.value_kind == P.VALUE_U32 else "f32",
         "data": f"synthetic (seeded {FAMILY[cfg['family']]} graph + mt19937_64 pairs)",
-        "config": {"workload": f"{args.config}: {FAMILY[cfg['family']]} n={g.n} m={g.m} k={cfg['k']} b={o.b}, "
-                               f"{batch} random pairs per step per GPU",
-                   "batch_per_gpu": batch, "l2_policy": (f"inputs >> L2 (boundary table {bg_gb:.1f} GB symmetric "
-                                 f"{'u32' if o.value_kind == P.VALUE_U32 else 'f32'}), fresh "
-                                 "pairs each step" if bg_gb > 0.126 else
-                                 f"small config: boundary table {bg_gb * 1e3:.1f} MB fits in L2"),
-                   "parallelism": (f"boundary-graph FW row-sharded over {world} GPUs (NCCL "
-                                   f"panel min-allreduce), queries sharded by rank, tables "
-                                   f"replicated" if world > 1 else "1 GPU")},
+        "config": workload_config(args.config, cfg, g.n, batch),
+        "parallelism": (f"boundary-graph FW row-sharded over {world} GPUs (NCCL panel "
+                        f"exchange), queries sharded by rank, tables replicated"
+                        if world > 1 else "1 GPU"),
+        "tables": {"b": o.b, "m": g.m, "boundary_table_gb": round(bg_gb, 2),
+                   "value_kind": "u32" if o.value_kind == P.VALUE_U32 else "f32"},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s",
                 "h2d_bytes_per_step": 8 * batch, "d2h_bytes_per_step": 8 * batch,
                 "api": f"psp_gpu_query_pipe_submit/wait ({depth} batches in flight, pinned host "
@@ -420,6 +431,13 @@ def run_ours(args, rank, world, local):
             "partition_s": round(st["partition_ms"] / 1e3, 3),
             "component_apsp_s": round(st["component_apsp_ms"] / 1e3, 3),
             "boundary_s": round(st["boundary_ms"] / 1e3, 3),
+            "preprocessing_s": round((st["partition_ms"] + st["component_apsp_ms"]
+                                      + st["boundary_ms"]) / 1e3, 3),
+            "host_subphases_s": {"split": round(st["split_ms"] / 1e3, 3),
+                                 "k1_order": round(st["k1_order_ms"] / 1e3, 3),
+                                 "k2_order_layout": round(st["bg_order_ms"] / 1e3, 3)},
+            "boundary_minus_k2_device_s": round((st["boundary_ms"] - st["k2_device_ms"]) / 1e3, 3),
+            "k2_positions": st["k2_positions"],
             "k1_device_s": round(k1_ms / 1e3, 4), "k2_device_s": round(k2_ms / 1e3, 4),
             "k2_relax_per_s": k2_rate, "k2_alu_frac_per_gpu": round(k2_rate / (peak_u32 * world), 4),
             "minplus_peak_relax_per_s": peak_u32, "peak_source": "measured in-run "
@@ -429,78 +447,169 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
     }
     if args.cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(g, cfg, args)
+        line["cpu_baseline"] = cpu_baseline(o, g, cfg, args)
     return line
 
 
 # ----------------------------------------------------------- reference ----
-def reference_oracle(g, cfg, workers):
+def ref_workload(name: str):
+    """The configuration's graph, drawn WITHOUT the product package:
+    workloads.py (numpy/scipy) or, for the grid family, the reference's own
+    generate_grid."""
     import oracle
+    import workloads
     R = oracle.RefLib()
-    rg = R.graph(g.n, g.eu, g.ev, g.ew)
-    t0 = time.time()
-    ro = rg.build_oracle(cfg["k"], workers, 0)
-    return R, ro, time.time() - t0
+
+    def grid(rows, cols, weights, seed):
+        rg = R.generate("grid", rows, cols, weights, seed)
+        eu, ev, ew = rg.edges()
+        return rg.n, eu, ev, ew
+
+    (n, eu, ev, ew), cfg = workloads.make_arrays(name, grid=grid)
+    return R, R.graph(n, eu, ev, ew), cfg
 
 
-def cpu_baseline(g, cfg, args, sample=100_000):
-    """The reference's own CPU implementation (oracle/_ref, unmodified
-    sources) on this box's host cores: full build_oracle, then batch_query
-    over a bounded sample of the same random-pair workload."""
-    import paper_1503_07192_b200 as P
-    cores = os.cpu_count() or 1
-    R, ro, build_s = reference_oracle(g, cfg, cores)
-    v1, v2 = P.random_pairs(g.n, sample, 77)
-    ro.batch_query(v1[:1000], v2[:1000], cores)
-    t0 = time.perf_counter()
-    ro.batch_query(v1, v2, cores)
-    qs = sample / (time.perf_counter() - t0)
-    return {"value": round(qs, 1), "unit": "queries/s", "cores": cores, "kind": "reference",
-            "sample": f"{sample} random pairs on the full reference oracle (build_oracle with "
-                      f"{cores} workers took {build_s:.1f} s: partition "
-                      f"{ro.stats['partition_ms'] / 1e3:.1f} s, component APSP "
-                      f"{ro.stats['component_apsp_ms'] / 1e3:.1f} s, boundary "
-                      f"{ro.stats['boundary_ms'] / 1e3:.1f} s)",
-            "build_s": round(build_s, 2),
-            "phases_ms": {k: ro.stats[k] for k in ("partition_ms", "component_apsp_ms",
-                                                   "boundary_ms")}}
+def sampled_pairs(ro, comps, count: int, seed: int):
+    """Uniform random pairs conditioned on the source lying in one of the
+    sampled components (the only rows a sampled reference oracle holds):
+    v1 uniform over those components' vertices, v2 uniform over all."""
+    assign_orig = ro.assignment[ro.permutation]  # original id -> component
+    members = np.flatnonzero(np.isin(assign_orig, comps)).astype(np.uint32)
+    rng = np.random.default_rng(seed)
+    v1 = members[rng.integers(0, len(members), count)]
+    v2 = rng.integers(0, ro.n, count).astype(np.uint32)
+    return v1, v2
+
+
+def reference_build(rg, cfg, cores):
+    """Reference preprocessing: build_oracle in full where its tables fit
+    the host, else Phases 1-2 in full + Phase 3 on REF_COMPONENTS seeded
+    components (ref_sampled_oracle). Returns (oracle, sampled components or
+    None, preprocessing dict)."""
+    if rg.n <= REF_FULL_MAX_N:
+        t0 = time.time()
+        ro = rg.build_oracle(cfg["k"], cores, 0)
+        wall = time.time() - t0
+        st = ro.stats
+        return ro, None, {
+            "mode": "full build_oracle", "workers": cores, "build_s": round(wall, 2),
+            "partition_s": round(st["partition_ms"] / 1e3, 3),
+            "component_apsp_s": round(st["component_apsp_ms"] / 1e3, 3),
+            "boundary_s": round(st["boundary_ms"] / 1e3, 3), "b": ro.b}
+    ro, comps, t = rg.sampled_oracle(cfg["k"], cores, REF_COMPONENTS, 0, 1)
+    # boundary_apsp does |B(C)| Dijkstra rows per component on `cores`
+    # threads; the sampled rows ran on the same threads, so wall time
+    # scales with the row count
+    boundary_s = (t["bg_build_ms"] + t["sampled_rows_ms"] * t["b"] / max(t["rows"], 1)) / 1e3
+    return ro, comps, {
+        "mode": (f"Phases 1-2 in full; Phase 3: build_boundary_graph in full + dijkstra_sssp "
+                 f"rows of {len(comps)} seeded components ({t['rows']} of b={t['b']} rows), "
+                 f"extrapolated x b/rows"),
+        "workers": cores,
+        "partition_s": round(t["partition_ms"] / 1e3, 3),
+        "component_apsp_s": round(t["component_apsp_ms"] / 1e3, 3),
+        "boundary_s": round(boundary_s, 2), "boundary_s_kind": "extrapolated",
+        "boundary_graph_build_s": round(t["bg_build_ms"] / 1e3, 3),
+        "sampled_rows": t["rows"], "sampled_rows_s": round(t["sampled_rows_ms"] / 1e3, 3),
+        "build_s": round((t["partition_ms"] + t["component_apsp_ms"]) / 1e3 + boundary_s, 2),
+        "build_s_kind": "measured phases 1-2 + extrapolated phase 3", "b": t["b"],
+        "bg_edges": t["bg_edges"]}
 
 
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the path (oracle/_ref,
+    unmodified sources) on this box's host cores, on our arm's config and
+    metric; each step is a bounded sample of the workload (args.ref_sample
+    pairs through psp::batch_query with all cores)."""
     if rank != 0:
         return None
-    import paper_1503_07192_b200 as P  # tooling only: graph + pair generators
-    from paper_1503_07192_b200 import graphs
-    g, cfg = graphs.make(args.config)
     cores = os.cpu_count() or 1
-    R, ro, build_s = reference_oracle(g, cfg, cores)
+    t0 = time.time()
+    R, rg, cfg = ref_workload(args.config)
+    gen_s = time.time() - t0
+    ro, comps, prep = reference_build(rg, cfg, cores)
     sample = args.ref_sample
-    v1, v2 = P.random_pairs(g.n, sample * (args.warmup + args.steps), 1000)
+    nsteps = args.warmup + args.steps
+    if comps is None:
+        v1, v2 = R.random_pairs(rg.n, sample * nsteps, 1000)
+        pairs_desc = "uniform random pairs (ref::random_pairs)"
+    else:
+        v1, v2 = sampled_pairs(ro, comps, sample * nsteps, 1000)
+        pairs_desc = (f"uniform random pairs with the source in the {len(comps)} sampled "
+                      f"components (the reference's f64 boundary tables do not fit host RAM)")
     for i in range(args.warmup):
         ro.batch_query(v1[i * sample:(i + 1) * sample], v2[i * sample:(i + 1) * sample], cores)
     t0 = time.perf_counter()
-    for i in range(args.warmup, args.warmup + args.steps):
+    for i in range(args.warmup, nsteps):
         ro.batch_query(v1[i * sample:(i + 1) * sample], v2[i * sample:(i + 1) * sample], cores)
     dt = time.perf_counter() - t0
     qps = sample * args.steps / dt
+    batch = args.batch or cfg["queries"]
     return {
         "impl": "reference", "metric": METRIC, "value": round(qps, 1), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded {FAMILY[cfg['family']]} graph + mt19937_64 pairs)",
-        "config": {"workload": f"{args.config}: {FAMILY[cfg['family']]} n={g.n} k={cfg['k']} b={ro.b}, "
-                               f"{sample} random pairs per step (bounded sample)"},
+        "config": workload_config(args.config, cfg, rg.n, batch),
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": cores,
                          "kind": "reference",
-                         "sample": f"{sample} pairs per step, batch_query with {cores} threads"},
+                         "sample": f"{sample} pairs per step ({pairs_desc}), psp::batch_query "
+                                   f"with {cores} threads, unmodified reference build"},
         "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "preprocessing": {"build_s": round(build_s, 2),
-                          "partition_s": ro.stats["partition_ms"] / 1e3,
-                          "component_apsp_s": ro.stats["component_apsp_ms"] / 1e3,
-                          "boundary_s": ro.stats["boundary_ms"] / 1e3, "workers": cores},
+        "preprocessing": dict(prep, graph_gen_s=round(gen_s, 2)),
     }
+
+
+def cpu_baseline(o, g, cfg, args, sample=100_000, steps=3):
+    """The reference's own query code (oracle/_ref, unmodified psp::batch_query)
+    on this box's host cores, over a bounded sample of the same workload. The
+    reference's preprocessing is timed by `--impl reference`; here its
+    psp::Oracle is assembled from the GPU build's exported f64 tables (bit-
+    identical to the reference's, tests/test_large_configs.py), with boundary
+    rows for REF_COMPONENTS seeded components where all of them would not
+    fit host RAM; pairs then start in those components."""
+    import oracle
+    R = oracle.RefLib()
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    k = o.k
+    full = g.n <= REF_FULL_MAX_N
+    rng = np.random.default_rng(1)
+    comps = np.arange(k) if full else np.sort(rng.choice(k, REF_COMPONENTS, replace=False))
+    cs = set(comps.tolist())
+    ct = [o.component_table(c) for c in range(k)]
+    bt = [o.boundary_rows(c) if c in cs else None for c in range(k)]
+    ro = oracle.assemble_oracle(R, g.n, k, o.permutation, o.assignment, o.boundary_flags,
+                                o.component_offset, o.boundary_offset, o.boundary_vertex, ct, bt)
+    del ct, bt
+    export_s = time.time() - t0
+    if full:
+        v1, v2 = R.random_pairs(g.n, sample * (steps + 1), 77)
+    else:
+        v1, v2 = sampled_pairs(ro, comps, sample * (steps + 1), 77)
+    ro.batch_query(v1[:sample], v2[:sample], cores)  # warm-up
+    t0 = time.perf_counter()
+    d = ro.batch_query(v1[sample:], v2[sample:], cores)
+    qs = sample * steps / (time.perf_counter() - t0)
+    # the GPU answers the same pairs bit for bit
+    assert np.array_equal(o.batch_query(v1[sample:], v2[sample:]), d), "GPU != reference"
+    return {"value": round(qs, 1), "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": (f"{sample * steps} random pairs"
+                       + ("" if full else f" with the source in {REF_COMPONENTS} seeded "
+                                          f"components")
+                       + f", psp::batch_query with {cores} threads on a psp::Oracle assembled "
+                         f"from the GPU build's f64 exports ({export_s:.1f} s); answers checked "
+                         f"equal to the GPU's. Reference preprocessing: see --impl reference")}
+
+
+def workload_config(name, cfg, n, batch):
+    """`config` of both arms (identical by construction)."""
+    return {"workload": f"{name}: {FAMILY[cfg['family']]} n={n} k={cfg['k']}, {batch} random "
+                        f"pairs per step per GPU", "batch_per_gpu": batch,
+            "l2_policy": "inputs >> L2 (boundary-graph table >> 126 MB), fresh pairs each step"
+                         if n > 100_000 else "small config: tables may fit in L2"}
 
 
 def main():

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PSP_GPU_ABI_VERSION 3
+#define PSP_GPU_ABI_VERSION 4
 
 typedef enum psp_status {
     PSP_OK = 0,
@@ -74,6 +74,14 @@ typedef struct psp_build_stats {
     int32_t value_kind;        /* PSP_VALUE_U32 or PSP_VALUE_F32               */
     int32_t fixed_point_shift; /* q: device value = weight * 2^q (u32 only)    */
     uint64_t device_bytes;     /* device memory held by the oracle             */
+    /* K2 working layout (ABI 4) */
+    uint64_t k2_positions;     /* rows of the K2 working matrix (>= b: tile-packing padding) */
+    int32_t k2_order;          /* 0 reference numbering, 1 elimination order   */
+    int32_t k2_spilled;        /* component tables left the device during K2   */
+    /* host sub-phases of the wall-clock phases (ABI 4) */
+    double split_ms;           /* reordered CSR -> per-component edge lists    */
+    double k1_order_ms;        /* nested-dissection orders (host threads)      */
+    double bg_order_ms;        /* K2 elimination order + layout (host)         */
 } psp_build_stats;
 
 typedef struct psp_oracle_info {

@@ -20,9 +20,10 @@
 //
 // Device-resident oracles: build_oracle returns a fully populated host
 // psp::Oracle (the reference tests and save_oracle read its tables) and keeps
-// the device tables alive in a registry keyed by the oracle's table storage;
-// query/batch_query look the device oracle up there (an Oracle copied or
-// loaded from a file is imported once with psp_gpu_oracle_import).
+// the device tables alive in a bounded registry keyed by the oracle's table
+// storage and verified against the host object on every lookup (see
+// Entry); query/batch_query look the device oracle up there (an Oracle
+// copied or loaded from a file is imported once with psp_gpu_oracle_import).
 #include <cstring>
 #include <map>
 #include <memory>
@@ -76,15 +77,121 @@ EdgeArrays edges_of(const psp::Graph& g) {
     return e;
 }
 
-// registry: table storage of a host Oracle -> its device oracle
+// Registry: host Oracle -> its device oracle. The reference's Oracle is a
+// plain value (include/psp/oracle.hpp:47-78) with no room for a handle, so an
+// entry is found by the address of its table storage and then VERIFIED
+// against the host object before use: n, k, b, the address and size of every
+// table buffer, and a fingerprint of 256 entries sampled across the ids and
+// all tables. A destroyed Oracle whose storage is reused by a different one
+// therefore fails verification and is imported afresh instead of answering
+// from stale device tables. The registry is bounded (kMaxEntries, least
+// recently used evicted, its device memory released).
 struct Entry {
     std::shared_ptr<psp_gpu_oracle> dev;
-    std::size_t n, k, b;
+    std::size_t n = 0, k = 0, b = 0;
+    std::vector<const void*> bufs;  // every component/boundary table buffer
+    std::vector<std::size_t> sizes;
+    uint64_t fingerprint = 0;
+    uint64_t last_use = 0;
 };
+constexpr std::size_t kMaxEntries = 16;
 std::mutex g_mu;
 std::map<const void*, Entry> g_registry;
+uint64_t g_clock = 0;
 
 const void* key_of(const psp::Oracle& o) { return o.component_tables.data(); }
+
+uint64_t mix(uint64_t h, uint64_t x) {
+    h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h * 0xff51afd7ed558ccdull;
+}
+
+uint64_t bits(double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, sizeof u);
+    return u;
+}
+
+// 256 entries spread over the id arrays and every table (fixed strides, so
+// the same Oracle always samples the same positions)
+uint64_t fingerprint(const psp::Oracle& o) {
+    uint64_t h = mix(mix(o.n, o.k), o.b());
+    const std::size_t n = o.n;
+    for (std::size_t i = 0; i < 32 && n; ++i) {
+        const std::size_t v = (i * 0x9e3779b1ull) % n;
+        h = mix(h, (uint64_t(o.permutation[v]) << 32) | o.partition.assignment[v]);
+    }
+    std::size_t total = 0;
+    for (uint32_t c = 0; c < o.k; ++c)
+        total += o.component_tables[c].data().size() + o.boundary_tables[c].data().size();
+    if (total == 0) return h;
+    const std::size_t samples = 224;
+    std::size_t c = 0, base = 0;
+    for (std::size_t i = 0; i < samples; ++i) {
+        std::size_t pos = (i * total) / samples + (i * 7919) % std::max<std::size_t>(1, total / samples);
+        pos = std::min(pos, total - 1);
+        // walk the concatenation component table c, boundary table c, c+1, ...
+        while (true) {
+            const std::size_t a = o.component_tables[c].data().size();
+            const std::size_t bsz = o.boundary_tables[c].data().size();
+            if (pos < base + a) {
+                h = mix(h, bits(o.component_tables[c].data()[pos - base]));
+                break;
+            }
+            if (pos < base + a + bsz) {
+                h = mix(h, bits(o.boundary_tables[c].data()[pos - base - a]));
+                break;
+            }
+            base += a + bsz;
+            ++c;
+        }
+    }
+    return h;
+}
+
+void describe(const psp::Oracle& o, Entry& e) {
+    e.n = o.n;
+    e.k = o.k;
+    e.b = o.b();
+    e.bufs.clear();
+    e.sizes.clear();
+    for (uint32_t c = 0; c < o.k; ++c) {
+        e.bufs.push_back(o.component_tables[c].data().data());
+        e.sizes.push_back(o.component_tables[c].data().size());
+        e.bufs.push_back(o.boundary_tables[c].data().data());
+        e.sizes.push_back(o.boundary_tables[c].data().size());
+    }
+    e.fingerprint = fingerprint(o);
+}
+
+bool matches(const psp::Oracle& o, const Entry& e) {
+    if (e.n != o.n || e.k != o.k || e.b != o.b() || o.component_tables.size() != o.k ||
+        o.boundary_tables.size() != o.k)
+        return false;
+    for (uint32_t c = 0; c < o.k; ++c) {
+        if (e.bufs[2 * c] != o.component_tables[c].data().data() ||
+            e.sizes[2 * c] != o.component_tables[c].data().size() ||
+            e.bufs[2 * c + 1] != o.boundary_tables[c].data().data() ||
+            e.sizes[2 * c + 1] != o.boundary_tables[c].data().size())
+            return false;
+    }
+    return e.fingerprint == fingerprint(o);
+}
+
+// caller holds g_mu
+void remember(const psp::Oracle& o, std::shared_ptr<psp_gpu_oracle> dev) {
+    if (g_registry.size() >= kMaxEntries && !g_registry.count(key_of(o))) {
+        auto lru = g_registry.begin();
+        for (auto it = g_registry.begin(); it != g_registry.end(); ++it)
+            if (it->second.last_use < lru->second.last_use) lru = it;
+        g_registry.erase(lru);  // in-flight users hold their own shared_ptr
+    }
+    Entry e;
+    e.dev = std::move(dev);
+    describe(o, e);
+    e.last_use = ++g_clock;
+    g_registry[key_of(o)] = std::move(e);
+}
 
 std::shared_ptr<psp_gpu_oracle> adopt(psp_gpu_oracle* h) {
     return std::shared_ptr<psp_gpu_oracle>(h, psp_gpu_oracle_free);
@@ -93,10 +200,12 @@ std::shared_ptr<psp_gpu_oracle> adopt(psp_gpu_oracle* h) {
 std::shared_ptr<psp_gpu_oracle> device_of(const psp::Oracle& o) {
     std::lock_guard<std::mutex> lock(g_mu);
     auto it = g_registry.find(key_of(o));
-    if (it != g_registry.end() && it->second.n == o.n && it->second.k == o.k &&
-        it->second.b == o.b())
+    if (it != g_registry.end() && matches(o, it->second)) {
+        it->second.last_use = ++g_clock;
         return it->second.dev;
-    // an Oracle we did not build (copied, or read by load_oracle): import it
+    }
+    // an Oracle we did not build (copied, read by load_oracle, or a new one
+    // in a destroyed one's storage): import it
     std::vector<uint64_t> co(o.component_offset.begin(), o.component_offset.end());
     std::vector<uint64_t> bo(o.boundary_offset.begin(), o.boundary_offset.end());
     std::vector<const double*> ct(o.k), bt(o.k);
@@ -109,7 +218,7 @@ std::shared_ptr<psp_gpu_oracle> device_of(const psp::Oracle& o) {
                                 o.partition.assignment.data(), co.data(), bo.data(), ct.data(),
                                 bt.data(), PSP_VALUE_AUTO, &h));
     auto dev = adopt(h);
-    g_registry[key_of(o)] = Entry{dev, o.n, o.k, o.b()};
+    remember(o, dev);
     return dev;
 }
 
@@ -198,7 +307,7 @@ Oracle build_oracle(const Graph& g, std::uint32_t k, unsigned workers, std::uint
         stats->peak_table_entries_per_worker = st.peak_table_entries_per_worker;
     }
     std::lock_guard<std::mutex> lock(g_mu);
-    g_registry[key_of(o)] = Entry{dev, o.n, o.k, o.b()};
+    remember(o, std::move(dev));
     return o;
 }
 

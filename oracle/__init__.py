@@ -91,6 +91,11 @@ class RefLib:
             lib.ref_sampled_build.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64,
                                               C.c_uint32, C.c_uint64, _f64p, _u64p]
             lib.ref_random_pairs.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]
+            lib.ref_sampled_oracle.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                               C.c_uint64, _f64p, _u64p, _u32p, C.POINTER(vp)]
+            lib.ref_oracle_assemble.argtypes = [C.c_uint64, C.c_uint32, _u32p, _u32p, _u8p, _u64p,
+                                                _u64p, _u32p, C.POINTER(C.c_void_p),
+                                                C.POINTER(C.c_void_p), C.POINTER(vp)]
             lib.ref_save_oracle.argtypes = [vp, C.c_char_p]
             lib.ref_load_oracle.argtypes = [C.c_char_p, C.POINTER(vp)]
             lib.ref_read_graph.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_char_p,
@@ -228,6 +233,42 @@ class RefGraph:
         return dict(partition_ms=times[0], component_apsp_ms=times[1], bg_build_ms=times[2],
                     sampled_dijkstra_ms=times[3], rows=rows, b=int(info[0]),
                     bg_edges=int(info[1]))
+
+
+    def sampled_oracle(self, k: int, workers: int, n_comps: int, seed: int = 0,
+                       sample_seed: int = 1):
+        """ref_sampled_oracle: the reference's Phases 1-2 in full, the
+        boundary graph in full, and the reference's Dijkstra rows for the
+        boundary vertices of `n_comps` seeded components only. Returns the
+        (partial) RefOracle, the sampled components and the phase times."""
+        times = np.zeros(4, np.float64)
+        info = np.zeros(3, np.uint64)
+        comps = np.zeros(max(1, min(n_comps, k)), np.uint32)
+        h = C.c_void_p()
+        self.ref._check(self.ref.lib.ref_sampled_oracle(self.h, k, workers, seed, n_comps,
+                                                        sample_seed, times, info, comps,
+                                                        C.byref(h)))
+        ro = RefOracle(self.ref, h, np.zeros(7))
+        return ro, comps, dict(partition_ms=times[0], component_apsp_ms=times[1],
+                               bg_build_ms=times[2], sampled_rows_ms=times[3],
+                               rows=int(info[2]), b=int(info[0]), bg_edges=int(info[1]))
+
+
+def assemble_oracle(ref: "RefLib", n, k, perm, assign, flags, comp_off, bnd_off, bvert,
+                    ct: list, bt: list) -> "RefOracle":
+    """ref_oracle_assemble: a psp::Oracle from plain arrays (bt[c] None =
+    component not sampled) so that the reference's batch_query runs on it."""
+    ctp = (C.c_void_p * k)(*[t.ctypes.data for t in ct])
+    btp = (C.c_void_p * k)(*[(t.ctypes.data if t is not None else None) for t in bt])
+    h = C.c_void_p()
+    ref._check(ref.lib.ref_oracle_assemble(
+        n, k, np.ascontiguousarray(perm, np.uint32), np.ascontiguousarray(assign, np.uint32),
+        np.ascontiguousarray(flags, np.uint8), np.ascontiguousarray(comp_off, np.uint64),
+        np.ascontiguousarray(bnd_off, np.uint64), np.ascontiguousarray(bvert, np.uint32),
+        ctp, btp, C.byref(h)))
+    ro = RefOracle(ref, h, np.zeros(7))
+    ro._keep = (ct, bt)
+    return ro
 
 
 STAT_KEYS = ("partition_ms", "component_apsp_ms", "boundary_ms", "boundary_total", "bg_edges",

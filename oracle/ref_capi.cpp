@@ -15,11 +15,13 @@
 //   apsp_dense / dijkstra_sssp                   include/psp/shortest_paths.hpp:39-43
 //   query / batch_query                          include/psp/query.hpp:36-46
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <random>
 #include <sstream>
 #include <string>
@@ -66,6 +68,37 @@ struct RefOracle {
     psp::Oracle o;
     psp::BuildStats stats;
 };
+
+// Parallel task pool of `workers` threads over [0, count) (the reference's
+// parallel_for, include/psp/parallel.hpp:15-47, is header-only and
+// internal; this is the same static fan-out with dynamic pickup).
+template <typename F>
+void pool_for(std::size_t count, uint32_t workers, F&& f) {
+    std::atomic<std::size_t> next{0};
+    std::vector<std::thread> pool;
+    for (uint32_t w = 0; w < std::max<uint32_t>(workers, 1); ++w) {
+        pool.emplace_back([&] {
+            for (;;) {
+                const std::size_t i = next.fetch_add(1);
+                if (i >= count) return;
+                f(i);
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+}
+
+// Seeded choice of `n_comps` distinct components (partial Fisher-Yates).
+std::vector<uint32_t> sample_components(uint32_t k, uint32_t n_comps, uint64_t seed) {
+    std::vector<uint32_t> ids(k);
+    for (uint32_t c = 0; c < k; ++c) ids[c] = c;
+    std::mt19937_64 rng(seed);
+    n_comps = std::min(n_comps, k);
+    for (uint32_t i = 0; i < n_comps; ++i) std::swap(ids[i], ids[i + rng() % (k - i)]);
+    ids.resize(n_comps);
+    std::sort(ids.begin(), ids.end());
+    return ids;
+}
 
 }  // namespace
 
@@ -276,6 +309,133 @@ int ref_sampled_build(const void* g, uint32_t k, uint32_t workers, uint64_t seed
             (void)d;
         }
         times[3] = ms(t0);
+    });
+}
+
+// The reference's build_oracle (src/oracle.cpp:144-194) for configurations
+// whose f64 boundary tables exceed host RAM (cfg3 needs
+// 145.8 GB): Phase 1 (partition_graph + reorder_vertices) and Phase 2
+// (apsp_dense per component on `workers` threads) run in FULL; Phase 3
+// builds the boundary graph in full (build_boundary_graph) and runs the
+// reference's dijkstra_sssp rows (exactly boundary_apsp's per-row work,
+// oracle.cpp:127-142) only for the boundary vertices of `n_comps` seeded
+// components, fanned out over `workers` threads. The result is a real
+// psp::Oracle on which the reference's own query/batch_query answer every
+// pair whose source lies in a sampled component (query reads only
+// boundary_tables[c1], src/query.cpp:29-46).
+// times: partition_ms, component_apsp_ms, bg_build_ms, sampled_rows_ms
+// info: b, bg_edges, rows computed; comps_out: the sampled components
+int ref_sampled_oracle(const void* g, uint32_t k, uint32_t workers, uint64_t seed,
+                       uint32_t n_comps, uint64_t sample_seed, double* times, uint64_t* info,
+                       uint32_t* comps_out, void** out) {
+    return guarded([&] {
+        using Clock = std::chrono::steady_clock;
+        auto ms = [](Clock::time_point t) {
+            return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+        };
+        const psp::Graph& gg = static_cast<const RefGraph*>(g)->g;
+        auto ro = std::make_unique<RefOracle>();
+        psp::Oracle& o = ro->o;
+        auto t0 = Clock::now();
+        psp::Partition op = psp::partition_graph(gg, k, seed);
+        auto [rg, part] = psp::reorder_vertices(gg, op);
+        times[0] = ms(t0);
+        o.n = gg.num_vertices();
+        o.k = k;
+        o.permutation = std::move(op.permutation);
+        o.inverse_permutation = std::move(op.inverse_permutation);
+        o.component_offset.assign(k + 1, 0);
+        for (uint32_t c = 0; c < k; ++c)
+            o.component_offset[c + 1] = o.component_offset[c] + part.component_members[c].size();
+        t0 = Clock::now();
+        o.component_tables.resize(k);
+        pool_for(k, std::min(workers, k), [&](std::size_t c) {
+            const std::size_t base = o.component_offset[c];
+            const std::size_t size = o.component_offset[c + 1] - base;
+            std::vector<psp::Edge> edges;
+            for (std::size_t i = 0; i < size; ++i)
+                for (const psp::Neighbor& nb : rg.neighbors(static_cast<psp::VertexId>(base + i)))
+                    if (nb.to >= base && nb.to < base + size && nb.to > base + i)
+                        edges.push_back({static_cast<psp::VertexId>(i),
+                                         static_cast<psp::VertexId>(nb.to - base), nb.weight});
+            o.component_tables[c] = psp::apsp_dense(psp::Graph(size, edges));
+        });
+        times[1] = ms(t0);
+        t0 = Clock::now();
+        psp::BoundaryGraph bg = psp::build_boundary_graph(rg, part, o.component_tables);
+        times[2] = ms(t0);
+        o.boundary_vertex = bg.global_of;
+        o.boundary_offset = bg.component_offset;
+        const std::size_t b = bg.global_of.size();
+        info[0] = b;
+        info[1] = bg.graph.num_edges();
+        const std::vector<uint32_t> comps = sample_components(k, n_comps, sample_seed);
+        std::vector<std::pair<uint32_t, std::size_t>> rows;  // (component, boundary id)
+        o.boundary_tables.resize(k);
+        for (uint32_t c : comps) {
+            const std::size_t lo = bg.component_offset[c], hi = bg.component_offset[c + 1];
+            o.boundary_tables[c] = psp::Matrix(hi - lo, b, psp::kUnreachable);
+            for (std::size_t i = lo; i < hi; ++i) rows.emplace_back(c, i);
+        }
+        t0 = Clock::now();
+        pool_for(rows.size(), workers, [&](std::size_t r) {
+            const auto [c, i] = rows[r];
+            std::vector<double> row = psp::dijkstra_sssp(bg.graph, static_cast<psp::VertexId>(i));
+            std::copy(row.begin(), row.end(),
+                      o.boundary_tables[c].row(i - bg.component_offset[c]));
+        });
+        times[3] = ms(t0);
+        info[2] = rows.size();
+        for (std::size_t i = 0; i < comps.size(); ++i) comps_out[i] = comps[i];
+        o.partition = std::move(part);
+        o.placement = psp::place_components(k, 1);
+        *out = ro.release();
+    });
+}
+
+// A psp::Oracle assembled from plain arrays (e.g. tables exported from the
+// GPU build, bit-identical to the reference's): the reference's own
+// batch_query then runs on it. bt[c] may be null (component not sampled:
+// queries must not start there). assign/flags are in the reordered space.
+int ref_oracle_assemble(uint64_t n, uint32_t k, const uint32_t* perm, const uint32_t* assign,
+                        const uint8_t* flags, const uint64_t* comp_off, const uint64_t* bnd_off,
+                        const uint32_t* bvert, const double* const* ct, const double* const* bt,
+                        void** out) {
+    return guarded([&] {
+        auto ro = std::make_unique<RefOracle>();
+        psp::Oracle& o = ro->o;
+        o.n = n;
+        o.k = k;
+        o.permutation.assign(perm, perm + n);
+        o.inverse_permutation.resize(n);
+        for (uint64_t v = 0; v < n; ++v) o.inverse_permutation[perm[v]] = static_cast<uint32_t>(v);
+        o.component_offset.assign(comp_off, comp_off + k + 1);
+        o.boundary_offset.assign(bnd_off, bnd_off + k + 1);
+        const uint64_t b = bnd_off[k];
+        o.boundary_vertex.assign(bvert, bvert + b);
+        o.partition.k = k;
+        o.partition.assignment.assign(assign, assign + n);
+        o.partition.boundary_flags.assign(flags, flags + n);
+        o.partition.component_members.assign(k, {});
+        for (uint64_t v = 0; v < n; ++v)
+            o.partition.component_members[assign[v]].push_back(static_cast<uint32_t>(v));
+        o.partition.permutation.resize(n);
+        o.partition.inverse_permutation.resize(n);
+        for (uint64_t v = 0; v < n; ++v)
+            o.partition.permutation[v] = o.partition.inverse_permutation[v] = static_cast<uint32_t>(v);
+        o.component_tables.resize(k);
+        o.boundary_tables.resize(k);
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint64_t s = comp_off[c + 1] - comp_off[c], bc = bnd_off[c + 1] - bnd_off[c];
+            o.component_tables[c] = psp::Matrix(s, s, psp::kUnreachable);
+            std::memcpy(o.component_tables[c].data().data(), ct[c], s * s * sizeof(double));
+            if (bt[c]) {
+                o.boundary_tables[c] = psp::Matrix(bc, b, psp::kUnreachable);
+                std::memcpy(o.boundary_tables[c].data().data(), bt[c], bc * b * sizeof(double));
+            }
+        }
+        o.placement = psp::place_components(k, 1);
+        *out = ro.release();
     });
 }
 

@@ -76,6 +76,12 @@ class BuildStats(C.Structure):
         ("value_kind", C.c_int32),
         ("fixed_point_shift", C.c_int32),
         ("device_bytes", C.c_uint64),
+        ("k2_positions", C.c_uint64),
+        ("k2_order", C.c_int32),
+        ("k2_spilled", C.c_int32),
+        ("split_ms", C.c_double),
+        ("k1_order_ms", C.c_double),
+        ("bg_order_ms", C.c_double),
     ]
 
     def as_dict(self) -> dict:

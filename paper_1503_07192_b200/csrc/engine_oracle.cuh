@@ -32,9 +32,36 @@ struct psp_gpu_oracle {
     std::mutex query_mu;
     DBuf query_stage;
     GroupWorkspace gw;
+    // per-stream workspaces for callers on their own streams (concurrent
+    // batches then run side by side; beyond kStreamWorkspaces streams they
+    // share `gw`, ordered by its event). Guarded by query_mu.
+    static constexpr size_t kStreamWorkspaces = 8;
+    std::map<cudaStream_t, std::unique_ptr<GroupWorkspace>> stream_gw;
+    GroupWorkspace& workspace_for(cudaStream_t s) {
+        if (s == ctx->stream) return gw;
+        auto it = stream_gw.find(s);
+        if (it != stream_gw.end()) return *it->second;
+        if (stream_gw.size() >= kStreamWorkspaces) return gw;
+        return *stream_gw.emplace(s, std::make_unique<GroupWorkspace>()).first->second;
+    }
     // block query layout of the boundary table (optional, see
     // build_query_blocks): BQ blocks and their offsets
     DBuf bq, d_bq_off;
+    // point-query server (query_server): mailbox in mapped pinned host
+    // memory, its stream, the last request number. Guarded by query_mu.
+    QueryMailbox* mb = nullptr;
+    cudaStream_t srv = nullptr;
+    unsigned long long srv_seq = 0;
+    psp_gpu_oracle() = default;
+    psp_gpu_oracle(const psp_gpu_oracle&) = delete;
+    psp_gpu_oracle& operator=(const psp_gpu_oracle&) = delete;
+    ~psp_gpu_oracle() {
+        if (srv) {
+            cudaStreamSynchronize(srv);  // the server exits after its idle time
+            cudaStreamDestroy(srv);
+        }
+        if (mb) cudaFreeHost(mb);
+    }
 };
 
 namespace {
@@ -210,6 +237,19 @@ uint64_t host_mem_available() {
     return 0;
 }
 
+// Memory-based layout choices (K1 grouping, the K2 order / packing / spill)
+// select different NCCL call sequences, so with more than one rank every
+// rank must take them from the same numbers: the minimum over ranks of each
+// value (one small AllReduce on the build stream). A no-op on one GPU.
+void agree_min(psp_gpu_ctx* ctx, uint64_t* vals, int count) {
+    if (ctx->world <= 1) return;
+    DBuf d(sizeof(uint64_t) * count);
+    CK(cudaMemcpyAsync(d.p, vals, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, ctx->stream));
+    NCK(nccl().AllReduce(d.p, d.p, count, ncclUint64, ncclMin, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(vals, d.p, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
 // Chosen before the boundary-graph arena exists: `npos` is the working
 // matrix size (positions incl. the tile-packing padding, >= b). Device
 // memory must hold the working matrix with its panel plus the table in
@@ -227,6 +267,11 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
     if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
     size_t free_b = 0, total_b = 0;
     mem_info(&free_b, &total_b);
+    // every rank decides from the smallest free device and host memory
+    uint64_t agreed[2] = {free_b, host_mem_available()};
+    agree_min(o->ctx, agreed, 2);
+    free_b = agreed[0];
+    const uint64_t host_avail = agreed[1];
     auto table_bytes = [](uint64_t n) {
         const uint64_t nb = (n + T - 1) / T;
         return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
@@ -284,15 +329,18 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
     const char* pk = std::getenv("PSP_BG_PACK");
     // measured: cfg3 K2 8.29 -> 8.05 s, cfg2 unchanged; on small matrices
     // (a few tiles per side) the padding costs more than it saves
-    const bool pack = !(pk && std::strcmp(pk, "0") == 0) && b >= 128ull * T;
+    // PSP_BG_PACK=0 turns packing off, PSP_BG_PACK=force turns it on at any
+    // size (tests: small graphs exercise the padding positions bitwise)
+    const bool force_pack = pk && std::strcmp(pk, "force") == 0;
+    const bool pack = force_pack || (!(pk && std::strcmp(pk, "0") == 0) && b >= 128ull * T);
     npos = pack ? bg_pack(ord.order, bsize, T, 16, start) : bg_pack(ord.order, bsize, 1, 0, start);
     const uint64_t parked = o->comps.tiles.bytes;
     // room to park them: only PSP_K2_SPILL=host needs host memory (the
     // default drops the component tables and recomputes them after K2)
     const char* sp = std::getenv("PSP_K2_SPILL");
     const bool host_room = !(sp && std::strcmp(sp, "host") == 0) ||
-                           host_mem_available() >= parked + (8ull << 30);
-    if (need(npos) > free_b && (need(npos) > free_b + parked || !host_room)) {
+                           host_avail >= parked + (8ull << 30);
+    if (!force_pack && need(npos) > free_b && (need(npos) > free_b + parked || !host_room)) {
         npos = bg_pack(ord.order, bsize, 1, 0, start);  // contiguous
     }
     if (need(npos) > free_b) {
@@ -341,11 +389,19 @@ bool k1_ordered(psp_gpu_oracle* o, const EdgeLists& L, uint32_t m0, uint32_t m1,
     size_t free_b = 0, total_b = 0;
     mem_info(&free_b, &total_b);
     lap("meminfo");
+    // with several ranks the ordered path (and the AllReduce + range
+    // broadcast behind it) is taken by all or none: agree on the smallest
+    // free memory, then on every rank's range fitting the budget
+    uint64_t fm = free_b;
+    agree_min(ctx, &fm, 1);
+    free_b = fm;
     const uint64_t margin = 1ull << 30;
-    if (free_b < margin) return false;
-    const uint64_t budget = free_b - margin;
-    for (uint32_t c = m0; c < m1; ++c)
-        if (need(c) > budget) return false;
+    uint64_t fits = free_b >= margin;
+    const uint64_t budget = fits ? free_b - margin : 0;
+    for (uint32_t c = m0; c < m1 && fits; ++c)
+        if (need(c) > budget) fits = 0;
+    agree_min(ctx, &fits, 1);
+    if (!fits) return false;
     const auto t0 = Clock::now();
     // intra-component edges bucketed by component
     std::vector<uint64_t> eoff(R.k + 1, 0);
@@ -456,11 +512,14 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     bool ordered = false;
     // Phase 2 as a unit: also re-run after K2 when the component tables had
     // to leave the device for the boundary-graph FW (`spill`, see below)
-    auto phase2 = [&] {
+    // force: -1 free choice, 0 dense walk, 1 ordered (the spill recompute
+    // must take the path that produced the tables K2 was seeded from, or
+    // f32 tables could round differently)
+    auto phase2 = [&](int force) {
         ordered = false;
         // this rank's components (all of them on one GPU)
         std::vector<uint32_t> cut{0, k};
-        if (want_order) {
+        if (want_order && force != 0) {
             const auto tc = Clock::now();
             o->comps.create(sizes, sizeof(V), false, s);
             create_ms = ms_since(tc);
@@ -491,6 +550,10 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                 k1_relax *= uint64_t(T) * T * T;
             }
         }
+        if (force == 1 && !ordered)
+            throw Fail{PSP_ENOMEM, "component tables recomputed after K2: the nested-dissection "
+                                   "path that built them no longer fits beside the boundary-graph "
+                                   "table (set PSP_K2_SPILL=host)"};
         if (!ordered) {  // reference numbering, dense walk, in place
             EventTimer t_init, t_k1;
             o->comps.create(sizes, sizeof(V), true, s);
@@ -509,7 +572,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             k1_relax = o->comps.relaxations();
         }
     };
-    phase2();
+    phase2(-1);
+    const bool first_ordered = ordered;
     const double component_ms = ms_since(t0);
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr,
@@ -524,8 +588,9 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     const uint64_t b = R.b();
     DBuf d_bnd = upload(R.bnd_off, s);
     unsigned long long clique = 0;
-    double k2_ms = 0.0;
-    uint64_t k2_relax = 0;
+    double k2_ms = 0.0, bg_order_ms = 0.0;
+    uint64_t k2_relax = 0, k2_npos = b;
+    bool k2_permuted = false, k2_spill = false;
     if (b > 0) {
         t_post.start(s);
         // K2 elimination order (bg_order.hpp): boundary id i sits at
@@ -534,7 +599,12 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         std::vector<uint32_t> posmap;
         bool spill = false;
         uint64_t npos = b;
+        const auto tord = Clock::now();
         const bool permuted = choose_bg_order<V>(o, L, posmap, npos, spill);
+        bg_order_ms = ms_since(tord);
+        k2_npos = permuted ? npos : b;
+        k2_permuted = permuted;
+        k2_spill = spill;
         o->bg.create({permuted ? npos : b}, sizeof(V), true, s);
         if (std::getenv("PSP_FW_PROFILE"))
             std::fprintf(stderr, "[psp] boundary phase: order chosen at %.1f ms\n", ms_since(t0));
@@ -637,8 +707,11 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             const double back0 = ms_since(t0);
             const double si = init_ms, sk = k1_ms, so = order_ms;
             const uint64_t sr = k1_relax;
-            phase2();
-            init_ms = si, k1_ms = sk, order_ms = so, k1_relax = sr;
+            const double sc = create_ms;
+            const std::string sl = k1_laps;
+            phase2(first_ordered ? 1 : 0);
+            init_ms = si, k1_ms = sk, order_ms = so, k1_relax = sr, create_ms = sc;
+            k1_laps = sl;
             if (std::getenv("PSP_FW_PROFILE"))
                 std::fprintf(stderr,
                              "[psp] component tables dropped during K2: FW done at %.0f ms, "
@@ -697,6 +770,12 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         st->value_kind = o->kind.kind;
         st->fixed_point_shift = o->kind.shift;
         st->device_bytes = o->device_bytes;
+        st->k2_positions = k2_npos;
+        st->k2_order = k2_permuted ? 1 : 0;
+        st->k2_spilled = k2_spill ? 1 : 0;
+        st->split_ms = split_ms;
+        st->k1_order_ms = order_ms;
+        st->bg_order_ms = bg_order_ms;
     }
 }
 
@@ -936,16 +1015,18 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     CK(cudaEventRecord(gw.done, s));
 }
 
-// Every batch goes through the pair-grouped kernel: measured on cfg2/cfg3 it
-// beats one-warp-per-query from 1K pairs up (8.4M vs 3.4M q/s at 1K, 393M vs
-// 17M at 1M; profiles/bench/r1_kernel_crossover.jsonl). query_warp remains
-// for k*k beyond 32-bit bin keys and as the PSP_QUERY_KERNEL=warp check.
+// Kernel choice by batch density (queries per component pair c1 <= c2):
+// the pair-grouped kernel reuses each B1 x B2 block from shared memory but
+// pays a counting sort over k^2 bins per batch; for batches much smaller than
+// that (no reuse to gain) query_cta answers each query with one CTA and no
+// sort. query_warp remains for k*k beyond 32-bit bin keys and as the
+// PSP_QUERY_KERNEL=warp check. All kernels return identical distances.
+// CTA_MAX_DENSITY: measured crossover (profiles/bench/r2_query_kernel_sweep).
 constexpr double GROUP_MIN_DENSITY = 0.0;
+constexpr double CTA_MAX_DENSITY = 0.05;
 
 template <class V>
-void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
-                    const uint32_t* v2, double* dist, cudaStream_t s, uint32_t* bad_id) {
-    if (count == 0) return;
+QueryView<V> query_view(const psp_gpu_oracle* o, uint32_t* bad_id) {
     QueryView<V> q{};
     q.n = static_cast<uint32_t>(o->R.n);
     q.bad_id = bad_id;
@@ -962,15 +1043,33 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     q.scale = o->scale;
     q.bq = o->bq.p ? o->bq.as<V>() : nullptr;
     q.bq_off = o->bq.p ? o->d_bq_off.as<uint64_t>() : nullptr;
+    return q;
+}
+
+template <class V>
+void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
+                    const uint32_t* v2, double* dist, cudaStream_t s, uint32_t* bad_id) {
+    if (count == 0) return;
+    const QueryView<V> q = query_view<V>(o, bad_id);
     const uint64_t k = o->R.k;
     const double pairs = double(k) * double(k + 1) / 2.0;
     // PSP_QUERY_KERNEL=warp|grouped overrides the density heuristic (tests,
     // profiling); both kernels return identical distances.
     const char* force = std::getenv("PSP_QUERY_KERNEL");
     bool grouped = double(count) >= GROUP_MIN_DENSITY * pairs;
-    if (force && std::strcmp(force, "warp") == 0) grouped = false;
-    if (force && std::strcmp(force, "grouped") == 0) grouped = true;
+    bool cta = double(count) < CTA_MAX_DENSITY * pairs;
+    if (force && std::strcmp(force, "warp") == 0) grouped = cta = false;
+    if (force && std::strcmp(force, "grouped") == 0) grouped = true, cta = false;
+    if (force && std::strcmp(force, "cta") == 0) cta = true;
+    if (cta) {
+        const unsigned blocks = unsigned(std::min<uint64_t>(count, uint64_t(o->ctx->sms) * 8));
+        query_cta<V><<<blocks, 32 * QC_WARPS, 0, s>>>(q, v1, v2, count, dist);
+        CK_LAUNCH();
+        return;
+    }
     if (grouped && k * k < (1ull << 31) && count < (1ull << 31)) {
+        // (callers hold o->query_mu: the workspace map and its growth)
+        GroupWorkspace& ws = const_cast<psp_gpu_oracle*>(o)->workspace_for(s);
         // the block query layout when it was built (PSP_QUERY_LAYOUT=tiles
         // forces the tile-packed path; both give identical distances)
         const char* lay = std::getenv("PSP_QUERY_LAYOUT");
@@ -978,16 +1077,16 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
         const bool lane_product = prod && std::strcmp(prod, "lane") == 0;
         const bool p8x8 = prod && std::strcmp(prod, "8x8") == 0;
         if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0) && lane_product)
-            launch_grouped<V, QM_BLOCKS_LANE>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+            launch_grouped<V, QM_BLOCKS_LANE>(ws, o->R.bnd_off,
                                               o->ctx->sms, q, count, v1, v2, dist, s);
         else if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0) && p8x8)
-            launch_grouped<V, QM_BLOCKS_8X8>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+            launch_grouped<V, QM_BLOCKS_8X8>(ws, o->R.bnd_off,
                                              o->ctx->sms, q, count, v1, v2, dist, s);
         else if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0))
-            launch_grouped<V, QM_BLOCKS>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+            launch_grouped<V, QM_BLOCKS>(ws, o->R.bnd_off,
                                          o->ctx->sms, q, count, v1, v2, dist, s);
         else
-            launch_grouped<V, QM_TILES>(const_cast<psp_gpu_oracle*>(o)->gw, o->R.bnd_off,
+            launch_grouped<V, QM_TILES>(ws, o->R.bnd_off,
                                         o->ctx->sms, q, count, v1, v2, dist, s);
         return;
     }
@@ -997,6 +1096,62 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
         unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(o->ctx->sms) * 16)));
     query_warp<V><<<blocks, 256, 0, s>>>(q, v1, v2, count, dist);
     CK_LAUNCH();
+}
+
+// Point queries (count <= MAILBOX_PAIRS) through the resident server CTA:
+// no launch and no stream sync per call while the server is up (it idles out
+// after PSP_SERVER_IDLE_US, default 200 us). Caller holds o->query_mu.
+template <class V>
+bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const uint32_t* v2,
+                   double* dist) {
+    if (count == 0 || count > uint64_t(MAILBOX_PAIRS)) return false;
+    if (std::getenv("PSP_NO_QUERY_SERVER")) return false;
+    if (!o->mb) {
+        void* p = nullptr;
+        CK(cudaHostAlloc(&p, sizeof(QueryMailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(p, 0, sizeof(QueryMailbox));
+        o->mb = static_cast<QueryMailbox*>(p);
+        CK(cudaStreamCreateWithFlags(&o->srv, cudaStreamNonBlocking));
+    }
+    const char* idle_env = std::getenv("PSP_SERVER_IDLE_US");
+    const unsigned long long idle_ns =
+        (idle_env ? std::strtoull(idle_env, nullptr, 10) : 200ull) * 1000ull;
+    QueryMailbox* mb = o->mb;
+    auto launch = [&] {
+        mb->alive = 1u;  // until the kernel says otherwise
+        query_server<V><<<1, 32 * QC_WARPS, 0, o->srv>>>(query_view<V>(o, nullptr), mb, idle_ns);
+        CK_LAUNCH();
+    };
+    mb->count = uint32_t(count);
+    for (uint64_t i = 0; i < count; ++i) {
+        mb->v1[i] = v1[i];
+        mb->v2[i] = v2[i];
+    }
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const unsigned long long seq = ++o->srv_seq;
+    mb->req_seq = seq;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    if (!mb->alive && cudaStreamQuery(o->srv) == cudaSuccess) launch();
+    const auto t0 = Clock::now();
+    for (uint64_t spin = 1; mb->done_seq != seq; ++spin) {
+        if ((spin & 255) == 0 && !mb->alive) {
+            // the server idled out (possibly racing this request): once its
+            // kernel is gone, start another unless the answer arrived
+            const cudaError_t e = cudaStreamQuery(o->srv);
+            if (e == cudaSuccess) {
+                if (mb->done_seq != seq) launch();
+            } else if (e != cudaErrorNotReady) {
+                CK(e);
+            }
+        }
+        if ((spin & 0xfffff) == 0 && ms_since(t0) > 60000.0)
+            throw Fail{PSP_ECUDA, "point-query server did not answer within 60 s"};
+    }
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const bool bad = mb->bad != 0;
+    for (uint64_t i = 0; i < count; ++i) dist[i] = mb->dist[i];
+    if (bad) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
+    return true;
 }
 
 }  // namespace

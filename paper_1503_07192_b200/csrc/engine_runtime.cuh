@@ -94,15 +94,27 @@ public:
     }
     bool give(void* p, size_t n) {
         if (n > kMaxBuf || off_) return false;
-        int dev = 0;
-        cudaGetDevice(&dev);
+        // file the block under the device that owns it, not the current one
+        // (a pipe or oracle may be released from another device's thread)
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+            cudaGetLastError();
+            return false;
+        }
+        const int dev = at.device;
         const size_t r = rounded(n);
         {
             std::lock_guard<std::mutex> lk(mu_);
             if (held_ + r > kMaxHeld) return false;
         }
-        if (cudaDeviceSynchronize() != cudaSuccess) return false;  // as cudaFree would
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        const bool idle = cudaDeviceSynchronize() == cudaSuccess;  // as cudaFree would
+        if (cur != dev) cudaSetDevice(cur);
+        if (!idle) return false;
         std::lock_guard<std::mutex> lk(mu_);
+        if (held_ + r > kMaxHeld) return false;  // another thread filled the cache meanwhile
         free_.emplace(std::make_pair(dev, r), p);
         held_ += r;
         return true;
@@ -137,8 +149,16 @@ BufCache& buf_cache() {
 // free device memory as the budgets see it: cached blocks count as free
 // (flushing them here costs 0.4-0.7 s of cudaFree on these boxes); a large
 // allocation that then does not fit flushes the cache and retries (DBuf::alloc)
+// But memory taken outside DBuf (NCCL buffers, lazy module loads, local-memory
+// resizes) cannot use cached blocks: when the real free memory drops under
+// kFlushBelow (the callers' margins are 1-2 GB), the cache is flushed first.
 void mem_info(size_t* free_b, size_t* total_b) {
+    constexpr size_t kFlushBelow = size_t(2) << 30;
     CK(cudaMemGetInfo(free_b, total_b));
+    if (*free_b < kFlushBelow && buf_cache().held() > 0) {
+        buf_cache().flush();
+        CK(cudaMemGetInfo(free_b, total_b));
+    }
     *free_b += buf_cache().held();
 }
 

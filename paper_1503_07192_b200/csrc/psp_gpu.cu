@@ -459,8 +459,25 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
         CK(cudaSetDevice(o->ctx->device));
         psp_gpu_oracle* mo = const_cast<psp_gpu_oracle*>(o);
         std::lock_guard<std::mutex> lock(mo->query_mu);
-        // ids are range-checked on the device (src/query.cpp:30 semantics:
-        // any bad id -> PSP_EINVAL and no output)
+        // a handful of pairs: the resident point-query server (no launch,
+        // no stream sync); ids are range-checked on the device
+        // (src/query.cpp:30 semantics: any bad id -> PSP_EINVAL)
+        if (count <= uint64_t(MAILBOX_PAIRS)) {
+            const bool served = o->kind.kind == PSP_VALUE_U32
+                                    ? point_queries<uint32_t>(mo, count, v1, v2, dist)
+                                    : point_queries<float>(mo, count, v1, v2, dist);
+            if (served) {
+                if (minplus_ops) {
+                    for (uint64_t i = 0; i < count; ++i) {
+                        const uint32_t c1 = R.assign[R.perm[v1[i]]], c2 = R.assign[R.perm[v2[i]]];
+                        const uint64_t b1 = R.bnd_off[c1 + 1] - R.bnd_off[c1];
+                        const uint64_t b2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
+                        minplus_ops[i] = b1 * b2 + b2;  // src/query.cpp:73
+                    }
+                }
+                return;
+            }
+        }
         const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t)) + 16;
         if (mo->query_stage.bytes < need) mo->query_stage.alloc(need);
         double* dd = mo->query_stage.as<double>();
@@ -591,7 +608,11 @@ psp_status psp_gpu_query_pipe_wait(psp_gpu_query_pipe* p) {
     });
 }
 
-void psp_gpu_query_pipe_destroy(psp_gpu_query_pipe* p) { delete p; }
+void psp_gpu_query_pipe_destroy(psp_gpu_query_pipe* p) {
+    if (!p) return;
+    cudaSetDevice(p->o->ctx->device);  // the slots' buffers belong to the oracle's device
+    delete p;
+}
 
 psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       const uint32_t* v1, const uint32_t* v2, double* dist,
@@ -599,6 +620,12 @@ psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
     return guarded([&] {
         if (!o) throw ArgError("query_batch_device: NULL oracle");
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : o->ctx->stream;
+        CK(cudaSetDevice(o->ctx->device));
+        // concurrent callers: the enqueue (workspace lookup and growth) is
+        // serialised; their batches then run on their own streams with
+        // their own workspaces
+        psp_gpu_oracle* mo = const_cast<psp_gpu_oracle*>(o);
+        std::lock_guard<std::mutex> lock(mo->query_mu);
         if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, v1, v2, dist, s, nullptr);
         else launch_queries<float>(o, count, v1, v2, dist, s, nullptr);
     });

@@ -1,105 +1,46 @@
-"""Synthetic planar inputs for the BASELINE.json configurations.
+"""Synthetic planar inputs for the BASELINE.json configurations as `Graph`s.
 
-The reference only generates (triangulated) grids (include/psp/generators.hpp:
-23-30) but loads any edge list (src/graph_io.cpp:50-91); the Delaunay and
-road-like families named in BASELINE.json are defined here, seeded and
-deterministic, and emitted as plain edge lists that both the GPU build and
-the CPU reference consume.
-
-* delaunay(n, seed): Delaunay triangulation (scipy Qhull) of n uniform points
-  in [0,1)^2 drawn with numpy default_rng(seed); unique undirected edges in
-  lexicographic order; integer weights rng.integers(1, 1025) drawn after the
-  points.
-* road_grid(rows, cols, seed): "road-like perturbed grid": a 4-neighbour grid
-  with ~10% of edges deleted (kept connected via a random spanning tree) and
-  jittered coordinates; f32-representable weights = Euclidean length of the
-  jittered embedding times U[1,2) rounded to f32 (the tolerance path).
+The workload definitions live in the repo-root ``workloads.py`` (plain
+numpy/scipy, shared with the reference arm of ``bench.py``, which must not
+load this package). The grid family is drawn by the library's own
+``generate_grid`` (the reference's mt19937_64 generator restated,
+csrc/host_graph.cpp).
 """
 from __future__ import annotations
 
-import numpy as np
+import os
+import sys
 
 from . import Graph
 
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+
+import workloads  # noqa: E402
+
+CONFIGS = workloads.CONFIGS
+
+
+def _graph(arrays) -> Graph:
+    n, eu, ev, ew = arrays
+    return Graph(n, eu, ev, ew)
+
 
 def delaunay(n: int, seed: int = 1) -> Graph:
-    from scipy.spatial import Delaunay
-
-    rng = np.random.default_rng(seed)
-    pts = rng.random((n, 2))
-    tri = Delaunay(pts)
-    s = tri.simplices.astype(np.int64)
-    e = np.concatenate([s[:, [0, 1]], s[:, [1, 2]], s[:, [0, 2]]])
-    e.sort(axis=1)
-    e = np.unique(e, axis=0)
-    w = rng.integers(1, 1025, size=len(e)).astype(np.float64)
-    return Graph(n, e[:, 0].astype(np.uint32), e[:, 1].astype(np.uint32), w)
+    return _graph(workloads.delaunay(n, seed))
 
 
 def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10) -> Graph:
-    """Road-like perturbed grid: jittered 4-neighbour grid, a random spanning
-    tree kept (minimum spanning tree under random keys, so deletions never
-    disconnect the network) and ~`drop` of the remaining edges removed;
-    weights = Euclidean length of the jittered embedding x U[1, 2), rounded to
-    f32 (the tolerance path: not dyadic, so the device computes in f32)."""
-    from scipy.sparse import coo_matrix
-    from scipy.sparse.csgraph import minimum_spanning_tree
-
-    rng = np.random.default_rng(seed)
-    n = rows * cols
-    r, c = np.divmod(np.arange(n, dtype=np.int64), cols)
-    xy = np.stack([c + rng.uniform(-0.3, 0.3, n), r + rng.uniform(-0.3, 0.3, n)], axis=1)
-    right = np.arange(n)[c + 1 < cols]
-    down = np.arange(n)[r + 1 < rows]
-    eu = np.concatenate([right, down])
-    ev = np.concatenate([right + 1, down + cols])
-    key = rng.random(len(eu)) + 1.0  # distinct positive keys -> random spanning tree
-    mst = minimum_spanning_tree(coo_matrix((key, (eu, ev)), shape=(n, n)).tocsr()).tocoo()
-    tree = np.zeros(len(eu), bool)
-    # map MST edges back to edge ids (the grid edge (u, v) is unique)
-    lin = eu * n + ev
-    order = np.argsort(lin)
-    mlin = np.minimum(mst.row, mst.col).astype(np.int64) * n + np.maximum(mst.row, mst.col)
-    pos = np.searchsorted(lin[order], mlin)
-    tree[order[pos]] = True
-    keep = tree | (rng.random(len(eu)) >= drop)
-    eu, ev = eu[keep], ev[keep]
-    length = np.linalg.norm(xy[eu] - xy[ev], axis=1)
-    w = (length * rng.uniform(1.0, 2.0, len(eu))).astype(np.float32).astype(np.float64)
-    return Graph(n, eu.astype(np.uint32), ev.astype(np.uint32), w)
+    return _graph(workloads.road_grid(rows, cols, seed, drop))
 
 
-CONFIGS = {
-    # BASELINE.json configs[0]: runs on the CPU reference too
-    "grid64_k16": dict(family="grid", rows=64, cols=64, weights=(1, 1025), seed=1, k=16,
-                       queries=10_000),
-    # configs[1]
-    "delaunay262k_k256": dict(family="delaunay", n=262_144, seed=1, k=256, queries=1_000_000),
-    # configs[2]
-    "delaunay1m_k1024": dict(family="delaunay", n=1_048_576, seed=1, k=1024,
-                             queries=10_000_000),
-    # configs[3]: road-like grid, float32 weights (tolerance path), for
-    # preprocessing scaling. k = 512 keeps the u32/f32 tables at ~121 GB per
-    # GPU (components 70 GB + boundary graph 51 GB) and minimises FW work.
-    "road4m_k512": dict(family="road", rows=2048, cols=2048, seed=7, k=512,
-                        queries=10_000_000),
-    # mid-size road grid (f32 kernels at a scale that builds in seconds)
-    "road1m_k256": dict(family="road", rows=1024, cols=1024, seed=7, k=256, queries=1_000_000),
-    # small road grid for tests
-    "road64k_k64": dict(family="road", rows=256, cols=256, seed=7, k=64, queries=1_000_000),
-}
+def _grid(rows, cols, weights, seed):
+    from . import generate_grid
+    g = generate_grid(rows, cols, weights, seed)
+    return g.n, g.eu, g.ev, g.ew
 
 
 def make(name: str) -> tuple[Graph, dict]:
-    cfg = dict(CONFIGS[name])
-    fam = cfg["family"]
-    if fam == "grid":
-        from . import generate_grid
-        g = generate_grid(cfg["rows"], cfg["cols"], cfg["weights"], cfg["seed"])
-    elif fam == "delaunay":
-        g = delaunay(cfg["n"], cfg["seed"])
-    elif fam == "road":
-        g = road_grid(cfg["rows"], cfg["cols"], cfg["seed"])
-    else:
-        raise ValueError(fam)
-    return g, cfg
+    arrays, cfg = workloads.make_arrays(name, grid=_grid)
+    return _graph(arrays), cfg

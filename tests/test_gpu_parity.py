@@ -261,7 +261,7 @@ def test_minplus_peak_probe(ctx):
     assert r_u32 > 1e12 and r_f32 > 1e12 and mhz > 500
 
 
-@pytest.mark.parametrize("kernel", ["warp", "grouped"])
+@pytest.mark.parametrize("kernel", ["warp", "grouped", "cta"])
 def test_both_query_kernels_bitwise(monkeypatch, golden_cfg1, kernel):
     # the dense (grouped by component pair) and sparse (warp per query)
     # kernels must return the reference's distances bit for bit
@@ -296,7 +296,7 @@ def test_large_boundaries_query_paths(monkeypatch):
     want = np.array([oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(s))[int(t)]
                      for s, t in zip(v1[:200], v2[:200])])
     dw = None
-    for kernel in ("warp", "grouped"):
+    for kernel in ("warp", "grouped", "cta"):
         monkeypatch.setenv("PSP_QUERY_KERNEL", kernel)
         d = o.batch_query(v1, v2)
         assert np.array_equal(d[:200], want)
@@ -460,6 +460,36 @@ def test_k2_order_and_sparse_walk_do_not_change_the_tables(monkeypatch, golden_c
 
 
 @pytest.mark.gpu
+def test_k2_tile_packed_layout_matches_dense_walk(monkeypatch, golden_cfg1):
+    """The tile-packed K2 layout (bg_pack: units swapped to avoid straddling
+    a tile, padding positions = isolated vertices) is what cfg2-cfg4 run;
+    it switches on by itself only from 128 tiles per side. PSP_BG_PACK=force
+    puts small graphs on it, and the tables and answers must equal the dense
+    walk in reference numbering bit for bit."""
+    from paper_1503_07192_b200 import graphs
+    z = golden_cfg1
+    cases = [(graph_of(z), 16), (graphs.delaunay(20_000, 4), 97),
+             (graphs.delaunay(60_000, 5), 160), (P.generate_grid(90, 90, (0.25, 2.0), 4), 48)]
+    for g, k in cases:
+        monkeypatch.setenv("PSP_FW_DENSE", "1")
+        monkeypatch.setenv("PSP_BG_ORDER", "natural")
+        od = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_FW_DENSE")
+        monkeypatch.delenv("PSP_BG_ORDER")
+        monkeypatch.setenv("PSP_BG_PACK", "force")
+        op = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_BG_PACK")
+        assert op.stats["k2_order"] == 1
+        # padding positions exist, so the packing really ran
+        assert op.stats["k2_positions"] > op.b, (op.stats["k2_positions"], op.b)
+        for c in range(k):
+            assert np.array_equal(op.boundary_rows(c), od.boundary_rows(c))
+            assert np.array_equal(op.component_table(c), od.component_table(c))
+        v1, v2 = P.random_pairs(g.n, 300_000, 13)
+        assert np.array_equal(op.batch_query(v1, v2), od.batch_query(v1, v2))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["recompute", "host"])
 def test_k2_spill_paths_give_the_same_oracle(monkeypatch, golden_cfg1, mode):
     """When the ordered K2 table does not fit beside the component tables
@@ -483,3 +513,104 @@ def test_k2_spill_paths_give_the_same_oracle(monkeypatch, golden_cfg1, mode):
             assert np.array_equal(o.boundary_rows(c), base.boundary_rows(c))
         v1, v2 = P.random_pairs(g.n, 100_000, 5)
         assert np.array_equal(o.batch_query(v1, v2), base.batch_query(v1, v2))
+
+
+@pytest.mark.gpu
+def test_concurrent_device_queries_on_own_streams(golden_cfg1):
+    """psp_gpu_query_batch_device from 4 host threads at once, each on its
+    own CUDA stream with its own pairs (the reference promises concurrent
+    queries are safe, proj/README.md:122-126): every batch equals the
+    serial answer bit for bit."""
+    import threading
+
+    import torch
+    from paper_1503_07192_b200 import graphs
+    g = graphs.delaunay(20_000, 4)
+    o = P.build_oracle(g, 97, 4, 0)
+    dev = torch.device("cuda", 0)
+    nthreads, iters, batch = 4, 12, 50_000
+    v1, v2 = P.random_pairs(g.n, nthreads * iters * batch, 21)
+    want = o.batch_query(v1, v2)
+    d1 = torch.from_numpy(v1.view(np.int32)).to(dev)
+    d2 = torch.from_numpy(v2.view(np.int32)).to(dev)
+    out = torch.empty(len(v1), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(t):
+        try:
+            st = torch.cuda.Stream(device=dev)
+            for i in range(iters):
+                j = (t * iters + i) * batch
+                # vary the size so workspaces grow while other threads run
+                cnt = batch - (i % 3) * 1000
+                o.batch_query_device(d1[j:].data_ptr(), d2[j:].data_ptr(), out[j:].data_ptr(),
+                                     cnt, st.cuda_stream)
+                if i % 3:
+                    o.batch_query_device(d1[j + cnt:].data_ptr(), d2[j + cnt:].data_ptr(),
+                                         out[j + cnt:].data_ptr(), batch - cnt, st.cuda_stream)
+            st.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(nthreads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.gpu
+def test_point_query_server(monkeypatch):
+    """Host calls with <= 32 pairs (the reference's query(o, u, v) in a loop)
+    go to the resident point-query server CTA (query_server): answers equal
+    the reference's (all-pairs Floyd-Warshall) bit for bit, across server
+    idle-outs and relaunches, for every request size 1..32, with the
+    reference's error on an out-of-range id."""
+    import time
+    g = P.generate_triangulated_grid(33, 33, (1.0, 9.0), 4)
+    truth = oracle.apsp_dense(g.n, g.eu, g.ev, g.ew)
+    o = P.build_oracle(g, 11, 4, 0)
+    rng = np.random.default_rng(3)
+    v1 = rng.integers(0, g.n, 4000)
+    v2 = rng.integers(0, g.n, 4000)
+    t0 = time.perf_counter()
+    for i in range(2000):
+        d, ops = o.query(int(v1[i]), int(v2[i]))
+        assert d == truth[v1[i], v2[i]]
+    per_query_us = (time.perf_counter() - t0) / 2000 * 1e6
+    print(f"point query: {per_query_us:.2f} us per call through the Python binding")
+    # the server idles out (200 us default) between these: relaunch path
+    for i in range(2000, 2040):
+        time.sleep(0.001)
+        assert o.query(int(v1[i]), int(v2[i]))[0] == truth[v1[i], v2[i]]
+    # every request size of the mailbox
+    pos = 0
+    for cnt in range(1, 33):
+        a, b = v1[pos:pos + cnt], v2[pos:pos + cnt]
+        assert np.array_equal(o.batch_query(a, b), truth[a, b])
+        pos += cnt
+    # a 1 us idle time makes the exit race the next request constantly
+    monkeypatch.setenv("PSP_SERVER_IDLE_US", "1")
+    for i in range(2040, 3000):
+        assert o.query(int(v1[i]), int(v2[i]))[0] == truth[v1[i], v2[i]]
+    monkeypatch.delenv("PSP_SERVER_IDLE_US")
+    with pytest.raises(ValueError):
+        o.query(0, g.n)
+    assert o.query(1, 2)[0] == truth[1, 2]  # still serving after the error
+    # f32 tables through the same server
+    gf = P.Graph(g.n, g.eu, g.ev, rng.uniform(1.0, 2.0, g.m).astype(np.float32).astype(np.float64))
+    tf = oracle.apsp_dense(gf.n, gf.eu, gf.ev, gf.ew)
+    of = P.build_oracle(gf, 11, 4, 0)
+    for i in range(300):
+        d = of.query(int(v1[i]), int(v2[i]))[0]
+        t = tf[v1[i], v2[i]]
+        assert abs(d - t) <= F32_RTOL * max(t, 1e-300)
+    # the server and the batch kernels agree on f32 rounding exactly
+    monkeypatch.setenv("PSP_QUERY_KERNEL", "grouped")
+    db = of.batch_query(v1[:300], v2[:300])
+    ds = np.array([of.query(int(v1[i]), int(v2[i]))[0] for i in range(300)])
+    assert np.array_equal(db, ds)
