@@ -188,6 +188,10 @@ SIGNATURES = {
 _lib = None
 
 
+# include/psp_gpu.h PSP_GPU_ABI_VERSION (struct layouts above follow it)
+ABI_VERSION = 4
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -200,6 +204,9 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.psp_gpu_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.psp_gpu_abi_version()}, this binding "
+                              f"expects {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 
