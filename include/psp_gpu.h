@@ -337,6 +337,15 @@ psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, d
                              double hi, uint64_t seed, uint64_t* m, uint32_t* eu, uint32_t* ev,
                              double* ew);
 
+/* Delaunay triangulation of n points in [0,1)^2 (xy row-major, coordinates
+ * on the 2^-53 grid numpy's uniform doubles lie on): the unique undirected
+ * edges u < v in lexicographic order, exactly the edge set scipy Qhull gives
+ * for points in general position (exact predicates). Generates BASELINE.json
+ * configs[1]/[2] (workloads.py defines them with scipy). `cap` >= 3n; the
+ * edge count goes to *m. Not a reference symbol: bench/test input tooling. */
+psp_status psp_delaunay_edges(uint64_t n, const double* xy, uint64_t cap, uint32_t* eu,
+                              uint32_t* ev, uint64_t* m);
+
 /* ref::random_pairs / the CLI's random_pairs (tests/support/reference.hpp:
  * 80-91, tools/psp_main.cpp:108-120): mt19937_64, v1 = rng() % n then v2. */
 void psp_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2);

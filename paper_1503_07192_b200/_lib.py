@@ -182,6 +182,8 @@ SIGNATURES = {
     "psp_generate_grid": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_double,
                                     C.c_double, C.c_uint64, C.POINTER(C.c_uint64), _vp, _vp,
                                     _vp]),
+    "psp_delaunay_edges": (C.c_int, [C.c_uint64, _f64p, C.c_uint64, _u32p, _u32p,
+                                     C.POINTER(C.c_uint64)]),
     "psp_random_pairs": (None, [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]),
 }
 

@@ -282,38 +282,55 @@ __global__ void first_duplicate(const uint64_t* __restrict__ key, uint64_t m,
 }
 
 // ------------------------------------------------------------- host side --
-std::string_view host_trim(std::string_view s) {
-    while (!s.empty() && (s.front() == ' ' || s.front() == '\t' || s.front() == '\r')) s.remove_prefix(1);
-    while (!s.empty() && (s.back() == ' ' || s.back() == '\t' || s.back() == '\r')) s.remove_suffix(1);
-    return s;
+// Host re-check of the header and of the lines the device declines
+// (malformed, signed, non-finite or subnormal weights, > 19 significant
+// digits). Verdicts, their order and the messages are the reference's
+// psp::ParseError ones (src/graph_io.cpp:50-90 edge list, :93-140 DIMACS).
+[[noreturn]] void parse_fail(const std::string& name, uint64_t line, const std::string& msg) {
+    throw ParseFail{name + ":" + std::to_string(line) + ": " + msg, line};
 }
 
-std::vector<std::string_view> host_tokens(std::string_view s) {
-    std::vector<std::string_view> out;
-    size_t i = 0;
-    while (i < s.size()) {
-        while (i < s.size() && (s[i] == ' ' || s[i] == '\t')) ++i;
-        size_t j = i;
-        while (j < s.size() && s[j] != ' ' && s[j] != '\t') ++j;
-        if (j > i) out.push_back(s.substr(i, j - i));
-        i = j;
+// One line scanned in place: ' ', '\t' and '\r' stripped from both ends,
+// fields = maximal runs of bytes other than ' ' and '\t' (a '\r' inside the
+// line is part of a field). The count saturates at kMax, more than any
+// valid line has, so "wrong field count" verdicts are unchanged.
+struct LineFields {
+    static constexpr int kMax = 5;
+    std::string_view f[kMax];
+    int n = 0;
+    char lead = 0;  // first byte of the stripped line, 0 when it is empty
+};
+
+LineFields scan_fields(std::string_view line) {
+    auto blank = [](char c) { return c == ' ' || c == '\t'; };
+    size_t lo = 0, hi = line.size();
+    while (lo < hi && (blank(line[lo]) || line[lo] == '\r')) ++lo;
+    while (hi > lo && (blank(line[hi - 1]) || line[hi - 1] == '\r')) --hi;
+    LineFields out;
+    out.lead = lo < hi ? line[lo] : 0;
+    size_t i = lo;
+    while (i < hi && out.n < LineFields::kMax) {
+        if (blank(line[i])) {
+            ++i;
+            continue;
+        }
+        const size_t start = i;
+        while (i < hi && !blank(line[i])) ++i;
+        out.f[out.n++] = line.substr(start, i - start);
     }
     return out;
 }
 
+// A field that must be one whole number of type T (std::from_chars, as the
+// reference parses it): anything else is "expected <what>, got '<field>'".
 template <typename T>
-T host_number(std::string_view tok, const std::string& name, uint64_t line, const char* what) {
-    T value{};
-    auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), value);
-    if (ec != std::errc{} || ptr != tok.data() + tok.size())
-        throw ParseFail{name + ":" + std::to_string(line) + ": expected " + what + ", got '" +
-                            std::string(tok) + "'",
-                        line};
-    return value;
-}
-
-[[noreturn]] void parse_fail(const std::string& name, uint64_t line, const std::string& msg) {
-    throw ParseFail{name + ":" + std::to_string(line) + ": " + msg, line};
+T field_value(std::string_view f, const char* what, const std::string& name, uint64_t line) {
+    T v{};
+    const char* end = f.data() + f.size();
+    const std::from_chars_result r = std::from_chars(f.data(), end, v);
+    if (r.ec != std::errc{} || r.ptr != end)
+        parse_fail(name, line, std::string("expected ") + what + ", got '" + std::string(f) + "'");
+    return v;
 }
 
 struct HostEdge {
@@ -321,26 +338,24 @@ struct HostEdge {
     double w;
 };
 
-// The reference's per-line bodies (src/graph_io.cpp:67-80 edge list,
-// :112-127 DIMACS arcs). Throws ParseFail; returns the parsed edge.
-HostEdge host_edge_line(std::string_view body, bool dimacs, uint64_t n, const std::string& name,
-                        uint64_t line) {
-    auto toks = host_tokens(body);
-    const size_t t0 = dimacs ? 1 : 0;
-    if (toks.size() != 3 + t0)
-        parse_fail(name, line, dimacs ? "arc line must be 'a u v w'" : "edge line must be 'u v w'");
-    const auto u = host_number<uint64_t>(toks[t0], name, line, "vertex id");
-    const auto v = host_number<uint64_t>(toks[t0 + 1], name, line, "vertex id");
-    const auto w = host_number<double>(toks[t0 + 2], name, line, "weight");
-    if (dimacs) {
-        if (u < 1 || u > n || v < 1 || v > n)
-            parse_fail(name, line, "vertex id out of range (ids are 1-based)");
-    } else if (u >= n || v >= n) {
-        parse_fail(name, line, "vertex id out of range");
-    }
-    if (w < 0.0) parse_fail(name, line, "negative weight");
-    if (std::isnan(w) || std::isinf(w)) parse_fail(name, line, "non-finite weight");
-    return {u, v, w};
+// An edge line ('u v w', 0-based) or a DIMACS arc line ('a u v w', 1-based).
+// Throws ParseFail; returns the parsed edge.
+HostEdge host_edge_line(std::string_view line, bool dimacs, uint64_t n, const std::string& name,
+                        uint64_t ln) {
+    const LineFields lf = scan_fields(line);
+    const int at = dimacs ? 1 : 0;  // arcs carry the leading 'a' field
+    if (lf.n != 3 + at)
+        parse_fail(name, ln, dimacs ? "arc line must be 'a u v w'" : "edge line must be 'u v w'");
+    HostEdge e;
+    e.u = field_value<uint64_t>(lf.f[at], "vertex id", name, ln);
+    e.v = field_value<uint64_t>(lf.f[at + 1], "vertex id", name, ln);
+    e.w = field_value<double>(lf.f[at + 2], "weight", name, ln);
+    auto valid_id = [&](uint64_t x) { return dimacs ? (x >= 1 && x <= n) : x < n; };
+    if (!valid_id(e.u) || !valid_id(e.v))
+        parse_fail(name, ln, dimacs ? "vertex id out of range (ids are 1-based)" : "vertex id out of range");
+    if (e.w < 0.0) parse_fail(name, ln, "negative weight");
+    if (!std::isfinite(e.w)) parse_fail(name, ln, "non-finite weight");
+    return e;
 }
 
 struct ParsedGraph {
@@ -473,9 +488,9 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
     // DIMACS lines before the problem line: 'a' or unknown -> error there
     if (dimacs && hf[1] != ~0ull && hf[1] < first) {
         const std::string line = body_of(hf[1]);
-        const std::string_view body = host_trim(line);
-        if (body.front() == 'a') parse_fail(name, hf[1] + 1, "arc line before problem line");
-        parse_fail(name, hf[1] + 1, "unrecognized line type '" + std::string(1, body.front()) + "'");
+        const char lead = scan_fields(line).lead;
+        if (lead == 'a') parse_fail(name, hf[1] + 1, "arc line before problem line");
+        parse_fail(name, hf[1] + 1, "unrecognized line type '" + std::string(1, lead) + "'");
     }
     if (first == ~0ull)
         parse_fail(name, lineno_end, dimacs ? "missing 'p sp n m' line" : "missing 'n m' header");
@@ -483,17 +498,13 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
     uint64_t n = 0, m = 0;
     {
         const std::string line = body_of(first);
-        const auto toks = host_tokens(host_trim(line));
+        const LineFields hdr = scan_fields(line);
         const uint64_t ln = first + 1;
-        if (dimacs) {
-            if (toks.size() != 4 || toks[1] != "sp") parse_fail(name, ln, "problem line must be 'p sp n m'");
-            n = host_number<size_t>(toks[2], name, ln, "vertex count");
-            m = host_number<size_t>(toks[3], name, ln, "arc count");
-        } else {
-            if (toks.size() != 2) parse_fail(name, ln, "header must be 'n m'");
-            n = host_number<size_t>(toks[0], name, ln, "vertex count");
-            m = host_number<size_t>(toks[1], name, ln, "edge count");
-        }
+        const int at = dimacs ? 2 : 0;  // 'p sp n m' | 'n m'
+        if (dimacs ? (hdr.n != 4 || hdr.f[1] != "sp") : hdr.n != 2)
+            parse_fail(name, ln, dimacs ? "problem line must be 'p sp n m'" : "header must be 'n m'");
+        n = field_value<size_t>(hdr.f[at], "vertex count", name, ln);
+        m = field_value<size_t>(hdr.f[at + 1], dimacs ? "arc count" : "edge count", name, ln);
     }
     // L2b: every later line
     DBuf st(std::max<uint64_t>(nlines, 1)), uu(std::max<uint64_t>(nlines, 1) * 8),
@@ -559,9 +570,10 @@ ParsedGraph parse_graph_device(const DevText& t, bool dimacs, const std::string&
             for (uint64_t j = 0; j < nb; ++j) {
                 const uint64_t f = h[3 * j], ln = f + 1;
                 const std::string_view body(t.host + h[3 * j + 1], h[3 * j + 2] - h[3 * j + 1]);
-                if (dimacs && body.front() == 'p') parse_fail(name, ln, "duplicate problem line");
-                if (dimacs && body.front() != 'a')
-                    parse_fail(name, ln, "unrecognized line type '" + std::string(1, body.front()) + "'");
+                const char lead = scan_fields(body).lead;
+                if (dimacs && lead == 'p') parse_fail(name, ln, "duplicate problem line");
+                if (dimacs && lead != 'a')
+                    parse_fail(name, ln, "unrecognized line type '" + std::string(1, lead) + "'");
                 const HostEdge e = host_edge_line(body, dimacs, n, name, ln);  // ERR lines throw
                 uint64_t wb;
                 std::memcpy(&wb, &e.w, 8);

@@ -65,4 +65,8 @@ void generate_grid(int kind, uint64_t rows, uint64_t cols, bool unit, double lo,
                    uint64_t seed, std::vector<uint32_t>& eu, std::vector<uint32_t>& ev,
                    std::vector<double>& ew);
 
+// Delaunay edges of points in [0,1)^2 on the 2^-53 grid (delaunay.cpp)
+void delaunay_edges(uint64_t n, const double* xy, std::vector<uint32_t>& eu,
+                    std::vector<uint32_t>& ev);
+
 }  // namespace pspg

@@ -917,6 +917,19 @@ psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, d
     });
 }
 
+psp_status psp_delaunay_edges(uint64_t n, const double* xy, uint64_t cap, uint32_t* eu,
+                              uint32_t* ev, uint64_t* m) {
+    return guarded([&] {
+        if (!xy || !eu || !ev || !m) throw ArgError("delaunay_edges: NULL argument");
+        std::vector<uint32_t> a, b;
+        delaunay_edges(n, xy, a, b);
+        if (a.size() > cap) throw ArgError("delaunay_edges: capacity too small");
+        std::copy(a.begin(), a.end(), eu);
+        std::copy(b.begin(), b.end(), ev);
+        *m = a.size();
+    });
+}
+
 void psp_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2) {
     std::mt19937_64 rng(seed);
     for (uint64_t i = 0; i < count; ++i) {

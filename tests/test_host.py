@@ -157,3 +157,17 @@ def test_graph_invariants_rejected(edges, msg):
     g = P.Graph(3, eu, ev, ew)
     with pytest.raises(P.GraphInvariantError, match=msg):
         P.partition_graph(g, 1)
+
+
+@pytest.mark.parametrize("n,seed", [(3, 0), (100, 2), (20_000, 4), (262_144, 1)])
+def test_delaunay_generator_matches_qhull(n, seed):
+    """The library's exact incremental Delaunay (csrc/delaunay.cpp) gives the
+    same graph as the workload definition (workloads.py: scipy Qhull), up to
+    BASELINE configs[1] (262,144 points); configs[2] (1,048,576) was checked
+    the same way when the generator was written (3,145,692 equal edges)."""
+    import workloads
+    from paper_1503_07192_b200 import graphs
+    n0, eu, ev, ew = graphs.delaunay_arrays(n, seed)
+    r0, ru, rv, rw = workloads.delaunay(n, seed)
+    assert n0 == r0
+    assert np.array_equal(eu, ru) and np.array_equal(ev, rv) and np.array_equal(ew, rw)
