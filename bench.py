@@ -182,16 +182,26 @@ def ncu_traffic(kernel: str):
     return (d["dram_bytes_per_launch"], d["source"]) if d else (None, None)
 
 
+def kernel_for(o, batch):
+    """The query kernel psp_gpu_query_batch_device picks for a batch
+    (engine_oracle.cuh launch_queries): query_cta below CTA_MAX_DENSITY
+    queries per component pair, else query_grouped; PSP_QUERY_KERNEL
+    overrides."""
+    import paper_1503_07192_b200 as P
+    forced = os.environ.get("PSP_QUERY_KERNEL")
+    if forced in ("warp", "grouped", "cta"):
+        return forced
+    pairs = o.k * (o.k + 1) / 2
+    return "cta" if batch < P.CTA_MAX_DENSITY * pairs else "grouped"
+
+
 def launches_per_batch(o, batch):
     """Kernels one psp_gpu_query_batch_device call launches (all ours,
     cub's scan is compiled into libpsp_gpu.so): the grouped path runs
     group_prep, group_tasks, 2 x (cub ScanInit + Scan), group_emit,
-    group_scatter, query_grouped, group_finish; the warp path runs
-    query_warp alone (engine_oracle.cuh launch_grouped / launch_queries)."""
-    import paper_1503_07192_b200 as P
-    pairs = o.k * (o.k + 1) / 2
-    dense = batch >= P.GROUP_MIN_DENSITY * pairs and os.environ.get("PSP_QUERY_KERNEL") != "warp"
-    return 10 if dense else 1
+    group_scatter, query_grouped, group_finish; query_cta / query_warp run
+    alone (engine_oracle.cuh launch_grouped / launch_queries)."""
+    return 10 if kernel_for(o, batch) == "grouped" else 1
 
 
 def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, world,
@@ -203,9 +213,7 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
     minplus_ops) per second per GPU against the in-run VIADDMNMX peak; the
     no-reuse HBM figure is reported beside it, never as a fraction > 1.
     Sparse batches run query_warp, which is HBM bound."""
-    import paper_1503_07192_b200 as P
-    pairs = o.k * (o.k + 1) / 2
-    dense = batch >= P.GROUP_MIN_DENSITY * pairs and os.environ.get("PSP_QUERY_KERNEL") != "warp"
+    dense = kernel_for(o, batch) == "grouped"
     secs = per_launch_ms / 1e3
     ops_launch = tops / steps
     bytes_launch = tb / steps
@@ -221,9 +229,10 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
                 "no_reuse_bytes_per_query": round(bytes_launch / batch, 1),
                 "no_reuse_equiv_gbs": round(bytes_launch / secs / 1e9, 1),
                 "hbm_peak_gbs": peaks["hbm_gbs"]}
-    traffic, src = ncu_traffic("query_warp")
+    kname = "query_" + kernel_for(o, batch)
+    traffic, src = ncu_traffic(kname)
     ach = bytes_launch / secs / 1e9
-    return {"kernel": "query_warp (K3, sparse batch)", "bound": "hbm", "achieved": round(ach, 1),
+    return {"kernel": f"{kname} (K3, sparse batch)", "bound": "hbm", "achieved": round(ach, 1),
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
             "traffic": traffic, "traffic_source": src, "peak_source": peaks["source"],
             "bytes_per_query": round(bytes_launch / batch, 1)}

@@ -39,10 +39,11 @@ __all__ = ["load_graph", "read_graph", "save_graph", "write_graph", "format_weig
            "load_oracle", "UNREACHABLE"]
 
 UNREACHABLE = float("inf")  # kUnreachable (include/psp/graph.hpp:14)
-# queries per component pair at which batches switch from the warp-per-query
-# kernel to the pair-grouped kernel (must match psp_gpu.cu GROUP_MIN_DENSITY):
-# 0 = always grouped (it wins at every measured batch size)
+# batch density (queries per component pair c1 <= c2) rules of the query
+# launcher (must match engine_oracle.cuh): below CTA_MAX_DENSITY a batch runs
+# query_cta (one CTA per query, no sort), else the pair-grouped kernel
 GROUP_MIN_DENSITY = 0.0
+CTA_MAX_DENSITY = 0.05
 
 
 @dataclasses.dataclass

@@ -11,6 +11,8 @@
 //                                                    FMA: 2/3 -> balanced pipes)
 //   f32        fminf(fminf(acc, a+b), a'+b')         2 FADD + 1 FMNMX3 / 2 relax
 //   f32_ffma   fma(a, one, b) instead of a + b       2 FFMA + 1 FMNMX3 / 2 relax
+//   u16x2      __viaddmin_u16x2 (DPX): two 16-bit relaxations per
+//              VIADDMNMX.U16x2 (packed halves)
 // `one` is a kernel argument equal to 1, so the compiler cannot fold a*one+b
 // into the add-min instruction.
 //
@@ -23,7 +25,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
     fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
 
-enum { VIADD = 0, IMAD_MIN3 = 1, MIX3 = 2, F32 = 3, F32_FFMA = 4 };
+enum { VIADD = 0, IMAD_MIN3 = 1, MIX3 = 2, F32 = 3, F32_FFMA = 4, U16X2 = 5 };
 
 template <int MODE, class V>
 __global__ void __launch_bounds__(256) probe(V* out, uint32_t iters, V one) {
@@ -51,6 +53,9 @@ __global__ void __launch_bounds__(256) probe(V* out, uint32_t iters, V one) {
                     // three relaxations: one fused, two through IMAD + VIMNMX3
                     V t = min(a[i] + b[j], acc[i][j]);
                     acc[i][j] = __vimin3_u32(t, c[i] * one + d[j], a[i] * one + d[j]);
+                } else if constexpr (MODE == U16X2) {
+                    acc[i][j] = __viaddmin_u16x2(a[i], b[j], acc[i][j]);
+                    acc[i][j] = __viaddmin_u16x2(c[i], d[j], acc[i][j]);
                 } else if constexpr (MODE == F32) {
                     acc[i][j] = fminf(fminf(acc[i][j], a[i] + b[j]), c[i] + d[j]);
                 } else {
@@ -72,6 +77,13 @@ __global__ void __launch_bounds__(256) probe(V* out, uint32_t iters, V one) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) s = s < acc[i][j] ? s : acc[i][j];
     if (s == V(12345)) out[blockIdx.x] = s;
+}
+
+__global__ void dpx_semantics(unsigned* out) {
+    out[0] = __viaddmin_u16x2(0x0000fff0u, 0x00000020u, 0xffffffffu);
+    out[1] = __viaddmin_u16x2(0x00008000u, 0x00008000u, 0xffffffffu);
+    out[2] = __viaddmin_u16x2(0x00000003u, 0x00000004u, 0x00000009u);
+    out[3] = __viaddmin_u16x2(0x7fff0000u, 0x7fff0000u, 0xffffffffu);
 }
 
 template <int MODE, class V>
@@ -117,7 +129,19 @@ int main() {
     if (run<IMAD_MIN3, uint32_t>("u32_imad_vimnmx3", 2, sms, false)) return 1;
     if (run<MIX3, uint32_t>("u32_mix_viaddmnmx_imad_vimnmx3", 3, sms, false)) return 1;
     if (run<F32, float>("f32_fadd_fmnmx3", 2, sms, false)) return 1;
-    if (run<F32_FFMA, float>("f32_ffma_fmnmx3", 2, sms, true)) return 1;
-    printf("  }\n}\n");
+    if (run<F32_FFMA, float>("f32_ffma_fmnmx3", 2, sms, false)) return 1;
+    // two 16-bit relaxations per instruction
+    if (run<U16X2, uint32_t>("u16x2_viaddmnmx", 4, sms, true)) return 1;
+    printf("  },\n");
+    // semantics of the packed add: wrap or saturate at 0xffff?
+    unsigned* d;
+    CK(cudaMalloc(&d, 16));
+    dpx_semantics<<<1, 1>>>(d);
+    unsigned h[4];
+    CK(cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost));
+    printf("  \"u16x2_semantics\": {\"min(0xfff0+0x0020, 0xffff)\": \"0x%04x\", "
+           "\"min(0x8000+0x8000, 0xffff)\": \"0x%04x\", \"min(0x0003+0x0004, 0x0009)\": "
+           "\"0x%04x\", \"hi half min(0x7fff+0x7fff, 0xffff)\": \"0x%04x\"}\n}\n",
+           h[0] & 0xffff, h[1] & 0xffff, h[2] & 0xffff, h[3] >> 16);
     return 0;
 }

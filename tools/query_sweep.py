@@ -35,11 +35,11 @@ def main():
     ap.add_argument("--config", default="delaunay1m_k1024")
     ap.add_argument("--sizes", default="1e3,1e4,1e5,1e6,1e7,1e8")
     ap.add_argument("--min-time", type=float, default=0.25, help="seconds per measurement")
-    ap.add_argument("--kernel", choices=["auto", "warp", "grouped"], default="auto",
-                    help="force a query kernel (PSP_QUERY_KERNEL) instead of the density rule")
+    ap.add_argument("--kernels", default="auto",
+                    help="comma list of auto|warp|grouped|cta: force a query kernel "
+                         "(PSP_QUERY_KERNEL) instead of the density rule, each measured")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    if args.kernel != "auto":
-        os.environ["PSP_QUERY_KERNEL"] = args.kernel
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -66,7 +66,12 @@ def main():
     build_s = time.time() - t0
     stream = torch.cuda.Stream(device=dev)
     lib = P._lib.lib()
-    for size in [int(float(x)) for x in args.sizes.split(",")]:
+    for size, kernel in [(int(float(x)), kname) for x in args.sizes.split(",")
+                         for kname in args.kernels.split(",")]:
+        if kernel == "auto":
+            os.environ.pop("PSP_QUERY_KERNEL", None)
+        else:
+            os.environ["PSP_QUERY_KERNEL"] = kernel
         v1, v2 = P.random_pairs(g.n, size, 500 + rank)
         d1 = torch.from_numpy(v1.view(np.int32)).to(dev)
         d2 = torch.from_numpy(v2.view(np.int32)).to(dev)
@@ -106,23 +111,26 @@ def main():
             P._lib.check(lib.psp_gpu_query_batch(o.h, size, h1.data_ptr(), h2.data_ptr(),
                                                  ho.data_ptr(), None))
 
-        for _ in range(3):
-            e2e()
-        if dist:
-            dist.barrier()
-        t = time.perf_counter()
-        for _ in range(reps):
-            e2e()
-        e2e_s = (time.perf_counter() - t) / reps
+        e2e_s = float("nan")
+        if not args.no_e2e:
+            for _ in range(3):
+                e2e()
+            if dist:
+                dist.barrier()
+            t = time.perf_counter()
+            for _ in range(reps):
+                e2e()
+            e2e_s = (time.perf_counter() - t) / reps
         times = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(times, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = times.tolist()
-        dense = (size >= P.GROUP_MIN_DENSITY * o.k * (o.k + 1) / 2 if args.kernel == "auto"
-                 else args.kernel == "grouped")
+        pairs = o.k * (o.k + 1) / 2
+        used = kernel if kernel != "auto" else (
+            "cta" if size < P.CTA_MAX_DENSITY * pairs else "grouped")
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "batch_per_gpu": size,
-                              "kernel": "query_grouped" if dense else "query_warp",
+                              "kernel": "query_" + used, "forced": kernel != "auto",
                               "queries_per_s": round(size * world / dev_s, 1),
                               "e2e_queries_per_s": round(size * world / e2e_s, 1),
                               "ms_per_batch": round(dev_s * 1e3, 4), "reps": reps,
