@@ -81,17 +81,23 @@ EdgeArrays edges_of(const psp::Graph& g) {
 // plain value (include/psp/oracle.hpp:47-78) with no room for a handle, so an
 // entry is found by the address of its table storage and then VERIFIED
 // against the host object before use: n, k, b, the address and size of every
-// table buffer, and a fingerprint of 256 entries sampled across the ids and
-// all tables. A destroyed Oracle whose storage is reused by a different one
+// table buffer, and 96 entries sampled across the ids and all tables (their
+// positions fixed when the entry is made, their values compared on every
+// lookup). A destroyed Oracle whose storage is reused by a different one
 // therefore fails verification and is imported afresh instead of answering
 // from stale device tables. The registry is bounded (kMaxEntries, least
 // recently used evicted, its device memory released).
+struct Sample {
+    uint32_t table;  // 2c: component table c, 2c + 1: boundary table c, ~0u: ids
+    std::size_t pos;
+    uint64_t bits;
+};
 struct Entry {
     std::shared_ptr<psp_gpu_oracle> dev;
     std::size_t n = 0, k = 0, b = 0;
     std::vector<const void*> bufs;  // every component/boundary table buffer
     std::vector<std::size_t> sizes;
-    uint64_t fingerprint = 0;
+    std::vector<Sample> samples;
     uint64_t last_use = 0;
 };
 constexpr std::size_t kMaxEntries = 16;
@@ -101,52 +107,18 @@ uint64_t g_clock = 0;
 
 const void* key_of(const psp::Oracle& o) { return o.component_tables.data(); }
 
-uint64_t mix(uint64_t h, uint64_t x) {
-    h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
-    return h * 0xff51afd7ed558ccdull;
-}
-
 uint64_t bits(double d) {
     uint64_t u;
     std::memcpy(&u, &d, sizeof u);
     return u;
 }
 
-// 256 entries spread over the id arrays and every table (fixed strides, so
-// the same Oracle always samples the same positions)
-uint64_t fingerprint(const psp::Oracle& o) {
-    uint64_t h = mix(mix(o.n, o.k), o.b());
-    const std::size_t n = o.n;
-    for (std::size_t i = 0; i < 32 && n; ++i) {
-        const std::size_t v = (i * 0x9e3779b1ull) % n;
-        h = mix(h, (uint64_t(o.permutation[v]) << 32) | o.partition.assignment[v]);
-    }
-    std::size_t total = 0;
-    for (uint32_t c = 0; c < o.k; ++c)
-        total += o.component_tables[c].data().size() + o.boundary_tables[c].data().size();
-    if (total == 0) return h;
-    const std::size_t samples = 224;
-    std::size_t c = 0, base = 0;
-    for (std::size_t i = 0; i < samples; ++i) {
-        std::size_t pos = (i * total) / samples + (i * 7919) % std::max<std::size_t>(1, total / samples);
-        pos = std::min(pos, total - 1);
-        // walk the concatenation component table c, boundary table c, c+1, ...
-        while (true) {
-            const std::size_t a = o.component_tables[c].data().size();
-            const std::size_t bsz = o.boundary_tables[c].data().size();
-            if (pos < base + a) {
-                h = mix(h, bits(o.component_tables[c].data()[pos - base]));
-                break;
-            }
-            if (pos < base + a + bsz) {
-                h = mix(h, bits(o.boundary_tables[c].data()[pos - base - a]));
-                break;
-            }
-            base += a + bsz;
-            ++c;
-        }
-    }
-    return h;
+uint64_t value_at(const psp::Oracle& o, const Sample& s) {
+    if (s.table == ~0u)
+        return (uint64_t(o.permutation[s.pos]) << 32) | o.partition.assignment[s.pos];
+    const psp::Matrix& m = (s.table & 1) ? o.boundary_tables[s.table >> 1]
+                                         : o.component_tables[s.table >> 1];
+    return bits(m.data()[s.pos]);
 }
 
 void describe(const psp::Oracle& o, Entry& e) {
@@ -155,13 +127,27 @@ void describe(const psp::Oracle& o, Entry& e) {
     e.b = o.b();
     e.bufs.clear();
     e.sizes.clear();
+    e.samples.clear();
+    std::vector<std::size_t> size_of;  // concatenation of all tables
     for (uint32_t c = 0; c < o.k; ++c) {
         e.bufs.push_back(o.component_tables[c].data().data());
         e.sizes.push_back(o.component_tables[c].data().size());
         e.bufs.push_back(o.boundary_tables[c].data().data());
         e.sizes.push_back(o.boundary_tables[c].data().size());
     }
-    e.fingerprint = fingerprint(o);
+    for (std::size_t i = 0; i < 16 && o.n; ++i)
+        e.samples.push_back({~0u, (i * 0x9e3779b1ull) % o.n, 0});
+    std::size_t total = 0;
+    for (std::size_t s : e.sizes) total += s;
+    constexpr std::size_t kTable = 80;
+    std::size_t t = 0, base = 0;
+    for (std::size_t i = 0; i < kTable && total; ++i) {
+        std::size_t pos = (i * total) / kTable + (i * 7919) % std::max<std::size_t>(1, total / kTable);
+        pos = std::min(pos, total - 1);
+        while (pos >= base + e.sizes[t]) base += e.sizes[t++];
+        e.samples.push_back({uint32_t(t), pos - base, 0});
+    }
+    for (Sample& s : e.samples) s.bits = value_at(o, s);
 }
 
 bool matches(const psp::Oracle& o, const Entry& e) {
@@ -175,7 +161,9 @@ bool matches(const psp::Oracle& o, const Entry& e) {
             e.sizes[2 * c + 1] != o.boundary_tables[c].data().size())
             return false;
     }
-    return e.fingerprint == fingerprint(o);
+    for (const Sample& s : e.samples)
+        if (value_at(o, s) != s.bits) return false;
+    return true;
 }
 
 // caller holds g_mu
@@ -349,8 +337,11 @@ std::vector<QueryResult> batch_query(const Oracle& o,
 }
 
 QueryResult query(const Oracle& o, VertexId v1, VertexId v2) {
-    const std::pair<VertexId, VertexId> p{v1, v2};
-    return batch_query(o, std::span<const std::pair<VertexId, VertexId>>(&p, 1), 1)[0];
+    // one pair: the device's point-query server answers it (no launch)
+    if (v1 >= o.n || v2 >= o.n) throw std::invalid_argument("query: vertex id out of range");
+    double d = 0.0;
+    check(psp_gpu_query_batch(device_of(o).get(), 1, &v1, &v2, &d, nullptr));
+    return result_for(o, v1, v2, d);
 }
 
 QueryResult query_parallel_inner(const Oracle& o, VertexId v1, VertexId v2, unsigned) {

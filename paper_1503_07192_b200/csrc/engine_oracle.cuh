@@ -52,10 +52,17 @@ struct psp_gpu_oracle {
     QueryMailbox* mb = nullptr;
     cudaStream_t srv = nullptr;
     unsigned long long srv_seq = 0;
+    // PSP_SERVER_PROFILE: calls, host round trip and device time (ns)
+    double srv_prof[3] = {0, 0, 0};
     psp_gpu_oracle() = default;
     psp_gpu_oracle(const psp_gpu_oracle&) = delete;
     psp_gpu_oracle& operator=(const psp_gpu_oracle&) = delete;
     ~psp_gpu_oracle() {
+        if (srv_prof[0] > 0)
+            std::fprintf(stderr,
+                         "[psp] point-query server: %.0f calls, %.3f us host round trip, %.3f us "
+                         "on the device (request seen -> answered)\n",
+                         srv_prof[0], srv_prof[1] / srv_prof[0] / 1e3, srv_prof[2] / srv_prof[0] / 1e3);
         if (srv) {
             cudaStreamSynchronize(srv);  // the server exits after its idle time
             cudaStreamDestroy(srv);
@@ -1117,29 +1124,51 @@ bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const 
     const unsigned long long idle_ns =
         (idle_env ? std::strtoull(idle_env, nullptr, 10) : 200ull) * 1000ull;
     QueryMailbox* mb = o->mb;
+    uint32_t seq = uint32_t(++o->srv_seq);
+    if (seq == 0) seq = uint32_t(++o->srv_seq);  // 0 is the initial (served) state
+    const unsigned long long tag = (unsigned long long)seq << 32;
     auto launch = [&] {
         mb->alive = 1u;  // until the kernel says otherwise
-        query_server<V><<<1, 32 * QC_WARPS, 0, o->srv>>>(query_view<V>(o, nullptr), mb, idle_ns);
+        const size_t smem = server_smem_bytes(o->R.n, o->R.k);
+        static bool attr_set = false;  // one per V (callers hold query_mu of some oracle)
+        static std::mutex attr_mu;
+        {
+            std::lock_guard<std::mutex> lk(attr_mu);
+            if (!attr_set) {
+                CK(cudaFuncSetAttribute(query_server<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        192 << 10));
+                attr_set = true;
+            }
+        }
+        query_server<V><<<1, 32 * QC_WARPS, smem, o->srv>>>(query_view<V>(o, nullptr), mb, seq - 1,
+                                                            idle_ns, smem ? 1 : 0);
         CK_LAUNCH();
     };
-    mb->count = uint32_t(count);
+    // every word carries the request number: order of the stores is free
     for (uint64_t i = 0; i < count; ++i) {
-        mb->v1[i] = v1[i];
-        mb->v2[i] = v2[i];
+        mb->req[1 + 2 * i] = tag | v1[i];
+        mb->req[2 + 2 * i] = tag | v2[i];
     }
-    std::atomic_thread_fence(std::memory_order_seq_cst);
-    const unsigned long long seq = ++o->srv_seq;
-    mb->req_seq = seq;
+    static const bool prof = std::getenv("PSP_SERVER_PROFILE") != nullptr;
+    const auto tp = prof ? Clock::now() : Clock::time_point{};
+    mb->req[0] = tag | count;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     if (!mb->alive && cudaStreamQuery(o->srv) == cudaSuccess) launch();
     const auto t0 = Clock::now();
-    for (uint64_t spin = 1; mb->done_seq != seq; ++spin) {
+    const uint64_t last_word = 2 * count;  // the bad flag, written with the rest
+    for (uint64_t spin = 1;; ++spin) {
+        bool done = true;
+        for (uint64_t w = 0; w <= last_word && done; ++w) done = uint32_t(mb->ans[w] >> 32) == seq;
+        if (done) break;
         if ((spin & 255) == 0 && !mb->alive) {
             // the server idled out (possibly racing this request): once its
             // kernel is gone, start another unless the answer arrived
             const cudaError_t e = cudaStreamQuery(o->srv);
             if (e == cudaSuccess) {
-                if (mb->done_seq != seq) launch();
+                bool arrived = true;
+                for (uint64_t w = 0; w <= last_word && arrived; ++w)
+                    arrived = uint32_t(mb->ans[w] >> 32) == seq;
+                if (!arrived) launch();
             } else if (e != cudaErrorNotReady) {
                 CK(e);
             }
@@ -1147,9 +1176,17 @@ bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const 
         if ((spin & 0xfffff) == 0 && ms_since(t0) > 60000.0)
             throw Fail{PSP_ECUDA, "point-query server did not answer within 60 s"};
     }
-    std::atomic_thread_fence(std::memory_order_seq_cst);
-    const bool bad = mb->bad != 0;
-    for (uint64_t i = 0; i < count; ++i) dist[i] = mb->dist[i];
+    if (prof) {
+        o->srv_prof[0] += 1;
+        o->srv_prof[1] += std::chrono::duration<double, std::nano>(Clock::now() - tp).count();
+        o->srv_prof[2] += double(mb->prof[1] - mb->prof[0]);
+    }
+    const bool bad = uint32_t(mb->ans[last_word]) != 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        const unsigned long long bits = (mb->ans[2 * i] & 0xffffffffull) |
+                                        ((mb->ans[2 * i + 1] & 0xffffffffull) << 32);
+        std::memcpy(&dist[i], &bits, sizeof(double));
+    }
     if (bad) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
     return true;
 }

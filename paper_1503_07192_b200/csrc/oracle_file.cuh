@@ -21,7 +21,6 @@
 namespace pspg {
 
 constexpr uint64_t CRC64_POLY = 0xC96C5795D7870F42ull;  // reflected ECMA-182
-constexpr uint32_t CRC_SEG = 4096;                      // bytes per GPU segment
 
 struct Crc64Table {
     uint64_t t[256];
@@ -37,29 +36,79 @@ inline Crc64Table make_crc64_table() {
     return tb;
 }
 
-// Raw (init 0, no final xor) CRC of each CRC_SEG-byte segment; the last
-// segment may be short.
-__global__ void crc64_segments(const uint8_t* __restrict__ data, uint64_t len, Crc64Table tb,
-                               uint64_t* __restrict__ out) {
-    __shared__ uint64_t t[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) t[i] = tb.t[i];
-    __syncthreads();
-    const uint64_t seg = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t begin = seg * CRC_SEG;
-    if (begin >= len) return;
-    const uint64_t end = min(len, begin + CRC_SEG);
-    uint64_t crc = 0;
-    uint64_t i = begin;
-    for (; i + 8 <= end; i += 8) {
-        uint64_t w = *reinterpret_cast<const uint64_t*>(data + i);  // 8-byte aligned
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            crc = t[(crc ^ w) & 0xff] ^ (crc >> 8);
-            w >>= 8;
-        }
+// CRC of the bulk bytes on the GPU: one CTA per CRC_BLOCK (64 KB) bytes.
+// The block is staged into shared memory with coalesced 16-byte loads; each
+// of the 256 threads takes a 256-byte leaf (slicing-by-8 over 8 tables in
+// shared memory, 8 bytes per step); the leaves are folded in a tree of 8
+// levels with the CRC append operator x^(8 L) mod P for L = 256 * 2^j bytes
+// (GF(2) 64x64 matrices in constant memory). Output: the raw CRC (zero
+// initial state, no final xor) of each full block; the host appends the
+// blocks and the sub-block tail.
+constexpr uint32_t CRC_LEAF = 256;
+constexpr uint32_t CRC_THREADS = 256;
+constexpr uint32_t CRC_BLOCK = CRC_LEAF * CRC_THREADS;  // 64 KB
+
+struct Crc64Slices {
+    uint64_t t[8][256];
+};
+struct CrcFold {
+    uint64_t col[8][64];  // append operator for 256 * 2^j bytes, j = 0..7
+};
+__constant__ CrcFold c_crc_fold;
+
+inline Crc64Slices make_crc64_slices() {
+    Crc64Slices sl{};
+    for (uint32_t i = 0; i < 256; ++i) {
+        uint64_t crc = i;
+        for (int bit = 0; bit < 8; ++bit) crc = (crc >> 1) ^ ((crc & 1) ? CRC64_POLY : 0);
+        sl.t[0][i] = crc;
     }
-    for (; i < end; ++i) crc = t[(crc ^ data[i]) & 0xff] ^ (crc >> 8);
-    out[seg] = crc;
+    for (int k = 1; k < 8; ++k)
+        for (uint32_t i = 0; i < 256; ++i)
+            sl.t[k][i] = (sl.t[k - 1][i] >> 8) ^ sl.t[0][sl.t[k - 1][i] & 0xff];
+    return sl;
+}
+
+__global__ void __launch_bounds__(CRC_THREADS) crc64_blocks(const uint8_t* __restrict__ data,
+                                                            const Crc64Slices* __restrict__ slices,
+                                                            uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char crc_smem[];
+    uint64_t* t = reinterpret_cast<uint64_t*>(crc_smem);            // 8 x 256
+    uint4* blk = reinterpret_cast<uint4*>(crc_smem + 8 * 256 * 8);  // CRC_BLOCK bytes
+    __shared__ uint64_t part[CRC_THREADS];
+    for (uint32_t i = threadIdx.x; i < 8 * 256; i += CRC_THREADS) t[i] = (&slices->t[0][0])[i];
+    const uint4* src = reinterpret_cast<const uint4*>(data + uint64_t(blockIdx.x) * CRC_BLOCK);
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < CRC_BLOCK / 16; i += CRC_THREADS) blk[i] = src[i];
+    __syncthreads();
+    // leaf: 32 words of 8 bytes; word w of thread x at w * 256 + x would be
+    // conflict-free, but the leaf must be contiguous: read word-by-word
+    const uint64_t* leaf = reinterpret_cast<const uint64_t*>(blk) + threadIdx.x * (CRC_LEAF / 8);
+    uint64_t crc = 0;
+#pragma unroll 4
+    for (uint32_t w = 0; w < CRC_LEAF / 8; ++w) {
+        crc ^= leaf[w];
+        crc = t[7 * 256 + (crc & 0xff)] ^ t[6 * 256 + ((crc >> 8) & 0xff)] ^
+              t[5 * 256 + ((crc >> 16) & 0xff)] ^ t[4 * 256 + ((crc >> 24) & 0xff)] ^
+              t[3 * 256 + ((crc >> 32) & 0xff)] ^ t[2 * 256 + ((crc >> 40) & 0xff)] ^
+              t[1 * 256 + ((crc >> 48) & 0xff)] ^ t[0 * 256 + (crc >> 56)];
+    }
+    part[threadIdx.x] = crc;
+    __syncthreads();
+    // tree: at level j, leaf run x (x % 2^(j+1) == 0) absorbs run x + 2^j,
+    // both 256 * 2^j bytes long: crc = M_j crc ^ crc'
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t stride = 1u << j;
+        if ((threadIdx.x & (2 * stride - 1)) == 0) {
+            uint64_t v = part[threadIdx.x], r = 0;
+#pragma unroll 8
+            for (int b = 0; b < 64; ++b)
+                if ((v >> b) & 1) r ^= c_crc_fold.col[j][b];
+            part[threadIdx.x] = r ^ part[threadIdx.x + stride];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = part[0];
 }
 
 // u32 / f32 tile-packed window -> dense f64 rows (the file's value format).
@@ -93,6 +142,8 @@ inline Gf2Mat gf2_mul(const Gf2Mat& a, const Gf2Mat& b) {  // a after b
 // Running CRC-64/XZ whose bulk bytes may be appended as (raw CRC, length).
 class Crc64Stream {
 public:
+    // append operator for 2^i bytes (i < 48)
+    const Gf2Mat& shift_pow2(int i) const { return pow2_[i]; }
     Crc64Stream() : tb_(make_crc64_table()) {
         // one zero byte: s -> T[s & 0xff] ^ (s >> 8)
         Gf2Mat z;

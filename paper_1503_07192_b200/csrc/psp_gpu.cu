@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <fstream>
+#include <future>
 #include <cstring>
 #include <memory>
 #include <map>
@@ -358,12 +359,14 @@ psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kin
         Crc64Stream crc;
         crc.update(buf, table_at);
         {
-            DBuf chunk(IO_CHUNK), seg;
-            std::vector<uint64_t> hseg;
+            DBuf chunk(IO_CHUNK);
+            GpuCrc gcrc(crc, s);
             for (uint64_t at = 0; at < table_bytes; at += IO_CHUNK) {
                 const uint64_t len = std::min<uint64_t>(IO_CHUNK, table_bytes - at);
                 CK(cudaMemcpyAsync(chunk.p, buf + table_at + at, len, cudaMemcpyHostToDevice, s));
-                crc_device_bytes(crc, chunk.as<uint8_t>(), len, seg, hseg, s);
+                const uint64_t nblk = gcrc.launch(chunk.as<uint8_t>(), len, s);
+                CK(cudaStreamSynchronize(s));
+                gcrc.fold(crc, nblk, buf + table_at + at, len);
             }
         }
         if (rd64(buf + payload) != crc.value())
