@@ -178,6 +178,193 @@ void run_fw_components_sharded(const MatArena& a, psp_gpu_ctx* ctx) {
 }
 
 
+// ------------------------------------------ peer-to-peer panel exchange --
+// Every rank of the row-sharded K2 owns an exchange region that all peers map
+// (CUDA IPC over NVLink):
+//   panel[2][nb][T*T] | flag[2][nb] | diag[2][T*T]  (V, double-buffered by
+//   k-block parity) | sync[8] (u64: [0] k-blocks whose diagonal tile this
+//   rank published, [1] k-blocks whose panel slots it finished, [7] error)
+// Per k-block kb (owner o = kb mod world):
+//   o:      phase 1, publish diag[kb&1], sync[0] = kb + 1
+//   others: pull_diag - wait for o's sync[0] > kb, copy o's diag into the
+//           local tile (kb, kb)
+//   all:    phase 2 on the slots this rank owns (home row mod world), into
+//           its own panel[kb&1] + flag[kb&1]; sync[1] = kb + 1
+//   all:    pull_panel - per slot J owned elsewhere: wait for the owner's
+//           sync[1] > kb, copy its activity flag and, only if the slot is
+//           active (holds a finite entry), its 64 KB tile
+// so the panel moves once per consumer and only where it carries work (the
+// NCCL path min-allreduced every slot, active or not). Reuse of a parity
+// buffer at kb + 2 is safe: a rank reaches it only after every peer's
+// sync[1] passed kb + 1, i.e. after their pulls of kb. Waits time out after
+// 60 s (sync[7] = 1, reported as PSP_ECUDA) instead of hanging the GPU.
+struct P2PRegion {
+    size_t panel_off[2], flag_off[2], diag_off[2], sync_off, bytes;
+    P2PRegion(uint32_t nb, size_t vb) {
+        size_t at = 0;
+        auto take = [&](size_t b) {
+            const size_t o = at;
+            at += (b + 255) / 256 * 256;
+            return o;
+        };
+        for (int i = 0; i < 2; ++i) panel_off[i] = take(size_t(nb) * TT * vb);
+        for (int i = 0; i < 2; ++i) flag_off[i] = take(size_t(nb) * vb);
+        for (int i = 0; i < 2; ++i) diag_off[i] = take(TT * vb);
+        sync_off = take(8 * sizeof(unsigned long long));
+        bytes = at;
+    }
+};
+
+__device__ __forceinline__ unsigned long long fw_global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// wait until *f >= want (a peer's counter, read over NVLink); false on timeout
+__device__ bool wait_counter(const volatile unsigned long long* f, unsigned long long want,
+                             volatile unsigned long long* err) {
+    const unsigned long long t0 = fw_global_ns();
+    while (*f < want) {
+        if (*err) return false;
+        if (fw_global_ns() - t0 > 60ull * 1000 * 1000 * 1000) {
+            *err = 1;
+            return false;
+        }
+        __nanosleep(64);
+    }
+    return true;
+}
+
+__global__ void p2p_signal(unsigned long long* f, unsigned long long v) {
+    // the previous kernels of this stream are complete: their writes are in
+    // this GPU's memory, where the peers' NVLink loads are served
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(f) = v;
+    __threadfence_system();
+}
+
+// copy the owner's published diagonal tile (TT values) into the local tile
+template <class V>
+__global__ void __launch_bounds__(256) pull_diag(const V* src, const unsigned long long* src_sync,
+                                                 unsigned long long want, V* dst,
+                                                 unsigned long long* err) {
+    __shared__ int ok;
+    if (threadIdx.x == 0)
+        ok = wait_counter(reinterpret_cast<const volatile unsigned long long*>(src_sync), want,
+                          reinterpret_cast<volatile unsigned long long*>(err));
+    __syncthreads();
+    if (!ok) return;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    constexpr uint32_t n4 = TT * sizeof(V) / 16;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
+        d4[i] = s4[i];
+}
+
+// one CTA per panel slot J != kb owned by another rank: its flag, and its
+// tile when active, from the owner's region into this rank's
+template <class V>
+__global__ void __launch_bounds__(256) pull_panel(unsigned char* const* peers, P2PRegion lay,
+                                                  int buf, uint32_t kb, uint32_t nb, uint32_t rank,
+                                                  uint32_t world, V* panel, V* flag,
+                                                  unsigned long long* err) {
+    const uint32_t J = blockIdx.x;
+    if (J == kb) return;
+    const uint32_t o = (J > kb ? kb : J) % world;  // home row's owner
+    if (o == rank) return;
+    const unsigned char* peer = peers[o];
+    __shared__ int act;
+    if (threadIdx.x == 0) {
+        act = 0;
+        if (wait_counter(reinterpret_cast<const volatile unsigned long long*>(peer + lay.sync_off) + 1,
+                         kb + 1, reinterpret_cast<volatile unsigned long long*>(err))) {
+            const V f = reinterpret_cast<const volatile V*>(peer + lay.flag_off[buf])[J];
+            flag[J] = f;
+            act = f == V(0);
+        }
+    }
+    __syncthreads();
+    if (!act) return;
+    const uint4* s4 = reinterpret_cast<const uint4*>(peer + lay.panel_off[buf]) + size_t(J) * (TT * sizeof(V) / 16);
+    uint4* d4 = reinterpret_cast<uint4*>(panel) + size_t(J) * (TT * sizeof(V) / 16);
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < TT * sizeof(V) / 16; i += blockDim.x) d4[i] = s4[i];
+}
+
+// The exchange regions of all ranks of a sharded build, mapped into this
+// process (the peers' through CUDA IPC).
+struct P2PExchange {
+    P2PRegion lay;
+    DBuf region, d_peers;
+    std::vector<unsigned char*> base;
+    std::vector<void*> opened;
+    P2PExchange(uint32_t nb, size_t vb) : lay(nb, vb) {}
+    ~P2PExchange() { close_peers(); }
+    void close_peers() {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        opened.clear();
+    }
+    unsigned char* mine(int rank) const { return base[rank]; }
+};
+
+// Sets the exchange up (allocation, zeroed counters, IPC handles gathered
+// over NCCL and opened); returns false when the peers cannot be mapped.
+template <class V>
+bool p2p_setup(P2PExchange& x, psp_gpu_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    const int G = ctx->world;
+    x.region.alloc(x.lay.bytes);
+    CK(cudaMemsetAsync(x.region.p, 0, x.lay.bytes, s));
+    cudaIpcMemHandle_t mine;
+    int ok = cudaIpcGetMemHandle(&mine, x.region.p) == cudaSuccess;
+    cudaGetLastError();
+    // every rank must agree before anyone uses the path
+    {
+        uint64_t v = ok;
+        DBuf d(8);
+        CK(cudaMemcpyAsync(d.p, &v, 8, cudaMemcpyHostToDevice, s));
+        NCK(nccl().AllReduce(d.p, d.p, 1, ncclUint64, ncclMin, ctx->comm, s));
+        CK(cudaMemcpyAsync(&v, d.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!v) return false;
+    }
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    DBuf dh(hb * G);
+    CK(cudaMemcpyAsync(static_cast<char*>(dh.p) + hb * ctx->rank, &mine, hb, cudaMemcpyHostToDevice, s));
+    NCK(nccl().AllGather(static_cast<char*>(dh.p) + hb * ctx->rank, dh.p, hb, ncclChar, ctx->comm, s));
+    std::vector<cudaIpcMemHandle_t> h(G);
+    CK(cudaMemcpyAsync(h.data(), dh.p, hb * G, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    x.base.assign(G, nullptr);
+    uint64_t opened_ok = 1;
+    for (int r = 0; r < G; ++r) {
+        if (r == ctx->rank) {
+            x.base[r] = x.region.as<unsigned char>();
+            continue;
+        }
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, h[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            opened_ok = 0;
+            continue;
+        }
+        x.opened.push_back(p);
+        x.base[r] = static_cast<unsigned char*>(p);
+    }
+    {
+        DBuf d(8);
+        CK(cudaMemcpyAsync(d.p, &opened_ok, 8, cudaMemcpyHostToDevice, s));
+        NCK(nccl().AllReduce(d.p, d.p, 1, ncclUint64, ncclMin, ctx->comm, s));
+        CK(cudaMemcpyAsync(&opened_ok, d.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    if (!opened_ok) return false;
+    x.d_peers = upload(x.base, s);  // the zeroed counters are in place on every rank (stream order
+                                    // + the AllReduce above): peers may signal from here on
+    return true;
+}
+
 // Row-sharded blocked FW of the boundary graph over ctx->world GPUs
 // (SURVEY §8e): tile row I is owned by rank I mod world. Per k-block the
 // owner closes the diagonal tile and broadcasts it; every rank updates the
@@ -206,7 +393,72 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     if (prof)
         for (auto& e : ev) CK(cudaEventCreate(&e));
     if (v.act_flag) CK(cudaMemsetAsync(v.act_work, 0, sizeof(unsigned long long), s));
-    for (uint32_t kb = 0; kb < nb; ++kb) {
+    // panel exchange: peer-to-peer pulls of the active slots over NVLink
+    // (default with the sparse walk), or PSP_K2_EXCHANGE=nccl: the
+    // min-allreduce of every slot
+    const char* xenv = std::getenv("PSP_K2_EXCHANGE");
+    std::unique_ptr<P2PExchange> x;
+    if (v.act_flag && nb > 1 && !(xenv && std::strcmp(xenv, "nccl") == 0)) {
+        x = std::make_unique<P2PExchange>(nb, sizeof(V));
+        if (!p2p_setup<V>(*x, ctx)) x.reset();  // every rank takes the same branch
+    }
+    for (uint32_t kb = 0; kb < nb && x; ++kb) {
+        const int owner = int(kb % ctx->world);
+        const int buf = int(kb & 1);
+        V* diag = tiles + tidx(kb, kb, nb) * TT;
+        const P2PRegion& L = x->lay;
+        unsigned char* me = x->mine(ctx->rank);
+        auto* my_sync = reinterpret_cast<unsigned long long*>(me + L.sync_off);
+        MatSet<V> vk = v;
+        vk.p2p = 1;
+        vk.panel = reinterpret_cast<V*>(me + L.panel_off[buf]);
+        vk.act_flag = reinterpret_cast<V*>(me + L.flag_off[buf]);
+        if (prof) CK(cudaEventRecord(ev[0], s));
+        if (owner == ctx->rank) {
+            fw_phase1<V><<<1, NTHREADS, 0, s>>>(vk, kb);
+            CK_LAUNCH();
+            CK(cudaMemcpyAsync(me + L.diag_off[buf], diag, TT * sizeof(V), cudaMemcpyDeviceToDevice, s));
+            p2p_signal<<<1, 1, 0, s>>>(my_sync, kb + 1);
+            CK_LAUNCH();
+        } else {
+            const unsigned char* ob = x->base[owner];
+            pull_diag<V><<<16, 256, 0, s>>>(reinterpret_cast<const V*>(ob + L.diag_off[buf]),
+                                            reinterpret_cast<const unsigned long long*>(ob + L.sync_off),
+                                            kb + 1, diag, my_sync + 7);
+            CK_LAUNCH();
+        }
+        if (prof) CK(cudaEventRecord(ev[1], s));
+        fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(vk, kb);
+        CK_LAUNCH();
+        p2p_signal<<<1, 1, 0, s>>>(my_sync + 1, kb + 1);
+        CK_LAUNCH();
+        if (prof) CK(cudaEventRecord(ev[2], s));
+        pull_panel<V><<<nb, 256, 0, s>>>(x->d_peers.as<unsigned char*>(), L, buf, kb, nb,
+                                         uint32_t(ctx->rank), uint32_t(ctx->world), vk.panel,
+                                         vk.act_flag, my_sync + 7);
+        CK_LAUNCH();
+        if (prof) CK(cudaEventRecord(ev[3], s));
+        launch_active_list<V>(vk, kb, s);
+        fw_phase3<V><<<ctx->sms, NTHREADS, P3_SMEM<V>, s>>>(vk, kb);
+        CK_LAUNCH();
+        if (prof) {
+            CK(cudaEventRecord(ev[4], s));
+            CK(cudaEventSynchronize(ev[4]));
+            for (int i = 0; i < 4; ++i) {
+                float t = 0;
+                CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+                acc_ms[i] += t;
+            }
+        }
+    }
+    if (x) {
+        unsigned long long err = 0;
+        CK(cudaMemcpyAsync(&err, x->mine(ctx->rank) + x->lay.sync_off + 7 * sizeof(err), sizeof(err),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (err) throw Fail{PSP_ECUDA, "K2 panel exchange: a peer did not signal within 60 s"};
+    }
+    for (uint32_t kb = 0; kb < nb && !x; ++kb) {
         const int owner = int(kb % ctx->world);
         V* diag = tiles + tidx(kb, kb, nb) * TT;
         if (prof) CK(cudaEventRecord(ev[0], s));
@@ -251,14 +503,25 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     }
     if (prof) {
         std::fprintf(stderr,
-                     "[psp] rank %d sharded FW nb=%u: phase1+bcast %.1f ms, phase2 %.1f ms, "
-                     "allreduce %.1f ms, phase3 %.1f ms\n",
-                     ctx->rank, nb, acc_ms[0], acc_ms[1], acc_ms[2], acc_ms[3]);
+                     "[psp] rank %d sharded FW nb=%u (%s exchange): phase1+diag %.1f ms, phase2 %.1f "
+                     "ms, panel exchange %.1f ms, phase3 %.1f ms\n",
+                     ctx->rank, nb, x ? "p2p" : "nccl", acc_ms[0], acc_ms[1], acc_ms[2], acc_ms[3]);
         for (auto& e : ev) cudaEventDestroy(e);
     }
     if (v.act_flag) {  // total phase-3 tiles over all ranks
         NCK(nccl().AllReduce(v.act_work, v.act_work, 1, ncclUint64, ncclSum, ctx->comm, s));
         read_walked_tiles(a, s);
+    }
+    if (x) {
+        // no rank may free its region while a peer still maps it: close the
+        // imports, then a barrier, then the regions go (CUDA IPC rules)
+        CK(cudaStreamSynchronize(s));
+        x->close_peers();
+        DBuf d(8);
+        CK(cudaMemsetAsync(d.p, 0, 8, s));
+        NCK(nccl().AllReduce(d.p, d.p, 1, ncclUint64, ncclMax, ctx->comm, s));
+        CK(cudaStreamSynchronize(s));
+        x.reset();
     }
     // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
     const uint32_t batch = 64;

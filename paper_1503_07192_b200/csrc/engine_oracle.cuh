@@ -1124,9 +1124,10 @@ bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const 
     const unsigned long long idle_ns =
         (idle_env ? std::strtoull(idle_env, nullptr, 10) : 200ull) * 1000ull;
     QueryMailbox* mb = o->mb;
-    uint32_t seq = uint32_t(++o->srv_seq);
-    if (seq == 0) seq = uint32_t(++o->srv_seq);  // 0 is the initial (served) state
-    const unsigned long long tag = (unsigned long long)seq << 32;
+    // 16-bit request tags; 0 is the initial (never requested) state
+    uint32_t seq = uint32_t(++o->srv_seq) & 0xffffu;
+    if (seq == 0) seq = uint32_t(++o->srv_seq) & 0xffffu;
+    const unsigned long long tag = (unsigned long long)seq << 48;
     auto launch = [&] {
         mb->alive = 1u;  // until the kernel says otherwise
         const size_t smem = server_smem_bytes(o->R.n, o->R.k);
@@ -1140,25 +1141,28 @@ bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const 
                 attr_set = true;
             }
         }
-        query_server<V><<<1, 32 * QC_WARPS, smem, o->srv>>>(query_view<V>(o, nullptr), mb, seq - 1,
-                                                            idle_ns, smem ? 1 : 0);
+        // `last` = any tag but this request's: the pending request is served
+        query_server<V><<<1, 32 * QC_WARPS, smem, o->srv>>>(query_view<V>(o, nullptr), mb,
+                                                            seq ^ 0x8000u, idle_ns, smem ? 1 : 0);
         CK_LAUNCH();
     };
-    // every word carries the request number: order of the stores is free
-    for (uint64_t i = 0; i < count; ++i) {
-        mb->req[1 + 2 * i] = tag | v1[i];
-        mb->req[2 + 2 * i] = tag | v2[i];
+    // every word carries the request tag: the order of the stores is free
+    // (the first line last, so a single poll usually sees a whole request)
+    for (uint64_t i = 1; i < count; ++i) {
+        mb->req[2 * i] = tag | v1[i];
+        mb->req[2 * i + 1] = tag | v2[i];
     }
     static const bool prof = std::getenv("PSP_SERVER_PROFILE") != nullptr;
     const auto tp = prof ? Clock::now() : Clock::time_point{};
-    mb->req[0] = tag | count;
+    mb->req[1] = tag | v2[0];
+    mb->req[0] = tag | (uint64_t(count) << 32) | v1[0];
     std::atomic_thread_fence(std::memory_order_seq_cst);
     if (!mb->alive && cudaStreamQuery(o->srv) == cudaSuccess) launch();
     const auto t0 = Clock::now();
     const uint64_t last_word = 2 * count;  // the bad flag, written with the rest
     for (uint64_t spin = 1;; ++spin) {
         bool done = true;
-        for (uint64_t w = 0; w <= last_word && done; ++w) done = uint32_t(mb->ans[w] >> 32) == seq;
+        for (uint64_t w = 0; w <= last_word && done; ++w) done = mb_tag(mb->ans[w]) == seq;
         if (done) break;
         if ((spin & 255) == 0 && !mb->alive) {
             // the server idled out (possibly racing this request): once its
@@ -1167,7 +1171,7 @@ bool point_queries(psp_gpu_oracle* o, uint64_t count, const uint32_t* v1, const 
             if (e == cudaSuccess) {
                 bool arrived = true;
                 for (uint64_t w = 0; w <= last_word && arrived; ++w)
-                    arrived = uint32_t(mb->ans[w] >> 32) == seq;
+                    arrived = mb_tag(mb->ans[w]) == seq;
                 if (!arrived) launch();
             } else if (e != cudaErrorNotReady) {
                 CK(e);

@@ -340,6 +340,7 @@ struct MatArena {
         v.nrows = world > 1 ? nrows : 0;
         v.rank = rank;
         v.world = world;
+        v.p2p = 0;
         const bool sp = sparse && panel.p && d_act.p;
         v.act_flag = sp ? panel.as<V>() + panel_elems : nullptr;
         unsigned char* ab = sp ? d_act.as<unsigned char>() : nullptr;

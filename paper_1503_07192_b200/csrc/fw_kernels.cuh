@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
         // computes it, every other rank contributes INF to the min-allreduce
         const uint32_t home_row = J > kb ? kb : J;
         if (home_row % ms.world != ms.rank) {
+            if (ms.p2p) return;  // its owner computes it, this rank pulls it
             V* panel = ms.panel + ms.panel_base[m] + uint64_t(J) * TT;
             for (int e = threadIdx.x * 4; e < TT; e += NTHREADS * 4) {
                 const V inf4[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};

@@ -105,6 +105,10 @@ template <class V> struct MatSet {
     const uint64_t* row_prefix; // prefix of their upper-tile counts (nrows + 1)
     uint32_t nrows;
     uint32_t rank, world;
+    // peer-to-peer panel exchange (engine_fw.cuh run_fw_sharded): phase 2
+    // leaves the slots other ranks compute untouched (they are pulled over
+    // NVLink instead of min-allreduced)
+    uint32_t p2p;
     // sparse walk (null: dense). Per k-block phase 2 writes act_flag[s + J]
     // (s = panel_base[m] / TT, matrix m's first panel slot; V-typed so the
     // sharded build min-allreduces it with the panel: 0 = panel slot J holds

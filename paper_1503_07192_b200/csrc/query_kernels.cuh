@@ -113,6 +113,7 @@ __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint
 // rows are unrolled by 4 so 4 x WQ_SLOTS independent row-segment loads are
 // in flight per warp (each a full 128-byte row segment of the block).
 constexpr int WQ_SLOTS = 8;  // 256 target boundary columns per window
+constexpr int GK = 16;        // rows per staged chunk (grouped kernel) = block-layout row padding
 
 // One lane's partial answer of a resolved query over the source-row chunks
 // i0 = row0, row0 + rstep, ... (32 rows each): min over those rows b1 and the
@@ -229,39 +230,70 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
     const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
     const V* row1 = q.cb + q.cb_off[c1] + uint64_t(l1) * cb_stride(B1);
     const V* col2 = q.cb + q.cb_off[c2] + uint64_t(l2) * cb_stride(B2);
+    // every load below depends only on the resolved ids: issue the
+    // same-component entry and the lane's col2 values before the block rows
+    // so that one memory round trip covers them all (point-query latency)
+    V same = Ops<V>::inf();
+    if (c1 == c2 && threadIdx.x == 0) same = same_component_entry(q, c1, l1, l2);
     V best = Ops<V>::inf();
     for (uint32_t j0 = 0; j0 < B2; j0 += 32 * WQ_SLOTS) {
         const uint32_t nslot = min(uint32_t(WQ_SLOTS), (B2 - j0 + 31) / 32);
-        V acc[WQ_SLOTS];
+        V acc[WQ_SLOTS], cv[WQ_SLOTS];
 #pragma unroll
-        for (int s = 0; s < WQ_SLOTS; ++s) acc[s] = Ops<V>::inf();
-        for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
+        for (int s = 0; s < WQ_SLOTS; ++s) {
+            const uint32_t j = j0 + s * 32 + lane;
+            acc[s] = Ops<V>::inf();
+            cv[s] = (uint32_t(s) < nslot && j < B2) ? col2[j] : Ops<V>::inf();
+        }
+        if (q.bq) {
+            // block query layout: block (c1 <= c2) stored [cg][B1p][32], so
+            // slot s of this lane reads column group j0/32 + s at row r as
+            // ps[s][r * 32]: one add per load, 128-byte rows per warp
+            const uint32_t B1p = (B1 + GK - 1) / GK * GK;
+            const V* bb = q.bq + q.bq_off[c1 * q.k + c2];
+            const V* ps[WQ_SLOTS];
 #pragma unroll
-            for (uint32_t dr = 0; dr < 4; ++dr) {
-                const uint32_t r = r0 + dr;
-                if (r < B1) {
-                    const V a = row1[r];
-                    const uint32_t gi = g1 + r;
+            for (int s = 0; s < WQ_SLOTS; ++s)
+                ps[s] = bb + (uint64_t(j0 >> 5) + s) * B1p * 32 + lane;
+            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
 #pragma unroll
-                    for (int s = 0; s < WQ_SLOTS; ++s) {
-                        const uint32_t j = j0 + s * 32 + lane;
-                        if (uint32_t(s) < nslot && j < B2) {
-                            const uint32_t gj = g2 + j;
-                            // c1 < c2: gi < gj, tile (gi/T, gj/T) is stored
-                            const V m = c1 != c2 ? q.bg[tidx(gi >> 7, gj >> 7, nb) * TT +
-                                                        uint64_t(gi & (T - 1)) * T + (gj & (T - 1))]
-                                                 : q.bg[sym_off(gi, gj, nb)];
-                            acc[s] = Ops<V>::addmin(a, m, acc[s]);
+                for (uint32_t dr = 0; dr < 4; ++dr) {
+                    const uint32_t r = r0 + dr;
+                    if (r < B1) {
+                        const V a = row1[r];
+#pragma unroll
+                        for (int s = 0; s < WQ_SLOTS; ++s)
+                            if (uint32_t(s) < nslot)  // padding columns hold INF
+                                acc[s] = Ops<V>::addmin(a, ps[s][r * 32], acc[s]);
+                    }
+                }
+            }
+        } else {
+            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
+#pragma unroll
+                for (uint32_t dr = 0; dr < 4; ++dr) {
+                    const uint32_t r = r0 + dr;
+                    if (r < B1) {
+                        const V a = row1[r];
+                        const uint32_t gi = g1 + r;
+#pragma unroll
+                        for (int s = 0; s < WQ_SLOTS; ++s) {
+                            const uint32_t j = j0 + s * 32 + lane;
+                            if (uint32_t(s) < nslot && j < B2) {
+                                const uint32_t gj = g2 + j;
+                                // c1 < c2: gi < gj, tile (gi/T, gj/T) is stored
+                                const V m = c1 != c2 ? q.bg[tidx(gi >> 7, gj >> 7, nb) * TT +
+                                                            uint64_t(gi & (T - 1)) * T + (gj & (T - 1))]
+                                                     : q.bg[sym_off(gi, gj, nb)];
+                                acc[s] = Ops<V>::addmin(a, m, acc[s]);
+                            }
                         }
                     }
                 }
             }
         }
 #pragma unroll
-        for (int s = 0; s < WQ_SLOTS; ++s) {
-            const uint32_t j = j0 + s * 32 + lane;
-            if (uint32_t(s) < nslot && j < B2) best = Ops<V>::addmin(acc[s], col2[j], best);
-        }
+        for (int s = 0; s < WQ_SLOTS; ++s) best = Ops<V>::addmin(acc[s], cv[s], best);
     }
     best = warp_min<V>(best);
     if (lane == 0) red[warp] = best;
@@ -271,8 +303,7 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
         V b = red[0];
 #pragma unroll
         for (int w = 1; w < QC_WARPS; ++w) b = Ops<V>::vmin(b, red[w]);
-        if (c1 == c2) b = Ops<V>::vmin(b, same_component_entry(q, c1, l1, l2));
-        out = Ops<V>::to_f64(b, q.scale);
+        out = Ops<V>::to_f64(Ops<V>::vmin(b, same), q.scale);
     }
     __syncthreads();  // red is reused by the next query
     return out;
@@ -297,19 +328,26 @@ __global__ void __launch_bounds__(32 * QC_WARPS) query_cta(QueryView<V> q,
 // latency-bound: a launch + stream sync per call costs more than the query.
 // One resident CTA instead polls a mailbox in mapped pinned host memory and
 // answers with cta_query. Every 8-byte word of a request or answer carries
-// the request number in its high half (as NCCL's LL protocol does), so a
-// word is valid on its own and one 16-byte PCIe read fetches the header and
-// a pair: no fences between payload and flag on either side. After idle_ns
+// the request number in its top 16 bits (as NCCL's LL protocol does), so a
+// word is valid on its own, and the first pair and the pair count share one
+// 16-byte line: one PCIe read per poll fetches a whole single-pair request.
+// Two polls stay in flight (tools/pcie_probe: a host<->GPU ping-pong takes
+// 2.3 us with one poll, 2.0 us with two, 3.6 us with four). After idle_ns
 // without a request the CTA clears `alive` and exits (device-wide syncs
 // elsewhere never wait on it for long); the host relaunches it on demand.
+//   req[0] = seq << 48 | count << 32 | v1_0     req[2i]   = seq << 48 | v1_i
+//   req[1] = seq << 48 | v2_0                    req[2i+1] = seq << 48 | v2_i
+//   ans[2i] = seq << 48 | low 32 bits of dist_i, ans[2i+1] = seq << 48 | high 32
+//   ans[2 count] = seq << 48 | bad-id flag
 constexpr int MAILBOX_PAIRS = 32;
 struct __align__(16) QueryMailbox {
-    volatile unsigned long long req[2 + 2 * MAILBOX_PAIRS];  // [0] seq|count, [1+2i] seq|v1, [2+2i] seq|v2
-    volatile unsigned long long ans[2 * MAILBOX_PAIRS + 2];  // [2i] seq|lo(dist), [2i+1] seq|hi, [2c] seq|bad
-    volatile uint32_t alive;                                  // device: server loop running
+    volatile unsigned long long req[2 * MAILBOX_PAIRS];
+    volatile unsigned long long ans[2 * MAILBOX_PAIRS + 2];
+    volatile uint32_t alive;                  // device: server loop running
     uint32_t pad_;
-    volatile unsigned long long prof[2];                      // globaltimer: request seen, answered
+    volatile unsigned long long prof[2];      // globaltimer: request seen, answered
 };
+__host__ __device__ inline uint32_t mb_tag(unsigned long long w) { return uint32_t(w >> 48); }
 
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -379,60 +417,43 @@ __global__ void __launch_bounds__(32 * QC_WARPS) query_server(QueryView<V> q, Qu
     for (;;) {
         if (threadIdx.x == 0) {
             s_stop = 0;
-            // a request is taken from one poll: the header and the first
-            // pair come in one round trip (two independent 16-byte reads:
-            // req[0] seq|count, req[1] v1_0, req[2] v2_0, req[3] v1_1)
-            auto take = [&](unsigned long long h, unsigned long long w0, unsigned long long w1,
-                            unsigned long long w2) -> bool {
-                const uint32_t seq = uint32_t(h >> 32);
-                if (seq == last) return false;
-                const uint32_t cnt = max(1u, min(uint32_t(h), uint32_t(MAILBOX_PAIRS)));
-                // the pairs: every word must carry this request number
-                bool ok = uint32_t(w0 >> 32) == seq && uint32_t(w1 >> 32) == seq;
+            // a request is taken from one poll (req[0..1]: tag, count and the
+            // first pair); further pairs, if any, are read after
+            auto take = [&](unsigned long long w0, unsigned long long w1) -> bool {
+                const uint32_t seq = mb_tag(w0);
+                if (seq == last || mb_tag(w1) != seq) return false;
+                const uint32_t cnt = max(1u, min((uint32_t(w0 >> 32) & 0xffffu), uint32_t(MAILBOX_PAIRS)));
                 s_v[0] = uint32_t(w0);
                 s_v[1] = uint32_t(w1);
-                // pair i: v1 at req[1 + 2i], v2 at req[2 + 2i]
-                for (uint32_t w = 4; w <= 2 * cnt && ok; w += 2) {
+                for (uint32_t i = 1; i < cnt; ++i) {
                     unsigned long long x, y;
-                    ld_sys_v2(&mb->req[w], x, y);  // v2_{w/2-1}, v1_{w/2}
-                    ok = uint32_t(x >> 32) == seq;
-                    s_v[w - 1] = uint32_t(x);
-                    if (w < 2 * cnt) {
-                        ok = ok && uint32_t(y >> 32) == seq;
-                        s_v[w] = uint32_t(y);
-                    }
+                    ld_sys_v2(&mb->req[2 * i], x, y);
+                    if (mb_tag(x) != seq || mb_tag(y) != seq) return false;  // still landing
+                    s_v[2 * i] = uint32_t(x);
+                    s_v[2 * i + 1] = uint32_t(y);
                 }
-                if (cnt > 1 && ok) {
-                    ok = uint32_t(w2 >> 32) == seq;
-                    s_v[2] = uint32_t(w2);
-                }
-                if (!ok) return false;  // words of this request still in flight
                 s_count = cnt;
                 s_seq = seq;
                 return true;
             };
             // two polls in flight, about half a PCIe round trip apart (the
-            // loop alternates them, so it keeps that spacing by itself): a
-            // request is seen ~RTT/4 after it lands on average, not ~RTT/2
-            unsigned long long ha, a0, a1, a2, hb, b0, b1, b2;
-            ld_sys_v2(&mb->req[0], ha, a0);
-            ld_sys_v2(&mb->req[2], a1, a2);
+            // loop consumes and reissues them in turn, so it keeps that
+            // spacing by itself)
+            unsigned long long a0, a1, b0, b1;
+            ld_sys_v2(&mb->req[0], a0, a1);
             __nanosleep(500);
-            ld_sys_v2(&mb->req[0], hb, b0);
-            ld_sys_v2(&mb->req[2], b1, b2);
+            ld_sys_v2(&mb->req[0], b0, b1);
             for (;;) {
-                if (take(ha, a0, a1, a2)) break;
-                ld_sys_v2(&mb->req[0], ha, a0);
-                ld_sys_v2(&mb->req[2], a1, a2);
-                if (take(hb, b0, b1, b2)) break;
-                ld_sys_v2(&mb->req[0], hb, b0);
-                ld_sys_v2(&mb->req[2], b1, b2);
+                if (take(a0, a1)) break;
+                ld_sys_v2(&mb->req[0], a0, a1);
+                if (take(b0, b1)) break;
+                ld_sys_v2(&mb->req[0], b0, b1);
                 if (global_ns() - t_idle > idle_ns) {
                     mb->alive = 0u;
                     __threadfence_system();
                     unsigned long long h, w0;
                     ld_sys_v2(&mb->req[0], h, w0);
-                    if (uint32_t(h >> 32) == last) {
+                    if (mb_tag(h) == last) {
                         s_stop = 1;
                         break;
                     }
@@ -454,7 +475,7 @@ __global__ void __launch_bounds__(32 * QC_WARPS) query_server(QueryView<V> q, Qu
         __syncthreads();
         // answers: lanes of warp 0 write one word each (posted PCIe writes)
         if (threadIdx.x < 32) {
-            const unsigned long long tag = (unsigned long long)seq << 32;
+            const unsigned long long tag = (unsigned long long)seq << 48;
             for (uint32_t w = threadIdx.x; w < 2 * cnt + 1; w += 32) {
                 unsigned long long val;
                 if (w == 2 * cnt) {
@@ -491,7 +512,6 @@ __global__ void __launch_bounds__(32 * QC_WARPS) query_server(QueryView<V> q, Qu
 // query meet in a global atomicMin (value bits are order-preserving: all
 // distances are >= 0), a last tiny kernel applies the same-component cap.
 constexpr int GQ = 32;           // queries per item (= max Q)
-constexpr int GK = 16;           // rows per staged chunk
 constexpr int GWARPS = 8;        // warps per CTA
 constexpr int GTHREADS = 32 * GWARPS;
 
