@@ -1006,7 +1006,10 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
         }
         cp_async_commit();
         if (lane == 0) {
-            fence_proxy_async();
+            // no proxy fence: b[] is only ever written by these bulk copies
+            // (its previous contents were read by LDS whose results the
+            // product already consumed before the __syncwarp that precedes
+            // this issue), so there is no generic write to order against
             mbar_expect_tx(&st->bar[buf], GK * 32 * sizeof(V));
             bulk_g2s(st->b[buf], bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(V), &st->bar[buf]);
         }

@@ -12,6 +12,15 @@ import sys
 import numpy as np
 import pytest
 
+# torch first: its libtorch_cuda needs the NCCL it ships (2.28). The library
+# dlopens "libnccl.so.2" on first multi-GPU use and binds to whichever copy
+# is already loaded; were the system NCCL (2.27) loaded first, a later
+# `import torch` in the same process would fail on a missing 2.28 symbol.
+try:
+    import torch  # noqa: F401
+except ImportError:  # pragma: no cover - CPU images without torch
+    pass
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
