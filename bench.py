@@ -192,7 +192,8 @@ def kernel_for(o, batch):
     if forced in ("warp", "grouped", "cta"):
         return forced
     pairs = o.k * (o.k + 1) / 2
-    return "cta" if batch < P.CTA_MAX_DENSITY * pairs else "grouped"
+    return ("cta" if batch < P.CTA_MAX_DENSITY * pairs or batch <= P.CTA_MAX_COUNT
+            else "grouped")
 
 
 def launches_per_batch(o, batch):
@@ -201,7 +202,14 @@ def launches_per_batch(o, batch):
     group_prep, group_tasks, 2 x (cub ScanInit + Scan), group_emit,
     group_scatter, query_grouped, group_finish; query_cta / query_warp run
     alone (engine_oracle.cuh launch_grouped / launch_queries)."""
-    return 10 if kernel_for(o, batch) == "grouped" else 1
+    import paper_1503_07192_b200 as P
+    if kernel_for(o, batch) != "grouped":
+        return 1
+    # sparse grouping: cub radix sort (onesweep: histogram + 3 passes for the
+    # <= 24-bit pair keys) and run-length encode (3) replace the bin pass
+    sparse = (o.k * o.k >= P.SPARSE_GROUPING_MIN_BINS
+              and batch * P.SPARSE_GROUPING_RATIO < o.k * o.k)
+    return 16 if sparse else 10
 
 
 def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, world,

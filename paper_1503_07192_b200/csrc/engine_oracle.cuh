@@ -940,6 +940,15 @@ void export_window(const psp_gpu_oracle* o, const MatArena& a, uint32_t m, uint3
     to_f64(h, dst, o->scale);
 }
 
+// Sparse grouping when count * SPARSE_GROUPING_RATIO < k^2 and k^2 is large.
+// Measured on cfg3 (k^2 = 1,048,576 bins, profiles/r2/query_kernel_sweep_cfg3.jsonl):
+// 1K pairs 12.9 (sparse) vs 12.7 (dense) M queries/s, 10K 38.7 vs 46.7, 100K
+// 70.9 vs 71.3: the k^2 passes are not what small batches wait on there (their
+// blocks are read with no reuse, and the per-task chunk pipeline is latency
+// bound), so the dense path stays up to 2^24 bins (k = 4096, 268 MB of bins).
+constexpr uint64_t SPARSE_GROUPING_RATIO = 4;
+constexpr uint64_t SPARSE_GROUPING_MIN_BINS = uint64_t(1) << 24;
+
 // Counting sort by component pair, task records, query_grouped, finish.
 // `bnd_off` is the host copy of the boundary offsets (task-count bound).
 template <class V, int MODE>
@@ -947,34 +956,65 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
                     const QueryView<V>& q, uint64_t count, const uint32_t* v1, const uint32_t* v2,
                     double* dist, cudaStream_t s) {
     const uint32_t k = q.k;
-    const uint32_t nbins = k * k;
+    // dense grouping: a counting sort over all k^2 pair bins; sparse (batches
+    // far smaller than k^2): radix sort of the batch's keys and its runs as
+    // the bins, so the cost follows the batch instead of k^2
+    const char* ge = std::getenv("PSP_GROUPING");  // dense|sparse override (tests)
+    bool sparse = uint64_t(k) * k >= SPARSE_GROUPING_MIN_BINS &&
+                  uint64_t(count) * SPARSE_GROUPING_RATIO < uint64_t(k) * k;
+    if (ge && std::strcmp(ge, "dense") == 0) sparse = false;
+    if (ge && std::strcmp(ge, "sparse") == 0) sparse = true;
+    const uint32_t nbins = sparse ? uint32_t(count) : k * k;
     if (!gw.done) CK(cudaEventCreateWithFlags(&gw.done, cudaEventDisableTiming));
     // the workspace is shared by all calls on this oracle: order after the
     // previous user, whatever stream it ran on
     CK(cudaStreamWaitEvent(s, gw.done, 0));
-    if (gw.count < count) {
+    const uint64_t per = sparse ? 11 : 7;  // u32 arrays of `count` in gw.buf
+    if (gw.count < count || gw.buf.bytes < (per * count + 4) * sizeof(uint32_t)) {
         CK(cudaStreamSynchronize(s));
-        gw.buf.alloc(count * 7 * sizeof(uint32_t));
-        gw.count = count;
+        gw.count = std::max<uint64_t>(gw.count, count);
+        gw.buf.alloc((per * gw.count + 4) * sizeof(uint32_t));
     }
     if (gw.bins.bytes < size_t(nbins + 1) * 4 * sizeof(uint32_t)) {
         CK(cudaStreamSynchronize(s));
         gw.bins.alloc(size_t(nbins + 1) * 4 * sizeof(uint32_t));
-        size_t t1 = 0;
+    }
+    uint32_t key_bits = 1;
+    while (key_bits < 32 && (uint64_t(1) << key_bits) < uint64_t(k) * k) ++key_bits;
+    {
+        size_t t1 = 0, t2 = 0, t3 = 0;
         CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                          int(nbins + 1), s));
-        gw.temp.alloc(t1);
-        gw.temp_bytes = t1;
+        if (sparse) {
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                               (uint32_t*)nullptr, (uint32_t*)nullptr, int(count), 0,
+                                               int(key_bits), s));
+            CK(cub::DeviceRunLengthEncode::Encode(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                  (uint32_t*)nullptr, (uint32_t*)nullptr, int(count), s));
+        }
+        const size_t need = std::max({t1, t2, t3});
+        if (gw.temp.bytes < need) {
+            CK(cudaStreamSynchronize(s));
+            gw.temp.alloc(need);
+        }
+        gw.temp_bytes = gw.temp.bytes;
     }
     GroupWork w;
     uint32_t* base = gw.buf.as<uint32_t>();
+    const uint64_t C = count;  // layout of this batch (the buffer holds >= per * count)
     w.key = base;
-    w.l1 = base + gw.count;
-    w.l2 = base + 2 * gw.count;
-    w.best = base + 3 * gw.count;
-    w.sorted = base + 4 * gw.count;
-    w.s_l1 = base + 5 * gw.count;
-    w.s_l2 = base + 6 * gw.count;
+    w.l1 = base + C;
+    w.l2 = base + 2 * C;
+    w.best = base + 3 * C;
+    w.sorted = base + 4 * C;
+    w.s_l1 = base + 5 * C;
+    w.s_l2 = base + 6 * C;
+    w.idx = sparse ? base + 7 * C : nullptr;
+    uint32_t* key_sorted = base + 8 * C;
+    uint32_t* idx_sorted = base + 9 * C;
+    uint32_t* run_key = sparse ? base + 10 * C : nullptr;
+    uint32_t* num_runs = base + 11 * C;
+    w.bin_key = run_key;
     uint32_t* bins = gw.bins.as<uint32_t>();
     w.bin_cnt = bins;
     w.bin_start = bins + (nbins + 1);
@@ -985,9 +1025,17 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     const unsigned qb = unsigned((count + 255) / 256);
     group_prep<V, MODE == QM_ROUTED><<<qb, 256, 0, s>>>(q, v1, v2, count, w);
     CK_LAUNCH();
+    size_t tb = gw.temp_bytes;
+    if (sparse) {
+        CK(cub::DeviceRadixSort::SortPairs(gw.temp.p, tb, w.key, key_sorted, w.idx, idx_sorted,
+                                           int(count), 0, int(key_bits), s));
+        tb = gw.temp_bytes;
+        CK(cub::DeviceRunLengthEncode::Encode(gw.temp.p, tb, key_sorted, run_key, w.bin_cnt,
+                                              num_runs, int(count), s));
+    }
     group_tasks<<<(nbins + 1 + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k);
     CK_LAUNCH();
-    size_t tb = gw.temp_bytes;
+    tb = gw.temp_bytes;
     CK(cub::DeviceScan::ExclusiveSum(gw.temp.p, tb, w.bin_cnt, w.bin_start, int(nbins + 1), s));
     tb = gw.temp_bytes;
     CK(cub::DeviceScan::ExclusiveSum(gw.temp.p, tb, w.task_cnt, w.task_start, int(nbins + 1), s));
@@ -1005,8 +1053,12 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     w.tasks = gw.tasks.as<uint4>();
     group_emit<<<(nbins + 255) / 256, 256, 0, s>>>(w, q.bnd_off, q.k, MODE == QM_BLOCKS);
     CK_LAUNCH();
-    CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins) * sizeof(uint32_t), s));
-    group_scatter<<<qb, 256, 0, s>>>(count, w);
+    if (sparse) {
+        group_scatter_sorted<<<qb, 256, 0, s>>>(count, idx_sorted, w);
+    } else {
+        CK(cudaMemsetAsync(w.bin_cnt, 0, size_t(nbins) * sizeof(uint32_t), s));
+        group_scatter<<<qb, 256, 0, s>>>(count, w);
+    }
     CK_LAUNCH();
     const int gsmem = GWARPS * sizeof(WarpStage<V>);
     static bool attr_set = false;  // one flag per <V, MODE> instantiation
@@ -1030,7 +1082,8 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
 // PSP_QUERY_KERNEL=warp check. All kernels return identical distances.
 // CTA_MAX_DENSITY: measured crossover (profiles/bench/r2_query_kernel_sweep).
 constexpr double GROUP_MIN_DENSITY = 0.0;
-constexpr double CTA_MAX_DENSITY = 0.05;
+constexpr double CTA_MAX_DENSITY = 0.0;
+constexpr uint64_t CTA_MAX_COUNT = 512;  // tiny batches: one launch, no sort
 
 template <class V>
 QueryView<V> query_view(const psp_gpu_oracle* o, uint32_t* bad_id) {
@@ -1064,7 +1117,7 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     // profiling); both kernels return identical distances.
     const char* force = std::getenv("PSP_QUERY_KERNEL");
     bool grouped = double(count) >= GROUP_MIN_DENSITY * pairs;
-    bool cta = double(count) < CTA_MAX_DENSITY * pairs;
+    bool cta = double(count) < CTA_MAX_DENSITY * pairs || count <= CTA_MAX_COUNT;
     if (force && std::strcmp(force, "warp") == 0) grouped = cta = false;
     if (force && std::strcmp(force, "grouped") == 0) grouped = true, cta = false;
     if (force && std::strcmp(force, "cta") == 0) cta = true;

@@ -22,6 +22,8 @@
 //   engine_graphio.cuh   graph text parsed on the GPU (load_graph), writer
 //   psp_gpu.cu           this file: the extern "C" entry points
 //   host_graph.cpp, partition.cpp   host graph plumbing and partitioner
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 

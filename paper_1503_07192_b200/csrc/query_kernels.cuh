@@ -530,6 +530,11 @@ struct GroupWork {
     uint32_t* task_start; // [nbins + 1]
     uint4* tasks;         // [max tasks] (c1, c2, first sorted query, m | cg << 8)
     uint32_t nbins;
+    // sparse grouping (batches far smaller than k^2): the "bins" are the
+    // runs of the radix-sorted keys, bin b holds pair bin_key[b]; null: the
+    // bin index is the pair key itself
+    const uint32_t* bin_key;
+    uint32_t* idx;        // [count] iota for the sort's values
 };
 
 template <class V, bool ROUTED>
@@ -544,15 +549,21 @@ __global__ void group_prep(QueryView<V> q, const uint32_t* __restrict__ v1,
     w.l1[i] = l1;
     w.l2[i] = l2;
     w.best[i] = Ops<V>::to_bits(Ops<V>::inf());
-    atomicAdd(&w.bin_cnt[key], 1u);
+    if (w.bin_key) w.idx[i] = static_cast<uint32_t>(i);  // sparse: sorted later
+    else atomicAdd(&w.bin_cnt[key], 1u);
 }
 
 __global__ void group_tasks(GroupWork w, const uint32_t* __restrict__ bnd_off, uint32_t k) {
     const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < w.nbins) {
-        const uint32_t c2 = b % k;
+        const uint32_t cnt = w.bin_cnt[b];
+        if (cnt == 0) {  // (sparse: runs past the last are zero-filled)
+            w.task_cnt[b] = 0;
+            return;
+        }
+        const uint32_t c2 = (w.bin_key ? w.bin_key[b] : b) % k;
         const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2];
-        w.task_cnt[b] = ((w.bin_cnt[b] + GQ - 1) / GQ) * ((B2 + 31) / 32);
+        w.task_cnt[b] = ((cnt + GQ - 1) / GQ) * ((B2 + 31) / 32);
     } else if (b == w.nbins) {
         w.task_cnt[b] = 0;
     }
@@ -565,7 +576,8 @@ __global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, ui
     if (b >= w.nbins) return;
     const uint32_t n = w.task_cnt[b];
     if (n == 0) return;
-    const uint32_t c1 = b / k, c2 = b % k;
+    const uint32_t key = w.bin_key ? w.bin_key[b] : b;
+    const uint32_t c1 = key / k, c2 = key % k;
     const uint32_t B2 = bnd_off[c2 + 1] - bnd_off[c2], ncg = (B2 + 31) / 32;
     const uint32_t start = w.bin_start[b], end = w.bin_start[b + 1];
     // balanced (register-blocked block-layout product, queries in steps of
@@ -587,6 +599,16 @@ __global__ void group_emit(GroupWork w, const uint32_t* __restrict__ bnd_off, ui
         const uint32_t half = (cg + 1 == ncg && B2 - cg * 32 <= 16) ? 1u : 0u;
         out[t] = make_uint4(c1, c2, q0, m | (half << 6) | (cg << 8));
     }
+}
+
+// sparse grouping: the radix sort already ordered the query ids
+__global__ void group_scatter_sorted(uint64_t count, const uint32_t* __restrict__ order, GroupWork w) {
+    const uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= count) return;
+    const uint32_t i = order[p];
+    w.sorted[p] = i;
+    w.s_l1[p] = w.l1[i];
+    w.s_l2[p] = w.l2[i];
 }
 
 __global__ void group_scatter(uint64_t count, GroupWork w) {

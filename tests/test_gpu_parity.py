@@ -614,3 +614,31 @@ def test_point_query_server(monkeypatch):
     db = of.batch_query(v1[:300], v2[:300])
     ds = np.array([of.query(int(v1[i]), int(v2[i]))[0] for i in range(300)])
     assert np.array_equal(db, ds)
+
+
+@pytest.mark.gpu
+def test_sparse_grouping_matches_dense(monkeypatch):
+    """Batches far smaller than k^2 are grouped by a radix sort of their pair
+    keys (runs as bins) instead of the k^2-bin counting sort: every size,
+    including runs of a single query and the tiny-batch query_cta path,
+    answers bit for bit like the dense grouping and the Dijkstra truth."""
+    from paper_1503_07192_b200 import graphs
+    g = graphs.delaunay(20_000, 4)
+    o = P.build_oracle(g, 97, 4, 0)  # k^2 = 9409 (sparse forced by PSP_GROUPING)
+    v1, v2 = P.random_pairs(g.n, 6000, 31)
+    truth = np.array([oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(s))[int(t)]
+                      for s, t in zip(v1[:40], v2[:40])])
+    for cnt in (1, 7, 512, 513, 1500, 2352, 2353, 6000):
+        a, b = v1[:cnt], v2[:cnt]
+        d_auto = o.batch_query(a, b)
+        monkeypatch.setenv("PSP_QUERY_KERNEL", "grouped")
+        monkeypatch.setenv("PSP_GROUPING", "dense")
+        d_dense = o.batch_query(a, b)
+        monkeypatch.setenv("PSP_GROUPING", "sparse")
+        d_sparse = o.batch_query(a, b)
+        monkeypatch.delenv("PSP_GROUPING")
+        monkeypatch.delenv("PSP_QUERY_KERNEL")
+        assert np.array_equal(d_auto, d_dense), cnt
+        assert np.array_equal(d_sparse, d_dense), cnt
+        m = min(cnt, 40)
+        assert np.array_equal(d_auto[:m], truth[:m]), cnt

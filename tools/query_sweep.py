@@ -127,7 +127,10 @@ def main():
         dev_s, e2e_s = times.tolist()
         pairs = o.k * (o.k + 1) / 2
         used = kernel if kernel != "auto" else (
-            "cta" if size < P.CTA_MAX_DENSITY * pairs else "grouped")
+            "cta" if size < P.CTA_MAX_DENSITY * pairs or size <= P.CTA_MAX_COUNT else "grouped")
+        if used == "grouped":
+            used += (" (sparse grouping)" if o.k * o.k >= P.SPARSE_GROUPING_MIN_BINS
+                     and size * P.SPARSE_GROUPING_RATIO < o.k * o.k else "")
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "batch_per_gpu": size,
                               "kernel": "query_" + used, "forced": kernel != "auto",
