@@ -314,7 +314,7 @@ template <class V>
 bool p2p_setup(P2PExchange& x, psp_gpu_ctx* ctx) {
     cudaStream_t s = ctx->stream;
     const int G = ctx->world;
-    x.region.alloc(x.lay.bytes);
+    x.region.alloc_ipc(x.lay.bytes);
     CK(cudaMemsetAsync(x.region.p, 0, x.lay.bytes, s));
     cudaIpcMemHandle_t mine;
     int ok = cudaIpcGetMemHandle(&mine, x.region.p) == cudaSuccess;

@@ -257,39 +257,33 @@ void agree_min(psp_gpu_ctx* ctx, uint64_t* vals, int count) {
     CK(cudaStreamSynchronize(ctx->stream));
 }
 
-// Chosen before the boundary-graph arena exists: `npos` is the working
-// matrix size (positions incl. the tile-packing padding, >= b). Device
-// memory must hold the working matrix with its panel plus the table in
-// reference numbering (2 GB spare).
-template <class V>
-bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<uint32_t>& posmap,
-                     uint64_t& npos, bool& spill) {
-    const Reordered& R = o->R;
+// The host half of the K2 order (no device, no collective): units (pieces or
+// components), the unit adjacency and the greedy elimination order. It only
+// needs the reordered graph and its edge lists, so device_build runs it on a
+// host thread while Phase 2 runs on the GPU.
+struct BgPlan {
+    bool use = false;          // an order that beats the reference numbering
+    bool by_component = false;
+    uint32_t nu = 0;
+    std::vector<uint32_t> unit;
+    std::vector<uint64_t> bsize;
+    BgOrder ord;
+};
+
+BgPlan plan_bg_order(const Reordered& R, const EdgeLists& L) {
+    BgPlan P;
     const uint32_t k = R.k;
     const uint64_t b = R.b();
-    spill = false;
-    npos = b;
     const char* env = std::getenv("PSP_BG_ORDER");
     const bool sparse = (b + T - 1) / T > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
-    if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
-    size_t free_b = 0, total_b = 0;
-    mem_info(&free_b, &total_b);
-    // every rank decides from the smallest free device and host memory
-    uint64_t agreed[2] = {free_b, host_mem_available()};
-    agree_min(o->ctx, agreed, 2);
-    free_b = agreed[0];
-    const uint64_t host_avail = agreed[1];
-    auto table_bytes = [](uint64_t n) {
-        const uint64_t nb = (n + T - 1) / T;
-        return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
-    };
-    auto need = [&](uint64_t n) { return table_bytes(n) + ((n + T - 1) / T + 1) * TT * sizeof(V) + table_bytes(b) + (2ull << 30); };
-    const bool by_component = env && std::strcmp(env, "component") == 0;
+    if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return P;
+    P.by_component = env && std::strcmp(env, "component") == 0;
     // unit of every boundary id: its component, or the connected part of
     // the component it lies in (union-find over the intra-component edges)
-    std::vector<uint32_t> unit(b);
+    std::vector<uint32_t>& unit = P.unit;
+    unit.assign(b, 0);
     uint32_t nu = 0;
-    if (by_component) {
+    if (P.by_component) {
         for (uint32_t c = 0; c < k; ++c)
             for (uint64_t i = R.bnd_off[c]; i < R.bnd_off[c + 1]; ++i) unit[i] = c;
         nu = k;
@@ -314,22 +308,57 @@ bool choose_bg_order(const psp_gpu_oracle* o, const EdgeLists& L, std::vector<ui
                 unit[i] = id_of_root[r];
             }
     }
-    if (nu < 3 || nu > 16384) return false;
-    std::vector<uint64_t> bsize(nu, 0);
-    for (uint64_t i = 0; i < b; ++i) ++bsize[unit[i]];
+    P.nu = nu;
+    if (nu < 3 || nu > 16384) return P;
+    P.bsize.assign(nu, 0);
+    for (uint64_t i = 0; i < b; ++i) ++P.bsize[unit[i]];
     std::vector<std::pair<uint32_t, uint32_t>> adj;
     adj.reserve(L.bi.size());
     for (size_t e = 0; e < L.bi.size(); ++e) adj.emplace_back(unit[L.bi[e]], unit[L.bj[e]]);
     std::sort(adj.begin(), adj.end());
     adj.erase(std::unique(adj.begin(), adj.end()), adj.end());
-    const BgOrder ord = bg_unit_order(nu, bsize, adj);
+    P.ord = bg_unit_order(nu, P.bsize, adj);
     bool ident = true;
-    for (uint32_t i = 0; i < nu && ident; ++i) ident = ord.order[i] == i;
+    for (uint32_t i = 0; i < nu && ident; ++i) ident = P.ord.order[i] == i;
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr, "[psp] K2 order over %u %s: simulated work %.3e (reference numbering %.3e)%s\n",
-                     nu, by_component ? "components" : "pieces", ord.work, ord.natural,
+                     nu, P.by_component ? "components" : "pieces", P.ord.work, P.ord.natural,
                      ident ? ", kept" : "");
-    if (ident) return false;
+    P.use = !ident;
+    return P;
+}
+
+// Chosen before the boundary-graph arena exists: `npos` is the working
+// matrix size (positions incl. the tile-packing padding, >= b). Device
+// memory must hold the working matrix with its panel plus the table in
+// reference numbering (2 GB spare).
+template <class V>
+bool choose_bg_order(const psp_gpu_oracle* o, const BgPlan& plan, std::vector<uint32_t>& posmap,
+                     uint64_t& npos, bool& spill) {
+    const Reordered& R = o->R;
+    const uint32_t k = R.k;
+    const uint64_t b = R.b();
+    spill = false;
+    npos = b;
+    const char* env = std::getenv("PSP_BG_ORDER");
+    const bool sparse = (b + T - 1) / T > 1 && std::getenv("PSP_FW_DENSE") == nullptr;
+    if (!sparse || k < 2 || (env && std::strcmp(env, "natural") == 0)) return false;
+    size_t free_b = 0, total_b = 0;
+    mem_info(&free_b, &total_b);
+    // every rank decides from the smallest free device and host memory
+    uint64_t agreed[2] = {free_b, host_mem_available()};
+    agree_min(o->ctx, agreed, 2);
+    free_b = agreed[0];
+    const uint64_t host_avail = agreed[1];
+    auto table_bytes = [](uint64_t n) {
+        const uint64_t nb = (n + T - 1) / T;
+        return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
+    };
+    auto need = [&](uint64_t n) { return table_bytes(n) + ((n + T - 1) / T + 1) * TT * sizeof(V) + table_bytes(b) + (2ull << 30); };
+    if (!plan.use) return false;
+    const std::vector<uint32_t>& unit = plan.unit;
+    const std::vector<uint64_t>& bsize = plan.bsize;
+    const BgOrder& ord = plan.ord;
     // positions: units in elimination order packed into tiles (bg_pack),
     // each unit's ids ascending; without room for the padding, contiguous
     std::vector<uint64_t> start;
@@ -579,6 +608,26 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             k1_relax = o->comps.relaxations();
         }
     };
+    // the K2 elimination order needs only host data: plan it on a host
+    // thread while Phase 2 runs on the device
+    BgPlan plan;
+    std::exception_ptr plan_err;
+    double plan_ms = 0.0;
+    std::thread planner([&] {
+        try {
+            const auto tp = Clock::now();
+            plan = plan_bg_order(R, L);
+            plan_ms = ms_since(tp);
+        } catch (...) {
+            plan_err = std::current_exception();
+        }
+    });
+    struct PlanJoin {
+        std::thread& t;
+        ~PlanJoin() {
+            if (t.joinable()) t.join();
+        }
+    } plan_join{planner};
     phase2(-1);
     const bool first_ordered = ordered;
     const double component_ms = ms_since(t0);
@@ -607,8 +656,11 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         bool spill = false;
         uint64_t npos = b;
         const auto tord = Clock::now();
-        const bool permuted = choose_bg_order<V>(o, L, posmap, npos, spill);
-        bg_order_ms = ms_since(tord);
+        planner.join();
+        if (plan_err) std::rethrow_exception(plan_err);
+        const bool permuted = choose_bg_order<V>(o, plan, posmap, npos, spill);
+        bg_order_ms = ms_since(tord);  // on the critical path (the plan overlapped Phase 2)
+        (void)plan_ms;
         k2_npos = permuted ? npos : b;
         k2_permuted = permuted;
         k2_spill = spill;

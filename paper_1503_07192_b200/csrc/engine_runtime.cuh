@@ -146,6 +146,118 @@ BufCache& buf_cache() {
     static BufCache* c = new BufCache;  // never destroyed: frees after CUDA teardown are unsafe
     return *c;
 }
+
+// Large blocks (> BufCache::kMaxBuf) come from a per-device stream-ordered
+// memory pool (cudaMallocFromPoolAsync) whose release threshold keeps freed
+// memory reserved, so a build's arenas (tens of GB) are re-served without
+// driver calls: on these boxes one cudaMalloc/cudaFree of that size costs
+// milliseconds and single calls have stalled for up to 0.8 s in the middle of
+// a build. Semantics stay cudaMalloc/cudaFree's: the allocation is complete
+// before it is handed out (its stream is synchronised), a free first
+// synchronises the device, and reserved-but-unused pool memory counts as free
+// (mem_info), trimmed when the real free memory runs low or an allocation
+// fails. IPC-exported buffers (DBuf::alloc_ipc) bypass the pool.
+// OFF by default: measured on cfg3 it made builds slower, not steadier
+// (boundary phase minus K2 0.10-0.82 s with cudaMalloc, 6.4-17 s with the
+// pool: growing a pool by tens of GB in the middle of a build and trimming it
+// when the real free memory runs low cost far more than the calls it saves;
+// profiles/r2/build_repeat_cfg3_{nopool,pool}.jsonl). PSP_POOL=1 turns it on.
+class BigPool {
+public:
+    static constexpr int kMaxDev = 64;
+    bool enabled() const { return !off_; }
+    void* take(size_t n) {
+        if (off_) return nullptr;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDev) return nullptr;
+        Dev& d = get(dev);
+        if (!d.pool) return nullptr;
+        void* p = nullptr;
+        cudaError_t e = cudaMallocFromPoolAsync(&p, n, d.pool, d.stream);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            cudaDeviceSynchronize();
+            cudaMemPoolTrimTo(d.pool, 0);
+            e = cudaMallocFromPoolAsync(&p, n, d.pool, d.stream);
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;  // the caller falls back to cudaMalloc (and its errors)
+        }
+        if (cudaStreamSynchronize(d.stream) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return p;
+    }
+    void give(void* p) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) == cudaSuccess) dev = at.device;
+        cudaGetLastError();
+        int cur = dev;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        cudaDeviceSynchronize();  // as cudaFree would
+        cudaFreeAsync(p, get(dev).stream);
+        if (cur != dev) cudaSetDevice(cur);
+    }
+    // reserved-but-unused bytes of the current device's pool
+    size_t idle() {
+        if (off_) return 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDev || !devs_[dev].pool) return 0;
+        uint64_t res = 0, used = 0;
+        cudaMemPoolGetAttribute(devs_[dev].pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(devs_[dev].pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        return res > used ? size_t(res - used) : 0;
+    }
+    void trim() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDev || !devs_[dev].pool) return;
+        cudaStreamSynchronize(devs_[dev].stream);
+        cudaMemPoolTrimTo(devs_[dev].pool, 0);
+    }
+
+private:
+    struct Dev {
+        cudaMemPool_t pool = nullptr;
+        cudaStream_t stream = nullptr;
+        bool tried = false;
+    };
+    Dev& get(int dev) {
+        std::lock_guard<std::mutex> lk(mu_);
+        Dev& d = devs_[dev];
+        if (!d.tried) {
+            d.tried = true;
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if (cudaMemPoolCreate(&d.pool, &props) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                if (cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess)
+                    d.pool = nullptr;
+            } else {
+                d.pool = nullptr;
+            }
+            cudaGetLastError();
+        }
+        return d;
+    }
+    std::mutex mu_;
+    Dev devs_[kMaxDev];
+    const bool off_ = std::getenv("PSP_POOL") == nullptr;
+};
+BigPool& big_pool() {
+    static BigPool* p = new BigPool;  // never destroyed (see buf_cache)
+    return *p;
+}
 // free device memory as the budgets see it: cached blocks count as free
 // (flushing them here costs 0.4-0.7 s of cudaFree on these boxes); a large
 // allocation that then does not fit flushes the cache and retries (DBuf::alloc)
@@ -155,28 +267,37 @@ BufCache& buf_cache() {
 void mem_info(size_t* free_b, size_t* total_b) {
     constexpr size_t kFlushBelow = size_t(2) << 30;
     CK(cudaMemGetInfo(free_b, total_b));
-    if (*free_b < kFlushBelow && buf_cache().held() > 0) {
+    if (*free_b < kFlushBelow && (buf_cache().held() > 0 || big_pool().idle() > 0)) {
         buf_cache().flush();
+        big_pool().trim();
         CK(cudaMemGetInfo(free_b, total_b));
     }
-    *free_b += buf_cache().held();
+    *free_b += buf_cache().held() + big_pool().idle();
 }
 
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool pooled = false, ipc = false;
     DBuf() = default;
     explicit DBuf(size_t n) { alloc(n); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), pooled(o.pooled), ipc(o.ipc) {
+        o.p = nullptr;
+        o.bytes = 0;
+        o.pooled = o.ipc = false;
+    }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
             reset();
             p = o.p;
             bytes = o.bytes;
+            pooled = o.pooled;
+            ipc = o.ipc;
             o.p = nullptr;
             o.bytes = 0;
+            o.pooled = o.ipc = false;
         }
         return *this;
     }
@@ -186,6 +307,10 @@ struct DBuf {
         if (n == 0) n = 16;
         bytes = n;
         if ((p = buf_cache().take(n))) return;
+        if (n > BufCache::kMaxBuf && (p = big_pool().take(n))) {
+            pooled = true;
+            return;
+        }
         const size_t r = n <= BufCache::kMaxBuf ? BufCache::rounded(n) : n;
         cudaError_t e = cudaMalloc(&p, r);
         if (e == cudaErrorMemoryAllocation) {
@@ -199,10 +324,23 @@ struct DBuf {
             CK(e);
         }
     }
+    // a plain cudaMalloc block (neither cached nor pooled): CUDA IPC
+    // handles (cudaIpcGetMemHandle) need one
+    void alloc_ipc(size_t n) {
+        reset();
+        if (n == 0) n = 16;
+        bytes = n;
+        ipc = true;
+        CK(cudaMalloc(&p, n));
+    }
     void reset() {
-        if (p && !buf_cache().give(p, bytes)) cudaFree(p);
+        if (p) {
+            if (pooled) big_pool().give(p);
+            else if (ipc || !buf_cache().give(p, bytes)) cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
+        pooled = ipc = false;
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
 };

@@ -166,7 +166,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
         cb_off[c] = used[sh->owner[c]];
         used[sh->owner[c]] += sz;
     }
-    sh->d_cb.alloc(used[me] * vb);
+    sh->d_cb.alloc_ipc(used[me] * vb);  // mapped into the peers (CUDA IPC)
     for (uint32_t c = 0; c < k; ++c)
         if (sh->owner[c] == me && src_off[c + 1] > src_off[c])
             CK(cudaMemcpyAsync(sh->d_cb.as<V>() + cb_off[c], o->d_cb.as<V>() + src_off[c],

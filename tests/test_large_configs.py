@@ -2,8 +2,10 @@
 (int weights) distances vs the CPU oracle on a 1M-vertex synthetic planar
 graph").
 
-Runs by default under ``-m gpu`` on configs[1] (Delaunay 262,144, k=256) and
-configs[2] (Delaunay 1,048,576, k=1024, the metric's configuration); both
+Runs by default under ``-m gpu`` on configs[1] (Delaunay 262,144, k=256),
+configs[2] (Delaunay 1,048,576, k=1024, the metric's configuration) and
+configs[3] (road-like 2048x2048 grid, f32 weights: the tolerance path, with
+the component tables dropped during K2 and recomputed); the Delaunay ones
 take the benchmarked K2 layout (tile-packed elimination order, asserted via
 ``k2_positions > b``). ``PSP_LARGE_CONFIGS`` overrides the list, e.g.
 ``PSP_LARGE_CONFIGS=delaunay262k_k256,delaunay1m_k1024,road4m_k512``.
@@ -32,7 +34,7 @@ from paper_1503_07192_b200 import graphs
 
 pytestmark = pytest.mark.gpu
 F32_RTOL = 1e-5
-DEFAULT = "delaunay262k_k256,delaunay1m_k1024"
+DEFAULT = "delaunay262k_k256,delaunay1m_k1024,road4m_k512"
 CONFIGS = [c for c in os.environ.get("PSP_LARGE_CONFIGS", DEFAULT).split(",") if c]
 SOURCES = 32
 TARGETS = 20_000
