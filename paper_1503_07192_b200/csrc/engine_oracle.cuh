@@ -1135,7 +1135,10 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
 // CTA_MAX_DENSITY: measured crossover (profiles/bench/r2_query_kernel_sweep).
 constexpr double GROUP_MIN_DENSITY = 0.0;
 constexpr double CTA_MAX_DENSITY = 0.0;
-constexpr uint64_t CTA_MAX_COUNT = 512;  // tiny batches: one launch, no sort
+// tiny batches: one launch, no sort (measured on cfg3, block layout:
+// query_cta 24.3 vs query_grouped 12.5 M queries/s at 1K pairs, 24.5 vs 27.4
+// at 3K; profiles/r2/query_sweep_cfg3_cta_blocks.jsonl)
+constexpr uint64_t CTA_MAX_COUNT = 2048;
 
 template <class V>
 QueryView<V> query_view(const psp_gpu_oracle* o, uint32_t* bad_id) {

@@ -236,47 +236,56 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
     V same = Ops<V>::inf();
     if (c1 == c2 && threadIdx.x == 0) same = same_component_entry(q, c1, l1, l2);
     V best = Ops<V>::inf();
-    for (uint32_t j0 = 0; j0 < B2; j0 += 32 * WQ_SLOTS) {
-        const uint32_t nslot = min(uint32_t(WQ_SLOTS), (B2 - j0 + 31) / 32);
-        V acc[WQ_SLOTS], cv[WQ_SLOTS];
+    if (q.bq) {
+        // block query layout, block (c1 <= c2) stored [cg][B1p][32]: thread
+        // t owns a quad of 4 adjacent columns (16-byte loads, a warp reads
+        // 4 full 128-byte row segments) and the rows of one phase
+        // (r = phase, phase + nphase, ...), so every load of the block is
+        // independent and a whole block arrives in ~B1 / nphase / 4 rounds;
+        // each thread adds col2 to its own partial minima (min distributes)
+        const uint32_t B1p = (B1 + GK - 1) / GK * GK;
+        const uint32_t ncg = (B2 + 31) / 32, nquad = ncg * 8;
+        const uint32_t nt = blockDim.x;
+        const uint32_t nphase = nquad >= nt ? 1u : nt / nquad;
+        const V* bb = q.bq + q.bq_off[c1 * q.k + c2];
+        for (uint32_t t = threadIdx.x; t < nquad * nphase; t += nt) {
+            const uint32_t quad = t % nquad, phase = t / nquad;
+            const uint32_t cg = quad >> 3, j = cg * 32 + (quad & 7) * 4;
+            V cv[4];
 #pragma unroll
-        for (int s = 0; s < WQ_SLOTS; ++s) {
-            const uint32_t j = j0 + s * 32 + lane;
-            acc[s] = Ops<V>::inf();
-            cv[s] = (uint32_t(s) < nslot && j < B2) ? col2[j] : Ops<V>::inf();
-        }
-        if (q.bq) {
-            // block query layout: block (c1 <= c2) stored [cg][B1p][32], so
-            // slot s of this lane reads column group j0/32 + s at row r as
-            // ps[s][r * 32]: one add per load, 128-byte rows per warp
-            const uint32_t B1p = (B1 + GK - 1) / GK * GK;
-            const V* bb = q.bq + q.bq_off[c1 * q.k + c2];
-            const V* ps[WQ_SLOTS];
-#pragma unroll
-            for (int s = 0; s < WQ_SLOTS; ++s)
-                ps[s] = bb + (uint64_t(j0 >> 5) + s) * B1p * 32 + lane;
-            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
-#pragma unroll
-                for (uint32_t dr = 0; dr < 4; ++dr) {
-                    const uint32_t r = r0 + dr;
-                    if (r < B1) {
-                        const V a = row1[r];
-#pragma unroll
-                        for (int s = 0; s < WQ_SLOTS; ++s)
-                            if (uint32_t(s) < nslot)  // padding columns hold INF
-                                acc[s] = Ops<V>::addmin(a, ps[s][r * 32], acc[s]);
-                    }
-                }
+            for (int u = 0; u < 4; ++u) cv[u] = j + u < B2 ? col2[j + u] : Ops<V>::inf();
+            const V* col = bb + uint64_t(cg) * B1p * 32 + (quad & 7) * 4;
+            V acc[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
+#pragma unroll 8
+            for (uint32_t r = phase; r < B1; r += nphase) {
+                const V a = row1[r];
+                const uint4 m = *reinterpret_cast<const uint4*>(col + uint64_t(r) * 32);
+                acc[0] = Ops<V>::addmin(a, Ops<V>::from_bits(m.x), acc[0]);
+                acc[1] = Ops<V>::addmin(a, Ops<V>::from_bits(m.y), acc[1]);
+                acc[2] = Ops<V>::addmin(a, Ops<V>::from_bits(m.z), acc[2]);
+                acc[3] = Ops<V>::addmin(a, Ops<V>::from_bits(m.w), acc[3]);
             }
-        } else {
-            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
 #pragma unroll
+            for (int u = 0; u < 4; ++u) best = Ops<V>::addmin(acc[u], cv[u], best);
+        }
+    } else {
+        for (uint32_t j0 = 0; j0 < B2; j0 += 32 * WQ_SLOTS) {
+            const uint32_t nslot = min(uint32_t(WQ_SLOTS), (B2 - j0 + 31) / 32);
+            V acc[WQ_SLOTS], cv[WQ_SLOTS];
+            #pragma unroll
+            for (int s = 0; s < WQ_SLOTS; ++s) {
+                const uint32_t j = j0 + s * 32 + lane;
+                acc[s] = Ops<V>::inf();
+                cv[s] = (uint32_t(s) < nslot && j < B2) ? col2[j] : Ops<V>::inf();
+            }
+            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
+                #pragma unroll
                 for (uint32_t dr = 0; dr < 4; ++dr) {
                     const uint32_t r = r0 + dr;
                     if (r < B1) {
                         const V a = row1[r];
                         const uint32_t gi = g1 + r;
-#pragma unroll
+                        #pragma unroll
                         for (int s = 0; s < WQ_SLOTS; ++s) {
                             const uint32_t j = j0 + s * 32 + lane;
                             if (uint32_t(s) < nslot && j < B2) {
@@ -291,9 +300,9 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
                     }
                 }
             }
+            #pragma unroll
+            for (int s = 0; s < WQ_SLOTS; ++s) best = Ops<V>::addmin(acc[s], cv[s], best);
         }
-#pragma unroll
-        for (int s = 0; s < WQ_SLOTS; ++s) best = Ops<V>::addmin(acc[s], cv[s], best);
     }
     best = warp_min<V>(best);
     if (lane == 0) red[warp] = best;
