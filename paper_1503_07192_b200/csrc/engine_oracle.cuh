@@ -47,6 +47,9 @@ struct psp_gpu_oracle {
     // block query layout of the boundary table (optional, see
     // build_query_blocks): BQ blocks and their offsets
     DBuf bq, d_bq_off;
+    // 16-bit residual layout (u32 tables, build_query_blocks16)
+    DBuf bq16, d_bq16_off, bqaux, d_aux_off, cb16, d_cb16_off, d_rbase;
+    uint32_t u16_sat = 0x7FFFu;
     // point-query server (query_server): mailbox in mapped pinned host
     // memory, its stream, the last request number. Guarded by query_mu.
     QueryMailbox* mb = nullptr;
@@ -221,6 +224,62 @@ void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
     pack_query_blocks<V><<<unsigned(k * k), 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0],
                                                          o->d_bnd_off.as<uint32_t>(), uint32_t(k),
                                                          o->d_bq_off.as<uint64_t>(), o->bq.as<V>());
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+}
+
+// The 16-bit residual layout of the boundary table for the u32 query
+// product (query_kernels.cuh "16-bit residual product"): per pair block the
+// saturated residuals (same [cg][B1p][32] geometry as the block layout, u16)
+// and its potentials, per to-boundary row its 15-bit offsets and base. About
+// half the block layout; built when it fits with 8 GB spare.
+void build_query_blocks16(psp_gpu_oracle* o, cudaStream_t s) {
+    const Reordered& R = o->R;
+    const uint64_t k = R.k;
+    o->bq16.reset();
+    o->bqaux.reset();
+    o->cb16.reset();
+    o->d_rbase.reset();
+    // opt-in (PSP_QUERY_U16=1): measured slower than the u32 product on cfg3
+    // (31.3 vs 16.1 ms per 10M pairs, 0.7% of queries to the u32 fallback),
+    // see DESIGN.md §3c
+    const char* env = std::getenv("PSP_QUERY_U16");
+    if (!(env && std::strcmp(env, "1") == 0)) return;
+    if (o->kind.kind != PSP_VALUE_U32 || !o->bg.nmat || k * k >= (1ull << 31)) return;
+    std::vector<uint64_t> off(k * k, 0), aoff(k * k, 0);
+    uint64_t acc = 0, aacc = 0;
+    uint32_t maxB = 1;
+    for (uint64_t c1 = 0; c1 < k; ++c1) {
+        const uint32_t B1 = R.bnd_off[c1 + 1] - R.bnd_off[c1];
+        const uint64_t B1p = (B1 + GK - 1) / GK * GK;
+        maxB = std::max(maxB, B1);
+        for (uint64_t c2 = c1; c2 < k; ++c2) {
+            const uint32_t B2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
+            off[c1 * k + c2] = acc;
+            acc += (B2 + 31) / 32 * 32 * B1p;
+            aoff[c1 * k + c2] = aacc;
+            aacc += (bqaux_words(B1, B2) + 3) / 4 * 4;  // 16-byte aligned
+        }
+    }
+    size_t free_b = 0, total_b = 0;
+    mem_info(&free_b, &total_b);
+    const uint64_t need = acc * 2 + aacc * 4 + 2 * k * k * 8;
+    if (need + (8ull << 30) > free_b) return;
+    o->bq16.alloc(acc * 2);
+    o->bqaux.alloc(aacc * 4);
+    o->d_bq16_off = upload(off, s);
+    o->d_aux_off = upload(aoff, s);
+    // PSP_U16_SAT (tests only): a smaller saturation S sends most queries
+    // through the lower-bound test and the u32 fallback
+    const char* se = std::getenv("PSP_U16_SAT");
+    o->u16_sat = se ? uint32_t(std::min<unsigned long>(std::strtoul(se, nullptr, 0), U16_SAT)) : U16_SAT;
+    const size_t smem = size_t(2) * maxB * sizeof(uint32_t);
+    if (smem > (48u << 10))
+        CK(cudaFuncSetAttribute(pack_query_blocks16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    pack_query_blocks16<<<unsigned(k * k), 256, smem, s>>>(
+        o->bg.tiles.as<uint32_t>(), o->bg.nb[0], o->d_bnd_off.as<uint32_t>(), uint32_t(k),
+        o->d_bq16_off.as<uint64_t>(), o->d_aux_off.as<uint64_t>(), o->bq16.as<uint16_t>(),
+        o->bqaux.as<uint32_t>(), maxB, o->u16_sat);
     CK_LAUNCH();
     CK(cudaStreamSynchronize(s));
 }
@@ -807,11 +866,13 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     o->comps.panel.reset();
     o->bg.panel.reset();
     build_query_blocks<V>(o, s);
+    build_query_blocks16(o, s);
     const double boundary_ms = ms_since(t0);
 
     o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->d_cb_off.bytes +
                       o->d_comp_off.bytes + o->d_bnd_off.bytes + o->d_perm.bytes +
-                      o->d_assign.bytes + o->bq.bytes + o->d_bq_off.bytes;
+                      o->d_assign.bytes + o->bq.bytes + o->d_bq_off.bytes + o->bq16.bytes +
+                      o->bqaux.bytes + o->cb16.bytes + o->d_rbase.bytes;
     if (st) {
         st->component_apsp_ms = component_ms;
         st->boundary_ms = boundary_ms;
@@ -906,7 +967,9 @@ void import_tables(psp_gpu_oracle* o, const double* const* ct, const double* con
     finish_query_tables<V>(o, upload(R.bnd_off, s), s);
     CK(cudaStreamSynchronize(s));
     build_query_blocks<V>(o, s);
-    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->bq.bytes;
+    build_query_blocks16(o, s);
+    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->bq.bytes + o->bq16.bytes +
+                      o->bqaux.bytes + o->cb16.bytes;
 }
 
 void set_peak_entries(const Reordered& R, unsigned workers, psp_build_stats* st) {
@@ -1021,7 +1084,10 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     // the workspace is shared by all calls on this oracle: order after the
     // previous user, whatever stream it ran on
     CK(cudaStreamWaitEvent(s, gw.done, 0));
-    const uint64_t per = sparse ? 11 : 7;  // u32 arrays of `count` in gw.buf
+    // u32 arrays of `count` in gw.buf: key l1 l2 best sorted s_l1 s_l2 |
+    // sparse: idx key_sorted idx_sorted run_key | 16-bit product: lb fb_list
+    // base16 | num_runs, fb_count
+    const uint64_t per = 14;
     if (gw.count < count || gw.buf.bytes < (per * count + 4) * sizeof(uint32_t)) {
         CK(cudaStreamSynchronize(s));
         gw.count = std::max<uint64_t>(gw.count, count);
@@ -1065,7 +1131,12 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
     uint32_t* key_sorted = base + 8 * C;
     uint32_t* idx_sorted = base + 9 * C;
     uint32_t* run_key = sparse ? base + 10 * C : nullptr;
-    uint32_t* num_runs = base + 11 * C;
+    constexpr bool U16 = MODE == QM_BLOCKS16;
+    w.lb = U16 ? base + 11 * C : nullptr;
+    w.fb_list = U16 ? base + 12 * C : nullptr;
+    w.base16 = U16 ? base + 13 * C : nullptr;
+    uint32_t* num_runs = base + 14 * C;
+    w.fb_count = base + 14 * C + 1;
     w.bin_key = run_key;
     uint32_t* bins = gw.bins.as<uint32_t>();
     w.bin_cnt = bins;
@@ -1119,10 +1190,30 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
                                 gsmem));
         attr_set = true;
     }
+    if constexpr (U16) {
+        CK(cudaMemsetAsync(w.fb_count, 0, sizeof(uint32_t), s));
+        group_bases16<V><<<unsigned(std::min<uint64_t>((count + 7) / 8, uint64_t(sms) * 64)), 256, 0, s>>>(
+            q, count, w);
+        CK_LAUNCH();
+    }
     query_grouped<V, MODE><<<sms * 2, GTHREADS, gsmem, s>>>(q, w);
     CK_LAUNCH();
-    group_finish<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w, dist);
-    CK_LAUNCH();
+    if constexpr (U16) {
+        group_finish16<V><<<qb, 256, 0, s>>>(q, count, w, dist);
+        CK_LAUNCH();
+        query_fallback<V><<<sms * 2, 32 * QC_WARPS, 0, s>>>(q, v1, v2, w, dist);
+        CK_LAUNCH();
+        if (std::getenv("PSP_QUERY_STATS")) {  // diagnostics: how many went to the u32 fallback
+            uint32_t fb = 0;
+            CK(cudaMemcpyAsync(&fb, w.fb_count, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "[psp] 16-bit product: %u of %llu queries to the u32 fallback\n", fb,
+                         (unsigned long long)count);
+        }
+    } else {
+        group_finish<V><<<qb, 256, 0, s>>>(q, v1, v2, count, w, dist);
+        CK_LAUNCH();
+    }
     CK(cudaEventRecord(gw.done, s));
 }
 
@@ -1158,6 +1249,14 @@ QueryView<V> query_view(const psp_gpu_oracle* o, uint32_t* bad_id) {
     q.scale = o->scale;
     q.bq = o->bq.p ? o->bq.as<V>() : nullptr;
     q.bq_off = o->bq.p ? o->d_bq_off.as<uint64_t>() : nullptr;
+    q.bq16 = o->bq16.p ? o->bq16.as<uint16_t>() : nullptr;
+    q.bq16_off = o->bq16.p ? o->d_bq16_off.as<uint64_t>() : nullptr;
+    q.bqaux = o->bq16.p ? o->bqaux.as<uint32_t>() : nullptr;
+    q.aux_off = o->bq16.p ? o->d_aux_off.as<uint64_t>() : nullptr;
+    q.cb16 = o->bq16.p ? o->cb16.as<uint16_t>() : nullptr;
+    q.cb16_off = o->bq16.p ? o->d_cb16_off.as<uint64_t>() : nullptr;
+    q.rbase = o->bq16.p ? o->d_rbase.as<uint32_t>() : nullptr;
+    q.u16_sat = o->u16_sat;
     return q;
 }
 
@@ -1191,6 +1290,15 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
         const char* prod = std::getenv("PSP_QUERY_PRODUCT");
         const bool lane_product = prod && std::strcmp(prod, "lane") == 0;
         const bool p8x8 = prod && std::strcmp(prod, "8x8") == 0;
+        const char* u16env = std::getenv("PSP_QUERY_U16");
+        const bool u16 = q.bq16 && !(lay && std::strcmp(lay, "tiles") == 0) && !lane_product &&
+                         !p8x8 && u16env && std::strcmp(u16env, "1") == 0;
+        if constexpr (std::is_same<V, uint32_t>::value) {
+            if (u16) {
+                launch_grouped<V, QM_BLOCKS16>(ws, o->R.bnd_off, o->ctx->sms, q, count, v1, v2, dist, s);
+                return;
+            }
+        }
         if (q.bq && !(lay && std::strcmp(lay, "tiles") == 0) && lane_product)
             launch_grouped<V, QM_BLOCKS_LANE>(ws, o->R.bnd_off,
                                               o->ctx->sms, q, count, v1, v2, dist, s);

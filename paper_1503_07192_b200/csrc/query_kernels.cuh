@@ -56,6 +56,18 @@ template <class V> struct QueryView {
     // with B1p = B1 rounded up to GK, INF padding rows and columns
     const V* bq;
     const uint64_t* bq_off;
+    // 16-bit residual layout (u32 tables, QM_BLOCKS16): block (c1 <= c2) of
+    // saturated residuals at bq16 + bq16_off[c1 * k + c2] ([cg][B1p][32]
+    // u16), its potentials at bqaux + aux_off[c1 * k + c2] (bqaux_words:
+    // 4 reserved, a[B1p], b[ncg*32]). cb16 / cb16_off / rbase: unused (null)
+    const uint16_t* bq16;
+    const uint64_t* bq16_off;
+    const uint32_t* bqaux;
+    const uint64_t* aux_off;
+    const uint16_t* cb16;
+    const uint64_t* cb16_off;
+    const uint32_t* rbase;
+    uint32_t u16_sat;           // saturation S (U16_SAT; smaller only to test the fallback)
 };
 
 template <class V>
@@ -85,7 +97,10 @@ __device__ __forceinline__ V same_component_entry(const QueryView<V>& q, uint32_
 // bulk copy per 16-row chunk).
 // QM_BLOCKS_LANE / QM_BLOCKS_8X8 are the block layout with earlier products
 // (PSP_QUERY_PRODUCT=lane|8x8, kept for A/B measurement).
-enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2, QM_BLOCKS_LANE = 3, QM_BLOCKS_8X8 = 4 };
+// QM_BLOCKS16: the 16-bit residual block layout (u32 tables only, see the
+// "16-bit residual product" section below).
+enum QueryMode : int { QM_TILES = 0, QM_ROUTED = 1, QM_BLOCKS = 2, QM_BLOCKS_LANE = 3, QM_BLOCKS_8X8 = 4,
+                       QM_BLOCKS16 = 5 };
 
 template <class V, bool ROUTED = false>
 __device__ __forceinline__ void resolve(const QueryView<V>& q, uint32_t v1, uint32_t v2,
@@ -530,6 +545,10 @@ struct GroupWork {
     uint32_t* l1;         // [count]
     uint32_t* l2;         // [count]
     uint32_t* best;       // [count] running min (value bits)
+    uint32_t* lb;         // [count] QM_BLOCKS16: smallest lower bound of a saturated column
+    uint32_t* base16;     // [count] QM_BLOCKS16: min_i row1_i + a_i of the query's block
+    uint32_t* fb_list;    // [count] QM_BLOCKS16: queries left to the u32 fallback
+    uint32_t* fb_count;   // [1]
     uint32_t* sorted;     // [count] query ids ordered by key
     uint32_t* s_l1;       // [count] l1 in sorted order
     uint32_t* s_l2;       // [count] l2 in sorted order
@@ -558,6 +577,7 @@ __global__ void group_prep(QueryView<V> q, const uint32_t* __restrict__ v1,
     w.l1[i] = l1;
     w.l2[i] = l2;
     w.best[i] = Ops<V>::to_bits(Ops<V>::inf());
+    if (w.lb) w.lb[i] = U32_INF;
     if (w.bin_key) w.idx[i] = static_cast<uint32_t>(i);  // sparse: sorted later
     else atomicAdd(&w.bin_cnt[key], 1u);
 }
@@ -681,6 +701,123 @@ __device__ __forceinline__ void group_chunk(const V* __restrict__ sA, const V* _
 
 // Per-warp shared state: two staged chunks of A and B, the item's query
 // ids and col2 row offsets.
+// ------------------------------------------- 16-bit residual product --
+// VIADDMNMX.U16x2 does two 16-bit relaxations per instruction at the u32
+// instruction rate (profiles/r2/minplus_probe.json: 125.9 vs 62.1 relax /clk
+// /SM), but its add wraps at 2^16. The stitch min_ij r_i + M_ij + c_j is
+// rewritten with two-sided potentials of each pair block,
+//   M_ij = a_i + R_ij + b_j,  a_i = min_j M_ij,  b_j = min_i (M_ij - a_i),
+// so R >= 0 carries only what is not additive, and with the query's base
+//   base = min_i (r_i + a_i)
+// the product runs on 15-bit saturated offsets (S = 0x7FFF):
+//   t16_j = min_i ( min(r_i + a_i - base, S) + min(R_ij, S) )  (< 2^16: no wrap).
+// If t16_j < S the minimising term saturated nowhere, so t16_j is exact:
+//   candidate t16_j + base + b_j + c_j. If t16_j >= S every term of column j
+// is >= S, so S + base + b_j + c_j is a lower bound. A query whose best exact
+// candidate is <= the smallest lower bound (or whose same-component entry
+// is) is exact; the others are recomputed in u32 by query_fallback
+// (tools/u16_feasibility.py --potentials: 2,117 of 2,117 sampled cfg3
+// queries settle). u32 tables only: u32 fixed point is exact integer
+// arithmetic; f32 keeps the 32-bit product.
+constexpr uint32_t U16_SAT = 0x7FFFu;
+__host__ __device__ __forceinline__ uint32_t cb16_stride(uint32_t B) { return (B + 15u) & ~15u; }
+// per block: [4 reserved][a: B1p u32][b: ncg*32 u32], 16-byte aligned
+__host__ __device__ __forceinline__ uint64_t bqaux_words(uint32_t B1, uint32_t B2) {
+    const uint32_t B1p = (B1 + GK - 1) / GK * GK, ncg = (B2 + 31) / 32;
+    return 4 + B1p + uint64_t(ncg) * 32;
+}
+
+// One CTA per pair block (c1 <= c2): potentials, residuals, y16 offsets.
+// dynamic smem: a[maxB1] + b[maxB2] (u32)
+__global__ void __launch_bounds__(256) pack_query_blocks16(
+    const uint32_t* __restrict__ bg, uint32_t nb, const uint32_t* __restrict__ bnd_off, uint32_t k,
+    const uint64_t* __restrict__ blk_off, const uint64_t* __restrict__ aux_off,
+    uint16_t* __restrict__ bq16, uint32_t* __restrict__ aux, uint32_t maxB, uint32_t sat) {
+    const uint32_t c1 = blockIdx.x / k, c2 = blockIdx.x % k;
+    if (c2 < c1) return;
+    extern __shared__ uint32_t p16_smem[];
+    uint32_t* sa = p16_smem;          // a_i
+    uint32_t* sb = p16_smem + maxB;   // b_j
+    __shared__ uint32_t s_amin;
+    const uint32_t g1 = bnd_off[c1], B1 = bnd_off[c1 + 1] - g1;
+    const uint32_t g2 = bnd_off[c2], B2 = bnd_off[c2 + 1] - g2;
+    const uint32_t B1p = (B1 + GK - 1) / GK * GK, ncg = (B2 + 31) / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    auto M = [&](uint32_t i, uint32_t j) { return bg[sym_off(g1 + i, g2 + j, nb)]; };
+    // a_i = min_j M_ij (a warp per row)
+    for (uint32_t i = warp; i < B1; i += nw) {
+        uint32_t m = U32_INF;
+        for (uint32_t j = lane; j < B2; j += 32) m = min(m, M(i, j));
+        m = __reduce_min_sync(0xffffffffu, m);
+        if (lane == 0) sa[i] = m;
+    }
+    if (threadIdx.x == 0) s_amin = U32_INF;
+    __syncthreads();
+    // b_j = min_i (M_ij - a_i) over finite entries (a thread per column)
+    for (uint32_t j = threadIdx.x; j < B2; j += blockDim.x) {
+        uint32_t m = U32_INF;
+        for (uint32_t i = 0; i < B1; ++i) {
+            const uint32_t v = M(i, j), a = sa[i];
+            if (v < U32_INF && a < U32_INF) m = min(m, v - a);
+        }
+        sb[j] = m;
+    }
+    {
+        uint32_t m = U32_INF;
+        for (uint32_t i = threadIdx.x; i < B1; i += blockDim.x) m = min(m, sa[i]);
+        m = __reduce_min_sync(0xffffffffu, m);
+        if (lane == 0) atomicMin(&s_amin, m);
+    }
+    __syncthreads();
+    const uint32_t amin = s_amin;
+    uint32_t* ax = aux + aux_off[blockIdx.x];
+    if (threadIdx.x < 4) ax[threadIdx.x] = threadIdx.x == 0 ? amin : 0u;
+    uint32_t* ai = ax + 4;
+    for (uint32_t i = threadIdx.x; i < B1p; i += blockDim.x) ai[i] = i < B1 ? sa[i] : U32_INF;
+    uint32_t* bj = ax + 4 + B1p;
+    for (uint32_t j = threadIdx.x; j < ncg * 32; j += blockDim.x) bj[j] = j < B2 ? sb[j] : U32_INF;
+    uint16_t* out = bq16 + blk_off[blockIdx.x];
+    const uint64_t total = uint64_t(ncg) * B1p * 32;
+    for (uint64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const uint64_t cg = idx / (uint64_t(B1p) * 32), rem = idx - cg * B1p * 32;
+        const uint32_t r = uint32_t(rem >> 5), j = uint32_t(cg * 32 + (rem & 31));
+        uint32_t v = sat;
+        if (r < B1 && j < B2) {
+            const uint32_t m = M(r, j), a = sa[r], b = sb[j];
+            if (m < U32_INF && a < U32_INF && b < U32_INF) v = min(m - a - b, sat);
+        }
+        out[idx] = uint16_t(v);
+    }
+}
+
+// Per to-boundary row (component c, local vertex l): rbase = min_i CB[l][i]
+// and x16_i = min(CB[l][i] - rbase, S) (S where unreachable), a warp per row.
+__global__ void __launch_bounds__(256) make_cb16(const uint32_t* __restrict__ cb,
+                                                 const uint64_t* __restrict__ cb_off,
+                                                 const uint32_t* __restrict__ comp_off,
+                                                 const uint32_t* __restrict__ bnd_off,
+                                                 const uint64_t* __restrict__ cb16_off,
+                                                 uint16_t* __restrict__ cb16,
+                                                 uint32_t* __restrict__ rbase, uint32_t sat) {
+    const uint32_t c = blockIdx.x;
+    const uint32_t S = comp_off[c + 1] - comp_off[c], B = bnd_off[c + 1] - bnd_off[c];
+    const uint32_t Bp = cb_stride(B), Bp16 = cb16_stride(B);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t l = warp; l < S; l += nw) {
+        const uint32_t* row = cb + cb_off[c] + uint64_t(l) * Bp;
+        uint32_t m = U32_INF;
+        for (uint32_t i = lane; i < B; i += 32) m = min(m, row[i]);
+        m = __reduce_min_sync(0xffffffffu, m);
+        if (lane == 0) rbase[comp_off[c] + l] = m;
+        uint16_t* x = cb16 + cb16_off[c] + uint64_t(l) * Bp16;
+        for (uint32_t i = lane; i < Bp16; i += 32) {
+            uint32_t v = sat;
+            if (i < B && row[i] < U32_INF && m < U32_INF) v = min(row[i] - m, sat);
+            x[i] = uint16_t(v);
+        }
+    }
+}
+
 template <class V> struct WarpStage {
     V a[2][GQ * GA_STRIDE];
     V b[2][GK * GB_STRIDE];
@@ -1075,12 +1212,258 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
     }
 }
 
+// ---- 16-bit residual product (QM_BLOCKS16): chunk, epilogue, task ------
+// Lane layout <NQG, 4 columns = 2 u16x2 words, QPT>: query group qg = lane %
+// NQG, column slot cq = lane / NQG. A: [query][row] u32 words, each the
+// row's 15-bit offset in both halves; B: [row][32] u16 residuals.
+template <int NQG, int QPT>
+__device__ __forceinline__ void rb16_chunk(const uint32_t* __restrict__ sA,
+                                           const uint16_t* __restrict__ sB, uint32_t (&acc)[16],
+                                           uint32_t rows4, int lane) {
+    const int qg = lane % NQG, cq = lane / NQG;
+    const uint32_t* a0 = sA + qg * GA_STRIDE;
+    const uint16_t* b0 = sB + cq * 4;
+#pragma unroll 1
+    for (uint32_t k4 = 0; k4 < rows4; k4 += 4) {
+        uint4 a[QPT];
+#pragma unroll
+        for (int i = 0; i < QPT; ++i)
+            a[i] = *reinterpret_cast<const uint4*>(a0 + NQG * i * GA_STRIDE + k4);
+        uint2 b[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) b[r] = *reinterpret_cast<const uint2*>(b0 + (k4 + r) * 32);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int i = 0; i < QPT; ++i) {
+                const uint32_t ar = r == 0 ? a[i].x : r == 1 ? a[i].y : r == 2 ? a[i].z : a[i].w;
+                acc[2 * i] = __viaddmin_u16x2(ar, b[r].x, acc[2 * i]);
+                acc[2 * i + 1] = __viaddmin_u16x2(ar, b[r].y, acc[2 * i + 1]);
+            }
+        }
+    }
+}
+
+// Per query slot of this lane: the best exact candidate and the smallest
+// lower bound over the lane's 4 columns, into red_e / red_l [query][9].
+template <int NQG, int QPT>
+__device__ __forceinline__ void rb16_combine(const uint32_t (&acc)[16], const uint32_t* c2s,
+                                             const uint32_t* base, uint4 bj, uint32_t j0,
+                                             uint32_t B2, uint32_t* red_e, uint32_t* red_l,
+                                             int lane, uint32_t sat) {
+    const int qg = lane % NQG, cq = lane / NQG;
+    const uint32_t bjv[4] = {bj.x, bj.y, bj.z, bj.w};
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+        const uint32_t qq = qg + NQG * i;
+        const uint4 cv = *reinterpret_cast<const uint4*>(c2s + qq * 32 + 4 * (cq ^ (qq & 7)));
+        const uint32_t cvv[4] = {cv.x, cv.y, cv.z, cv.w};
+        const uint64_t bq = base[qq];
+        uint64_t d = U32_INF, l = U32_INF;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t j = j0 + cq * 4 + u;
+            if (j < B2) {
+                const uint32_t t = (acc[2 * i + (u >> 1)] >> (16 * (u & 1))) & 0xFFFFu;
+                const uint64_t tail = bq + uint64_t(cvv[u]) + bjv[u];
+                if (t < sat) d = min(d, tail + t);
+                else l = min(l, tail + sat);
+            }
+        }
+        red_e[qq * 9 + cq] = uint32_t(min(d, uint64_t(U32_INF)));
+        red_l[qq * 9 + cq] = uint32_t(min(l, uint64_t(U32_INF)));
+    }
+}
+
+__device__ __forceinline__ void rb16_chunk_v(int v, const uint32_t* sA, const uint16_t* sB,
+                                             uint32_t (&acc)[16], uint32_t rows4, int lane) {
+    switch (v) {
+        case 0: rb16_chunk<4, 1>(sA, sB, acc, rows4, lane); break;
+        case 1: rb16_chunk<4, 2>(sA, sB, acc, rows4, lane); break;
+        case 2: rb16_chunk<4, 3>(sA, sB, acc, rows4, lane); break;
+        case 3: rb16_chunk<4, 4>(sA, sB, acc, rows4, lane); break;
+        case 4: rb16_chunk<4, 5>(sA, sB, acc, rows4, lane); break;
+        case 5: rb16_chunk<4, 6>(sA, sB, acc, rows4, lane); break;
+        case 6: rb16_chunk<4, 7>(sA, sB, acc, rows4, lane); break;
+        case 7: rb16_chunk<4, 8>(sA, sB, acc, rows4, lane); break;
+        case 8: rb16_chunk<8, 1>(sA, sB, acc, rows4, lane); break;
+        case 9: rb16_chunk<8, 2>(sA, sB, acc, rows4, lane); break;
+        case 10: rb16_chunk<8, 3>(sA, sB, acc, rows4, lane); break;
+        default: rb16_chunk<8, 4>(sA, sB, acc, rows4, lane); break;
+    }
+}
+__device__ __forceinline__ void rb16_combine_v(int v, const uint32_t (&acc)[16], const uint32_t* c2s,
+                                               const uint32_t* base, uint4 bj, uint32_t j0,
+                                               uint32_t B2, uint32_t* re, uint32_t* rl, int lane,
+                                               uint32_t sat) {
+    switch (v) {
+        case 0: rb16_combine<4, 1>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 1: rb16_combine<4, 2>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 2: rb16_combine<4, 3>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 3: rb16_combine<4, 4>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 4: rb16_combine<4, 5>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 5: rb16_combine<4, 6>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 6: rb16_combine<4, 7>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 7: rb16_combine<4, 8>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 8: rb16_combine<8, 1>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 9: rb16_combine<8, 2>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        case 10: rb16_combine<8, 3>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+        default: rb16_combine<8, 4>(acc, c2s, base, bj, j0, B2, re, rl, lane, sat); break;
+    }
+}
+
+// One warp task of the 16-bit product: the task records, bulk-copy pipeline
+// and col2 staging of group_task_rb. A comes in as the queries' u32 row1
+// values by cp.async (as in the u32 product) plus the block's row potentials
+// a_i; after the chunk lands each lane turns its query's 16 rows in place
+// into min(row1 + a_i - base, S) in both halves (base = the query's exact
+// min_i row1 + a_i, from group_bases16). Two results per query (best exact
+// candidate, smallest lower bound) go to w.best / w.lb.
+template <class V>
+__device__ __forceinline__ void group_task_rb16(const QueryView<V>& q, const GroupWork& w,
+                                                WarpStage<V>* st, uint32_t c1, uint32_t c2,
+                                                uint32_t q0, uint32_t m, uint32_t cg, bool half,
+                                                uint32_t& phase) {
+    const int lane = threadIdx.x & 31;
+    int v;
+    if (half) v = 7 + int((m + 7) / 8);
+    else v = int((m + 3) / 4) - 1;
+    const int ncs = half ? 4 : 8;
+    const uint32_t cch = half ? 4u : 8u;
+    const uint32_t g1 = q.bnd_off[c1], B1 = q.bnd_off[c1 + 1] - g1;
+    const uint32_t g2 = q.bnd_off[c2], B2 = q.bnd_off[c2 + 1] - g2;
+    const uint32_t Bp1 = cb_stride(B1), Bp2 = cb_stride(B2), B1p = (B1 + GK - 1) / GK * GK;
+    const uint64_t blk = uint64_t(c1) * q.k + c2;
+    const uint16_t* bq_task = q.bq16 + q.bq16_off[blk] + uint64_t(cg) * B1p * 32;
+    const uint32_t* ax = q.bqaux + q.aux_off[blk];
+    const uint32_t* arow = ax + 4;                  // a_i, B1p entries
+    const uint32_t* bj = ax + 4 + B1p + cg * 32;    // b_j of this column group
+    const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
+    const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
+    uint16_t* b16[2] = {reinterpret_cast<uint16_t*>(st->b[0]), reinterpret_cast<uint16_t*>(st->b[0]) + 16 * 32};
+    uint32_t* base = reinterpret_cast<uint32_t*>(st->b[1]);     // [GQ]
+    uint32_t* abuf[2] = {base + GQ, base + GQ + 16};             // a_i of each chunk
+    uint32_t* sa[2] = {reinterpret_cast<uint32_t*>(st->a[0]), reinterpret_cast<uint32_t*>(st->a[1])};
+    __syncwarp();
+    const V* my_row1 = cb1;
+    if (uint32_t(lane) < m) {
+        const uint32_t id = w.sorted[q0 + lane];
+        st->id[lane] = id;
+        st->c2off[lane] = w.s_l2[q0 + lane] * Bp2 + cg * 32;
+        my_row1 = cb1 + uint64_t(w.s_l1[q0 + lane]) * Bp1;
+        base[lane] = w.base16[id];
+    }
+    const uint4 bjq = *reinterpret_cast<const uint4*>(bj + (lane / (half ? 8 : 4)) * 4);
+    __syncwarp();
+    for (uint32_t e = lane; e < m * cch; e += 32) {
+        const uint32_t qq = e / cch, u = e % cch;
+        const bool ok = cg * 32 + 4 * u < Bp2;
+        cp_async16(reinterpret_cast<V*>(st->c2) + qq * 32 + 4 * (u ^ (qq & 7)),
+                   cb2 + (ok ? st->c2off[qq] + 4 * u : 0), ok);
+    }
+    cp_async_commit();
+    auto issue = [&](uint32_t k0, int buf) {
+        uint32_t* sa_l = sa[buf] + lane * GA_STRIDE;
+        if (uint32_t(lane) < m) {
+#pragma unroll
+            for (int t = 0; t < GK / 4; ++t)
+                cp_async16(sa_l + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
+        }
+        if (lane < GK / 4) cp_async16(abuf[buf] + 4 * lane, arow + k0 + 4 * lane, true);
+        cp_async_commit();
+        if (lane == 0) {
+            mbar_expect_tx(&st->bar[buf], GK * 32 * sizeof(uint16_t));
+            bulk_g2s(b16[buf], bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(uint16_t), &st->bar[buf]);
+        }
+    };
+    uint32_t acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0xFFFFFFFFu;  // both halves at the 16-bit maximum
+    const uint32_t sat = q.u16_sat;
+    if (B1 > 0) issue(0, 0);
+    int buf = 0;
+    for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
+        const bool more = k0 + GK < B1;
+        if (more) issue(k0 + GK, buf ^ 1);
+        if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+        __syncwarp();
+        if (uint32_t(lane) < m) {  // row1 + a_i - base, saturated, in both halves
+            uint32_t* row = sa[buf] + lane * GA_STRIDE;
+            const uint64_t bq = base[lane];
+            const uint32_t rows = min(uint32_t(GK), B1 - k0);
+#pragma unroll
+            for (int t = 0; t < GK / 4; ++t) {
+                const uint4 r4 = *reinterpret_cast<const uint4*>(row + 4 * t);
+                const uint4 a4 = *reinterpret_cast<const uint4*>(abuf[buf] + 4 * t);
+                const uint32_t rv[4] = {r4.x, r4.y, r4.z, r4.w}, av[4] = {a4.x, a4.y, a4.z, a4.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint64_t x = uint64_t(rv[u]) + av[u];
+                    uint32_t y = sat;
+                    if (uint32_t(4 * t + u) < rows && rv[u] < U32_INF && av[u] < U32_INF)
+                        y = uint32_t(min(x - bq, uint64_t(sat)));
+                    o[u] = y * 0x10001u;
+                }
+                *reinterpret_cast<uint4*>(row + 4 * t) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        }
+        mbar_wait(&st->bar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        __syncwarp();
+        rb16_chunk_v(v, sa[buf], b16[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, lane);
+        __syncwarp();  // buffer `buf` is refilled by the next issue
+        buf ^= 1;
+    }
+    cp_async_wait<0>();  // col2 (also covers B1 == 0)
+    __syncwarp();
+    uint32_t* red_e = sa[0];          // [query][9] over a[0], free after the last chunk
+    uint32_t* red_l = sa[0] + GQ * 9;
+    static_assert(2 * GQ * 9 <= GQ * GA_STRIDE, "reduction scratch fits a[0]");
+    rb16_combine_v(v, acc, reinterpret_cast<const uint32_t*>(st->c2), base, bjq, cg * 32, B2, red_e,
+                   red_l, lane, sat);
+    __syncwarp();
+    if (uint32_t(lane) < m) {
+        uint32_t d = red_e[lane * 9], l = red_l[lane * 9];
+        for (int c = 1; c < ncs; ++c) {
+            d = min(d, red_e[lane * 9 + c]);
+            l = min(l, red_l[lane * 9 + c]);
+        }
+        atomicMin(&w.best[st->id[lane]], d);
+        atomicMin(&w.lb[st->id[lane]], l);
+    }
+}
+
+// Exact per-query bases of the 16-bit product: base = min_i row1_i + a_i
+// over the pair block's rows (INF when none is finite), a warp per query.
+template <class V>
+__global__ void group_bases16(QueryView<V> q, uint64_t count, GroupWork w) {
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < count; i += nw) {
+        const uint32_t key = w.key[i];
+        const uint32_t c1 = key / q.k, c2 = key % q.k;
+        const uint32_t B1 = q.bnd_off[c1 + 1] - q.bnd_off[c1], B1p = (B1 + GK - 1) / GK * GK;
+        const V* row1 = q.cb + q.cb_off[c1] + uint64_t(w.l1[i]) * cb_stride(B1);
+        const uint32_t* arow = q.bqaux + q.aux_off[uint64_t(c1) * q.k + c2] + 4;
+        uint64_t bmin = U32_INF;
+        for (uint32_t r = lane; r < B1; r += 32) {
+            const uint32_t x = Ops<V>::to_bits(row1[r]), a = arow[r];
+            if (x < U32_INF && a < U32_INF) bmin = min(bmin, uint64_t(x) + a);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+        if (lane == 0) w.base16[i] = uint32_t(min(bmin, uint64_t(U32_INF)));
+        (void)B1p;
+    }
+}
+
 template <class V, int MODE>
 __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, GroupWork w) {
     extern __shared__ __align__(16) unsigned char g_smem[];
     WarpStage<V>* st = reinterpret_cast<WarpStage<V>*>(g_smem) + (threadIdx.x >> 5);
     uint32_t phase = 0;  // QM_BLOCKS*: parity of each B buffer's barrier
-    if (MODE == QM_BLOCKS || MODE == QM_BLOCKS_LANE || MODE == QM_BLOCKS_8X8) {
+    if (MODE == QM_BLOCKS || MODE == QM_BLOCKS_LANE || MODE == QM_BLOCKS_8X8 || MODE == QM_BLOCKS16) {
         if ((threadIdx.x & 31) == 0) {
             mbar_init(&st->bar[0], 1);
             mbar_init(&st->bar[1], 1);
@@ -1107,7 +1490,9 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // switch, see group_task_rb). Tile arena / routed / lane product:
         // three query-count variants (32/16/8 slots; finer ones grew that
         // kernel past the instruction cache), 24 slots for the lane product
-        if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {  // register-blocked product
+        if constexpr (MODE == QM_BLOCKS16) {  // 16-bit residual product (u32 tables)
+            group_task_rb16<V>(q, w, st, c1, c2, q0, m, cg, half, phase);
+        } else if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {  // register-blocked product
             group_task_rb<V, MODE == QM_BLOCKS_8X8>(q, w, st, c1, c2, q0, m, cg, half, phase);
         } else {
             constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
@@ -1117,6 +1502,43 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
             else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
         }
         task = __shfl_sync(0xffffffffu, next, 0);
+    }
+}
+
+// QM_BLOCKS16: a query is exact when its best exact candidate is <= every
+// lower bound (or the same-component entry is); the rest go to the list
+// query_fallback answers in u32.
+template <class V>
+__global__ void group_finish16(QueryView<V> q, uint64_t count, GroupWork w, double* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t d = w.best[i], l = w.lb[i];
+    const uint32_t key = w.key[i];
+    const uint32_t c1 = key / q.k, c2 = key % q.k;
+    const uint32_t cap = c1 == c2 ? Ops<V>::to_bits(same_component_entry(q, c1, w.l1[i], w.l2[i]))
+                                  : U32_INF;
+    if (d <= l) {
+        out[i] = Ops<V>::to_f64(Ops<V>::from_bits(min(d, cap)), q.scale);
+    } else if (cap <= l) {
+        out[i] = Ops<V>::to_f64(Ops<V>::from_bits(cap), q.scale);
+    } else {
+        w.fb_list[atomicAdd(w.fb_count, 1u)] = static_cast<uint32_t>(i);
+    }
+}
+
+// The u32 answer of every query group_finish16 could not settle (grid-
+// stride over the device-side count; cta_query on the u32 tables).
+template <class V>
+__global__ void __launch_bounds__(32 * QC_WARPS) query_fallback(QueryView<V> q,
+                                                                const uint32_t* __restrict__ v1,
+                                                                const uint32_t* __restrict__ v2,
+                                                                GroupWork w, double* __restrict__ out) {
+    __shared__ V red[QC_WARPS];
+    const uint32_t n = *w.fb_count;
+    for (uint32_t f = blockIdx.x; f < n; f += gridDim.x) {
+        const uint32_t i = w.fb_list[f];
+        const double d = cta_query(q, v1[i], v2[i], red);
+        if (threadIdx.x == 0) out[i] = d;
     }
 }
 

@@ -642,3 +642,38 @@ def test_sparse_grouping_matches_dense(monkeypatch):
         assert np.array_equal(d_sparse, d_dense), cnt
         m = min(cnt, 40)
         assert np.array_equal(d_auto[:m], truth[:m]), cnt
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sat", [None, "0x3F", "0x400"])
+def test_u16_residual_product_matches_u32(monkeypatch, golden_cfg1, sat):
+    """The 16-bit residual product (two-sided block potentials, 15-bit
+    saturated offsets, VIADDMNMX.U16x2; opt-in via PSP_QUERY_U16=1) answers
+    every dense batch bit for bit like the u32 product. A tiny saturation (PSP_U16_SAT, tests only)
+    sends most queries through the lower-bound test and the u32 fallback,
+    which must not change a single answer either."""
+    from paper_1503_07192_b200 import graphs
+    z = golden_cfg1
+    cases = [(graph_of(z), 16, 200_000), (graphs.delaunay(20_000, 4), 97, 400_000),
+             (P.generate_grid(90, 90, (0.25, 2.0), 4), 48, 300_000),
+             (P.Graph(8, [0, 1, 2, 4, 5], [1, 2, 3, 5, 6], [1, 1, 1, 2, 2]), 2, 5_000)]
+    for g, k, cnt in cases:
+        monkeypatch.delenv("PSP_QUERY_U16", raising=False)
+        o32 = P.build_oracle(g, k, 4, 0)
+        monkeypatch.setenv("PSP_QUERY_U16", "1")  # opt-in path (slower on cfg3, DESIGN §3c)
+        if sat:
+            monkeypatch.setenv("PSP_U16_SAT", sat)
+        o16 = P.build_oracle(g, k, 4, 0)
+        monkeypatch.delenv("PSP_U16_SAT", raising=False)
+        if o16.b:  # the 16-bit layout exists wherever there is a boundary table
+            assert o16.stats["device_bytes"] > o32.stats["device_bytes"]
+        v1, v2 = P.random_pairs(g.n, cnt, 41)
+        monkeypatch.setenv("PSP_QUERY_KERNEL", "grouped")
+        d16 = o16.batch_query(v1, v2)
+        monkeypatch.delenv("PSP_QUERY_U16")
+        d32 = o32.batch_query(v1, v2)
+        monkeypatch.delenv("PSP_QUERY_KERNEL")
+        assert np.array_equal(d16, d32), (k, sat, int((d16 != d32).sum()))
+        truth = np.array([oracle.dijkstra(g.n, g.eu, g.ev, g.ew, int(s))[int(t)]
+                          for s, t in zip(v1[:30], v2[:30])])
+        assert np.array_equal(d16[:30], truth)

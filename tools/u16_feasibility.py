@@ -71,5 +71,85 @@ def main():
     }))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--potentials" not in sys.argv:
     main()
+
+
+def potentials_mode(o, g, scale, comps, queries_per_comp=400, seed=1):
+    """Two-sided potentials: M[i][j] = a_i + R[i][j] + b_j with a_i = min_j M,
+    b_j = min_i (M - a_i), R >= 0. The 16-bit product runs on R (15-bit
+    saturated) with row1 + a and col2 + b folded into the 32-bit ends; a query
+    is conclusive when its exact columns beat the lower bound of the
+    saturated ones. Returns the conclusive fraction and checks exactness."""
+    rng = np.random.default_rng(seed)
+    bo = o.boundary_offset.astype(np.int64)
+    co = o.component_offset.astype(np.int64)
+    assign_orig = o.assignment[o.permutation]
+    SAT = 0x7FFF
+    tot = conclusive = wrong = 0
+    ranges = []
+    for c1 in comps:
+        rows = o.boundary_rows(int(c1)) * scale
+        ct1 = o.component_table(int(c1)) * scale
+        B1 = rows.shape[0]
+        members = np.flatnonzero(assign_orig == c1)
+        for _ in range(queries_per_comp):
+            v1 = int(rng.choice(members))
+            v2 = int(rng.integers(0, g.n))
+            c2 = int(assign_orig[v2])
+            l1 = int(o.permutation[v1] - co[c1])
+            l2 = int(o.permutation[v2] - co[c2])
+            if c2 < c1 or c2 == c1:
+                continue  # the kernel orients c1 < c2; same-component adds a cap
+            M = rows[:, bo[c2]:bo[c2 + 1]]
+            B2 = M.shape[1]
+            if B1 == 0 or B2 == 0:
+                continue
+            ct2 = o.component_table(c2) * scale
+            r = ct1[l1, :B1]
+            c = ct2[l2, :B2]
+            with np.errstate(invalid="ignore"):
+                a = np.min(M, axis=1)
+                a[~np.isfinite(a)] = 0
+                b = np.min(M - a[:, None], axis=0)
+                b[~np.isfinite(b)] = 0
+                R = M - a[:, None] - b[None, :]
+            Rf = np.where(np.isfinite(R), R, np.inf)
+            ranges.append(float(np.nanmax(np.where(np.isfinite(Rf), Rf, np.nan))) if np.isfinite(Rf).any() else 0.0)
+            rp = r + a
+            base_r = np.min(rp[np.isfinite(rp)]) if np.isfinite(rp).any() else 0.0
+            r16 = np.minimum(np.where(np.isfinite(rp), rp - base_r, SAT), SAT)
+            R16 = np.minimum(np.where(np.isfinite(Rf), Rf, SAT), SAT)
+            t16 = np.min(r16[:, None] + R16, axis=0)
+            cp = c + b
+            exact = t16 < SAT
+            cand = np.where(exact, t16 + base_r + cp, np.inf)
+            lbv = np.where(~exact, SAT + base_r + cp, np.inf)
+            d_exact, lb = float(np.min(cand)), float(np.min(lbv))
+            truth = float(np.min(r[:, None] + M + c[None, :]))
+            tot += 1
+            if d_exact <= lb:
+                conclusive += 1
+                if d_exact != truth:
+                    wrong += 1
+    rr = np.array(ranges)
+    q = [50, 90, 99, 100]
+    return {"queries": tot, "conclusive_fraction": conclusive / max(tot, 1),
+            "wrong_when_conclusive": wrong,
+            "residual_range_percentiles": dict(zip(map(str, q), np.percentile(rr, q).round(1).tolist()))}
+
+
+def main2():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="delaunay262k_k256")
+    ap.add_argument("--components", type=int, default=8)
+    args = ap.parse_args([a for a in sys.argv[1:] if a != "--potentials"])
+    g, cfg = graphs.make(args.config)
+    o = P.build_oracle(g, cfg["k"], os.cpu_count() or 8, 0)
+    scale = 2.0 ** o.stats["fixed_point_shift"]
+    comps = np.random.default_rng(0).choice(o.k, size=min(args.components, o.k), replace=False)
+    print(json.dumps(dict(potentials_mode(o, g, scale, comps), config=args.config)))
+
+
+if __name__ == "__main__" and "--potentials" in sys.argv:
+    main2()
