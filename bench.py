@@ -171,14 +171,18 @@ def query_bytes_and_ops(o, v1, v2):
     return float(byts.sum()), float(ops.sum())
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, config: str | None = None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed `ncu --set full` capture of this kernel on this workload."""
+    committed `ncu --set full` capture of this kernel on this workload
+    (`kernel@config` first, then the kernel's generic entry)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as f:
-        d = json.load(f).get(kernel)
+        table = json.load(f)
+    d = table.get(f"{kernel}@{config}") if config else None
+    if d is None:
+        d = table.get(kernel)
     return (d["dram_bytes_per_launch"], d["source"]) if d else (None, None)
 
 
@@ -213,7 +217,7 @@ def launches_per_batch(o, batch):
 
 
 def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, world,
-                   peak_insn="VIADDMNMX.U32"):
+                   peak_insn="VIADDMNMX.U32", config=None):
     """Dominant kernel of the query step. Dense batches (>= 2 queries per
     component pair) run query_grouped, which reuses each pair's boundary
     block from shared memory: it is bound by the min-plus ALU rate, so
@@ -226,7 +230,7 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
     ops_launch = tops / steps
     bytes_launch = tb / steps
     if dense:
-        traffic, src = ncu_traffic("query_grouped")
+        traffic, src = ncu_traffic("query_grouped", config)
         ach = ops_launch / secs
         return {"kernel": "query_grouped (K3, dense batch)", "bound": "alu",
                 "achieved": round(ach / 1e12, 4), "peak": round(peak_u32 / 1e12, 4),
@@ -238,7 +242,7 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
                 "no_reuse_equiv_gbs": round(bytes_launch / secs / 1e9, 1),
                 "hbm_peak_gbs": peaks["hbm_gbs"]}
     kname = "query_" + kernel_for(o, batch)
-    traffic, src = ncu_traffic(kname)
+    traffic, src = ncu_traffic(kname, config)
     ach = bytes_launch / secs / 1e9
     return {"kernel": f"{kname} (K3, sparse batch)", "bound": "hbm", "achieved": round(ach, 1),
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
@@ -442,7 +446,7 @@ def run_ours(args, rank, world, local):
                 "sync_api": "psp_gpu_query_batch (one blocking call per step)"},
         "gpu_launches": args.steps * launches_per_batch(o, batch),
         "roofline": roofline_entry(o, batch, args.steps, tb, tops, per_launch_ms, peaks,
-                                   peak_u32, world, peak_insn),
+                                   peak_u32, world, peak_insn, args.config),
         "preprocessing": {
             "graph_gen_s": round(gen_s, 2),
             "partition_s": round(st["partition_ms"] / 1e3, 3),
