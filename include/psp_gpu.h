@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PSP_GPU_ABI_VERSION 4
+#define PSP_GPU_ABI_VERSION 5
 
 typedef enum psp_status {
     PSP_OK = 0,
@@ -109,6 +109,22 @@ void psp_gpu_ctx_destroy(psp_gpu_ctx* ctx);
 psp_status psp_gpu_nccl_unique_id(void* out128);
 /* The context's CUDA stream (cudaStream_t) for callers that time kernels. */
 void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx);
+
+/* Where later multi-GPU builds keep the boundary-graph table (the reference
+ * keeps Oracle::boundary_tables, |B(C)| x b per component, on one host,
+ * include/psp/oracle.hpp:60):
+ *   PSP_STORAGE_REPLICATED  every rank ends the build with the whole table
+ *                           (default; all query entry points work);
+ *   PSP_STORAGE_ROW_SHARDED each rank keeps only the tile rows it computed in
+ *                           the row-sharded K2 (about 1/world of the table, so
+ *                           a table larger than one GPU builds across
+ *                           several). Such an oracle answers through
+ *                           psp_gpu_shard_create + psp_gpu_routed_query_batch
+ *                           only; the replicated query, export-boundary-rows
+ *                           and save entry points return PSP_EINVAL.
+ * With world == 1 both mean replicated. */
+enum psp_boundary_storage { PSP_STORAGE_REPLICATED = 0, PSP_STORAGE_ROW_SHARDED = 1 };
+psp_status psp_gpu_ctx_set_boundary_storage(psp_gpu_ctx* ctx, int storage);
 
 /* ------------------------------------------------------- preprocessing -- */
 /* psp::build_oracle (include/psp/oracle.hpp:85-86, src/oracle.cpp:144-194):

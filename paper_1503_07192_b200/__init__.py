@@ -36,9 +36,12 @@ __all__ = ["load_graph", "read_graph", "save_graph", "write_graph", "format_weig
            "boundary_apsp", "partition_graph", "generate_grid", "generate_triangulated_grid",
            "random_pairs", "VALUE_AUTO", "VALUE_U32", "VALUE_F32", "PspError", "PspValueError",
            "GraphInvariantError", "OracleIoError", "FormatVersionError", "ChecksumError",
-           "load_oracle", "UNREACHABLE"]
+           "load_oracle", "UNREACHABLE", "STORAGE_REPLICATED", "STORAGE_ROW_SHARDED"]
 
 UNREACHABLE = float("inf")  # kUnreachable (include/psp/graph.hpp:14)
+# boundary-graph table storage of multi-GPU builds (psp_boundary_storage)
+STORAGE_REPLICATED = 0
+STORAGE_ROW_SHARDED = 1
 # batch density (queries per component pair c1 <= c2) rules of the query
 # launcher (must match engine_oracle.cuh): below CTA_MAX_DENSITY a batch runs
 # query_cta (one CTA per query, no sort), else the pair-grouped kernel
@@ -92,6 +95,13 @@ class Context:
     @property
     def stream(self) -> int:
         return _lib.lib().psp_gpu_ctx_stream(self.h) or 0
+
+    def set_boundary_storage(self, storage: int) -> None:
+        """STORAGE_REPLICATED (default) or STORAGE_ROW_SHARDED for later
+        multi-GPU builds (include/psp_gpu.h psp_gpu_ctx_set_boundary_storage):
+        row-sharded oracles keep ~1/world of the boundary-graph table per GPU
+        and answer through RoutedOracle only."""
+        _lib.check(_lib.lib().psp_gpu_ctx_set_boundary_storage(self.h, int(storage)))
 
     def minplus_peak(self, value_kind: int = VALUE_U32):
         r, mhz = C.c_double(), C.c_double()

@@ -133,6 +133,7 @@ SIGNATURES = {
     "psp_gpu_ctx_destroy": (None, [_vp]),
     "psp_gpu_nccl_unique_id": (C.c_int, [_vp]),
     "psp_gpu_ctx_stream": (_vp, [_vp]),
+    "psp_gpu_ctx_set_boundary_storage": (C.c_int, [_vp, C.c_int]),
     "psp_gpu_build_oracle": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
                                        C.c_uint32, C.c_uint32, C.c_uint64, C.c_int,
                                        C.POINTER(_vp), C.POINTER(BuildStats)]),
@@ -191,7 +192,7 @@ _lib = None
 
 
 # include/psp_gpu.h PSP_GPU_ABI_VERSION (struct layouts above follow it)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 def lib():

@@ -10,6 +10,7 @@ struct psp_gpu_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;  // world > 1 only
+    int storage = PSP_STORAGE_REPLICATED;  // boundary-graph table of later builds
 };
 
 namespace {
@@ -29,10 +30,13 @@ void set_kernel_attrs() {
 
 template <class V>
 void fill_arena(MatArena& a, cudaStream_t s, int sms) {
-    const uint64_t n = a.tile_elems;
-    const int blocks = int(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 32));
-    fill_value<V><<<std::max(blocks, 1), 256, 0, s>>>(a.tiles.as<V>(), n, Ops<V>::inf());
-    CK_LAUNCH();
+    for (const auto& r : a.backed_ranges()) {  // all of it unless row-sharded
+        const uint64_t n = r.second / sizeof(V);
+        const int blocks = int(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 32));
+        fill_value<V><<<std::max(blocks, 1), 256, 0, s>>>(a.tiles_as<V>() + r.first / sizeof(V), n,
+                                                          Ops<V>::inf());
+        CK_LAUNCH();
+    }
     if (a.nmat) {
         set_diag_zero<V><<<a.nmat, 256, 0, s>>>(a.view<V>());
         CK_LAUNCH();
@@ -371,7 +375,11 @@ bool p2p_setup(P2PExchange& x, psp_gpu_ctx* ctx) {
 // panel tiles whose home row it owns (others contribute INF) and one
 // min-allreduce assembles the full row panel; phase 3 then touches owned rows
 // only. At the end every row is broadcast from its owner so each GPU holds
-// the complete table (queries stay replicated, no per-query traffic).
+// the complete table (queries stay replicated, no per-query traffic) --
+// unless the arena is row-sharded storage (MatArena::part: only the owned
+// rows exist on this rank), which stays distributed for routed queries; the
+// diagonal tile of a k-block this rank does not own then goes to a scratch
+// tile (MatSet::diag) instead of its slot in the table.
 template <class V>
 void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     cudaStream_t s = ctx->stream;
@@ -383,7 +391,10 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
     const uint64_t my_work = std::max<uint64_t>(1, a.nrows ? (a.nrows * uint64_t(nb)) : 1);
     const int g3 = int(std::min<uint64_t>(my_work, uint64_t(ctx->sms)));
     const ncclDataType_t dt = nccl_type<V>();
-    V* tiles = a.tiles.as<V>();
+    V* tiles = a.tiles_as<V>();
+    const bool row_storage = a.part != nullptr;
+    DBuf diag_scratch;
+    if (row_storage) diag_scratch.alloc(TT * sizeof(V));
     // PSP_FW_PROFILE=1: per-phase CUDA-event breakdown on stderr (diagnostics)
     const bool prof = std::getenv("PSP_FW_PROFILE") != nullptr;
     const char* dm = std::getenv("PSP_DIAG_MODE");
@@ -422,9 +433,11 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
             CK_LAUNCH();
         } else {
             const unsigned char* ob = x->base[owner];
+            V* dst = diag;
+            if (row_storage) vk.diag = dst = diag_scratch.as<V>();
             pull_diag<V><<<16, 256, 0, s>>>(reinterpret_cast<const V*>(ob + L.diag_off[buf]),
                                             reinterpret_cast<const unsigned long long*>(ob + L.sync_off),
-                                            kb + 1, diag, my_sync + 7);
+                                            kb + 1, dst, my_sync + 7);
             CK_LAUNCH();
         }
         if (prof) CK(cudaEventRecord(ev[1], s));
@@ -466,7 +479,11 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
             fw_phase1<V><<<1, NTHREADS, 0, s>>>(v, kb);
             CK_LAUNCH();
         }
-        if (diag_allreduce) {
+        MatSet<V> vk = v;
+        if (row_storage && owner != ctx->rank) {
+            vk.diag = diag_scratch.as<V>();
+            NCK(nccl().Broadcast(diag, diag_scratch.p, TT, dt, owner, ctx->comm, s));
+        } else if (diag_allreduce) {
             // owners contribute the closed tile, everyone else INF
             if (owner != ctx->rank) fill_value<V><<<16, 256, 0, s>>>(diag, TT, Ops<V>::inf());
             NCK(nccl().AllReduce(diag, diag, TT, dt, ncclMin, ctx->comm, s));
@@ -475,7 +492,7 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
         }
         if (prof) CK(cudaEventRecord(ev[1], s));
         if (nb > 1) {
-            fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(v, kb);
+            fw_phase2<V><<<dim3(1, nb), NTHREADS, smem, s>>>(vk, kb);
             CK_LAUNCH();
             if (prof) CK(cudaEventRecord(ev[2], s));
             // sparse: the activity flags follow the panel slots in the same buffer
@@ -522,6 +539,10 @@ void run_fw_sharded(MatArena& a, psp_gpu_ctx* ctx) {
         NCK(nccl().AllReduce(d.p, d.p, 1, ncclUint64, ncclMax, ctx->comm, s));
         CK(cudaStreamSynchronize(s));
         x.reset();
+    }
+    if (row_storage) {
+        CK(cudaStreamSynchronize(s));  // the diagonal scratch dies here
+        return;
     }
     // replicate: row I (tiles (I, I..nb-1), contiguous) from its owner
     const uint32_t batch = 64;

@@ -27,6 +27,12 @@ struct psp_gpu_oracle {
     MatArena comps, bg;
     DBuf d_perm, d_assign, d_comp_off, d_bnd_off, d_cb_off, d_cb;
     uint64_t device_bytes = 0;
+    // PSP_STORAGE_ROW_SHARDED build (world > 1): `bg` is the K2 working
+    // matrix with only this rank's tile rows backed (MatArena::part);
+    // boundary id i sits at position d_bg_pos[i] of it. The oracle then
+    // answers through psp_gpu_shard (routed queries) only.
+    bool row_storage = false;
+    DBuf d_bg_pos;
     // grow-only staging for the host-pointer query API (one call at a time;
     // the tables themselves are read-only, src/query.cpp is re-entrant too)
     std::mutex query_mu;
@@ -75,6 +81,15 @@ struct psp_gpu_oracle {
 };
 
 namespace {
+
+// Operations that read the whole boundary-graph table from this GPU.
+void require_replicated(const psp_gpu_oracle* o, const char* what) {
+    if (o->row_storage)
+        throw ArgError(std::string(what) +
+                       ": the boundary-graph table is row-sharded over the ranks "
+                       "(PSP_STORAGE_ROW_SHARDED); query through psp_gpu_shard_create + "
+                       "psp_gpu_routed_query_batch");
+}
 
 struct EdgeLists {
     std::vector<uint32_t> mat, ii, jj;  // intra-component (local ids)
@@ -413,7 +428,16 @@ bool choose_bg_order(const psp_gpu_oracle* o, const BgPlan& plan, std::vector<ui
         const uint64_t nb = (n + T - 1) / T;
         return ntiles_upper(uint32_t(nb)) * TT * sizeof(V);
     };
-    auto need = [&](uint64_t n) { return table_bytes(n) + ((n + T - 1) / T + 1) * TT * sizeof(V) + table_bytes(b) + (2ull << 30); };
+    // row-sharded storage: this rank's rows of the working matrix only, no
+    // table in reference numbering (the shard gathers from the working one)
+    const bool rows_only = o->row_storage;
+    const uint64_t G = uint64_t(o->ctx->world);
+    auto need = [&](uint64_t n) {
+        if (rows_only)
+            return table_bytes(n) / G + table_bytes(n) / (G * 8) + ((n + T - 1) / T + 1) * TT * sizeof(V) +
+                   (2ull << 30);
+        return table_bytes(n) + ((n + T - 1) / T + 1) * TT * sizeof(V) + table_bytes(b) + (2ull << 30);
+    };
     if (!plan.use) return false;
     const std::vector<uint32_t>& unit = plan.unit;
     const std::vector<uint64_t>& bsize = plan.bsize;
@@ -439,11 +463,11 @@ bool choose_bg_order(const psp_gpu_oracle* o, const BgPlan& plan, std::vector<ui
         npos = bg_pack(ord.order, bsize, 1, 0, start);  // contiguous
     }
     if (need(npos) > free_b) {
-        if (need(npos) > free_b + parked || !host_room) return false;
+        if (rows_only || need(npos) > free_b + parked || !host_room) return false;
         spill = true;
     }
     // PSP_K2_FORCE_SPILL=1 (tests): take the spill path on any size
-    if (std::getenv("PSP_K2_FORCE_SPILL")) spill = true;
+    if (std::getenv("PSP_K2_FORCE_SPILL") && !rows_only) spill = true;
     if (std::getenv("PSP_FW_PROFILE"))
         std::fprintf(stderr, "[psp] K2 layout: %llu positions for %llu boundary vertices%s\n",
                      (unsigned long long)npos, (unsigned long long)b, spill ? " (component tables off the device during K2)" : "");
@@ -723,7 +747,8 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         k2_npos = permuted ? npos : b;
         k2_permuted = permuted;
         k2_spill = spill;
-        o->bg.create({permuted ? npos : b}, sizeof(V), true, s);
+        const int row_shard[3] = {ctx->device, ctx->rank, ctx->world};
+        o->bg.create({permuted ? npos : b}, sizeof(V), true, s, -1, o->row_storage ? row_shard : nullptr);
         if (std::getenv("PSP_FW_PROFILE"))
             std::fprintf(stderr, "[psp] boundary phase: order chosen at %.1f ms\n", ms_since(t0));
         if (!permuted) {
@@ -788,7 +813,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         // allocation stalls inside the K2 window) unless the component
         // tables must leave the device first
         MatArena ref;
-        if (permuted && !spill) ref.create({b}, sizeof(V), false, s);
+        if (permuted && !spill && !o->row_storage) ref.create({b}, sizeof(V), false, s);
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
@@ -799,7 +824,13 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             if (park_fail.st != PSP_OK) throw park_fail;
             o->comps.tiles.reset();
         }
-        if (permuted) {
+        if (o->row_storage) {
+            // the working matrix stays distributed (rows of this rank), with
+            // its position map, for psp_gpu_shard_create to gather from
+            t_k2.stop(s);
+            o->bg.panel.reset();
+            o->d_bg_pos = std::move(d_pos);
+        } else if (permuted) {
             const double p0 = ms_since(t0);
             if (spill) {
                 o->bg.panel.reset();
@@ -847,7 +878,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                              "at %.0f ms, copy back %.0f ms (boundary phase so far %.0f ms)\n",
                              parked_bytes / 1e9, fw_done_ms, ms_since(t0) - back0, ms_since(t0));
         }
-        if (!permuted || spill) t_k2.stop(s);
+        if (!o->row_storage && (!permuted || spill)) t_k2.stop(s);
         CK(cudaStreamSynchronize(s));
         k2_ms = t_k2.ms();
         if (std::getenv("PSP_FW_PROFILE"))
@@ -865,8 +896,10 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     // panels are build-time scratch
     o->comps.panel.reset();
     o->bg.panel.reset();
-    build_query_blocks<V>(o, s);
-    build_query_blocks16(o, s);
+    if (!o->row_storage) {  // replicated queries only
+        build_query_blocks<V>(o, s);
+        build_query_blocks16(o, s);
+    }
     const double boundary_ms = ms_since(t0);
 
     o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->d_cb_off.bytes +
@@ -999,6 +1032,7 @@ psp_gpu_oracle* build_from_csr(psp_gpu_ctx* ctx, const Csr& g, uint32_t k,
         st->partition_ms = partition_ms + ms_since(t0);
     }
     CK(cudaSetDevice(ctx->device));
+    o->row_storage = ctx->storage == PSP_STORAGE_ROW_SHARDED && ctx->world > 1;
     if (o->kind.kind == PSP_VALUE_U32) device_build<uint32_t>(o.get(), st);
     else device_build<float>(o.get(), st);
     return o.release();

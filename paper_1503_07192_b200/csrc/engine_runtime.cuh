@@ -397,6 +397,154 @@ inline void staged_copy(void* dst, const void* src, size_t bytes, bool to_host, 
         if (f.st != PSP_OK) throw f;
 }
 
+// ------------------------------------------------- partially backed range --
+// One contiguous virtual range of which only chosen byte ranges own device
+// memory (CUDA virtual memory management; driver entry points fetched through
+// the runtime, no -lcuda). The rest maps, in pieces, onto one small shared
+// "sink" allocation: kernels may then address the whole range as one array
+// and write anywhere (initialisation passes that sweep every tile), while
+// only the backed ranges hold data. Readers must stay inside backed ranges.
+// Used for the row-sharded boundary-graph table (PSP_STORAGE_ROW_SHARDED):
+// rank r backs the tile rows it owns, about 1/world of the table.
+struct VmmApi {
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) set_access = nullptr;
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    bool ok = false;
+};
+const VmmApi& vmm_api() {
+    static VmmApi a = [] {
+        VmmApi v;
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q{};
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn;
+        };
+        v.ok = get("cuMemAddressReserve", reinterpret_cast<void**>(&v.reserve)) &&
+               get("cuMemAddressFree", reinterpret_cast<void**>(&v.addr_free)) &&
+               get("cuMemCreate", reinterpret_cast<void**>(&v.create)) &&
+               get("cuMemRelease", reinterpret_cast<void**>(&v.release)) &&
+               get("cuMemMap", reinterpret_cast<void**>(&v.map)) &&
+               get("cuMemUnmap", reinterpret_cast<void**>(&v.unmap)) &&
+               get("cuMemSetAccess", reinterpret_cast<void**>(&v.set_access)) &&
+               get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&v.granularity));
+        cudaGetLastError();
+        return v;
+    }();
+    return a;
+}
+
+struct PartialRange {
+    CUdeviceptr va = 0;
+    size_t size = 0, gran = 0, backed = 0, sink_bytes = 0;
+    std::vector<std::pair<size_t, size_t>> maps;   // (offset, length) of every mapping
+    std::vector<std::pair<size_t, size_t>> owned;  // backed byte ranges (granule-aligned)
+    // cuMemMap maps whole allocations only (offset 0, full size): one
+    // allocation per backed run, and sinks of power-of-two granule counts,
+    // each mapped wherever a piece of its size falls in the unbacked gaps
+    std::vector<CUmemGenericAllocationHandle> runs;
+    std::map<size_t, CUmemGenericAllocationHandle> sinks;
+
+    PartialRange() = default;
+    PartialRange(const PartialRange&) = delete;
+    PartialRange& operator=(const PartialRange&) = delete;
+    ~PartialRange() { reset(); }
+
+    static void dck(CUresult r, const char* what) {
+        if (r != CUDA_SUCCESS)
+            throw Fail{r == CUDA_ERROR_OUT_OF_MEMORY ? PSP_ENOMEM : PSP_ECUDA,
+                       std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")"};
+    }
+    // `want`: byte ranges that must hold data (any order, may overlap)
+    void create(int device, size_t bytes, std::vector<std::pair<size_t, size_t>> want) {
+        reset();
+        const VmmApi& api = vmm_api();
+        if (!api.ok) throw Fail{PSP_ECUDA, "CUDA virtual memory management entry points unavailable"};
+        CUmemAllocationProp prop{};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = device;
+        dck(api.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+        size = std::max(gran, (bytes + gran - 1) / gran * gran);
+        // granule-aligned, merged ranges
+        for (auto& w : want) {
+            const size_t a = w.first / gran * gran;
+            const size_t b = std::min(size, (w.first + w.second + gran - 1) / gran * gran);
+            if (b > a) owned.emplace_back(a, b - a);
+        }
+        std::sort(owned.begin(), owned.end());
+        std::vector<std::pair<size_t, size_t>> merged;
+        for (auto& r : owned) {
+            if (!merged.empty() && r.first <= merged.back().first + merged.back().second)
+                merged.back().second = std::max(merged.back().first + merged.back().second,
+                                                r.first + r.second) - merged.back().first;
+            else merged.push_back(r);
+        }
+        owned.swap(merged);
+        for (auto& r : owned) backed += r.second;
+        const size_t max_sink = std::max(gran, size_t(64) << 20);
+        try {
+            dck(api.reserve(&va, size, gran, 0, 0), "cuMemAddressReserve");
+            auto map_sink = [&](size_t from, size_t to) {
+                for (size_t o = from; o < to;) {
+                    size_t len = gran;  // largest power-of-two granule count that fits
+                    while (len * 2 <= std::min(max_sink, to - o)) len *= 2;
+                    auto it = sinks.find(len);
+                    if (it == sinks.end()) {
+                        CUmemGenericAllocationHandle h = 0;
+                        dck(api.create(&h, len, &prop, 0), "cuMemCreate(sink)");
+                        it = sinks.emplace(len, h).first;
+                        sink_bytes += len;
+                    }
+                    dck(api.map(va + o, len, 0, it->second, 0), "cuMemMap(sink)");
+                    maps.emplace_back(o, len);
+                    o += len;
+                }
+            };
+            size_t at = 0;
+            for (auto& r : owned) {
+                map_sink(at, r.first);
+                CUmemGenericAllocationHandle h = 0;
+                dck(api.create(&h, r.second, &prop, 0), "cuMemCreate(table rows)");
+                runs.push_back(h);
+                dck(api.map(va + r.first, r.second, 0, h, 0), "cuMemMap(rows)");
+                maps.emplace_back(r.first, r.second);
+                at = r.first + r.second;
+            }
+            map_sink(at, size);
+            CUmemAccessDesc acc{};
+            acc.location = prop.location;
+            acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+            dck(api.set_access(va, size, &acc, 1), "cuMemSetAccess");
+        } catch (...) {
+            reset();
+            throw;
+        }
+    }
+    void reset() {
+        const VmmApi& api = vmm_api();
+        if (va) {
+            cudaDeviceSynchronize();  // as cudaFree would
+            for (auto& m : maps) api.unmap(va + m.first, m.second);
+            api.addr_free(va, size);
+        }
+        for (auto h : runs) api.release(h);
+        for (auto& kv : sinks) api.release(kv.second);
+        va = 0;
+        runs.clear();
+        sinks.clear();
+        size = backed = sink_bytes = 0;
+        maps.clear();
+        owned.clear();
+    }
+    void* ptr() const { return reinterpret_cast<void*>(va); }
+};
+
 // A batch of symmetric tile-packed matrices (see minplus.cuh).
 struct MatArena {
     uint32_t nmat = 0, nb_max = 0;
@@ -416,6 +564,11 @@ struct MatArena {
     DBuf d_act;
     uint64_t walked_tiles = 0;
     uint64_t nslots = 0;  // sum of nb over the matrices (= panel slots)
+    // row-sharded storage (a single matrix over `world` ranks): only the
+    // tile rows I with I mod world == rank are backed by device memory
+    std::unique_ptr<PartialRange> part;
+    void* tiles_p() const { return part ? part->ptr() : tiles.p; }
+    template <class V> V* tiles_as() const { return static_cast<V*>(tiles_p()); }
 
     void shard_rows(uint32_t r, uint32_t g, cudaStream_t s) {
         rank = r;
@@ -433,8 +586,10 @@ struct MatArena {
 
     // sparse_walk: -1 = the default (a single matrix, i.e. the boundary
     // graph), 0 / 1 = off / on for a batch of matrices
+    // row_shard = {device, rank, world}: back only this rank's tile rows
+    // (nmat == 1, see PartialRange); nullptr = one ordinary allocation
     void create(const std::vector<uint64_t>& sizes, size_t value_bytes, bool with_panel,
-                cudaStream_t s, int sparse_walk = -1) {
+                cudaStream_t s, int sparse_walk = -1, const int* row_shard = nullptr) {
         vbytes = value_bytes;
         nmat = static_cast<uint32_t>(sizes.size());
         nb.resize(nmat);
@@ -453,7 +608,18 @@ struct MatArena {
             work_prefix[m + 1] = work_prefix[m] + ntiles_upper(nb[m]);
         }
         nslots = panel_elems / TT;
-        tiles.alloc(tile_elems * vbytes);
+        part.reset();
+        tiles.reset();
+        if (row_shard && nmat == 1) {
+            const uint32_t r = uint32_t(row_shard[1]), g = uint32_t(row_shard[2]);
+            std::vector<std::pair<size_t, size_t>> rows;
+            for (uint32_t I = r; I < nb[0]; I += g)
+                rows.emplace_back(tidx(I, I, nb[0]) * TT * vbytes, uint64_t(nb[0] - I) * TT * vbytes);
+            part = std::make_unique<PartialRange>();
+            part->create(row_shard[0], tile_elems * vbytes, rows);
+        } else {
+            tiles.alloc(tile_elems * vbytes);
+        }
         sparse = with_panel && nb_max > 1 && std::getenv("PSP_FW_DENSE") == nullptr &&
                  (sparse_walk < 0 ? nmat == 1 : sparse_walk > 0);
         if (with_panel) panel.alloc((panel_elems + (sparse ? nslots : 0)) * vbytes);
@@ -465,7 +631,8 @@ struct MatArena {
     }
     template <class V> MatSet<V> view() const {
         MatSet<V> v;
-        v.tiles = tiles.as<V>();
+        v.tiles = tiles_as<V>();
+        v.diag = nullptr;
         v.panel = panel.as<V>();
         v.tile_base = d_tile_base.as<uint64_t>();
         v.panel_base = d_panel_base.as<uint64_t>();
@@ -503,7 +670,14 @@ struct MatArena {
         for (uint32_t m = 0; m < nmat; ++m) r += ntiles_upper(nb[m]) * nb[m];
         return r * uint64_t(T) * T * T;
     }
-    size_t bytes() const { return tiles.bytes + panel.bytes; }
+    size_t bytes() const {
+        return (part ? part->backed + part->sink_bytes : tiles.bytes) + panel.bytes;
+    }
+    // backed byte ranges of the tile storage (all of it when not row-sharded)
+    std::vector<std::pair<size_t, size_t>> backed_ranges() const {
+        if (part) return part->owned;
+        return {{0, tile_elems * vbytes}};
+    }
 };
 
 }  // namespace

@@ -56,6 +56,31 @@ __global__ void gather_bt_rows(const V* __restrict__ bg, uint32_t nb, uint64_t b
     }
 }
 
+// Row-sharded storage (psp_gpu_oracle::row_storage): rows `row_gid`
+// (boundary ids) of the full table as far as this rank holds them -- element
+// (p, q) of the K2 working matrix lives in tile row min(p, q) / T, owned by
+// rank (that row mod world) -- and INF elsewhere. The destination rank
+// min-reduces every rank's part (ncclReduce), so each element arrives from
+// exactly the rank that holds it. grid: (column blocks, rows).
+template <class V>
+__global__ void gather_bt_part(const V* __restrict__ W, uint32_t nbW, const uint32_t* __restrict__ pos,
+                               uint32_t rank, uint32_t world, uint64_t b,
+                               const uint32_t* __restrict__ row_gid, uint64_t stride,
+                               V* __restrict__ out) {
+    const uint64_t r = blockIdx.y;
+    const uint32_t p = pos[row_gid[r]];
+    V* dst = out + r * stride;
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < stride;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        V v = Ops<V>::inf();
+        if (j < b) {
+            const uint32_t q = pos[j];
+            if ((min(p, q) / T) % world == rank) v = W[sym_off(p, q, nbW)];
+        }
+        dst[j] = v;
+    }
+}
+
 struct RouteView {
     const uint32_t* perm;
     const uint32_t* assign;
@@ -184,9 +209,42 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
     sh->bt_rows = gid.size();
     sh->d_bt_row0 = upload(row0, s);
     sh->d_bt.alloc(sh->bt_rows * sh->bt_stride * vb);
-    if (sh->bt_rows && o->bg.nmat) {
+    if (o->row_storage) {
+        // the table is spread over the ranks by tile row: every rank sends
+        // its part of each destination's rows, min-reduced at the destination
+        // (rank order, destination rows in chunks of <= 256 MB)
+        auto& api = pspg::nccl();
+        const uint64_t row_bytes = sh->bt_stride * vb;
+        const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(65535, (256ull << 20) / row_bytes));
+        std::vector<uint32_t> all_gid;
+        std::vector<uint64_t> dst_off(ctx->world + 1, 0);
+        for (int d = 0; d < ctx->world; ++d) {
+            for (uint32_t c = 0; c < k; ++c)
+                if (sh->owner[c] == uint32_t(d))
+                    for (uint32_t t = R.bnd_off[c]; t < R.bnd_off[c + 1]; ++t) all_gid.push_back(t);
+            dst_off[d + 1] = all_gid.size();
+        }
+        DBuf d_all = upload(all_gid, s);
+        DBuf stage(std::min<uint64_t>(per, std::max<uint64_t>(1, all_gid.size())) * row_bytes);
+        const ncclDataType_t dt = std::is_same<V, float>::value ? ncclFloat32 : ncclUint32;
+        const unsigned gx = unsigned(std::min<uint64_t>(8, (sh->bt_stride + 1023) / 1024));
+        for (int d = 0; d < ctx->world; ++d) {
+            for (uint64_t r0 = dst_off[d]; r0 < dst_off[d + 1]; r0 += per) {
+                const uint64_t nr = std::min<uint64_t>(per, dst_off[d + 1] - r0);
+                gather_bt_part<V><<<dim3(gx, unsigned(nr)), 1024, 0, s>>>(
+                    o->bg.tiles_as<V>(), o->bg.nb[0], o->d_bg_pos.as<uint32_t>(), me,
+                    uint32_t(ctx->world), sh->b, d_all.as<uint32_t>() + r0, sh->bt_stride,
+                    stage.as<V>());
+                CK_LAUNCH();
+                V* recv = d == int(me) ? sh->d_bt.as<V>() + (r0 - dst_off[d]) * sh->bt_stride : stage.as<V>();
+                nccl_check(api.Reduce(stage.p, recv, nr * sh->bt_stride, dt, ncclMin, d, ctx->comm, s),
+                           "ncclReduce(boundary rows)");
+            }
+        }
+        CK(cudaStreamSynchronize(s));  // d_all and stage die here
+    } else if (sh->bt_rows && o->bg.nmat) {
         DBuf d_gid = upload(gid, s);
-        gather_bt_rows<V><<<ctx->sms * 8, 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0], sh->b,
+        gather_bt_rows<V><<<ctx->sms * 8, 256, 0, s>>>(o->bg.tiles_as<V>(), o->bg.nb[0], sh->b,
                                                        d_gid.as<uint32_t>(), sh->bt_rows,
                                                        sh->bt_stride, sh->d_bt.as<V>());
         CK_LAUNCH();

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fw_phase2(MatSet<V> ms, uint32_t 
     __shared__ uint64_t bar;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     V* base = ms.tiles + ms.tile_base[m];
-    const V* diag = base + tidx(kb, kb, nb) * TT;
+    const V* diag = ms.diag ? ms.diag : base + tidx(kb, kb, nb) * TT;
     V* panel = ms.panel + ms.panel_base[m] + uint64_t(J) * TT;
     const bool upper = J > kb;
     V* home = base + (upper ? tidx(kb, J, nb) : tidx(J, kb, nb)) * TT;

@@ -109,6 +109,10 @@ template <class V> struct MatSet {
     // leaves the slots other ranks compute untouched (they are pulled over
     // NVLink instead of min-allreduced)
     uint32_t p2p;
+    // the closed diagonal tile of the current k-block when it is not in this
+    // rank's storage (row-sharded table, pulled from its owner); null: the
+    // matrix's own tile (kb, kb)
+    const V* diag;
     // sparse walk (null: dense). Per k-block phase 2 writes act_flag[s + J]
     // (s = panel_base[m] / TT, matrix m's first panel slot; V-typed so the
     // sharded build min-allreduces it with the panel: 0 = panel slot J holds

@@ -25,6 +25,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -141,6 +142,18 @@ psp_status psp_gpu_nccl_unique_id(void* out128) {
 
 void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
+psp_status psp_gpu_ctx_set_boundary_storage(psp_gpu_ctx* ctx, int storage) {
+    return guarded([&] {
+        if (!ctx) throw ArgError("ctx_set_boundary_storage: NULL ctx");
+        if (storage != PSP_STORAGE_REPLICATED && storage != PSP_STORAGE_ROW_SHARDED)
+            throw ArgError("ctx_set_boundary_storage: storage must be PSP_STORAGE_REPLICATED or "
+                           "PSP_STORAGE_ROW_SHARDED");
+        if (storage == PSP_STORAGE_ROW_SHARDED && !vmm_api().ok)
+            throw Fail{PSP_ECUDA, "ctx_set_boundary_storage: CUDA virtual memory management unavailable"};
+        ctx->storage = storage;
+    });
+}
+
 psp_status psp_gpu_build_oracle(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* eu,
                                 const uint32_t* ev, const double* ew, uint32_t k,
                                 uint32_t workers, uint64_t seed, int value_kind,
@@ -238,6 +251,7 @@ psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
 psp_status psp_gpu_oracle_save(const psp_gpu_oracle* o, const char* path) {
     return guarded([&] {
         if (!o || !path) throw ArgError("oracle_save: NULL argument");
+        require_replicated(o, "oracle_save");
         CK(cudaSetDevice(o->ctx->device));
         const Reordered& R = o->R;
         std::FILE* f = std::fopen(path, "wb");
@@ -445,6 +459,7 @@ psp_status psp_gpu_export_boundary_rows(const psp_gpu_oracle* o, uint32_t c, dou
     return guarded([&] {
         if (!o || !dst) throw ArgError("export_boundary_rows: NULL argument");
         if (c >= o->R.k) throw ArgError("export_boundary_rows: component out of range");
+        require_replicated(o, "export_boundary_rows");
         const uint32_t g = o->R.bnd_off[c], B = o->R.bnd_off[c + 1] - g;
         const uint32_t b = static_cast<uint32_t>(o->R.b());
         if (B == 0 || b == 0) return;
@@ -457,6 +472,7 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
                                const uint32_t* v2, double* dist, uint64_t* minplus_ops) {
     return guarded([&] {
         if (!o) throw ArgError("query_batch: NULL oracle");
+        require_replicated(o, "query_batch");
         if (count == 0) return;
         if (!v1 || !v2 || !dist) throw ArgError("query_batch: NULL array");
         const Reordered& R = o->R;
@@ -547,6 +563,7 @@ psp_status psp_gpu_query_pipe_create(const psp_gpu_oracle* o, int depth, psp_gpu
     return guarded([&] {
         if (!o || !out) throw ArgError("query_pipe_create: NULL argument");
         if (depth < 1 || depth > 64) throw ArgError("query_pipe_create: depth must be in 1..64");
+        require_replicated(o, "query_pipe_create");
         CK(cudaSetDevice(o->ctx->device));
         auto p = std::make_unique<psp_gpu_query_pipe>();
         p->o = o;
@@ -624,6 +641,7 @@ psp_status psp_gpu_query_batch_device(const psp_gpu_oracle* o, uint64_t count,
                                       void* stream) {
     return guarded([&] {
         if (!o) throw ArgError("query_batch_device: NULL oracle");
+        require_replicated(o, "query_batch_device");
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : o->ctx->stream;
         CK(cudaSetDevice(o->ctx->device));
         // concurrent callers: the enqueue (workspace lookup and growth) is

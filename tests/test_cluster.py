@@ -3,6 +3,7 @@ the host mirrors against the reference build, the reference's own
 test_cluster.cpp cases restated, and (GPU) routed_query / the sharded
 RoutedOracle against the reference's routed_query and ClusterSim."""
 import io
+import json
 import os
 import subprocess
 import sys
@@ -189,3 +190,30 @@ def test_routed_oracle_multi_rank():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "routed_check: ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_row_sharded_storage_full_size():
+    """STORAGE_ROW_SHARDED at configs[1] size on 2-4 ranks: each rank keeps
+    ~1/world of the boundary-graph table, RoutedOracle gathers its rows, and
+    routed distances equal f64 Dijkstra (tools/row_storage_check.py)."""
+    n = P._lib.lib().psp_gpu_device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={min(n, 4)}", "--master-addr=127.0.0.1",
+                        "--master-port=29534", os.path.join(ROOT, "tools", "row_storage_check.py"),
+                        "--config", "delaunay262k_k256"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "row_storage_check: ok" in r.stdout
+    line = json.loads(next(x for x in r.stdout.splitlines() if x.startswith("{")))
+    world = line["world"]
+    for owned in line["owned_row_bytes_per_rank"]:
+        assert owned <= line["table_bytes"] / world * 1.05
+
+
+def test_set_boundary_storage_rejects_bad_values():
+    # host-side argument check, no GPU needed: a NULL context is refused first
+    L = P._lib.lib()
+    assert L.psp_gpu_ctx_set_boundary_storage(None, P.STORAGE_ROW_SHARDED) == P._lib.PSP_EINVAL

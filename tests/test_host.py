@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(L, s), s
     # and the Python binding covers exactly that surface
     assert set(syms) == set(_lib.SIGNATURES)
-    assert L.psp_gpu_abi_version() == 4
+    assert L.psp_gpu_abi_version() == 5
 
 
 def test_no_gpu_fails_loudly_or_works():

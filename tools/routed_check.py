@@ -9,7 +9,13 @@ owner(C2)'s GPU over NVLink. Checks, per policy:
      ClusterSim's (tests/golden/ref_cluster_cfg1.npz, p = world);
   B. every rank submits its own random pairs on a 30k-vertex Delaunay graph:
      distances bit-equal to the replicated oracle's batch_query;
-  C. an out-of-range id on the last rank fails the batch on every rank.
+  C. an out-of-range id on the last rank fails the batch on every rank;
+  D. row-sharded storage (STORAGE_ROW_SHARDED): the same graphs built with
+     only each rank's tile rows of the boundary-graph table on its GPU (the
+     Delaunay one also with the tile-packed K2 layout forced); replicated
+     queries are refused and RoutedOracle answers A's and B's pairs bit-equal
+     to the replicated oracle. (Tables this small fit in a few 2 MB granules,
+     so the memory share is checked at full size: tools/row_storage_check.py.)
 Prints "routed_check: ok" on rank 0 when every rank passed.
 """
 import os
@@ -89,6 +95,49 @@ def main():
         except ValueError:
             pass
         rd.close()
+
+    # D: row-sharded boundary-graph storage
+    ctx.set_boundary_storage(P.STORAGE_ROW_SHARDED)
+    want_a = o.batch_query(zc["v1"], zc["v2"])
+    rep_bytes = od.stats["device_bytes"]
+    for force_pack in (False, True):
+        if force_pack:
+            os.environ["PSP_BG_PACK"] = "force"
+        os_ = P.build_oracle(g, 16, 4, 0, ctx=ctx)
+        ods = P.build_oracle(gd, 173, 4, 0, ctx=ctx)
+        os.environ.pop("PSP_BG_PACK", None)
+        tag = "D/packed" if force_pack else "D"
+        try:
+            ods.batch_query(v1[:10], v2[:10])
+            fails.append(f"{tag}: replicated query on a row-sharded oracle not refused")
+        except ValueError:
+            pass
+        st = ods.stats
+        nb = (st["k2_positions"] + 127) // 128
+        table = nb * (nb + 1) // 2 * 128 * 128 * 4
+        rows = range(rank, nb, world)
+        mine_bytes = sum((nb - I) * 128 * 128 * 4 for I in rows)
+        print(f"rank {rank}/{world} {tag}: table {table / 1e6:.1f} MB, owned rows {mine_bytes / 1e6:.1f} MB, "
+              f"oracle device bytes {st['device_bytes'] / 1e6:.1f} MB (replicated {rep_bytes / 1e6:.1f} MB), "
+              f"k2 positions {st['k2_positions']} order {st['k2_order']}", flush=True)
+        if force_pack and not (st["k2_order"] == 1 and st["k2_positions"] > ods.b):
+            fails.append(f"{tag}: tile-packed layout not taken ({st['k2_positions']} positions)")
+        for pol_i, policy in ((0, P.ROUND_ROBIN), (1, P.PAIRS_PER_GPU)):
+            ro = P.RoutedOracle(os_, P.place_components(16, world, policy))
+            mine = (zc["v1"], zc["v2"]) if rank == 0 else (np.empty(0, np.uint32),) * 2
+            d = ro.run_batch(*mine)
+            if rank == 0 and not np.array_equal(d, want_a):
+                fails.append(f"{tag}/A/{policy}: distances differ from the replicated oracle")
+            ro.close()
+            rd = P.RoutedOracle(ods, P.place_components(173, world, policy))
+            got = rd.run_batch(v1, v2)
+            if not np.array_equal(got, want_d):
+                bad = np.nonzero(got != want_d)[0]
+                fails.append(f"{tag}/B/{policy}: {len(bad)} distances differ, first {bad[:3]}")
+            rd.close()
+        os_.close()
+        ods.close()
+    ctx.set_boundary_storage(P.STORAGE_REPLICATED)
 
     ok = torch.tensor([0 if fails else 1])
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
