@@ -1130,11 +1130,27 @@ __device__ __forceinline__ void rb_combine_v(int v, const V (&acc)[32], const V*
     }
 }
 
+// A task's per-lane query metadata (lane < m): id, l1 and l2 in sorted
+// order, loaded one task ahead (TaskMeta::load inside the previous task) so
+// the task start does not wait on them.
+struct TaskMeta {
+    uint32_t id = 0, l1 = 0, l2 = 0;
+    __device__ __forceinline__ void load(const GroupWork& w, const uint4& rec, int lane) {
+        const uint32_t q0 = rec.z, m = rec.w & 0x3fu;
+        if (uint32_t(lane) < m) {
+            id = w.sorted[q0 + lane];
+            l1 = w.s_l1[q0 + lane];
+            l2 = w.s_l2[q0 + lane];
+        }
+    }
+};
+
 template <class V, bool ALT>
 __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const GroupWork& w,
                                               WarpStage<V>* st, uint32_t c1, uint32_t c2,
                                               uint32_t q0, uint32_t m, uint32_t cg, bool half,
-                                              uint32_t& phase) {
+                                              uint32_t& phase, const TaskMeta& me,
+                                              const uint4& rec_next, TaskMeta& me_next) {
     const int lane = threadIdx.x & 31;
     // variant and its column-slot count (NCS lanes share a query)
     int v, ncs;
@@ -1148,12 +1164,13 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
     const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
     const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
     const V* bq_task = q.bq + q.bq_off[c1 * q.k + c2] + uint64_t(cg) * ((B1 + GK - 1) / GK * GK) * 32;
+    (void)q0;
     __syncwarp();
     const V* my_row1 = cb1;
     if (uint32_t(lane) < m) {
-        st->id[lane] = w.sorted[q0 + lane];
-        st->c2off[lane] = w.s_l2[q0 + lane] * Bp2 + cg * 32;
-        my_row1 = cb1 + uint64_t(w.s_l1[q0 + lane]) * Bp1;
+        st->id[lane] = me.id;
+        st->c2off[lane] = me.l2 * Bp2 + cg * 32;
+        my_row1 = cb1 + uint64_t(me.l1) * Bp1;
     }
     __syncwarp();
     // col2: chunk u (4 columns) of query qq -> st->c2[qq * 32 + 4 * (u ^ (qq & 7))];
@@ -1187,6 +1204,8 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
 #pragma unroll
     for (int i = 0; i < 32; ++i) acc[i] = Ops<V>::inf();
     if (B1 > 0) issue(0, 0);
+    // the next task's metadata, in flight while this task computes
+    me_next.load(w, rec_next, lane);
     int buf = 0;
     for (uint32_t k0 = 0; k0 < B1; k0 += GK) {
         const bool more = k0 + GK < B1;
@@ -1480,6 +1499,32 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
     uint32_t* const queue = w.task_cnt + w.nbins;
     const bool lead = (threadIdx.x & 31) == 0;
     uint32_t task = blockIdx.x * GWARPS + (threadIdx.x >> 5);
+    if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {
+        // two tasks ahead: the atomic for task t + 2 and the descriptor and
+        // per-lane metadata of task t + 1 are in flight while task t runs
+        const int lane = threadIdx.x & 31;
+        uint32_t nxt = 0;
+        if (lead) nxt = atomicAdd(queue, 1u) + nwarps;
+        uint4 rec = task < total ? w.tasks[task] : make_uint4(0, 0, 0, 0);
+        TaskMeta me;
+        me.load(w, rec, lane);
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        while (task < total) {
+            uint32_t nn = 0;
+            if (lead) nn = atomicAdd(queue, 1u) + nwarps;
+            const uint4 rec_next = nxt < total ? w.tasks[nxt] : make_uint4(0, 0, 0, 0);
+            TaskMeta me_next;
+            const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0x3fu, cg = rec.w >> 8;
+            const bool half = (rec.w >> 6) & 1u;
+            group_task_rb<V, MODE == QM_BLOCKS_8X8>(q, w, st, c1, c2, q0, m, cg, half, phase, me,
+                                                    rec_next, me_next);
+            task = nxt;
+            rec = rec_next;
+            me = me_next;
+            nxt = __shfl_sync(0xffffffffu, nn, 0);
+        }
+        return;
+    }
     while (task < total) {
         uint32_t next = 0;
         if (lead) next = atomicAdd(queue, 1u) + nwarps;
@@ -1492,8 +1537,6 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
         // kernel past the instruction cache), 24 slots for the lane product
         if constexpr (MODE == QM_BLOCKS16) {  // 16-bit residual product (u32 tables)
             group_task_rb16<V>(q, w, st, c1, c2, q0, m, cg, half, phase);
-        } else if constexpr (MODE == QM_BLOCKS || MODE == QM_BLOCKS_8X8) {  // register-blocked product
-            group_task_rb<V, MODE == QM_BLOCKS_8X8>(q, w, st, c1, c2, q0, m, cg, half, phase);
         } else {
             constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
             if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
