@@ -47,7 +47,7 @@ STORAGE_ROW_SHARDED = 1
 # query_cta (one CTA per query, no sort), else the pair-grouped kernel
 GROUP_MIN_DENSITY = 0.0
 CTA_MAX_DENSITY = 0.0
-CTA_MAX_COUNT = 2048         # batches up to this size: query_cta (one launch)
+CTA_MAX_COUNT = 16384        # batches up to this size: query_cta (one launch)
 SPARSE_GROUPING_RATIO = 4    # grouped batches with count * 4 < k^2 ...
 SPARSE_GROUPING_MIN_BINS = 1 << 24  # ... and k^2 >= 2^24: radix-sort grouping
 

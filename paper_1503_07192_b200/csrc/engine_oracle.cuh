@@ -1260,10 +1260,11 @@ void launch_grouped(GroupWorkspace& gw, const std::vector<uint32_t>& bnd_off, in
 // CTA_MAX_DENSITY: measured crossover (profiles/bench/r2_query_kernel_sweep).
 constexpr double GROUP_MIN_DENSITY = 0.0;
 constexpr double CTA_MAX_DENSITY = 0.0;
-// tiny batches: one launch, no sort (measured on cfg3, block layout:
-// query_cta 24.3 vs query_grouped 12.5 M queries/s at 1K pairs, 24.5 vs 27.4
-// at 3K; profiles/r2/query_sweep_cfg3_cta_blocks.jsonl)
-constexpr uint64_t CTA_MAX_COUNT = 2048;
+// small batches: one launch, no sort (measured on cfg3, block layout, 16-warp
+// query_cta: 44.3 vs query_grouped 11.8 M queries/s at 1K pairs, 50.4 vs 47.5
+// at 10K, 55.4 vs 62.6 at 30K; profiles/r2/query_cta_shapes_cfg3.jsonl,
+// profiles/r2/query_sweep_cfg3_cta_blocks.jsonl)
+constexpr uint64_t CTA_MAX_COUNT = 16384;
 
 template <class V>
 QueryView<V> query_view(const psp_gpu_oracle* o, uint32_t* bad_id) {
@@ -1311,7 +1312,8 @@ void launch_queries(const psp_gpu_oracle* o, uint64_t count, const uint32_t* v1,
     if (force && std::strcmp(force, "cta") == 0) cta = true;
     if (cta) {
         const unsigned blocks = unsigned(std::min<uint64_t>(count, uint64_t(o->ctx->sms) * 8));
-        query_cta<V><<<blocks, 32 * QC_WARPS, 0, s>>>(q, v1, v2, count, dist);
+        query_cta<V, QC_BATCH_WARPS, 4, QC_BATCH_MINB><<<blocks, 32 * QC_BATCH_WARPS, 0, s>>>(
+            q, v1, v2, count, dist);
         CK_LAUNCH();
         return;
     }

@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
 }
 
 // ------------------------------------------- small batches: CTA/query --
-// One CTA (QC_WARPS warps) per query, for batches far smaller than k^2 (no
+// One CTA (QC_WARPS warps; QC_BATCH_WARPS for batches, below) per query, for
+// batches far smaller than k^2 (no
 // pair reuse to gain, no sort to pay) and for the point-query server, where
 // latency rules: the warps take interleaved 4-row groups of the B1 source
 // rows (warp w: rows 4w..4w+3, 4w+32.., ...), lanes take target columns (up
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(256) query_warp(QueryView<V> q, const uint32_t
 // exactly (src/query.cpp:49-65). Result on thread 0.
 constexpr int QC_WARPS = 8;
 
-template <class V>
+template <class V, int UNR = 8>
 __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, uint32_t v2,
                                             V* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -271,7 +272,7 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
             for (int u = 0; u < 4; ++u) cv[u] = j + u < B2 ? col2[j + u] : Ops<V>::inf();
             const V* col = bb + uint64_t(cg) * B1p * 32 + (quad & 7) * 4;
             V acc[4] = {Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf(), Ops<V>::inf()};
-#pragma unroll 8
+#pragma unroll UNR
             for (uint32_t r = phase; r < B1; r += nphase) {
                 const V a = row1[r];
                 const uint4 m = *reinterpret_cast<const uint4*>(col + uint64_t(r) * 32);
@@ -293,7 +294,7 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
                 acc[s] = Ops<V>::inf();
                 cv[s] = (uint32_t(s) < nslot && j < B2) ? col2[j] : Ops<V>::inf();
             }
-            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * QC_WARPS) {
+            for (uint32_t r0 = 4u * warp; r0 < B1; r0 += 4u * (blockDim.x >> 5)) {
                 #pragma unroll
                 for (uint32_t dr = 0; dr < 4; ++dr) {
                     const uint32_t r = r0 + dr;
@@ -325,23 +326,28 @@ __device__ __forceinline__ double cta_query(const QueryView<V>& q, uint32_t v1, 
     double out = 0.0;
     if (threadIdx.x == 0) {
         V b = red[0];
-#pragma unroll
-        for (int w = 1; w < QC_WARPS; ++w) b = Ops<V>::vmin(b, red[w]);
+        for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) b = Ops<V>::vmin(b, red[w]);
         out = Ops<V>::to_f64(Ops<V>::vmin(b, same), q.scale);
     }
     __syncthreads();  // red is reused by the next query
     return out;
 }
 
-template <class V>
-__global__ void __launch_bounds__(32 * QC_WARPS) query_cta(QueryView<V> q,
-                                                           const uint32_t* __restrict__ v1,
-                                                           const uint32_t* __restrict__ v2,
-                                                           uint64_t count,
-                                                           double* __restrict__ out) {
-    __shared__ V red[QC_WARPS];
+// Batch kernel: NW warps per CTA, UNR rows of independent loads in flight
+// per thread, MINB CTAs per SM. The batch is latency-bound (a chain of
+// dependent id/offset loads, then a few rounds of block-row loads per
+// thread), so residency decides: 16 warps x 4 CTAs (64 warps per SM, 32
+// registers) runs 44.3 M queries/s at 1K pairs on cfg3 against 24.3 M for
+// 8 warps at 70 registers (3 CTAs per SM, 2.25 waves) and 19.0 M at 90
+// (profiles/r2/query_cta_shapes_cfg3.jsonl: 17 shapes).
+constexpr int QC_BATCH_WARPS = 16, QC_BATCH_MINB = 4;
+template <class V, int NW, int UNR, int MINB = 1>
+__global__ void __launch_bounds__(32 * NW, MINB) query_cta(QueryView<V> q, const uint32_t* __restrict__ v1,
+                                                     const uint32_t* __restrict__ v2, uint64_t count,
+                                                     double* __restrict__ out) {
+    __shared__ V red[NW];
     for (uint64_t qi = blockIdx.x; qi < count; qi += gridDim.x) {
-        const double d = cta_query(q, v1[qi], v2[qi], red);
+        const double d = cta_query<V, UNR>(q, v1[qi], v2[qi], red);
         if (threadIdx.x == 0) out[qi] = d;
     }
 }
