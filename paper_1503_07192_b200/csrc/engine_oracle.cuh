@@ -211,36 +211,67 @@ __global__ void pack_query_blocks(const V* __restrict__ bg, uint32_t nb,
     }
 }
 
-template <class V>
-void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
-    const Reordered& R = o->R;
+// Host half of build_query_blocks: the block offsets and the layout's
+// allocation (no stream work, so the build runs it on a helper thread while
+// K2 executes: the 48 GB cudaMalloc at cfg3 then costs no wall time).
+// Returns the offsets, empty when the layout is not made.
+// Block offsets of the layout (elements, per pair c1 <= c2); false when no
+// layout is made (PSP_QUERY_LAYOUT=tiles, b == 0, k^2 past 31-bit keys).
+bool query_block_offsets(const Reordered& R, std::vector<uint64_t>& off, uint64_t& elems) {
     const uint64_t k = R.k;
-    o->bq.reset();
-    o->d_bq_off.reset();
+    off.clear();
+    elems = 0;
     const char* lay = std::getenv("PSP_QUERY_LAYOUT");
-    if (lay && std::strcmp(lay, "tiles") == 0) return;
-    if (!o->bg.nmat || k * k >= (1ull << 31)) return;
-    std::vector<uint64_t> off(k * k, 0);
-    uint64_t acc = 0;
+    if (lay && std::strcmp(lay, "tiles") == 0) return false;
+    if (R.b() == 0 || k * k >= (1ull << 31)) return false;
+    off.assign(k * k, 0);
     for (uint64_t c1 = 0; c1 < k; ++c1) {
         const uint64_t B1 = R.bnd_off[c1 + 1] - R.bnd_off[c1], B1p = (B1 + GK - 1) / GK * GK;
         for (uint64_t c2 = c1; c2 < k; ++c2) {
             const uint64_t B2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
-            off[c1 * k + c2] = acc;
-            acc += (B2 + 31) / 32 * 32 * B1p;
+            off[c1 * k + c2] = elems;
+            elems += (B2 + 31) / 32 * 32 * B1p;
         }
     }
+    return true;
+}
+
+template <class V>
+std::vector<uint64_t> plan_query_blocks(psp_gpu_oracle* o) {
+    o->bq.reset();
+    o->d_bq_off.reset();
+    std::vector<uint64_t> off;
+    uint64_t acc = 0;
+    if (!query_block_offsets(o->R, off, acc)) return {};
     size_t free_b = 0, total_b = 0;
     mem_info(&free_b, &total_b);
     const uint64_t need = acc * sizeof(V) + off.size() * 8;
-    if (need + (8ull << 30) > free_b) return;  // keep 8 GB for query workspaces
+    if (need + (8ull << 30) > free_b) return {};  // keep 8 GB for query workspaces
     o->bq.alloc(acc * sizeof(V));
+    return off;
+}
+
+// Device half: upload the offsets and pack the blocks from the finished
+// reference-numbered boundary table.
+template <class V>
+void pack_query_layout(psp_gpu_oracle* o, const std::vector<uint64_t>& off, cudaStream_t s) {
+    const uint64_t k = o->R.k;
+    if (off.empty() || !o->bq.p || !o->bg.nmat) {
+        o->bq.reset();
+        return;
+    }
     o->d_bq_off = upload(off, s);
     pack_query_blocks<V><<<unsigned(k * k), 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0],
                                                          o->d_bnd_off.as<uint32_t>(), uint32_t(k),
                                                          o->d_bq_off.as<uint64_t>(), o->bq.as<V>());
     CK_LAUNCH();
     CK(cudaStreamSynchronize(s));
+}
+
+template <class V>
+void build_query_blocks(psp_gpu_oracle* o, cudaStream_t s) {
+    const std::vector<uint64_t> off = plan_query_blocks<V>(o);
+    pack_query_layout<V>(o, off, s);
 }
 
 // The 16-bit residual layout of the boundary table for the u32 query
@@ -723,7 +754,25 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                      k1_laps.c_str());
 
     // ---- Phase 3: BG init + K2 + query tables
+    std::vector<uint64_t> bq_off;
+    uint64_t bq_elems = 0;
+    DBuf bq_reused;
+    std::exception_ptr bq_err;
+    std::thread bq_planner;
+    struct BqJoin {
+        std::thread& t;
+        ~BqJoin() {
+            if (t.joinable()) t.join();
+        }
+    } bq_join{bq_planner};
+    bool bq_planned = false;
     t0 = Clock::now();
+    const bool prof = std::getenv("PSP_FW_PROFILE") != nullptr;
+    auto lap = [&](const char* what) {  // PSP_FW_PROFILE: synchronised wall-clock laps
+        if (!prof) return;
+        CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[psp] boundary lap: %s at %.1f ms\n", what, ms_since(t0));
+    };
     const uint64_t b = R.b();
     DBuf d_bnd = upload(R.bnd_off, s);
     unsigned long long clique = 0;
@@ -748,14 +797,33 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         k2_permuted = permuted;
         k2_spill = spill;
         const int row_shard[3] = {ctx->device, ctx->rank, ctx->world};
+        // ordered K2: its working matrix dies right after the permutation, when
+        // the block layout is packed -- one allocation serves both (no 40 GB
+        // cudaFree + 48 GB cudaMalloc between K2 and the layout; such calls
+        // have stalled for up to 0.18 s on these boxes)
+        bool reuse_bq = false;
+        if (permuted && !spill && !o->row_storage && query_block_offsets(R, bq_off, bq_elems)) {
+            const uint64_t work = ntiles_upper(uint32_t((npos + T - 1) / T)) * TT * sizeof(V);
+            const uint64_t lay = bq_elems * sizeof(V);
+            size_t free_b = 0, total_b = 0;
+            mem_info(&free_b, &total_b);
+            const uint64_t table = ntiles_upper(uint32_t((b + T - 1) / T)) * TT * sizeof(V);
+            const uint64_t panel = ((npos + T - 1) / T + 1) * TT * sizeof(V);
+            reuse_bq = std::max(work, lay) + table + panel + (10ull << 30) <= free_b;
+            o->bg.min_tile_bytes = reuse_bq ? lay : 0;
+        }
+        if (!reuse_bq) bq_off.clear();
         o->bg.create({permuted ? npos : b}, sizeof(V), true, s, -1, o->row_storage ? row_shard : nullptr);
+        o->bg.min_tile_bytes = 0;
         if (std::getenv("PSP_FW_PROFILE"))
             std::fprintf(stderr, "[psp] boundary phase: order chosen at %.1f ms\n", ms_since(t0));
         if (!permuted) {
             posmap.resize(b);
             for (uint64_t i = 0; i < b; ++i) posmap[i] = static_cast<uint32_t>(i);
         }
+        lap("table allocated");
         fill_arena<V>(o->bg, s, ctx->sms);
+        lap("table filled");
         DBuf d_pos = upload(posmap, s);
         DBuf d_clique(sizeof(unsigned long long));
         CK(cudaMemsetAsync(d_clique.p, 0, sizeof(unsigned long long), s));
@@ -775,6 +843,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         }
         CK(cudaMemcpyAsync(&clique, d_clique.p, sizeof(clique), cudaMemcpyDeviceToHost, s));
         t_post.stop(s);
+        lap("edges scattered");
         CK(cudaStreamSynchronize(s));
         init_ms += t_post.ms();
         // `spill`: the component tables leave the device for K2. Default:
@@ -814,6 +883,19 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         // tables must leave the device first
         MatArena ref;
         if (permuted && !spill && !o->row_storage) ref.create({b}, sizeof(V), false, s);
+        // the block query layout's offsets and allocation on a helper thread
+        // while K2 runs (not beside spilled component tables: the memory is
+        // K2's then)
+        if (!o->row_storage && !spill && !reuse_bq) {
+            bq_planner = std::thread([&, dev = ctx->device] {
+                try {
+                    CK(cudaSetDevice(dev));
+                    bq_off = plan_query_blocks<V>(o);
+                } catch (...) {
+                    bq_err = std::current_exception();
+                }
+            });
+        }
         t_k2.start(s);
         if (ctx->world > 1) run_fw_sharded<V>(o->bg, ctx);
         else run_fw<V>(o->bg, s, ctx->sms);
@@ -846,6 +928,7 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
             CK(cudaStreamSynchronize(s));
             const double p2 = ms_since(t0);
             o->bg.panel.reset();
+            if (reuse_bq) bq_reused = std::move(o->bg.tiles);  // becomes the block layout
             o->bg = std::move(ref);
             if (std::getenv("PSP_FW_PROFILE"))
                 std::fprintf(stderr,
@@ -888,16 +971,30 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
                          fw_done_ms, k2_ms, ms_since(t0));
     }
     // query-side tables
+    lap("K2 done");
     t_post.start(s);
     finish_query_tables<V>(o, std::move(d_bnd), s);
     t_post.stop(s);
     CK(cudaStreamSynchronize(s));
     init_ms += t_post.ms();
+    lap("to-boundary tables");
     // panels are build-time scratch
     o->comps.panel.reset();
     o->bg.panel.reset();
+    lap("panels freed");
     if (!o->row_storage) {  // replicated queries only
-        build_query_blocks<V>(o, s);
+        if (bq_planner.joinable()) {
+            bq_planner.join();
+            if (bq_err) std::rethrow_exception(bq_err);
+            bq_planned = !bq_off.empty();  // else retried below, with K2's scratch freed
+        }
+        if (bq_reused.p) {
+            o->bq = std::move(bq_reused);
+            bq_planned = true;
+        }
+        if (!bq_planned) bq_off = plan_query_blocks<V>(o);
+        pack_query_layout<V>(o, bq_off, s);
+        lap("block layout");
         build_query_blocks16(o, s);
     }
     const double boundary_ms = ms_since(t0);

@@ -279,14 +279,15 @@ struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
     bool pooled = false, ipc = false;
+    bool borrowed = false;  // a view into another buffer: never freed here
     DBuf() = default;
     explicit DBuf(size_t n) { alloc(n); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), pooled(o.pooled), ipc(o.ipc) {
+    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), pooled(o.pooled), ipc(o.ipc), borrowed(o.borrowed) {
         o.p = nullptr;
         o.bytes = 0;
-        o.pooled = o.ipc = false;
+        o.pooled = o.ipc = o.borrowed = false;
     }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
@@ -295,11 +296,18 @@ struct DBuf {
             bytes = o.bytes;
             pooled = o.pooled;
             ipc = o.ipc;
+            borrowed = o.borrowed;
             o.p = nullptr;
             o.bytes = 0;
-            o.pooled = o.ipc = false;
+            o.pooled = o.ipc = o.borrowed = false;
         }
         return *this;
+    }
+    void borrow(void* at, size_t n) {
+        reset();
+        p = at;
+        bytes = n;
+        borrowed = true;
     }
     ~DBuf() { reset(); }
     void alloc(size_t n) {
@@ -334,13 +342,13 @@ struct DBuf {
         CK(cudaMalloc(&p, n));
     }
     void reset() {
-        if (p) {
+        if (p && !borrowed) {
             if (pooled) big_pool().give(p);
             else if (ipc || !buf_cache().give(p, bytes)) cudaFree(p);
         }
         p = nullptr;
         bytes = 0;
-        pooled = ipc = false;
+        pooled = ipc = borrowed = false;
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
@@ -567,6 +575,7 @@ struct MatArena {
     // row-sharded storage (a single matrix over `world` ranks): only the
     // tile rows I with I mod world == rank are backed by device memory
     std::unique_ptr<PartialRange> part;
+    size_t min_tile_bytes = 0;  // tiles allocation at least this large (reused later)
     void* tiles_p() const { return part ? part->ptr() : tiles.p; }
     template <class V> V* tiles_as() const { return static_cast<V*>(tiles_p()); }
 
@@ -618,11 +627,15 @@ struct MatArena {
             part = std::make_unique<PartialRange>();
             part->create(row_shard[0], tile_elems * vbytes, rows);
         } else {
-            tiles.alloc(tile_elems * vbytes);
+            tiles.alloc(std::max<size_t>(tile_elems * vbytes, min_tile_bytes));
         }
         sparse = with_panel && nb_max > 1 && std::getenv("PSP_FW_DENSE") == nullptr &&
                  (sparse_walk < 0 ? nmat == 1 : sparse_walk > 0);
-        if (with_panel) panel.alloc((panel_elems + (sparse ? nslots : 0)) * vbytes);
+        const size_t panel_bytes = (panel_elems + (sparse ? nslots : 0)) * vbytes;
+        const size_t tail = (tile_elems * vbytes + 255) / 256 * 256;
+        if (with_panel && !part && tail + panel_bytes <= tiles.bytes)
+            panel.borrow(static_cast<char*>(tiles.p) + tail, panel_bytes);  // spare room of a larger allocation
+        else if (with_panel) panel.alloc(panel_bytes);
         if (sparse) d_act.alloc(act_bytes());
         d_tile_base = upload(tile_base, s);
         d_panel_base = upload(panel_base, s);
