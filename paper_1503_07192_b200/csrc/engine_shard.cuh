@@ -172,6 +172,12 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
     const Reordered& R = o->R;
     const uint32_t k = R.k, me = static_cast<uint32_t>(ctx->rank);
     const size_t vb = sizeof(V);
+    const auto t0 = Clock::now();
+    auto lap = [&](const char* what) {  // PSP_FW_PROFILE: synchronised laps
+        if (!std::getenv("PSP_FW_PROFILE")) return;
+        CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[psp] rank %d shard lap: %s at %.1f ms\n", ctx->rank, what, ms_since(t0));
+    };
     auto d2d = [&](DBuf& dst, const DBuf& src) {
         dst.alloc(src.bytes);
         CK(cudaMemcpyAsync(dst.p, src.p, src.bytes, cudaMemcpyDeviceToDevice, s));
@@ -197,6 +203,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
             CK(cudaMemcpyAsync(sh->d_cb.as<V>() + cb_off[c], o->d_cb.as<V>() + src_off[c],
                                (src_off[c + 1] - src_off[c]) * vb, cudaMemcpyDeviceToDevice, s));
     sh->d_cb_off = upload(cb_off, s);
+    lap("to-boundary rows");
 
     // dense full boundary rows of the owned components
     sh->bt_stride = std::max<uint64_t>(4, (sh->b + 3) & ~uint64_t(3));
@@ -209,6 +216,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
     sh->bt_rows = gid.size();
     sh->d_bt_row0 = upload(row0, s);
     sh->d_bt.alloc(sh->bt_rows * sh->bt_stride * vb);
+    lap("boundary rows allocated");
     if (o->row_storage) {
         // the table is spread over the ranks by tile row: every rank sends
         // its part of each destination's rows, min-reduced at the destination
@@ -251,6 +259,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
         CK(cudaStreamSynchronize(s));  // d_gid is freed on return
     }
 
+    lap("boundary rows gathered");
     // full component tables of the owned components (same-component cap)
     std::vector<uint64_t> sizes(k, 0);
     for (uint32_t c = 0; c < k; ++c)
@@ -287,6 +296,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
             bases[r] = reinterpret_cast<uint64_t>(p);
         }
     }
+    lap("component tables + peer mapping");
     sh->d_cb_peer = upload(bases, s);
     if (ctx->world > 1) {
         // open the point-to-point channels now: NCCL connects send/recv
@@ -303,6 +313,7 @@ void shard_build(psp_gpu_shard* sh, const psp_gpu_oracle* o) {
         nccl_check(api.GroupEnd(), "ncclGroupEnd");
     }
     CK(cudaStreamSynchronize(s));
+    lap("NCCL send/recv channels connected");
     sh->device_bytes = sh->d_cb.bytes + sh->d_bt.bytes + sh->comps.bytes() + sh->d_perm.bytes +
                        sh->d_assign.bytes;
 }
