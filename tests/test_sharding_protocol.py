@@ -13,7 +13,13 @@ the ownership and exchange logic:
   owned active slots); exchange "allreduce" (PSP_K2_EXCHANGE=nccl): non-owned
   slots are INF and flagged inactive, one min-allreduce of tiles and flags;
 * the K2 elimination order: the matrix is closed in a permuted numbering and
-  permuted back, which must not change a single entry.
+  permuted back, which must not change a single entry;
+* row-sharded storage (PSP_STORAGE_ROW_SHARDED): rows a rank does not own
+  hold garbage (NaN here, the sink allocation on GPUs) and must never be
+  read -- the diagonal tile of a foreign k-block goes to a scratch tile --,
+  there is no replication, and each destination's boundary rows are
+  assembled by a min-reduce of every rank's part (engine_shard.cuh
+  gather_bt_part + ncclReduce).
 """
 from __future__ import annotations
 
@@ -35,9 +41,11 @@ def free_port() -> int:
 
 
 def sharded_fw(D: np.ndarray, rank: int, world: int, dist, mode: str = "p2p",
-               perm: np.ndarray | None = None) -> tuple[np.ndarray, int]:
+               perm: np.ndarray | None = None, rows_only: bool = False) -> tuple[np.ndarray, int]:
     """Returns the closed matrix (original numbering) and the number of bytes
-    of panel tiles this rank received."""
+    of panel tiles this rank received. rows_only: row-sharded storage; the
+    result then holds only the rows t with t % world == rank (others NaN),
+    gathered from every rank's owned tile rows."""
     import torch
     n = D.shape[0]
     if perm is not None:  # position perm[i] holds vertex i
@@ -50,6 +58,10 @@ def sharded_fw(D: np.ndarray, rank: int, world: int, dist, mode: str = "p2p",
     M[:n, :n] = D
     np.fill_diagonal(M, 0.0)
     tile = lambda I, J: (slice(I * T, (I + 1) * T), slice(J * T, (J + 1) * T))
+    if rows_only:  # rows of other ranks are not stored: garbage that must never be read
+        for I in range(nb):
+            if I % world != rank:
+                M[I * T:(I + 1) * T, :] = np.nan
     received = 0
     for kb in range(nb):
         owner = kb % world
@@ -61,8 +73,11 @@ def sharded_fw(D: np.ndarray, rank: int, world: int, dist, mode: str = "p2p",
             M[K] = d
         t = torch.from_numpy(np.ascontiguousarray(M[K]))
         dist.broadcast(t, src=owner)  # p2p: pull_diag from the owner's region
-        M[K] = t.numpy()
-        dkk = M[K]
+        if rows_only and rank != owner:
+            dkk = t.numpy().copy()  # MatSet::diag scratch tile
+        else:
+            M[K] = t.numpy()
+            dkk = M[K]
         # phase 2 on owned slots: slot J = D[kb rows][J cols]; flag 0 = active
         panel = np.full((nb, T, T), np.inf)
         flag = np.ones(nb, np.int8)
@@ -117,6 +132,28 @@ def sharded_fw(D: np.ndarray, rank: int, world: int, dist, mode: str = "p2p",
                 A, B = panel[I], panel[J]          # A[k][i] = D[i][k] by symmetry
                 M[tile(I, J)] = np.minimum(M[tile(I, J)],
                                            np.min(A[:, :, None] + B[:, None, :], axis=0))
+    if rows_only:
+        # gather_bt_part: destination d's rows (here t % world == d), each
+        # element from the rank holding its tile row min(p, q) / T, INF from
+        # the others; min-reduced at d
+        pos = perm if perm is not None else np.arange(n)
+        mine_rows = None
+        for d in range(world):
+            rows = np.arange(d, n, world)
+            part = np.full((len(rows), n), np.inf)
+            for a, t in enumerate(rows):
+                p = pos[t]
+                for j in range(n):
+                    q = pos[j]
+                    if (min(p, q) // T) % world == rank:
+                        part[a, j] = M[min(p, q), max(p, q)] if p // T <= q // T else M[q, p]
+            pt = torch.from_numpy(part)
+            dist.reduce(pt, dst=d, op=dist.ReduceOp.MIN)
+            if d == rank:
+                mine_rows = (rows, pt.numpy())
+        out = np.full((n, n), np.nan)
+        out[mine_rows[0]] = mine_rows[1]
+        return out, received
     for I in range(nb):  # replicate rows from their owners
         rowt = torch.from_numpy(np.ascontiguousarray(M[I * T:(I + 1) * T, I * T:]))
         dist.broadcast(rowt, src=I % world)
@@ -131,12 +168,12 @@ def sharded_fw(D: np.ndarray, rank: int, world: int, dist, mode: str = "p2p",
     return full, received
 
 
-def _worker(rank, world, port, D, mode, perm, out_q):
+def _worker(rank, world, port, D, mode, perm, out_q, rows_only=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    res = sharded_fw(D, rank, world, dist, mode, perm)
+    res = sharded_fw(D, rank, world, dist, mode, perm, rows_only)
     out_q.put((rank, res))
     dist.barrier()
     dist.destroy_process_group()
@@ -190,3 +227,33 @@ def test_row_sharded_fw_protocol_gloo(world, mode, case):
         # only active slots move: less than the all-reduce's full panels
         nb = -(-n // T)
         assert sum(results[r][1] for r in range(world)) < world * nb * nb * T * T * 8
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["p2p", "allreduce"])
+def test_row_sharded_storage_protocol_gloo(world, mode):
+    # no rank reads a row it does not own (NaN would spread), and the
+    # min-reduce gather gives every destination its exact rows
+    import torch.multiprocessing as mp
+    n, eu, ev, ew = _two_pieces()
+    perm = np.random.default_rng(7).permutation(n)
+    D = np.full((n, n), np.inf)
+    D[eu, ev] = ew
+    D[ev, eu] = ew
+    np.fill_diagonal(D, 0)
+    truth = oracle.apsp_dense(n, eu, ev, ew)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, D, mode, perm, q, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        rows = np.arange(r, n, world)
+        got = results[r][0][rows]
+        assert not np.isnan(got).any(), f"rank {r} read a row it does not own"
+        assert np.array_equal(got, truth[rows]), f"rank {r}"
