@@ -1029,6 +1029,42 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
     }
 }
 
+// The id maps of an imported / loaded oracle (validated as
+// psp_gpu_oracle_import documents).
+void reordered_from_ids(Reordered& R, uint64_t n, uint32_t k, const uint32_t* permutation,
+                        const uint32_t* assignment, const uint64_t* component_offset,
+                        const uint64_t* boundary_offset) {
+    R.n = n;
+    R.k = k;
+    R.perm.assign(permutation, permutation + n);
+    R.inv.assign(n, 0);
+    std::vector<uint8_t> seen(n, 0);
+    for (uint64_t v = 0; v < n; ++v) {
+        if (R.perm[v] >= n || seen[R.perm[v]]++) throw ArgError("oracle_import: bad permutation");
+        R.inv[R.perm[v]] = static_cast<uint32_t>(v);
+    }
+    R.assign.assign(assignment, assignment + n);
+    R.comp_off.resize(k + 1);
+    R.bnd_off.resize(k + 1);
+    for (uint32_t c = 0; c <= k; ++c) {
+        R.comp_off[c] = static_cast<uint32_t>(component_offset[c]);
+        R.bnd_off[c] = static_cast<uint32_t>(boundary_offset[c]);
+    }
+    if (R.comp_off[0] != 0 || R.comp_off[k] != n || R.bnd_off[0] != 0)
+        throw ArgError("oracle_import: offsets do not cover the graph");
+    R.flags.assign(n, 0);
+    for (uint32_t c = 0; c < k; ++c) {
+        const uint32_t s = R.comp_off[c + 1] - R.comp_off[c];
+        const uint32_t bc = R.bnd_off[c + 1] - R.bnd_off[c];
+        if (R.comp_off[c + 1] < R.comp_off[c] || R.bnd_off[c + 1] < R.bnd_off[c] || bc > s)
+            throw ArgError("oracle_import: inconsistent offsets");
+        for (uint32_t i = 0; i < s; ++i) {
+            if (R.assign[R.comp_off[c] + i] != c) throw ArgError("oracle_import: assignment/offset mismatch");
+            R.flags[R.comp_off[c] + i] = i < bc;  // boundary-first local ids
+        }
+    }
+}
+
 // Kind for imported tables: u32 when every finite entry is exact in fixed
 // point 2^q (q <= 24) below INF, else f32.
 Kind choose_kind_tables(int requested, const std::vector<const double*>& ptr,
@@ -1053,6 +1089,18 @@ Kind choose_kind_tables(int requested, const std::vector<const double*>& ptr,
     if (requested == PSP_VALUE_U32)
         throw Fail{PSP_EOVERFLOW, "import: tables are not exact in u32 fixed point"};
     return {PSP_VALUE_F32, 0};
+}
+
+// Query-side tables of an imported or loaded oracle.
+template <class V>
+void finish_import(psp_gpu_oracle* o) {
+    cudaStream_t s = o->ctx->stream;
+    finish_query_tables<V>(o, upload(o->R.bnd_off, s), s);
+    CK(cudaStreamSynchronize(s));
+    build_query_blocks<V>(o, s);
+    build_query_blocks16(o, s);
+    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->bq.bytes + o->bq16.bytes +
+                      o->bqaux.bytes + o->cb16.bytes;
 }
 
 template <class V>
@@ -1094,12 +1142,7 @@ void import_tables(psp_gpu_oracle* o, const double* const* ct, const double* con
             CK(cudaStreamSynchronize(s));
         }
     }
-    finish_query_tables<V>(o, upload(R.bnd_off, s), s);
-    CK(cudaStreamSynchronize(s));
-    build_query_blocks<V>(o, s);
-    build_query_blocks16(o, s);
-    o->device_bytes = o->comps.bytes() + o->bg.bytes() + o->d_cb.bytes + o->bq.bytes + o->bq16.bytes +
-                      o->bqaux.bytes + o->cb16.bytes;
+    finish_import<V>(o);
 }
 
 void set_peak_entries(const Reordered& R, unsigned workers, psp_build_stats* st) {

@@ -121,6 +121,108 @@ __global__ void window_to_f64(MatSet<V> ms, uint32_t m, uint32_t row0, uint32_t 
     out[idx] = Ops<V>::to_f64(ms.tiles[ms.tile_base[m] + sym_off(row0 + r, c, ms.nb[m])], scale);
 }
 
+// ---- PSP1 load on the device: the table section streamed in chunks.
+// Pieces in file order: start[t] (elements) for t < k the component tables
+// (s_c x s_c), for k <= t < 2k the boundary rows (B_c x b), start[2k] = end.
+struct Psp1Map {
+    const uint64_t* start;    // [2k + 1]
+    const uint32_t* size;     // [k] component sizes s_c
+    const uint32_t* bnd_off;  // [k + 1]
+    uint32_t k, b;
+};
+
+// Fixed-point need of one value (choose_kind_tables semantics): the
+// smallest q with x * 2^q integral, 0 for +inf (unreachable), 1 << 20 when
+// no q works (negative or NaN).
+__device__ __forceinline__ int psp1_need_q(double x) {
+    if (isinf(x) && x > 0) return 0;
+    if (!(x >= 0)) return 1 << 20;
+    if (x == 0) return 0;
+    const unsigned long long bits = __double_as_longlong(x);
+    const int ef = int((bits >> 52) & 0x7ff);
+    unsigned long long sig = bits & ((1ull << 52) - 1);
+    int e;
+    if (ef == 0) {
+        e = -1074;  // subnormal
+    } else {
+        sig |= 1ull << 52;
+        e = ef - 1075;
+    }
+    e += __ffsll(static_cast<long long>(sig)) - 1;  // drop trailing zero bits
+    return e >= 0 ? 0 : -e;
+}
+
+// One chunk of f64 elements [e0, e0 + cnt): each thread takes PER
+// consecutive elements (one binary search over the pieces), writes the
+// upper-tile entries of the tables (the writers' rule, minplus.cuh) as V at
+// fixed point 2^shift, and folds the chunk's largest finite value and
+// fixed-point need into maxbits / need (atomicMax).
+template <class V, int PER>
+__global__ void __launch_bounds__(256) psp1_convert(const double* __restrict__ chunk, uint64_t e0,
+                                                    uint64_t cnt, Psp1Map map, MatSet<V> comps,
+                                                    MatSet<V> bg, int shift,
+                                                    unsigned long long* __restrict__ maxbits,
+                                                    int* __restrict__ need) {
+    const uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * PER;
+    double mx = 0.0;
+    int nq = 0;
+    if (i0 < cnt) {
+        uint64_t e = e0 + i0;
+        uint32_t lo = 0, hi = 2 * map.k;  // piece t: start[t] <= e < start[t + 1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (map.start[mid] <= e) lo = mid;
+            else hi = mid;
+        }
+        uint32_t t = lo;
+        const double scale = ldexp(1.0, shift);
+        for (int u = 0; u < PER && i0 + u < cnt; ++u, ++e) {
+            while (e >= map.start[t + 1]) ++t;
+            const double x = chunk[i0 + u];
+            if (isfinite(x)) mx = fmax(mx, x);
+            nq = max(nq, psp1_need_q(x));
+            V v;
+            if (std::is_same<V, float>::value) v = Ops<V>::from_bits(__float_as_uint(float(x)));
+            else v = isinf(x) ? Ops<V>::inf() : V(static_cast<uint32_t>(x * scale));
+            const uint64_t local = e - map.start[t];
+            if (t < map.k) {
+                const uint32_t sz = map.size[t];
+                const uint32_t i = uint32_t(local / sz), j = uint32_t(local - uint64_t(i) * sz);
+                if (i / T <= j / T)
+                    comps.tiles[comps.tile_base[t] + tidx(i / T, j / T, comps.nb[t]) * TT +
+                                uint64_t(i % T) * T + j % T] = v;
+            } else {
+                const uint32_t c = t - map.k;
+                const uint32_t r = uint32_t(local / map.b), j = uint32_t(local - uint64_t(r) * map.b);
+                const uint32_t g = map.bnd_off[c] + r;
+                if (g / T <= j / T)
+                    bg.tiles[tidx(g / T, j / T, bg.nb[0]) * TT + uint64_t(g % T) * T + j % T] = v;
+            }
+        }
+    }
+    // block reduction, one atomic per block
+    __shared__ double smx[8];
+    __shared__ int snq[8];
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nq = max(nq, __shfl_xor_sync(0xffffffffu, nq, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        smx[w] = mx;
+        snq[w] = nq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < int(blockDim.x >> 5); ++i) {
+            mx = fmax(mx, smx[i]);
+            nq = max(nq, snq[i]);
+        }
+        atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(mx)));
+        atomicMax(need, nq);
+    }
+}
+
 // GF(2) 64x64 matrices for the CRC append operator.
 struct Gf2Mat {
     uint64_t col[64];  // image of bit i

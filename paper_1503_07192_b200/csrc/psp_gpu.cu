@@ -29,6 +29,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -201,35 +204,7 @@ psp_status psp_gpu_oracle_import(psp_gpu_ctx* ctx, uint64_t n, uint32_t k,
         auto o = std::make_unique<psp_gpu_oracle>();
         o->ctx = ctx;
         Reordered& R = o->R;
-        R.n = n;
-        R.k = k;
-        R.perm.assign(permutation, permutation + n);
-        R.inv.assign(n, 0);
-        std::vector<uint8_t> seen(n, 0);
-        for (uint64_t v = 0; v < n; ++v) {
-            if (R.perm[v] >= n || seen[R.perm[v]]++) throw ArgError("oracle_import: bad permutation");
-            R.inv[R.perm[v]] = static_cast<uint32_t>(v);
-        }
-        R.assign.assign(assignment, assignment + n);
-        R.comp_off.resize(k + 1);
-        R.bnd_off.resize(k + 1);
-        for (uint32_t c = 0; c <= k; ++c) {
-            R.comp_off[c] = static_cast<uint32_t>(component_offset[c]);
-            R.bnd_off[c] = static_cast<uint32_t>(boundary_offset[c]);
-        }
-        if (R.comp_off[0] != 0 || R.comp_off[k] != n || R.bnd_off[0] != 0)
-            throw ArgError("oracle_import: offsets do not cover the graph");
-        R.flags.assign(n, 0);
-        for (uint32_t c = 0; c < k; ++c) {
-            const uint32_t s = R.comp_off[c + 1] - R.comp_off[c];
-            const uint32_t bc = R.bnd_off[c + 1] - R.bnd_off[c];
-            if (R.comp_off[c + 1] < R.comp_off[c] || R.bnd_off[c + 1] < R.bnd_off[c] || bc > s)
-                throw ArgError("oracle_import: inconsistent offsets");
-            for (uint32_t i = 0; i < s; ++i) {
-                if (R.assign[R.comp_off[c] + i] != c) throw ArgError("oracle_import: assignment/offset mismatch");
-                R.flags[R.comp_off[c] + i] = i < bc;  // boundary-first local ids
-            }
-        }
+        reordered_from_ids(R, n, k, permutation, assignment, component_offset, boundary_offset);
         std::vector<const double*> ptr;
         std::vector<uint64_t> len;
         for (uint32_t c = 0; c < k; ++c) {
@@ -285,17 +260,23 @@ psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kin
                                psp_gpu_oracle** out) {
     return guarded([&] {
         if (!ctx || !path || !out) throw ArgError("oracle_load: NULL argument");
+        if (value_kind != PSP_VALUE_AUTO && value_kind != PSP_VALUE_U32 && value_kind != PSP_VALUE_F32)
+            throw ArgError("value_kind must be PSP_VALUE_AUTO, PSP_VALUE_U32 or PSP_VALUE_F32");
         const std::string name(path);
         auto io = [&](const std::string& msg) { return Fail{PSP_EIO, name + ": " + msg}; };
-        std::ifstream in(name, std::ios::binary);
-        if (!in) throw io("cannot open for reading");
-        in.seekg(0, std::ios::end);
-        const int64_t total = in.tellg();
-        in.seekg(0, std::ios::beg);
+        const int fd = ::open(path, O_RDONLY);
+        if (fd < 0) throw io("cannot open for reading");
+        struct Fd {
+            int fd;
+            ~Fd() { ::close(fd); }
+        } fd_guard{fd};
+        struct stat sb {};
+        if (::fstat(fd, &sb) != 0) throw io("cannot open for reading");
+        const int64_t total = sb.st_size;
         if (total < 4 + 4 + 8) throw io("truncated oracle file");
         // validation order and messages follow read_oracle (src/oracle_io.cpp:129-255)
         uint8_t head[32] = {0};  // magic, version, n, k, b
-        in.read(reinterpret_cast<char*>(head), std::min<int64_t>(32, total));
+        pread_all(fd, head, uint64_t(std::min<int64_t>(32, total)), 0, name);
         if (std::memcmp(head, "PSP1", 4) != 0) throw Fail{PSP_EFORMAT, name + ": not an oracle file"};
         uint32_t version;
         std::memcpy(&version, head + 4, 4);
@@ -312,15 +293,11 @@ psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kin
         if (k < 1 || k > n || b > n || n > 0xffffffffull) throw io("inconsistent oracle header");
         const uint64_t fixed = 16 * n + (n + 7) / 8 + 8 * (k + 1);
         if (remaining < fixed) throw io("truncated oracle file");
-        // read everything with the table section 8-byte aligned in memory
+        // the header and id sections on the host; the tables stream to the device
         const uint64_t table_at = 32 + fixed;
-        const size_t pad = (8 - table_at % 8) % 8;
-        std::vector<uint64_t> store((uint64_t(total) + pad + 7) / 8 + 1);
-        uint8_t* buf = reinterpret_cast<uint8_t*>(store.data()) + pad;
-        in.seekg(0, std::ios::beg);
-        in.read(reinterpret_cast<char*>(buf), total);
-        if (in.gcount() != total) throw io("truncated oracle file");
-        const uint8_t* p = buf + 32;
+        std::vector<uint8_t> hdr(table_at);
+        pread_all(fd, hdr.data(), table_at, 0, name);
+        const uint8_t* p = hdr.data() + 32;
         auto rd64 = [&](const uint8_t* q) {
             uint64_t v;
             std::memcpy(&v, q, 8);
@@ -369,38 +346,52 @@ psp_status psp_gpu_oracle_load(psp_gpu_ctx* ctx, const char* path, int value_kin
         if (payload - table_at != table_bytes)
             throw io(payload - table_at < table_bytes ? "truncated oracle file"
                                                       : "oracle file has trailing data");
-        // checksum: header on the host, tables on the device
         CK(cudaSetDevice(ctx->device));
+        auto o = std::make_unique<psp_gpu_oracle>();
+        o->ctx = ctx;
+        reordered_from_ids(o->R, n, uint32_t(k), perm.data(), assign.data(), co.data(), bo.data());
         cudaStream_t s = ctx->stream;
-        Crc64Stream crc;
-        crc.update(buf, table_at);
-        {
-            DBuf chunk(IO_CHUNK);
-            GpuCrc gcrc(crc, s);
-            for (uint64_t at = 0; at < table_bytes; at += IO_CHUNK) {
-                const uint64_t len = std::min<uint64_t>(IO_CHUNK, table_bytes - at);
-                CK(cudaMemcpyAsync(chunk.p, buf + table_at + at, len, cudaMemcpyHostToDevice, s));
-                const uint64_t nblk = gcrc.launch(chunk.as<uint8_t>(), len, s);
-                CK(cudaStreamSynchronize(s));
-                gcrc.fold(crc, nblk, buf + table_at + at, len);
+        std::vector<uint64_t> sizes(k);
+        for (uint64_t c = 0; c < k; ++c) sizes[c] = co[c + 1] - co[c];
+        // one streamed pass: CRC + conversion (u32 at q = 0 unless f32 is
+        // asked for) + the kind analysis; a second pass converts again only
+        // when the tables need another kind (fractional or huge weights)
+        auto pass = [&](bool f32, int shift, Crc64Stream* crc) {
+            const size_t vb = 4;
+            o->comps.create(sizes, vb, false, s);
+            if (b > 0) o->bg.create({b}, vb, false, s);
+            else o->bg = MatArena();
+            if (f32) {
+                fill_arena<float>(o->comps, s, ctx->sms);
+                if (b > 0) fill_arena<float>(o->bg, s, ctx->sms);
+                return stream_psp1_tables<float>(o.get(), fd, name, table_at, table_bytes, shift, crc);
             }
+            fill_arena<uint32_t>(o->comps, s, ctx->sms);
+            if (b > 0) fill_arena<uint32_t>(o->bg, s, ctx->sms);
+            return stream_psp1_tables<uint32_t>(o.get(), fd, name, table_at, table_bytes, shift, crc);
+        };
+        Crc64Stream crc;
+        crc.update(hdr.data(), table_at);
+        const Psp1Analysis a = pass(value_kind == PSP_VALUE_F32, 0, &crc);
+        uint64_t stored = 0;
+        pread_all(fd, &stored, 8, payload, name);
+        if (stored != crc.value()) throw Fail{PSP_ECHECKSUM, name + ": oracle checksum mismatch"};
+        // choose_kind_tables: the smallest q with every finite entry integral
+        // at 2^q, if 2 * max * 2^q stays below INF
+        Kind kind{PSP_VALUE_F32, 0};
+        if (value_kind != PSP_VALUE_F32) {
+            const int q = a.need_q;
+            if (q <= 24 && 2.0 * a.maxv * std::ldexp(1.0, q) < double(U32_INF)) kind = {PSP_VALUE_U32, q};
+            else if (value_kind == PSP_VALUE_U32)
+                throw Fail{PSP_EOVERFLOW, "import: tables are not exact in u32 fixed point"};
+            if (kind.kind != PSP_VALUE_U32 || kind.shift != 0)
+                pass(kind.kind == PSP_VALUE_F32, kind.shift, nullptr);
         }
-        if (rd64(buf + payload) != crc.value())
-            throw Fail{PSP_ECHECKSUM, name + ": oracle checksum mismatch"};
-        std::vector<const double*> ct(k), bt(k);
-        const double* tp = reinterpret_cast<const double*>(buf + table_at);
-        for (uint64_t c = 0; c < k; ++c) {
-            ct[c] = tp;
-            tp += (co[c + 1] - co[c]) * (co[c + 1] - co[c]);
-        }
-        for (uint64_t c = 0; c < k; ++c) {
-            bt[c] = tp;
-            tp += (bo[c + 1] - bo[c]) * b;
-        }
-        const psp_status st = psp_gpu_oracle_import(ctx, n, uint32_t(k), perm.data(), assign.data(),
-                                                    co.data(), bo.data(), ct.data(), bt.data(),
-                                                    value_kind, out);
-        if (st != PSP_OK) throw Fail{st, g_err};
+        o->kind = kind;
+        o->scale = std::ldexp(1.0, -kind.shift);
+        if (kind.kind == PSP_VALUE_U32) finish_import<uint32_t>(o.get());
+        else finish_import<float>(o.get());
+        *out = o.release();
     });
 }
 

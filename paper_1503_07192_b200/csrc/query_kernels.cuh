@@ -1529,28 +1529,28 @@ __global__ void __launch_bounds__(GTHREADS, 2) query_grouped(QueryView<V> q, Gro
             me = me_next;
             nxt = __shfl_sync(0xffffffffu, nn, 0);
         }
-        return;
-    }
-    while (task < total) {
-        uint32_t next = 0;
-        if (lead) next = atomicAdd(queue, 1u) + nwarps;
-        const uint4 rec = w.tasks[task];
-        const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0x3fu, cg = rec.w >> 8;
-        const bool half = (rec.w >> 6) & 1u;  // last column group, <= 16 columns
-        // block layout: the register-blocked product (12 variants behind one
-        // switch, see group_task_rb). Tile arena / routed / lane product:
-        // three query-count variants (32/16/8 slots; finer ones grew that
-        // kernel past the instruction cache), 24 slots for the lane product
-        if constexpr (MODE == QM_BLOCKS16) {  // 16-bit residual product (u32 tables)
-            group_task_rb16<V>(q, w, st, c1, c2, q0, m, cg, half, phase);
-        } else {
-            constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
-            if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-            else if (TM == QM_BLOCKS && m > 16) group_task<V, 6, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-            else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
-            else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+    } else {
+        while (task < total) {
+            uint32_t next = 0;
+            if (lead) next = atomicAdd(queue, 1u) + nwarps;
+            const uint4 rec = w.tasks[task];
+            const uint32_t c1 = rec.x, c2 = rec.y, q0 = rec.z, m = rec.w & 0x3fu, cg = rec.w >> 8;
+            const bool half = (rec.w >> 6) & 1u;  // last column group, <= 16 columns
+            // block layout: the register-blocked product (12 variants behind one
+            // switch, see group_task_rb). Tile arena / routed / lane product:
+            // three query-count variants (32/16/8 slots; finer ones grew that
+            // kernel past the instruction cache), 24 slots for the lane product
+            if constexpr (MODE == QM_BLOCKS16) {  // 16-bit residual product (u32 tables)
+                group_task_rb16<V>(q, w, st, c1, c2, q0, m, cg, half, phase);
+            } else {
+                constexpr int TM = MODE == QM_BLOCKS_LANE ? QM_BLOCKS : MODE;
+                if (m > 24 || (TM != QM_BLOCKS && m > 16)) group_task<V, 8, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+                else if (TM == QM_BLOCKS && m > 16) group_task<V, 6, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+                else if (m > 8) group_task<V, 4, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+                else group_task<V, 2, TM>(q, w, st, c1, c2, q0, m, cg, phase);
+            }
+            task = __shfl_sync(0xffffffffu, next, 0);
         }
-        task = __shfl_sync(0xffffffffu, next, 0);
     }
 }
 
