@@ -54,39 +54,75 @@ struct GpuCrc {
     }
 };
 
+inline void pwrite_all(int fd, const void* src, uint64_t len, uint64_t off) {
+    constexpr int kThreads = 8;
+    const uint64_t per = (len + kThreads - 1) / kThreads;
+    std::atomic<bool> failed{false};
+    std::vector<std::thread> th;
+    for (int t = 0; t < kThreads; ++t) {
+        const uint64_t a = std::min(len, t * per), b = std::min(len, a + per);
+        if (a >= b) break;
+        th.emplace_back([&, a, b] {
+            for (uint64_t at = a; at < b && !failed;) {
+                const ssize_t r = ::pwrite(fd, static_cast<const char*>(src) + at, b - at, off + at);
+                if (r <= 0) failed = true;
+                else at += uint64_t(r);
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    if (failed) throw Fail{PSP_EIO, "oracle write failed"};
+}
+
 // Tables in file order (component tables, then boundary rows), converted to
-// f64 on the device window by window, CRC'd on the device, copied to pinned
-// host memory and written; the fwrite of one window overlaps the device work
-// of the next (two staging buffers, one write in flight).
+// f64 on the device into a 64 MB staging chunk (windows packed back to
+// back), CRC'd on the device, copied to pinned host memory and written with
+// parallel pwrites at `off`; the write of one chunk overlaps the device work
+// of the next (two staging buffers, one write in flight). Returns the end
+// offset.
 template <class V>
-void save_tables(const psp_gpu_oracle* o, std::FILE* f, Crc64Stream& crc) {
+uint64_t save_tables(const psp_gpu_oracle* o, int fd, uint64_t off, Crc64Stream& crc) {
     cudaStream_t s = o->ctx->stream;
     DBuf chunk[2] = {DBuf(IO_CHUNK), DBuf(IO_CHUNK)};
     PinnedBuf host[2] = {PinnedBuf(IO_CHUNK), PinnedBuf(IO_CHUNK)};
     GpuCrc gcrc(crc, s);
-    std::future<bool> writing;
+    std::future<void> writing;
     int cur = 0;
+    uint64_t fill = 0;  // bytes staged in chunk[cur]
     auto finish_write = [&] {
-        if (writing.valid() && !writing.get()) throw Fail{PSP_EIO, "oracle write failed"};
+        if (writing.valid()) writing.get();  // rethrows a write failure
+    };
+    auto flush = [&] {
+        if (!fill) return;
+        const uint64_t nblk = gcrc.launch(chunk[cur].as<uint8_t>(), fill, s);
+        CK(cudaMemcpyAsync(host[cur].p, chunk[cur].p, fill, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint8_t* h = static_cast<const uint8_t*>(host[cur].p);
+        gcrc.fold(crc, nblk, h, fill);
+        finish_write();  // the previous chunk (the other buffer)
+        writing = std::async(std::launch::async, [fd, h, len = fill, at = off] { pwrite_all(fd, h, len, at); });
+        off += fill;
+        fill = 0;
+        cur ^= 1;
     };
     auto emit = [&](const MatArena& a, uint32_t m, uint32_t row0, uint32_t nrows, uint32_t ncols) {
         if (!nrows || !ncols) return;
-        const uint32_t per = uint32_t(std::max<uint64_t>(1, IO_CHUNK / (uint64_t(ncols) * 8)));
-        for (uint32_t r0 = 0; r0 < nrows; r0 += per) {
-            const uint32_t nr = std::min(per, nrows - r0);
-            const uint64_t cnt = uint64_t(nr) * ncols, bytes = cnt * 8;
+        const uint64_t row_bytes = uint64_t(ncols) * 8;
+        if (row_bytes > IO_CHUNK) throw Fail{PSP_EINVAL, "oracle_save: rows longer than 8M entries"};
+        for (uint32_t r0 = 0; r0 < nrows;) {
+            const uint64_t room = (IO_CHUNK - fill) / row_bytes;
+            if (room == 0) {
+                flush();
+                continue;
+            }
+            const uint32_t nr = uint32_t(std::min<uint64_t>(room, nrows - r0));
+            const uint64_t cnt = uint64_t(nr) * ncols;
             window_to_f64<V><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(
-                a.view<V>(), m, row0 + r0, nr, ncols, o->scale, chunk[cur].as<double>());
+                a.view<V>(), m, row0 + r0, nr, ncols, o->scale,
+                reinterpret_cast<double*>(chunk[cur].as<uint8_t>() + fill));
             CK_LAUNCH();
-            const uint64_t nblk = gcrc.launch(chunk[cur].as<uint8_t>(), bytes, s);
-            CK(cudaMemcpyAsync(host[cur].p, chunk[cur].p, bytes, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            const uint8_t* h = static_cast<const uint8_t*>(host[cur].p);
-            gcrc.fold(crc, nblk, h, bytes);
-            finish_write();  // the previous window (the other buffer)
-            writing = std::async(std::launch::async,
-                                 [f, h, bytes] { return std::fwrite(h, 1, bytes, f) == bytes; });
-            cur ^= 1;
+            fill += cnt * 8;
+            r0 += nr;
         }
     };
     const Reordered& R = o->R;
@@ -96,7 +132,9 @@ void save_tables(const psp_gpu_oracle* o, std::FILE* f, Crc64Stream& crc) {
     }
     for (uint32_t c = 0; c < R.k; ++c)
         emit(o->bg, 0, R.bnd_off[c], R.bnd_off[c + 1] - R.bnd_off[c], uint32_t(R.b()));
+    flush();
     finish_write();
+    return off;
 }
 
 void put_u64s(std::vector<uint8_t>& buf, uint64_t v) {

@@ -229,9 +229,12 @@ psp_status psp_gpu_oracle_save(const psp_gpu_oracle* o, const char* path) {
         require_replicated(o, "oracle_save");
         CK(cudaSetDevice(o->ctx->device));
         const Reordered& R = o->R;
-        std::FILE* f = std::fopen(path, "wb");
-        if (!f) throw Fail{PSP_EIO, std::string(path) + ": cannot open for writing"};
-        std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, std::fclose);
+        const int fd = ::open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (fd < 0) throw Fail{PSP_EIO, std::string(path) + ": cannot open for writing"};
+        struct Fd {
+            int fd;
+            ~Fd() { ::close(fd); }
+        } fd_guard{fd};
         Crc64Stream crc;
         // header and id sections (src/oracle_io.cpp:106-127)
         std::vector<uint8_t> head = {'P', 'S', 'P', '1', 1, 0, 0, 0};
@@ -246,13 +249,11 @@ psp_status psp_gpu_oracle_save(const psp_gpu_oracle* o, const char* path) {
         head.insert(head.end(), packed.begin(), packed.end());
         for (uint32_t c = 0; c <= R.k; ++c) put_u64s(head, R.comp_off[c]);
         crc.update(head.data(), head.size());
-        if (std::fwrite(head.data(), 1, head.size(), f) != head.size())
-            throw Fail{PSP_EIO, "oracle write failed"};
-        if (o->kind.kind == PSP_VALUE_U32) save_tables<uint32_t>(o, f, crc);
-        else save_tables<float>(o, f, crc);
+        pwrite_all(fd, head.data(), head.size(), 0);
+        const uint64_t end = o->kind.kind == PSP_VALUE_U32 ? save_tables<uint32_t>(o, fd, head.size(), crc)
+                                                          : save_tables<float>(o, fd, head.size(), crc);
         const uint64_t sum = crc.value();
-        if (std::fwrite(&sum, 1, 8, f) != 8 || std::fflush(f) != 0)
-            throw Fail{PSP_EIO, "oracle write failed"};
+        pwrite_all(fd, &sum, 8, end);
     });
 }
 
