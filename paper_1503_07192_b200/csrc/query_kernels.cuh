@@ -1365,10 +1365,12 @@ __device__ __forceinline__ void group_task_rb16(const QueryView<V>& q, const Gro
     const uint32_t* bj = ax + 4 + B1p + cg * 32;    // b_j of this column group
     const V* __restrict__ cb1 = q.cb + q.cb_off[c1];
     const V* __restrict__ cb2 = q.cb + q.cb_off[c2];
-    uint16_t* b16[2] = {reinterpret_cast<uint16_t*>(st->b[0]), reinterpret_cast<uint16_t*>(st->b[0]) + 16 * 32};
+    // chunk buffers by arithmetic (arrays of pointers indexed by `buf` went to local memory)
+    uint16_t* const b16_0 = reinterpret_cast<uint16_t*>(st->b[0]);
+    auto b16 = [&](int bb) { return b16_0 + bb * (16 * 32); };
     uint32_t* base = reinterpret_cast<uint32_t*>(st->b[1]);     // [GQ]
-    uint32_t* abuf[2] = {base + GQ, base + GQ + 16};             // a_i of each chunk
-    uint32_t* sa[2] = {reinterpret_cast<uint32_t*>(st->a[0]), reinterpret_cast<uint32_t*>(st->a[1])};
+    auto abuf = [&](int bb) { return base + GQ + 16 * bb; };    // a_i of each chunk
+    auto sa = [&](int bb) { return reinterpret_cast<uint32_t*>(st->a[bb]); };
     __syncwarp();
     const V* my_row1 = cb1;
     if (uint32_t(lane) < m) {
@@ -1388,17 +1390,17 @@ __device__ __forceinline__ void group_task_rb16(const QueryView<V>& q, const Gro
     }
     cp_async_commit();
     auto issue = [&](uint32_t k0, int buf) {
-        uint32_t* sa_l = sa[buf] + lane * GA_STRIDE;
+        uint32_t* sa_l = sa(buf) + lane * GA_STRIDE;
         if (uint32_t(lane) < m) {
 #pragma unroll
             for (int t = 0; t < GK / 4; ++t)
                 cp_async16(sa_l + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
         }
-        if (lane < GK / 4) cp_async16(abuf[buf] + 4 * lane, arow + k0 + 4 * lane, true);
+        if (lane < GK / 4) cp_async16(abuf(buf) + 4 * lane, arow + k0 + 4 * lane, true);
         cp_async_commit();
         if (lane == 0) {
             mbar_expect_tx(&st->bar[buf], GK * 32 * sizeof(uint16_t));
-            bulk_g2s(b16[buf], bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(uint16_t), &st->bar[buf]);
+            bulk_g2s(b16(buf), bq_task + uint64_t(k0) * 32, GK * 32 * sizeof(uint16_t), &st->bar[buf]);
         }
     };
     uint32_t acc[16];
@@ -1413,13 +1415,13 @@ __device__ __forceinline__ void group_task_rb16(const QueryView<V>& q, const Gro
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncwarp();
         if (uint32_t(lane) < m) {  // row1 + a_i - base, saturated, in both halves
-            uint32_t* row = sa[buf] + lane * GA_STRIDE;
+            uint32_t* row = sa(buf) + lane * GA_STRIDE;
             const uint64_t bq = base[lane];
             const uint32_t rows = min(uint32_t(GK), B1 - k0);
 #pragma unroll
             for (int t = 0; t < GK / 4; ++t) {
                 const uint4 r4 = *reinterpret_cast<const uint4*>(row + 4 * t);
-                const uint4 a4 = *reinterpret_cast<const uint4*>(abuf[buf] + 4 * t);
+                const uint4 a4 = *reinterpret_cast<const uint4*>(abuf(buf) + 4 * t);
                 const uint32_t rv[4] = {r4.x, r4.y, r4.z, r4.w}, av[4] = {a4.x, a4.y, a4.z, a4.w};
                 uint32_t o[4];
 #pragma unroll
@@ -1436,14 +1438,14 @@ __device__ __forceinline__ void group_task_rb16(const QueryView<V>& q, const Gro
         mbar_wait(&st->bar[buf], (phase >> buf) & 1u);
         phase ^= 1u << buf;
         __syncwarp();
-        rb16_chunk_v(v, sa[buf], b16[buf], acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, lane);
+        rb16_chunk_v(v, sa(buf), b16(buf), acc, (min(uint32_t(GK), B1 - k0) + 3) & ~3u, lane);
         __syncwarp();  // buffer `buf` is refilled by the next issue
         buf ^= 1;
     }
     cp_async_wait<0>();  // col2 (also covers B1 == 0)
     __syncwarp();
-    uint32_t* red_e = sa[0];          // [query][9] over a[0], free after the last chunk
-    uint32_t* red_l = sa[0] + GQ * 9;
+    uint32_t* red_e = sa(0);          // [query][9] over a[0], free after the last chunk
+    uint32_t* red_l = sa(0) + GQ * 9;
     static_assert(2 * GQ * 9 <= GQ * GA_STRIDE, "reduction scratch fits a[0]");
     rb16_combine_v(v, acc, reinterpret_cast<const uint32_t*>(st->c2), base, bjq, cg * 32, B2, red_e,
                    red_l, lane, sat);
