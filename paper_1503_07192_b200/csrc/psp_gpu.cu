@@ -491,12 +491,47 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
                 return;
             }
         }
+        auto ops = [&] {
+            if (!minplus_ops) return;
+            for (uint64_t i = 0; i < count; ++i) {
+                const uint32_t c1 = R.assign[R.perm[v1[i]]], c2 = R.assign[R.perm[v2[i]]];
+                const uint64_t b1 = R.bnd_off[c1 + 1] - R.bnd_off[c1];
+                const uint64_t b2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
+                minplus_ops[i] = b1 * b2 + b2;  // src/query.cpp:73
+            }
+        };
         const size_t need = count * (sizeof(double) + 2 * sizeof(uint32_t)) + 16;
         if (mo->query_stage.bytes < need) mo->query_stage.alloc(need);
         double* dd = mo->query_stage.as<double>();
         uint32_t* d1 = reinterpret_cast<uint32_t*>(dd + count);
         uint32_t* d2 = d1 + count;
         uint32_t* dbad = d2 + count;
+        if (count <= psp_gpu_oracle::kPinnedPairs) {
+            // device staging is [dist | v1 | v2 | bad]: the pairs go in with one
+            // copy from pinned memory, [dist | ... | bad] come back in two, one sync
+            if (mo->host_stage_bytes < need) {
+                if (mo->host_stage) cudaFreeHost(mo->host_stage);
+                mo->host_stage = nullptr;
+                mo->host_stage_bytes = 0;
+                CK(cudaMallocHost(&mo->host_stage, need));
+                mo->host_stage_bytes = need;
+            }
+            double* hd = static_cast<double*>(mo->host_stage);
+            uint32_t* h1 = reinterpret_cast<uint32_t*>(hd + count);
+            std::memcpy(h1, v1, count * 4);
+            std::memcpy(h1 + count, v2, count * 4);
+            h1[2 * count] = 0;  // bad flag
+            CK(cudaMemcpyAsync(d1, h1, (2 * count + 1) * 4, cudaMemcpyHostToDevice, s));
+            if (o->kind.kind == PSP_VALUE_U32) launch_queries<uint32_t>(o, count, d1, d2, dd, s, dbad);
+            else launch_queries<float>(o, count, d1, d2, dd, s, dbad);
+            CK(cudaMemcpyAsync(hd, dd, count * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h1 + 2 * count, dbad, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (h1[2 * count]) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
+            std::memcpy(dist, hd, count * 8);
+            ops();
+            return;
+        }
         CK(cudaMemsetAsync(dbad, 0, sizeof(uint32_t), s));
         CK(cudaMemcpyAsync(d1, v1, count * 4, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d2, v2, count * 4, cudaMemcpyHostToDevice, s));
@@ -507,14 +542,7 @@ psp_status psp_gpu_query_batch(const psp_gpu_oracle* o, uint64_t count, const ui
         CK(cudaStreamSynchronize(s));
         if (bad) throw ArgError("query: vertex id out of range");  // src/query.cpp:30
         CK(cudaMemcpyAsync(dist, dd, count * 8, cudaMemcpyDeviceToHost, s));
-        if (minplus_ops) {
-            for (uint64_t i = 0; i < count; ++i) {
-                const uint32_t c1 = R.assign[R.perm[v1[i]]], c2 = R.assign[R.perm[v2[i]]];
-                const uint64_t b1 = R.bnd_off[c1 + 1] - R.bnd_off[c1];
-                const uint64_t b2 = R.bnd_off[c2 + 1] - R.bnd_off[c2];
-                minplus_ops[i] = b1 * b2 + b2;  // src/query.cpp:73
-            }
-        }
+        ops();
         CK(cudaStreamSynchronize(s));
     });
 }
