@@ -171,6 +171,36 @@ def query_bytes_and_ops(o, v1, v2):
     return float(byts.sum()), float(ops.sum())
 
 
+def grouped_executed_relaxations(k, bsize, c1, c2):
+    """Relaxations query_grouped EXECUTES for a batch (thread level, incl. the
+    padding of its lane layout), from the task rules of group_tasks /
+    group_emit and group_task_rb (query_kernels.cuh): pairs oriented c1 <= c2
+    and binned; a bin's nq queries split into ceil(nq / 32) balanced items
+    (mbig = min(32, ceil(nq / items) rounded up to 4)); per item and 32-column
+    group, 4 * ceil(m / 4) query slots x 32 columns (the pair's last group, if
+    it holds <= 16 columns: 8 * ceil(m / 8) slots x 16 columns) x the rows
+    walked (16-row chunks, each rounded up to 4 rows) plus one pass for the
+    col2 combine. `useful / executed` is the padding share of the ALU work."""
+    a = np.minimum(c1, c2).astype(np.int64)
+    b = np.maximum(c1, c2).astype(np.int64)
+    keys, nq = np.unique(a * k + b, return_counts=True)
+    B1 = bsize[keys // k].astype(np.int64)
+    B2 = bsize[keys % k].astype(np.int64)
+    items = (nq + 31) // 32
+    mbig = np.minimum(32, ((nq + items - 1) // items + 3) // 4 * 4)
+    m_last = nq - (items - 1) * mbig
+    ncg = (B2 + 31) // 32
+    half = (B2 - (ncg - 1) * 32) <= 16
+    rows = 16 * (B1 // 16) + (B1 % 16 + 3) // 4 * 4 + 1
+
+    def per_item(m):
+        full = (ncg - half) * (4 * ((m + 3) // 4)) * 32
+        tail = half * (8 * ((m + 7) // 8)) * 16
+        return (full + tail) * rows
+
+    return float(((items - 1) * per_item(mbig) + per_item(m_last)).sum())
+
+
 def ncu_traffic(kernel: str, config: str | None = None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
     committed `ncu --set full` capture of this kernel on this workload
@@ -217,7 +247,7 @@ def launches_per_batch(o, batch):
 
 
 def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, world,
-                   peak_insn="VIADDMNMX.U32", config=None):
+                   peak_insn="VIADDMNMX.U32", config=None, texec=None):
     """Dominant kernel of the query step. Dense batches (>= 2 queries per
     component pair) run query_grouped, which reuses each pair's boundary
     block from shared memory: it is bound by the min-plus ALU rate, so
@@ -238,6 +268,11 @@ def roofline_entry(o, batch, steps, tb, tops, per_launch_ms, peaks, peak_u32, wo
                 "traffic": traffic, "traffic_source": src,
                 "peak_source": f"in-run min-plus probe ({peak_insn}), see profiles/r1_minplus_peak.json",
                 "ops_per_query": round(ops_launch / batch, 1),
+                # the kernel's own ALU rate: executed relaxations incl. the
+                # lane layout's padding (grouped_executed_relaxations; within
+                # 0.5% of ncu's VIADDMNMX count x 32 at cfg3)
+                "executed_frac": round(texec / steps / secs / peak_u32, 4) if texec else None,
+                "useful_share_of_executed": round(tops / texec, 4) if texec else None,
                 "no_reuse_bytes_per_query": round(bytes_launch / batch, 1),
                 "no_reuse_equiv_gbs": round(bytes_launch / secs / 1e9, 1),
                 "hbm_peak_gbs": peaks["hbm_gbs"]}
@@ -333,6 +368,17 @@ def run_ours(args, rank, world, local):
     barrier()
     # algorithmic bytes of the timed launches
     tb, tops = query_bytes_and_ops(o, v1[args.warmup * batch:], v2[args.warmup * batch:])
+    texec = None
+    if kernel_for(o, batch) == "grouped":
+        # executed (padded) relaxations: exact for the first timed batch, the
+        # others are draws of the same distribution (x steps)
+        comp = o.assignment[o.permutation]
+        bsize = np.diff(o.boundary_offset).astype(np.int64)
+        i0 = args.warmup * batch
+        texec = args.steps * grouped_executed_relaxations(o.k, bsize, comp[v1[i0:i0 + batch]],
+                                                          comp[v2[i0:i0 + batch]])
+        tops0 = query_bytes_and_ops(o, v1[i0:i0 + batch], v2[i0:i0 + batch])[1]
+        texec *= (tops / args.steps) / tops0  # same useful work as the timed steps on average
 
     # ---- e2e through the public host API (pinned host buffers)
     h_v1 = torch.from_numpy(v1.view(np.int32)).pin_memory()
@@ -446,7 +492,7 @@ def run_ours(args, rank, world, local):
                 "sync_api": "psp_gpu_query_batch (one blocking call per step)"},
         "gpu_launches": args.steps * launches_per_batch(o, batch),
         "roofline": roofline_entry(o, batch, args.steps, tb, tops, per_launch_ms, peaks,
-                                   peak_u32, world, peak_insn, args.config),
+                                   peak_u32, world, peak_insn, args.config, texec),
         "preprocessing": {
             "graph_gen_s": round(gen_s, 2),
             "partition_s": round(st["partition_ms"] / 1e3, 3),
