@@ -166,7 +166,39 @@ psp_status psp_gpu_build_oracle(psp_gpu_ctx* ctx, uint64_t n, uint64_t m, const 
         if (workers < 1) throw ArgError("build_oracle: workers must be at least 1");
         const Csr g = build_csr(n, m, eu, ev, ew);
         auto t0 = Clock::now();
-        const std::vector<uint32_t> a = partition_graph(g, k, seed, workers);
+        // multi-GPU: the partition is deterministic (workers never change it,
+        // include/psp/oracle.hpp:80-84), so rank 0 computes it with all host
+        // threads and broadcasts it instead of every rank competing for the
+        // same cores
+        std::vector<uint32_t> a;
+        if (ctx->world > 1) {
+            CK(cudaSetDevice(ctx->device));
+            uint64_t ok = 1;
+            std::exception_ptr err;  // rank 0's failure, rethrown after the broadcast
+            if (ctx->rank == 0) {
+                try {
+                    a = partition_graph(g, k, seed, workers);
+                } catch (...) {
+                    ok = 0;
+                    err = std::current_exception();
+                }
+            }
+            DBuf d((size_t(n) + 2) * 4);
+            if (ctx->rank == 0) {
+                if (ok) CK(cudaMemcpyAsync(d.as<uint32_t>() + 2, a.data(), size_t(n) * 4, cudaMemcpyHostToDevice, ctx->stream));
+                CK(cudaMemcpyAsync(d.p, &ok, 8, cudaMemcpyHostToDevice, ctx->stream));
+            }
+            NCK(nccl().Broadcast(d.p, d.p, (size_t(n) + 2) * 4, ncclUint8, 0, ctx->comm, ctx->stream));
+            CK(cudaMemcpyAsync(&ok, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            if (err) std::rethrow_exception(err);
+            if (!ok) throw ArgError("partition_graph failed on rank 0");
+            a.resize(n);
+            CK(cudaMemcpyAsync(a.data(), d.as<uint32_t>() + 2, size_t(n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        } else {
+            a = partition_graph(g, k, seed, workers);
+        }
         const double part_ms = ms_since(t0);
         psp_gpu_oracle* o = build_from_csr(ctx, g, k, a, ew, m, value_kind, part_ms, stats);
         set_peak_entries(o->R, workers, stats);
