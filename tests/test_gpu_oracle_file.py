@@ -105,3 +105,31 @@ def test_damaged_files_raise_the_reference_error_classes(tmp_path):
         P.load_oracle(write("trail.psp", data + b"\0"))
     with pytest.raises(P.OracleIoError):
         P.load_oracle(str(tmp_path / "missing.psp"))
+
+
+def test_streamed_load_value_kinds(ref, tmp_path):
+    # the streamed loader decides the value kind from the whole table section
+    # (choose_kind_tables semantics): a reference image of a graph with
+    # non-dyadic f64 weights cannot be u32 -> EOVERFLOW when u32 is demanded,
+    # f32 within 1e-5 of the reference otherwise; a dyadic (1/1024-lattice)
+    # one loads as exact u32 at q > 0 (the second conversion pass)
+    rng = np.random.default_rng(4)
+    g0 = P.generate_grid(20, 20)
+    v1, v2 = P.random_pairs(g0.n, 4000, 5)
+    for weights, want_kind in ((rng.uniform(1, 2, g0.m), P.VALUE_F32),
+                               (np.round(rng.uniform(1, 2, g0.m) * 1024) / 1024, P.VALUE_U32)):
+        g = P.Graph(g0.n, g0.eu, g0.ev, weights)
+        ro = ref.graph(g.n, g.eu, g.ev, g.ew).build_oracle(6, 1, 0)
+        f = str(tmp_path / f"kind{want_kind}.psp")
+        ro.save(f)
+        truth = ro.batch_query(v1, v2, 1)
+        od = P.load_oracle(f)
+        assert od.value_kind == want_kind
+        d = od.batch_query(v1, v2)
+        if want_kind == P.VALUE_U32:
+            assert od.fixed_point_shift > 0
+            assert np.array_equal(d, truth)
+        else:
+            assert np.allclose(d, truth, rtol=1e-5, atol=0)
+            with pytest.raises(P.PspValueError):
+                P.load_oracle(f, value_kind=P.VALUE_U32)
