@@ -11,17 +11,22 @@
 // c1 < c2). In u32 the result is exact either way; in f32 the three-term sums
 // may round differently, which the 1e-5 tolerance covers.
 //
-// Two kernels:
-//  * query_grouped (dense batches): queries are counting-sorted by the
-//    component pair (c1, c2). One CTA takes up to QT queries of one pair and
-//    streams that pair's B1 x B2 boundary block through shared memory ONCE
-//    for all of them, as a register-blocked min-plus product
-//    (QT queries x B1) (x) (B1 x B2) followed by the combine with col2.
-//    HBM traffic drops from B1*B2*4 bytes per query to per (pair, 32
-//    queries); the kernel is then bound by the min-plus ALU rate.
-//  * query_warp (sparse batches, < ~4 queries per pair): one warp per query,
-//    lanes own target columns, every row segment of the block is fetched by
-//    the whole warp at once so DRAM sees full contiguous segments.
+// Kernels:
+//  * query_grouped (batches above 16K pairs): queries are grouped by the
+//    component pair (c1, c2); one warp takes up to 32 queries of one pair x
+//    one 32-column group and streams that block through shared memory ONCE
+//    for all of them, as a register-blocked min-plus product followed by
+//    the combine with col2. HBM traffic drops from B1*B2*4 bytes per query
+//    to per (pair, 32 queries); the kernel is then bound by the min-plus
+//    ALU rate.
+//  * query_cta (batches up to 16K pairs, no grouping pass): one CTA per
+//    query over the same block layout; latency-bound, so shaped for
+//    residency (64 warps per SM).
+//  * query_server: one resident CTA answering point queries from a mailbox
+//    in mapped host memory (no launch per call).
+//  * query_warp (PSP_QUERY_KERNEL=warp, k^2 past 31-bit keys): one warp per
+//    query, lanes own target columns, every row segment of the block is
+//    fetched by the whole warp at once so DRAM sees full segments.
 #pragma once
 #include "fw_kernels.cuh"  // mbarrier / bulk-copy helpers
 #include "minplus.cuh"
