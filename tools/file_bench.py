@@ -1,7 +1,8 @@
 """PSP1 oracle file throughput: build a configuration on
 cuda:0, write its oracle file from the device tables (psp_gpu_oracle_save:
-f64 conversion + CRC-64/XZ on the GPU, fwrite overlapped with the next
-window), read it back (psp_gpu_oracle_load: CRC on the GPU, import), check
+f64 conversion + CRC-64/XZ on the GPU, parallel pwrites overlapped with the
+next chunk), read it back (psp_gpu_oracle_load: parallel preads streamed to
+the device, CRC and conversion there), check
 the reloaded oracle answers like the original, report GB/s.
 
   python tools/file_bench.py --config delaunay262k_k256 [--dir /tmp]
