@@ -362,6 +362,14 @@ psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, d
 psp_status psp_delaunay_edges(uint64_t n, const double* xy, uint64_t cap, uint32_t* eu,
                               uint32_t* ev, uint64_t* m);
 
+/* Minimum spanning forest of an edge list under the keys `key` (Kruskal;
+ * in_tree[e] = 1 for forest edges). With distinct keys it is the unique
+ * forest scipy's minimum_spanning_tree returns; used by the road-like grid of
+ * BASELINE.json configs[3] (workloads.py road_grid). Not a reference symbol:
+ * bench/test input tooling. */
+psp_status psp_min_spanning_forest(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                                   const double* key, uint8_t* in_tree);
+
 /* ref::random_pairs / the CLI's random_pairs (tests/support/reference.hpp:
  * 80-91, tools/psp_main.cpp:108-120): mt19937_64, v1 = rng() % n then v2. */
 void psp_random_pairs(uint64_t n, uint64_t count, uint64_t seed, uint32_t* v1, uint32_t* v2);

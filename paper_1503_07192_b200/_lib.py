@@ -183,6 +183,7 @@ SIGNATURES = {
     "psp_generate_grid": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_double,
                                     C.c_double, C.c_uint64, C.POINTER(C.c_uint64), _vp, _vp,
                                     _vp]),
+    "psp_min_spanning_forest": (C.c_int, [C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p, _u8p]),
     "psp_delaunay_edges": (C.c_int, [C.c_uint64, _f64p, C.c_uint64, _u32p, _u32p,
                                      C.POINTER(C.c_uint64)]),
     "psp_random_pairs": (None, [C.c_uint64, C.c_uint64, C.c_uint64, _u32p, _u32p]),

@@ -4,6 +4,7 @@
 #include "host_graph.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -184,6 +185,51 @@ void generate_grid(int kind, uint64_t rows, uint64_t cols, bool unit, double lo,
                 else push(v + 1, v + cols, draw());
             }
         }
+}
+
+void min_spanning_forest(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                         const double* key, uint8_t* in_tree) {
+    // stable LSD radix sort of the edge ids by key: non-negative doubles
+    // order like their bit patterns (negative keys: sorted by value below)
+    std::vector<uint64_t> bits(m);
+    bool nonneg = true;
+    for (uint64_t e = 0; e < m; ++e) {
+        if (!(key[e] >= 0.0)) nonneg = false;
+        std::memcpy(&bits[e], &key[e], 8);
+    }
+    std::vector<uint32_t> order(m), tmp(m);
+    std::iota(order.begin(), order.end(), 0u);
+    if (nonneg) {
+        uint64_t diff = 0;  // only the bit positions that vary need passes
+        for (uint64_t e = 1; e < m; ++e) diff |= bits[e] ^ bits[0];
+        for (int shift = 0; shift < 64 && (diff >> shift); shift += 16) {
+            std::vector<uint64_t> cnt(65537, 0);
+            for (uint64_t e = 0; e < m; ++e) ++cnt[((bits[order[e]] >> shift) & 0xffff) + 1];
+            for (int d = 0; d < 65536; ++d) cnt[d + 1] += cnt[d];
+            for (uint64_t e = 0; e < m; ++e) tmp[cnt[(bits[order[e]] >> shift) & 0xffff]++] = order[e];
+            order.swap(tmp);
+        }
+    } else {
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
+    }
+    std::vector<uint32_t> parent(n), size(n, 1);
+    std::iota(parent.begin(), parent.end(), 0u);
+    auto find = [&](uint32_t x) {
+        while (parent[x] != x) {
+            parent[x] = parent[parent[x]];
+            x = parent[x];
+        }
+        return x;
+    };
+    std::fill(in_tree, in_tree + m, uint8_t(0));
+    for (uint32_t e : order) {
+        uint32_t a = find(eu[e]), b = find(ev[e]);
+        if (a == b) continue;
+        if (size[a] < size[b]) std::swap(a, b);
+        parent[b] = a;
+        size[a] += size[b];
+        in_tree[e] = 1;
+    }
 }
 
 }  // namespace pspg

@@ -61,6 +61,12 @@ Reordered reorder(const Csr& g, uint32_t k, const std::vector<uint32_t>& assignm
 std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, unsigned threads);
 
 // generators (src/generators.cpp:50-93)
+// Minimum spanning forest under edge keys (Kruskal: keys sorted stably, ties
+// by edge index; union-find). in_tree[e] = 1 for forest edges. With distinct
+// keys the forest is unique, so it equals scipy's minimum_spanning_tree.
+void min_spanning_forest(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                         const double* key, uint8_t* in_tree);
+
 void generate_grid(int kind, uint64_t rows, uint64_t cols, bool unit, double lo, double hi,
                    uint64_t seed, std::vector<uint32_t>& eu, std::vector<uint32_t>& ev,
                    std::vector<double>& ew);

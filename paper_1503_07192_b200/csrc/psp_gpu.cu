@@ -992,6 +992,17 @@ psp_status psp_generate_grid(int kind, uint64_t rows, uint64_t cols, int unit, d
     });
 }
 
+psp_status psp_min_spanning_forest(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev,
+                                   const double* key, uint8_t* in_tree) {
+    return guarded([&] {
+        if (m && (!eu || !ev || !key || !in_tree)) throw ArgError("min_spanning_forest: NULL argument");
+        if (n > 0xffffffffull || m > 0xffffffffull) throw ArgError("min_spanning_forest: too large");
+        for (uint64_t e = 0; e < m; ++e)
+            if (eu[e] >= n || ev[e] >= n) throw ArgError("min_spanning_forest: vertex id out of range");
+        min_spanning_forest(n, m, eu, ev, key, in_tree);
+    });
+}
+
 psp_status psp_delaunay_edges(uint64_t n, const double* xy, uint64_t cap, uint32_t* eu,
                               uint32_t* ev, uint64_t* m) {
     return guarded([&] {

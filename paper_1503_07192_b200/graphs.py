@@ -51,8 +51,22 @@ def delaunay(n: int, seed: int = 1) -> Graph:
     return _graph(delaunay_arrays(n, seed))
 
 
+def spanning_forest_mask(n, eu, ev, key):
+    """C++ Kruskal (psp_min_spanning_forest): the same forest as scipy's for
+    distinct keys, without the sparse-matrix round trip."""
+    import numpy as np
+
+    from . import _lib
+    eu = np.ascontiguousarray(eu, np.uint32)
+    ev = np.ascontiguousarray(ev, np.uint32)
+    mask = np.empty(len(eu), np.uint8)
+    _lib.check(_lib.lib().psp_min_spanning_forest(n, len(eu), eu, ev,
+                                                   np.ascontiguousarray(key, np.float64), mask))
+    return mask.astype(bool)
+
+
 def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10) -> Graph:
-    return _graph(workloads.road_grid(rows, cols, seed, drop))
+    return _graph(workloads.road_grid(rows, cols, seed, drop, tree_mask=spanning_forest_mask))
 
 
 def _grid(rows, cols, weights, seed):
@@ -65,5 +79,5 @@ def make(name: str) -> tuple[Graph, dict]:
     cfg = dict(CONFIGS[name])
     if cfg["family"] == "delaunay":
         return _graph(delaunay_arrays(cfg["n"], cfg["seed"])), cfg
-    arrays, cfg = workloads.make_arrays(name, grid=_grid)
+    arrays, cfg = workloads.make_arrays(name, grid=_grid, tree_mask=spanning_forest_mask)
     return _graph(arrays), cfg

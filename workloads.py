@@ -56,15 +56,31 @@ def delaunay(n: int, seed: int = 1):
     return n, e[:, 0].astype(np.uint32), e[:, 1].astype(np.uint32), w
 
 
-def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10):
+def scipy_tree_mask(n, eu, ev, key):
+    """Edges of the minimum spanning forest under `key` (scipy), as a mask."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import minimum_spanning_tree
+
+    mst = minimum_spanning_tree(coo_matrix((key, (eu, ev)), shape=(n, n)).tocsr()).tocoo()
+    tree = np.zeros(len(eu), bool)
+    # map MST edges back to edge ids (the grid edge (u, v) is unique)
+    lin = eu * n + ev
+    order = np.argsort(lin)
+    mlin = np.minimum(mst.row, mst.col).astype(np.int64) * n + np.maximum(mst.row, mst.col)
+    pos = np.searchsorted(lin[order], mlin)
+    tree[order[pos]] = True
+    return tree
+
+
+def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10, tree_mask=None):
     """Road-like perturbed grid: jittered 4-neighbour grid, a random spanning
     tree kept (minimum spanning tree under random keys, so deletions never
     disconnect the network) and ~`drop` of the remaining edges removed;
     weights = Euclidean length of the jittered embedding x U[1, 2), rounded to
-    f32 (the tolerance path: not dyadic, so the device computes in f32)."""
-    from scipy.sparse import coo_matrix
-    from scipy.sparse.csgraph import minimum_spanning_tree
-
+    f32 (the tolerance path: not dyadic, so the device computes in f32).
+    `tree_mask(n, eu, ev, key)` computes the spanning forest (default: scipy;
+    the product passes its C++ Kruskal, psp_min_spanning_forest)."""
+    tree_mask = tree_mask or scipy_tree_mask
     rng = np.random.default_rng(seed)
     n = rows * cols
     r, c = np.divmod(np.arange(n, dtype=np.int64), cols)
@@ -74,14 +90,7 @@ def road_grid(rows: int, cols: int, seed: int = 7, drop: float = 0.10):
     eu = np.concatenate([right, down])
     ev = np.concatenate([right + 1, down + cols])
     key = rng.random(len(eu)) + 1.0  # distinct positive keys -> random spanning tree
-    mst = minimum_spanning_tree(coo_matrix((key, (eu, ev)), shape=(n, n)).tocsr()).tocoo()
-    tree = np.zeros(len(eu), bool)
-    # map MST edges back to edge ids (the grid edge (u, v) is unique)
-    lin = eu * n + ev
-    order = np.argsort(lin)
-    mlin = np.minimum(mst.row, mst.col).astype(np.int64) * n + np.maximum(mst.row, mst.col)
-    pos = np.searchsorted(lin[order], mlin)
-    tree[order[pos]] = True
+    tree = tree_mask(n, eu, ev, key)
     keep = tree | (rng.random(len(eu)) >= drop)
     eu, ev = eu[keep], ev[keep]
     length = np.linalg.norm(xy[eu] - xy[ev], axis=1)
@@ -110,7 +119,7 @@ CONFIGS = {
 }
 
 
-def make_arrays(name: str, grid=None):
+def make_arrays(name: str, grid=None, tree_mask=None):
     """(n, eu, ev, ew), cfg for a named configuration. The grid family is the
     reference's generate_grid (mt19937_64 weights): pass `grid(rows, cols,
     weights, seed) -> (n, eu, ev, ew)` from whichever library should draw it."""
@@ -123,7 +132,7 @@ def make_arrays(name: str, grid=None):
     elif fam == "delaunay":
         arrays = delaunay(cfg["n"], cfg["seed"])
     elif fam == "road":
-        arrays = road_grid(cfg["rows"], cfg["cols"], cfg["seed"])
+        arrays = road_grid(cfg["rows"], cfg["cols"], cfg["seed"], tree_mask=tree_mask)
     else:
         raise ValueError(fam)
     return arrays, cfg
