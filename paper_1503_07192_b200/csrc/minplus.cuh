@@ -85,8 +85,11 @@ __host__ __device__ __forceinline__ uint64_t sym_off(uint32_t i, uint32_t j, uin
     return tidx(i / T, j / T, nb) * TT + uint64_t(i % T) * T + (j % T);
 }
 
-// Row stride of the query-side to-boundary tables: |B(C)| rounded up to 4.
-__host__ __device__ __forceinline__ uint32_t cb_stride(uint32_t B) { return (B + 3u) & ~3u; }
+// Row stride of the query-side to-boundary tables: |B(C)| rounded up to 16
+// (INF padded), so a query's row1 for any 16-row chunk of its pair block
+// (rows < B1 rounded up to 16) lies inside its row: the grouped product
+// stages it with unpredicated 16-byte copies.
+__host__ __device__ __forceinline__ uint32_t cb_stride(uint32_t B) { return (B + 15u) & ~15u; }
 
 // A batch of matrices sharing one tile arena (component tables: k matrices;
 // boundary graph: one). Arrays are device pointers indexed by matrix.

@@ -1198,7 +1198,7 @@ __device__ __forceinline__ void group_task_rb(const QueryView<V>& q, const Group
         V* sa = st->a[buf] + lane * GA_STRIDE;
         if (uint32_t(lane) < m) {
 #pragma unroll
-            for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, k0 + 4 * t < Bp1);
+            for (int t = 0; t < GK / 4; ++t) cp_async16(sa + 4 * t, my_row1 + k0 + 4 * t, true);  // k0 + 16 <= B1p <= Bp1
         }
         cp_async_commit();
         if (lane == 0) {
