@@ -313,6 +313,13 @@ def run_ours(args, rank, world, local):
     g, cfg = graphs.make(args.config)
     gen_s = time.time() - t0
     threads = os.cpu_count() or 8
+
+    def alloc_stats():
+        out = np.zeros(4, np.uint64)
+        P._lib.check(P._lib.lib().psp_gpu_alloc_stats(out))
+        return out.astype(np.float64)
+
+    alloc0 = alloc_stats()
     if world > 1:
         # one host partition (all cores, rank 0), broadcast, then the
         # collective device build with the boundary-graph FW row-sharded
@@ -330,6 +337,7 @@ def run_ours(args, rank, world, local):
     else:
         o = P.build_oracle(g, cfg["k"], threads, 0, ctx=ctx)
     st = o.stats
+    alloc = alloc_stats() - alloc0  # host time inside cudaMalloc / cudaFree during the build
 
     stream = torch.cuda.Stream(device=dev)
     batch = args.batch or cfg["queries"]
@@ -504,6 +512,10 @@ def run_ours(args, rank, world, local):
                                  "k1_order": round(st["k1_order_ms"] / 1e3, 3),
                                  "k2_order_layout": round(st["bg_order_ms"] / 1e3, 3)},
             "boundary_minus_k2_device_s": round((st["boundary_ms"] - st["k2_device_ms"]) / 1e3, 3),
+            # driver time inside the build's cudaMalloc / cudaFree calls (single
+            # calls have stalled for 0.1-1 s on these boxes: the wall-clock noise)
+            "driver_alloc": {"malloc_s": round(alloc[0] / 1e9, 3), "malloc_calls": int(alloc[1]),
+                             "free_s": round(alloc[2] / 1e9, 3), "free_calls": int(alloc[3])},
             "k2_positions": st["k2_positions"],
             "k1_device_s": round(k1_ms / 1e3, 4), "k2_device_s": round(k2_ms / 1e3, 4),
             "k2_relax_per_s": k2_rate, "k2_alu_frac_per_gpu": round(k2_rate / (peak_u32 * world), 4),

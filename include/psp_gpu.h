@@ -126,6 +126,11 @@ void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx);
 enum psp_boundary_storage { PSP_STORAGE_REPLICATED = 0, PSP_STORAGE_ROW_SHARDED = 1 };
 psp_status psp_gpu_ctx_set_boundary_storage(psp_gpu_ctx* ctx, int storage);
 
+/* Process totals of the host time spent inside cudaMalloc / cudaFree of the
+ * library's device buffers (diagnostics: single calls can stall for 0.1-1 s
+ * on a busy driver): out4 = {malloc ns, malloc calls, free ns, free calls}. */
+psp_status psp_gpu_alloc_stats(uint64_t* out4);
+
 /* ------------------------------------------------------- preprocessing -- */
 /* psp::build_oracle (include/psp/oracle.hpp:85-86, src/oracle.cpp:144-194):
  * partition + reorder on the host (identical assignment to the reference's

@@ -134,6 +134,7 @@ SIGNATURES = {
     "psp_gpu_nccl_unique_id": (C.c_int, [_vp]),
     "psp_gpu_ctx_stream": (_vp, [_vp]),
     "psp_gpu_ctx_set_boundary_storage": (C.c_int, [_vp, C.c_int]),
+    "psp_gpu_alloc_stats": (C.c_int, [_u64p]),
     "psp_gpu_build_oracle": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _u32p, _u32p, _f64p,
                                        C.c_uint32, C.c_uint32, C.c_uint64, C.c_int,
                                        C.POINTER(_vp), C.POINTER(BuildStats)]),

@@ -175,10 +175,15 @@ struct EventTimer {
 };
 
 // Query-side tables and id maps on the device (shared by build and import).
+// The id maps and the to-boundary arena, allocated and uploaded ahead of
+// time: the build does it before K2, where device allocations are quick
+// (right after K2 single small cudaMalloc calls have taken ~0.1 s each on
+// these boxes, PSP_ALLOC_LOG), and finish_query_tables only fills them.
 template <class V>
-void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
+void alloc_query_tables(psp_gpu_oracle* o, cudaStream_t s) {
     const Reordered& R = o->R;
     const uint32_t k = R.k;
+    if (o->d_cb.p && o->d_perm.p) return;
     std::vector<uint64_t> cb_off(k + 1, 0);
     for (uint32_t c = 0; c < k; ++c)
         cb_off[c + 1] = cb_off[c] + uint64_t(R.comp_off[c + 1] - R.comp_off[c]) *
@@ -186,9 +191,15 @@ void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
     o->d_cb.alloc(cb_off[k] * sizeof(V));
     o->d_cb_off = upload(cb_off, s);
     o->d_comp_off = upload(R.comp_off, s);
-    o->d_bnd_off = std::move(d_bnd);
     o->d_perm = upload(R.perm, s);
     o->d_assign = upload(R.assign, s);
+}
+
+template <class V>
+void finish_query_tables(psp_gpu_oracle* o, DBuf d_bnd, cudaStream_t s) {
+    const uint32_t k = o->R.k;
+    alloc_query_tables<V>(o, s);
+    o->d_bnd_off = std::move(d_bnd);
     extract_to_boundary<V><<<std::max(k, 1u), 256, 0, s>>>(
         o->comps.view<V>(), o->d_comp_off.as<uint32_t>(), o->d_bnd_off.as<uint32_t>(),
         o->d_cb_off.as<uint64_t>(), o->d_cb.as<V>());
@@ -268,7 +279,7 @@ void pack_query_layout(psp_gpu_oracle* o, const std::vector<uint64_t>& off, cuda
         o->bq.reset();
         return;
     }
-    o->d_bq_off = upload(off, s);
+    if (!o->d_bq_off.p || o->d_bq_off.bytes < off.size() * sizeof(uint64_t)) o->d_bq_off = upload(off, s);
     pack_query_blocks<V><<<unsigned(k * k), 256, 0, s>>>(o->bg.tiles.as<V>(), o->bg.nb[0],
                                                          o->d_bnd_off.as<uint32_t>(), uint32_t(k),
                                                          o->d_bq_off.as<uint64_t>(), o->bq.as<V>());
@@ -891,6 +902,21 @@ void device_build(psp_gpu_oracle* o, psp_build_stats* st) {
         // tables must leave the device first
         MatArena ref;
         if (permuted && !spill && !o->row_storage) ref.create({b}, sizeof(V), false, s);
+        // query-side buffers now, while allocations are quick (see
+        // alloc_query_tables); the spill path frees the component tables
+        // first and allocates after K2 as before
+        if (!spill) {
+            uint64_t cb_elems = 0;
+            for (uint32_t c = 0; c < k; ++c)
+                cb_elems += uint64_t(R.comp_off[c + 1] - R.comp_off[c]) *
+                            cb_stride(R.bnd_off[c + 1] - R.bnd_off[c]);
+            size_t free_b = 0, total_b = 0;
+            mem_info(&free_b, &total_b);
+            if (cb_elems * sizeof(V) + (4ull << 30) < free_b) {  // else after K2, as before
+                alloc_query_tables<V>(o, s);
+                if (reuse_bq) o->d_bq_off = upload(bq_off, s);
+            }
+        }
         // the block query layout's offsets and allocation on a helper thread
         // while K2 runs (not beside spilled component tables: the memory is
         // K2's then)

@@ -275,6 +275,25 @@ void mem_info(size_t* free_b, size_t* total_b) {
     *free_b += buf_cache().held() + big_pool().idle();
 }
 
+// Host time spent inside cudaMalloc / cudaFree of device buffers (process
+// totals, psp_gpu_alloc_stats): on these boxes single calls have stalled for
+// 0.1-1 s, which is most of the build's wall-clock noise.
+std::atomic<uint64_t> g_malloc_ns{0}, g_free_ns{0}, g_malloc_calls{0}, g_free_calls{0};
+struct AllocTimer {
+    std::atomic<uint64_t>& ns;
+    size_t bytes = 0;
+    const char* what = "";
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~AllocTimer() {
+        const uint64_t d = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                        std::chrono::steady_clock::now() - t0).count());
+        ns += d;
+        static const bool log = std::getenv("PSP_ALLOC_LOG") != nullptr;  // calls over 2 ms
+        if (log && d > 2000000)
+            std::fprintf(stderr, "[psp] %s of %.3f GB took %.1f ms\n", what, bytes / 1e9, d / 1e6);
+    }
+};
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -320,11 +339,16 @@ struct DBuf {
             return;
         }
         const size_t r = n <= BufCache::kMaxBuf ? BufCache::rounded(n) : n;
-        cudaError_t e = cudaMalloc(&p, r);
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            buf_cache().flush();
+        cudaError_t e;
+        {
+            AllocTimer t{g_malloc_ns, r, "cudaMalloc"};
+            ++g_malloc_calls;
             e = cudaMalloc(&p, r);
+            if (e == cudaErrorMemoryAllocation) {
+                cudaGetLastError();
+                buf_cache().flush();
+                e = cudaMalloc(&p, r);
+            }
         }
         if (e != cudaSuccess) {
             p = nullptr;
@@ -343,8 +367,13 @@ struct DBuf {
     }
     void reset() {
         if (p && !borrowed) {
-            if (pooled) big_pool().give(p);
-            else if (ipc || !buf_cache().give(p, bytes)) cudaFree(p);
+            if (pooled) {
+                big_pool().give(p);
+            } else if (ipc || !buf_cache().give(p, bytes)) {
+                AllocTimer t{g_free_ns, bytes, "cudaFree"};
+                ++g_free_calls;
+                cudaFree(p);
+            }
         }
         p = nullptr;
         bytes = 0;

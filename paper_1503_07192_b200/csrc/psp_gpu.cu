@@ -145,6 +145,16 @@ psp_status psp_gpu_nccl_unique_id(void* out128) {
 
 void* psp_gpu_ctx_stream(psp_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
+psp_status psp_gpu_alloc_stats(uint64_t* out4) {
+    return guarded([&] {
+        if (!out4) throw ArgError("alloc_stats: NULL output");
+        out4[0] = g_malloc_ns.load();
+        out4[1] = g_malloc_calls.load();
+        out4[2] = g_free_ns.load();
+        out4[3] = g_free_calls.load();
+    });
+}
+
 psp_status psp_gpu_ctx_set_boundary_storage(psp_gpu_ctx* ctx, int storage) {
     return guarded([&] {
         if (!ctx) throw ArgError("ctx_set_boundary_storage: NULL ctx");
