@@ -142,14 +142,15 @@ __device__ __forceinline__ void load_ab(const V* __restrict__ sA, const V* __res
 }
 
 // k advances in pairs so each accumulator takes two relaxations per update
-// (Ops::addmin2: 2 x VIADDMNMX for u32, FADD x2 + FMNMX3 for f32). Four pairs
-// per loop trip cut the loop's address/branch ALU work (cfg3 K2 8.05 s with
-// one pair, 7.83 s with two, 7.74 s with four; road4m f32 K2 20.2 -> 19.2 s
-// with two; 189 -> 239 registers, one CTA/SM either way).
+// (Ops::addmin2: 2 x VIADDMNMX for u32, FADD x2 + FMNMX3 for f32). Eight
+// pairs per loop trip cut the loop's address/branch ALU work (cfg3 K2: 8.05 s
+// with one pair, 7.83 s with two, 7.74 s with four, 7.64 s with eight, 7.69 s
+// with sixteen; road4m f32 K2 20.2 -> 19.2 s with two; 189 -> 239
+// registers, one CTA/SM either way).
 template <class V, bool A_KMAJOR>
 __device__ __forceinline__ void minplus_tile(const V* __restrict__ sA, const V* __restrict__ sB,
                                              V (&acc)[8][8], int ty, int tx) {
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < T; k += 2) {
         V a0[8], b0[8], a1[8], b1[8];
         load_ab<V, A_KMAJOR>(sA, sB, k, ty, tx, a0, b0);

@@ -1,0 +1,7 @@
+# round 2: FW min-plus tile loop unrolled by 16 k-pairs (A/B vs 8): parity + cfg3 K2 time
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x > gpurun_out/r2bj_parity.log 2>&1; echo parity_rc=$?
+tail -1 gpurun_out/r2bj_parity.log
+timeout 900 python tools/build_repeat.py --config delaunay1m_k1024 --builds 2 > gpurun_out/r2bj_repeat.jsonl 2>&1; echo rc=$?
+grep k2_device gpurun_out/r2bj_repeat.jsonl | cut -c1-220
