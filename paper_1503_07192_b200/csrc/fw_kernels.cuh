@@ -30,6 +30,8 @@
 // The inner loop (phase 2/3) per k: 2 LDS.128 for A (broadcast within a
 // warp), 2 LDS.128 for B, 64 fused add-min (VIADDMNMX.U32 / FADD+FMNMX).
 #pragma once
+#include <type_traits>
+
 #include "minplus.cuh"
 
 namespace pspg {
@@ -145,12 +147,13 @@ __device__ __forceinline__ void load_ab(const V* __restrict__ sA, const V* __res
 // (Ops::addmin2: 2 x VIADDMNMX for u32, FADD x2 + FMNMX3 for f32). Eight
 // pairs per loop trip cut the loop's address/branch ALU work (cfg3 K2: 8.05 s
 // with one pair, 7.83 s with two, 7.74 s with four, 7.64 s with eight, 7.69 s
-// with sixteen; road4m f32 K2 20.2 -> 19.2 s with two; 189 -> 239
-// registers, one CTA/SM either way).
+// with sixteen; road4m f32 K2 20.2 s with one, 19.2 s with two, 20.0 s with
+// eight, so f32 keeps two; one CTA/SM either way).
 template <class V, bool A_KMAJOR>
 __device__ __forceinline__ void minplus_tile(const V* __restrict__ sA, const V* __restrict__ sB,
                                              V (&acc)[8][8], int ty, int tx) {
-#pragma unroll 8
+    constexpr int kUnroll = std::is_same<V, float>::value ? 2 : 8;
+#pragma unroll kUnroll
     for (int k = 0; k < T; k += 2) {
         V a0[8], b0[8], a1[8], b1[8];
         load_ab<V, A_KMAJOR>(sA, sB, k, ty, tx, a0, b0);
