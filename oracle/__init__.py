@@ -256,9 +256,10 @@ class RefGraph:
 
 def assemble_oracle(ref: "RefLib", n, k, perm, assign, flags, comp_off, bnd_off, bvert,
                     ct: list, bt: list) -> "RefOracle":
-    """ref_oracle_assemble: a psp::Oracle from plain arrays (bt[c] None =
-    component not sampled) so that the reference's batch_query runs on it."""
-    ctp = (C.c_void_p * k)(*[t.ctypes.data for t in ct])
+    """ref_oracle_assemble: a psp::Oracle from plain arrays (bt[c] / ct[c]
+    None = component not sampled) so that the reference's batch_query runs on
+    it over pairs that touch sampled components only."""
+    ctp = (C.c_void_p * k)(*[(t.ctypes.data if t is not None else None) for t in ct])
     btp = (C.c_void_p * k)(*[(t.ctypes.data if t is not None else None) for t in bt])
     h = C.c_void_p()
     ref._check(ref.lib.ref_oracle_assemble(

@@ -427,8 +427,10 @@ int ref_oracle_assemble(uint64_t n, uint32_t k, const uint32_t* perm, const uint
         o.boundary_tables.resize(k);
         for (uint32_t c = 0; c < k; ++c) {
             const uint64_t s = comp_off[c + 1] - comp_off[c], bc = bnd_off[c + 1] - bnd_off[c];
-            o.component_tables[c] = psp::Matrix(s, s, psp::kUnreachable);
-            std::memcpy(o.component_tables[c].data().data(), ct[c], s * s * sizeof(double));
+            if (ct[c]) {  // NULL: component not sampled (queries never touch it)
+                o.component_tables[c] = psp::Matrix(s, s, psp::kUnreachable);
+                std::memcpy(o.component_tables[c].data().data(), ct[c], s * s * sizeof(double));
+            }
             if (bt[c]) {
                 o.boundary_tables[c] = psp::Matrix(bc, b, psp::kUnreachable);
                 std::memcpy(o.boundary_tables[c].data().data(), bt[c], bc * b * sizeof(double));
