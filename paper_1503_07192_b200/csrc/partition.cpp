@@ -274,6 +274,17 @@ private:
     std::vector<uint8_t> dirty_;
 };
 
+// PSP_PART_PROFILE: summed thread time of the phases (ns)
+std::atomic<uint64_t> g_ns_grow{0}, g_ns_recenter{0}, g_ns_finalize{0};
+struct PhaseTimer {
+    std::atomic<uint64_t>& acc;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~PhaseTimer() {
+        acc += uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 // The restart chain and finalize on local storage: `assign` and `hop` are
 // indexed by local position, seeds are original ids.
 struct Part {
@@ -287,10 +298,13 @@ struct Part {
     // is evaluated here, in local order.
     void grow(const std::vector<uint32_t>& seeds, std::vector<uint32_t>& assign,
               std::vector<uint32_t>& hop) const {
+        PhaseTimer pt{g_ns_grow};
         const uint64_t n = g.n;
         assign.assign(n, kNone);
         hop.assign(n, kNone);
-        std::vector<uint32_t> frontier, next, claim(n, kNone);
+        // claim[x]: the claimant's position; claim_id[x] its original id (the
+        // comparison key, kept beside it so a contest needs no id lookup)
+        std::vector<uint32_t> frontier, next, claim(n, kNone), claim_id(n);
         for (uint32_t c = 0; c < seeds.size(); ++c) {
             const uint32_t u = g.pos[seeds[c]];
             assign[u] = c;  // a repeated seed keeps its last component, as in the reference
@@ -301,17 +315,21 @@ struct Part {
         while (!frontier.empty()) {
             ++round;
             next.clear();
-            for (uint32_t u : frontier)
+            for (uint32_t u : frontier) {
+                const uint32_t iu = g.id[u];
                 for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
                     const uint32_t x = g.to[e];
                     if (assign[x] != kNone) continue;
                     if (claim[x] == kNone) {
                         claim[x] = u;
+                        claim_id[x] = iu;
                         next.push_back(x);
-                    } else if (g.id[u] < g.id[claim[x]]) {
+                    } else if (iu < claim_id[x]) {
                         claim[x] = u;
+                        claim_id[x] = iu;
                     }
                 }
+            }
             for (uint32_t x : next) {
                 assign[x] = assign[claim[x]];
                 hop[x] = round;
@@ -325,6 +343,7 @@ struct Part {
     // smallest-id boundary vertex), again an order-free rule.
     std::vector<uint32_t> recenter(const std::vector<uint32_t>& a,
                                    const std::vector<uint32_t>& old) const {
+        PhaseTimer pt{g_ns_recenter};
         const uint64_t n = g.n;
         std::vector<uint32_t> seeds(old);
         const std::vector<uint8_t> flags = local_boundary(g, a);
@@ -560,6 +579,7 @@ struct Part {
     // when `out` is given, the assignment in original id order
     uint64_t finalize(std::vector<uint32_t> assign, const std::vector<uint32_t>& hop,
                       std::vector<uint32_t>* out) const {
+        PhaseTimer pt{g_ns_finalize};
         const uint64_t n = g.n;
         std::vector<uint64_t> sz(k, 0);
         for (uint64_t u = 0; u < n; ++u)
@@ -641,6 +661,9 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
             seed_sets[r] = P.recenter(grown[r][round - 1].assign, seed_sets[r]);
             P.grow(seed_sets[r], grown[r][round].assign, grown[r][round].hop);
         }
+        if (prof && round + 1 == kRounds)
+            std::fprintf(stderr, "[partition] chain %d grown %.3f s\n", r,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
         tasks.push(false, [&, r, round] {
             const Grown& gr = grown[r][round];
             cost[size_t(r) * kRounds + round] = P.finalize(gr.assign, gr.hop, nullptr);
@@ -679,6 +702,9 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
             S.relax_from(s[c]);
         }
         seed_sets[r] = std::move(s);
+        if (prof)
+            std::fprintf(stderr, "[partition] seeds of restart %d drawn %.3f s\n", r,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
         tasks.push(true, [&, r] { chain_step(r, 0); });
     }
     lap("seeds drawn");
@@ -691,6 +717,9 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     const Grown& gw = grown[win / kRounds][win % kRounds];
     P.finalize(gw.assign, gw.hop, &assignment);
     lap("winner finalized");
+    if (prof)
+        std::fprintf(stderr, "[partition] thread time: grow %.3f s, recenter %.3f s, finalize %.3f s\n",
+                     g_ns_grow.load() / 1e9, g_ns_recenter.load() / 1e9, g_ns_finalize.load() / 1e9);
     std::vector<uint64_t> sz(k, 0);
     for (uint32_t c : assignment) ++sz[c];
     for (uint32_t c = 0; c < k; ++c)

@@ -1,0 +1,14 @@
+# round 2: host partitioner timeline on the GPU box's CPU (cfg3, 16 and 32 threads)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nproc
+python - <<'PY'
+import sys, numpy as np
+sys.path.insert(0, '.')
+from paper_1503_07192_b200 import graphs
+g, cfg = graphs.make("delaunay1m_k1024")
+with open('/tmp/cfg3.bin', 'wb') as f:
+    np.array([g.n, len(g.eu)], np.uint64).tofile(f)
+    g.eu.astype(np.uint32).tofile(f); g.ev.astype(np.uint32).tofile(f); g.ew.astype(np.float64).tofile(f)
+PY
+for t in 16 32; do PSP_PART_PROFILE=1 ./tools/part_bench /tmp/cfg3.bin 1024 $t 1 2>&1 | grep -v "^$"; done
