@@ -54,6 +54,7 @@
 #include <numeric>
 #include <random>
 #include <stdexcept>
+#include <barrier>
 #include <thread>
 #include <vector>
 
@@ -336,6 +337,81 @@ struct Part {
             }
             frontier.swap(next);
         }
+    }
+
+    // grow() on `T` threads, level-synchronous: the claim of x is the packed
+    // (original id, position) of its smallest-id frontier neighbour, settled by
+    // compare-and-swap, so any visiting order gives grow()'s result. Used for
+    // the last restarts' chains, which are the partitioner's critical path
+    // (the other cores are busy with earlier chains and finalize passes).
+    void grow_par(const std::vector<uint32_t>& seeds, std::vector<uint32_t>& assign,
+                  std::vector<uint32_t>& hop, unsigned T) const {
+        PhaseTimer pt{g_ns_grow};
+        const uint64_t n = g.n;
+        assign.assign(n, kNone);
+        hop.assign(n, kNone);
+        std::vector<std::atomic<uint64_t>> claim(n);
+        std::vector<uint32_t> frontier, next;
+        for (uint32_t c = 0; c < seeds.size(); ++c) {
+            const uint32_t u = g.pos[seeds[c]];
+            assign[u] = c;  // a repeated seed keeps its last component, as in the reference
+            hop[u] = 0;
+        }
+        for (uint32_t c = 0; c < seeds.size(); ++c) frontier.push_back(g.pos[seeds[c]]);
+        std::vector<std::vector<uint32_t>> local(T);
+        std::barrier sync(static_cast<std::ptrdiff_t>(T));
+        uint32_t round = 0;
+        bool done = false;
+        auto work = [&](unsigned t) {
+            // claims start empty (~0): every thread clears its share
+            for (uint64_t x = t; x < n; x += T) claim[x].store(~uint64_t(0), std::memory_order_relaxed);
+            sync.arrive_and_wait();
+            for (;;) {
+                if (done) return;
+                // phase 1: claims
+                std::vector<uint32_t>& mine = local[t];
+                mine.clear();
+                const size_t f = frontier.size(), lo = f * t / T, hi = f * (t + 1) / T;
+                for (size_t i = lo; i < hi; ++i) {
+                    const uint32_t u = frontier[i];
+                    const uint64_t key = (uint64_t(g.id[u]) << 32) | u;
+                    for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
+                        const uint32_t x = g.to[e];
+                        if (assign[x] != kNone) continue;
+                        uint64_t cur = claim[x].load(std::memory_order_relaxed);
+                        while (key < cur) {
+                            if (claim[x].compare_exchange_weak(cur, key, std::memory_order_relaxed)) {
+                                if (cur == ~uint64_t(0)) mine.push_back(x);
+                                break;
+                            }
+                        }
+                    }
+                }
+                sync.arrive_and_wait();
+                if (t == 0) {  // the next frontier, then its assignment
+                    ++round;
+                    next.clear();
+                    for (auto& l : local) next.insert(next.end(), l.begin(), l.end());
+                }
+                sync.arrive_and_wait();
+                const size_t m = next.size(), a0 = m * t / T, a1 = m * (t + 1) / T;
+                for (size_t i = a0; i < a1; ++i) {
+                    const uint32_t x = next[i];
+                    assign[x] = assign[uint32_t(claim[x].load(std::memory_order_relaxed))];
+                    hop[x] = round;
+                }
+                sync.arrive_and_wait();
+                if (t == 0) {
+                    frontier.swap(next);
+                    done = frontier.empty();
+                }
+                sync.arrive_and_wait();
+            }
+        };
+        std::vector<std::thread> team;
+        for (unsigned t = 1; t < T; ++t) team.emplace_back(work, t);
+        work(0);
+        for (auto& th : team) th.join();
     }
 
     // recenter (:77-119): per component, the smallest-id vertex of the
@@ -654,12 +730,21 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     };
     std::function<void(int, int)> chain_step;  // outlives the pool (running tasks call it)
     TaskPool tasks(std::max(1u, threads));
+    // the last restarts' chains finish last (their seeds are drawn last):
+    // their grows run on a few threads each
+    const unsigned par = std::getenv("PSP_PART_SERIAL") ? 1u : std::min(4u, std::max(1u, threads / 4));
+    const char* pl = std::getenv("PSP_PART_PAR_LAST");  // A/B: how many of the last chains
+    const int par_last = pl ? std::atoi(pl) : 4;
+    auto grow_step = [&](int r, std::vector<uint32_t>& as, std::vector<uint32_t>& hp) {
+        if (par > 1 && r >= kRestarts - par_last) P.grow_par(seed_sets[r], as, hp, par);
+        else P.grow(seed_sets[r], as, hp);
+    };
     chain_step = [&](int r, int round) {
         if (round == 0) {
-            P.grow(seed_sets[r], grown[r][0].assign, grown[r][0].hop);
+            grow_step(r, grown[r][0].assign, grown[r][0].hop);
         } else {
             seed_sets[r] = P.recenter(grown[r][round - 1].assign, seed_sets[r]);
-            P.grow(seed_sets[r], grown[r][round].assign, grown[r][round].hop);
+            grow_step(r, grown[r][round].assign, grown[r][round].hop);
         }
         if (prof && round + 1 == kRounds)
             std::fprintf(stderr, "[partition] chain %d grown %.3f s\n", r,
