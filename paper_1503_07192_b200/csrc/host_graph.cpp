@@ -4,11 +4,13 @@
 #include "host_graph.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <cmath>
 #include <limits>
 #include <numeric>
 #include <random>
+#include <thread>
 
 namespace pspg {
 
@@ -16,14 +18,47 @@ namespace {
 std::string pair_str(uint32_t u, uint32_t v) {
     return "(" + std::to_string(u) + "," + std::to_string(v) + ")";
 }
+
+// fn(lo, hi) over [0, n) in contiguous slices on up to 16 host threads
+// (serial below 64K items, where thread start-up would dominate)
+template <class F>
+void par_slices(uint64_t n, F&& fn) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint64_t t = n < (uint64_t(1) << 16) ? 1 : std::min<uint64_t>(hw, n);
+    if (t <= 1) {
+        fn(uint64_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (uint64_t i = 1; i < t; ++i) pool.emplace_back([&, i] { fn(n * i / t, n * (i + 1) / t); });
+    fn(uint64_t(0), n / t);
+    for (auto& th : pool) th.join();
+}
 }  // namespace
 
 Csr build_csr(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev, const double* ew) {
     Csr g;
     g.n = n;
     g.off.assign(n + 1, 0);
-    // validation order of src/graph.cpp:22-36: range, self-loop, NaN/inf, negative
-    for (uint64_t e = 0; e < m; ++e) {
+    // validation order of src/graph.cpp:22-36: range, self-loop, NaN/inf,
+    // negative; the first offending edge is found in parallel, then reported
+    // exactly as a serial scan would
+    auto bad = [&](uint64_t e) {
+        const uint32_t u = eu[e], v = ev[e];
+        const double w = ew[e];
+        return u >= n || v >= n || u == v || std::isnan(w) || std::isinf(w) || w < 0.0;
+    };
+    std::atomic<uint64_t> first_bad{m};
+    par_slices(m, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t e = lo; e < hi; ++e)
+            if (bad(e)) {
+                uint64_t cur = first_bad.load();
+                while (e < cur && !first_bad.compare_exchange_weak(cur, e)) {}
+                return;
+            }
+    });
+    if (first_bad.load() < m) {
+        const uint64_t e = first_bad.load();
         const uint32_t u = eu[e], v = ev[e];
         const double w = ew[e];
         if (u >= n || v >= n)
@@ -32,46 +67,74 @@ Csr build_csr(uint64_t n, uint64_t m, const uint32_t* eu, const uint32_t* ev, co
         if (u == v) throw GraphError("self-loop at vertex " + std::to_string(u));
         if (std::isnan(w) || std::isinf(w))
             throw GraphError("non-finite weight on edge " + pair_str(u, v));
-        if (w < 0.0) throw GraphError("negative weight on edge " + pair_str(u, v));
-        ++g.off[u + 1];
-        ++g.off[v + 1];
+        throw GraphError("negative weight on edge " + pair_str(u, v));
     }
+    // degree count and scatter with relaxed atomics: the slot order inside a
+    // neighbour list is arbitrary, but the sort below makes the result unique
+    // (equal keys are duplicates, which are rejected)
+    par_slices(m, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t e = lo; e < hi; ++e) {
+            std::atomic_ref<uint64_t>(g.off[eu[e] + 1]).fetch_add(1, std::memory_order_relaxed);
+            std::atomic_ref<uint64_t>(g.off[ev[e] + 1]).fetch_add(1, std::memory_order_relaxed);
+        }
+    });
     for (uint64_t v = 0; v < n; ++v) g.off[v + 1] += g.off[v];
     g.to.resize(2 * m);
     g.w.resize(2 * m);
     std::vector<uint64_t> cur(g.off.begin(), g.off.end() - 1);
-    for (uint64_t e = 0; e < m; ++e) {
-        const uint64_t a = cur[eu[e]]++, b = cur[ev[e]]++;
-        g.to[a] = ev[e];
-        g.w[a] = ew[e];
-        g.to[b] = eu[e];
-        g.w[b] = ew[e];
-    }
-    std::vector<std::pair<uint32_t, double>> tmp;
-    for (uint64_t v = 0; v < n; ++v) {
-        const uint64_t lo = g.off[v], hi = g.off[v + 1];
-        tmp.clear();
-        for (uint64_t e = lo; e < hi; ++e) tmp.emplace_back(g.to[e], g.w[e]);
-        std::sort(tmp.begin(), tmp.end(),
-                  [](const auto& a, const auto& b) { return a.first < b.first; });
+    par_slices(m, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t e = lo; e < hi; ++e) {
-            g.to[e] = tmp[e - lo].first;
-            g.w[e] = tmp[e - lo].second;
-            if (e > lo && g.to[e] == g.to[e - 1])
-                throw GraphError("duplicate edge " + pair_str(static_cast<uint32_t>(v), g.to[e]));
+            const uint64_t a = std::atomic_ref<uint64_t>(cur[eu[e]]).fetch_add(1, std::memory_order_relaxed);
+            const uint64_t b = std::atomic_ref<uint64_t>(cur[ev[e]]).fetch_add(1, std::memory_order_relaxed);
+            g.to[a] = ev[e];
+            g.w[a] = ew[e];
+            g.to[b] = eu[e];
+            g.w[b] = ew[e];
         }
+    });
+    // per-vertex neighbour sort; the lowest vertex holding a duplicate is the
+    // one a serial scan reports
+    std::atomic<uint64_t> dup_v{n};
+    par_slices(n, [&](uint64_t vlo, uint64_t vhi) {
+        std::vector<std::pair<uint32_t, double>> tmp;
+        for (uint64_t v = vlo; v < vhi; ++v) {
+            const uint64_t lo = g.off[v], hi = g.off[v + 1];
+            tmp.clear();
+            for (uint64_t e = lo; e < hi; ++e) tmp.emplace_back(g.to[e], g.w[e]);
+            std::sort(tmp.begin(), tmp.end(),
+                      [](const auto& a, const auto& b) { return a.first < b.first; });
+            bool dup = false;
+            for (uint64_t e = lo; e < hi; ++e) {
+                g.to[e] = tmp[e - lo].first;
+                g.w[e] = tmp[e - lo].second;
+                dup |= e > lo && g.to[e] == g.to[e - 1];
+            }
+            if (dup) {
+                uint64_t cur = dup_v.load();
+                while (v < cur && !dup_v.compare_exchange_weak(cur, v)) {}
+                return;
+            }
+        }
+    });
+    if (dup_v.load() < n) {
+        const uint64_t v = dup_v.load();
+        for (uint64_t e = g.off[v] + 1; e < g.off[v + 1]; ++e)
+            if (g.to[e] == g.to[e - 1])
+                throw GraphError("duplicate edge " + pair_str(static_cast<uint32_t>(v), g.to[e]));
     }
     return g;
 }
 
 std::vector<uint8_t> compute_boundary(const Csr& g, const std::vector<uint32_t>& a) {
     std::vector<uint8_t> flags(g.n, 0);
-    for (uint64_t v = 0; v < g.n; ++v)
-        for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e)
-            if (a[g.to[e]] != a[v]) {
-                flags[v] = 1;
-                break;
-            }
+    par_slices(g.n, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t v = lo; v < hi; ++v)
+            for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e)
+                if (a[g.to[e]] != a[v]) {
+                    flags[v] = 1;
+                    break;
+                }
+    });
     return flags;
 }
 
@@ -107,33 +170,39 @@ Reordered reorder(const Csr& g, uint32_t k, const std::vector<uint32_t>& assignm
     const std::vector<uint8_t> flags0 = compute_boundary(g, assignment);
     r.perm = reorder_permutation(k, assignment, flags0);
     r.inv.resize(n);
-    for (uint64_t v = 0; v < n; ++v) r.inv[r.perm[v]] = static_cast<uint32_t>(v);
     r.assign.resize(n);
     r.flags.resize(n);
-    for (uint64_t v = 0; v < n; ++v) {
-        r.assign[r.perm[v]] = assignment[v];
-        r.flags[r.perm[v]] = flags0[v];
-    }
-    // relabelled CSR, neighbour lists re-sorted by new id (:458-470)
     Csr& rg = r.g;
     rg.n = n;
     rg.off.assign(n + 1, 0);
-    for (uint64_t v = 0; v < n; ++v) rg.off[r.perm[v] + 1] = g.degree(static_cast<uint32_t>(v));
+    // perm is a bijection, so the scatters below write disjoint slots
+    par_slices(n, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t v = lo; v < hi; ++v) {
+            const uint32_t p = r.perm[v];
+            r.inv[p] = static_cast<uint32_t>(v);
+            r.assign[p] = assignment[v];
+            r.flags[p] = flags0[v];
+            rg.off[p + 1] = g.degree(static_cast<uint32_t>(v));
+        }
+    });
+    // relabelled CSR, neighbour lists re-sorted by new id (:458-470)
     for (uint64_t v = 0; v < n; ++v) rg.off[v + 1] += rg.off[v];
     rg.to.resize(g.to.size());
     rg.w.resize(g.w.size());
-    std::vector<std::pair<uint32_t, double>> tmp;
-    for (uint64_t v = 0; v < n; ++v) {
-        tmp.clear();
-        for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) tmp.emplace_back(r.perm[g.to[e]], g.w[e]);
-        std::sort(tmp.begin(), tmp.end(),
-                  [](const auto& a, const auto& b) { return a.first < b.first; });
-        uint64_t at = rg.off[r.perm[v]];
-        for (const auto& t : tmp) {
-            rg.to[at] = t.first;
-            rg.w[at++] = t.second;
+    par_slices(n, [&](uint64_t lo, uint64_t hi) {
+        std::vector<std::pair<uint32_t, double>> tmp;
+        for (uint64_t v = lo; v < hi; ++v) {
+            tmp.clear();
+            for (uint64_t e = g.off[v]; e < g.off[v + 1]; ++e) tmp.emplace_back(r.perm[g.to[e]], g.w[e]);
+            std::sort(tmp.begin(), tmp.end(),
+                      [](const auto& a, const auto& b) { return a.first < b.first; });
+            uint64_t at = rg.off[r.perm[v]];
+            for (const auto& t : tmp) {
+                rg.to[at] = t.first;
+                rg.w[at++] = t.second;
+            }
         }
-    }
+    });
     r.comp_off.assign(k + 1, 0);
     r.bnd_off.assign(k + 1, 0);
     for (uint64_t v = 0; v < n; ++v) {

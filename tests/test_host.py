@@ -159,6 +159,35 @@ def test_graph_invariants_rejected(edges, msg):
         P.partition_graph(g, 1)
 
 
+@pytest.mark.parametrize("bad,msg", [
+    ((7, 7, 1.0), r"self-loop at vertex 7$"),
+    ((5, 6, -2.0), r"negative weight on edge \(5,6\)$"),
+    ((1, 2, 1.0), r"duplicate edge \(1,2\)$"),
+])
+def test_graph_invariants_first_error_large(bad, msg):
+    """Above 64K edges build_csr validates and sorts on several threads; the
+    error must still be the one a serial scan meets first (src/graph.cpp:22-36):
+    the earliest bad edge, or the lowest vertex with a duplicate neighbour."""
+    g = P.generate_grid(400, 400)
+    eu, ev, ew = list(g.eu), list(g.ev), list(g.ew)
+    u, v, w = bad
+    late = len(eu) - 3  # a second, later offence of another kind
+    eu.insert(late, 100)
+    ev.insert(late, 100)
+    ew.insert(late, 1.0)
+    eu.insert(1000, u)
+    ev.insert(1000, v)
+    ew.insert(1000, w)
+    if msg.startswith("duplicate"):
+        eu.append(159_000)  # a duplicate at a higher vertex too
+        ev.append(159_001)
+        ew.append(1.0)
+        del eu[late + 1], ev[late + 1], ew[late + 1]  # only duplicates remain
+    G = P.Graph(g.n, np.array(eu, np.uint32), np.array(ev, np.uint32), np.array(ew))
+    with pytest.raises(P.GraphInvariantError, match=msg):
+        P.partition_graph(G, 1)
+
+
 @pytest.mark.parametrize("n,seed", [(3, 0), (100, 2), (20_000, 4), (262_144, 1)])
 def test_delaunay_generator_matches_qhull(n, seed):
     """The library's exact incremental Delaunay (csrc/delaunay.cpp) gives the
