@@ -460,6 +460,90 @@ struct Part {
         return seeds;
     }
 
+    // recenter() on `T` threads for the last restarts' chains: the BFS
+    // levels (depth from the component's boundary inside the component) do
+    // not depend on the visiting order, and the pick -- the smallest id at
+    // the deepest level -- is taken after the BFS from per-thread minima, so
+    // the seeds are recenter()'s.
+    std::vector<uint32_t> recenter_par(const std::vector<uint32_t>& a,
+                                       const std::vector<uint32_t>& old, unsigned T) const {
+        PhaseTimer pt{g_ns_recenter};
+        const uint64_t n = g.n;
+        std::vector<uint32_t> seeds(old);
+        std::vector<std::atomic<uint8_t>> visited(n);
+        std::vector<uint32_t> depth(n, kNone), frontier;
+        std::vector<std::vector<uint32_t>> local(T);
+        // per thread and component: (depth, id) of the best vertex seen
+        std::vector<std::vector<uint64_t>> pick(T);
+        std::barrier sync(static_cast<std::ptrdiff_t>(T));
+        uint32_t round = 0;
+        bool done = false;
+        auto work = [&](unsigned t) {
+            std::vector<uint32_t>& mine = local[t];
+            mine.clear();
+            const uint64_t v0 = n * t / T, v1 = n * (t + 1) / T;
+            for (uint64_t u = v0; u < v1; ++u) {
+                visited[u].store(0, std::memory_order_relaxed);
+                for (uint64_t e = g.begin(u); e < g.end(u); ++e)
+                    if (a[g.to[e]] != a[u]) {
+                        visited[u].store(1, std::memory_order_relaxed);
+                        depth[u] = 0;
+                        mine.push_back(static_cast<uint32_t>(u));
+                        break;
+                    }
+            }
+            sync.arrive_and_wait();
+            if (t == 0) {
+                frontier.clear();
+                for (auto& l : local) frontier.insert(frontier.end(), l.begin(), l.end());
+                done = frontier.empty();
+            }
+            sync.arrive_and_wait();
+            while (!done) {
+                const uint32_t level = round + 1;
+                mine.clear();
+                const size_t f = frontier.size(), lo = f * t / T, hi = f * (t + 1) / T;
+                for (size_t i = lo; i < hi; ++i) {
+                    const uint32_t u = frontier[i];
+                    for (uint64_t e = g.begin(u); e < g.end(u); ++e) {
+                        const uint32_t x = g.to[e];
+                        if (a[x] != a[u] || visited[x].load(std::memory_order_relaxed)) continue;
+                        if (visited[x].exchange(1, std::memory_order_relaxed) == 0) {
+                            depth[x] = level;
+                            mine.push_back(x);
+                        }
+                    }
+                }
+                sync.arrive_and_wait();
+                if (t == 0) {
+                    round = level;
+                    frontier.clear();
+                    for (auto& l : local) frontier.insert(frontier.end(), l.begin(), l.end());
+                    done = frontier.empty();
+                }
+                sync.arrive_and_wait();
+            }
+            // deepest level first, then the smallest original id
+            std::vector<uint64_t>& pk = pick[t];
+            pk.assign(seeds.size(), ~uint64_t(0));
+            for (uint64_t u = v0; u < v1; ++u) {
+                if (depth[u] == kNone) continue;
+                const uint64_t key = (uint64_t(kNone - depth[u]) << 32) | g.id[u];
+                pk[a[u]] = std::min(pk[a[u]], key);
+            }
+        };
+        std::vector<std::thread> team;
+        for (unsigned t = 1; t < T; ++t) team.emplace_back(work, t);
+        work(0);
+        for (auto& th : team) th.join();
+        for (uint32_t c = 0; c < seeds.size(); ++c) {
+            uint64_t best = ~uint64_t(0);
+            for (unsigned t = 0; t < T; ++t) best = std::min(best, pick[t][c]);
+            if (best != ~uint64_t(0)) seeds[c] = static_cast<uint32_t>(best);
+        }
+        return seeds;
+    }
+
     // rebalance (:125-175)
     void rebalance(std::vector<uint32_t>& a, const std::vector<uint32_t>& hop,
                    std::vector<uint64_t>& size) const {
@@ -743,7 +827,9 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
         if (round == 0) {
             grow_step(r, grown[r][0].assign, grown[r][0].hop);
         } else {
-            seed_sets[r] = P.recenter(grown[r][round - 1].assign, seed_sets[r]);
+            seed_sets[r] = par > 1 && r >= kRestarts - par_last
+                               ? P.recenter_par(grown[r][round - 1].assign, seed_sets[r], par)
+                               : P.recenter(grown[r][round - 1].assign, seed_sets[r]);
             grow_step(r, grown[r][round].assign, grown[r][round].hop);
         }
         if (prof && round + 1 == kRounds)
