@@ -737,8 +737,9 @@ struct Part {
 
     // the finalize lambda (:393-420); returns the candidate's cost and,
     // when `out` is given, the assignment in original id order
+    // `out`: the assignment in original ids; `local_out`: in local positions
     uint64_t finalize(std::vector<uint32_t> assign, const std::vector<uint32_t>& hop,
-                      std::vector<uint32_t>* out) const {
+                      std::vector<uint32_t>* out, std::vector<uint32_t>* local_out = nullptr) const {
         PhaseTimer pt{g_ns_finalize};
         const uint64_t n = g.n;
         std::vector<uint64_t> sz(k, 0);
@@ -765,6 +766,7 @@ struct Part {
             out->resize(n);
             for (uint64_t v = 0; v < n; ++v) (*out)[v] = assign[g.pos[v]];
         }
+        if (local_out) local_out->swap(assign);
         return cost;
     }
 };
@@ -796,8 +798,8 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     //   * every grown (restart, round) state immediately spawns its
     //     finalize(), costs only, on whichever pool thread is free (chain
     //     steps first: they are the critical path);
-    // then the reference's winner -- the first strict minimum in (restart,
-    // round) order -- is finalized once more to materialise its assignment.
+    // the reference's winner -- the first strict minimum in (restart, round)
+    // order -- is the finalized state kept by the pass that produced it.
     constexpr int kRounds = kRecenterRounds + 1;
     struct Grown {
         std::vector<uint32_t> assign, hop;
@@ -812,6 +814,12 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start)
                              .count());
     };
+    // the best finalized state so far: the smallest (cost, restart * rounds
+    // + round), i.e. the reference's first strict minimum, kept in local order
+    std::mutex win_mu;
+    uint64_t win_cost = ~uint64_t(0);
+    size_t win_idx = ~size_t(0);
+    std::vector<uint32_t> win_local;
     std::function<void(int, int)> chain_step;  // outlives the pool (running tasks call it)
     TaskPool tasks(std::max(1u, threads));
     // the last restarts' chains finish last (their seeds are drawn last):
@@ -819,6 +827,7 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     const unsigned par = std::getenv("PSP_PART_SERIAL") ? 1u : std::min(4u, std::max(1u, threads / 4));
     const char* pl = std::getenv("PSP_PART_PAR_LAST");  // A/B: how many of the last chains
     const int par_last = pl ? std::atoi(pl) : 4;
+    const bool serial_recenter = std::getenv("PSP_PART_SERIAL_RECENTER") != nullptr;  // A/B
     auto grow_step = [&](int r, std::vector<uint32_t>& as, std::vector<uint32_t>& hp) {
         if (par > 1 && r >= kRestarts - par_last) P.grow_par(seed_sets[r], as, hp, par);
         else P.grow(seed_sets[r], as, hp);
@@ -827,7 +836,7 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
         if (round == 0) {
             grow_step(r, grown[r][0].assign, grown[r][0].hop);
         } else {
-            seed_sets[r] = par > 1 && r >= kRestarts - par_last
+            seed_sets[r] = par > 1 && r >= kRestarts - par_last && !serial_recenter
                                ? P.recenter_par(grown[r][round - 1].assign, seed_sets[r], par)
                                : P.recenter(grown[r][round - 1].assign, seed_sets[r]);
             grow_step(r, grown[r][round].assign, grown[r][round].hop);
@@ -837,7 +846,16 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
         tasks.push(false, [&, r, round] {
             const Grown& gr = grown[r][round];
-            cost[size_t(r) * kRounds + round] = P.finalize(gr.assign, gr.hop, nullptr);
+            std::vector<uint32_t> fin;
+            const size_t idx = size_t(r) * kRounds + round;
+            const uint64_t c = P.finalize(gr.assign, gr.hop, nullptr, &fin);
+            cost[idx] = c;
+            std::lock_guard<std::mutex> lk(win_mu);
+            if (c < win_cost || (c == win_cost && idx < win_idx)) {
+                win_cost = c;
+                win_idx = idx;
+                win_local.swap(fin);
+            }
         });
         if (round + 1 < kRounds) tasks.push(true, [&, r, round] { chain_step(r, round + 1); });
     };
@@ -884,10 +902,10 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     size_t win = 0;
     for (size_t t = 1; t < cost.size(); ++t)
         if (cost[t] < cost[win]) win = t;
-    std::vector<uint32_t> assignment;
-    const Grown& gw = grown[win / kRounds][win % kRounds];
-    P.finalize(gw.assign, gw.hop, &assignment);
-    lap("winner finalized");
+    if (win != win_idx) throw std::logic_error("partition_graph: winner bookkeeping mismatch");
+    std::vector<uint32_t> assignment(n);
+    for (uint64_t v = 0; v < n; ++v) assignment[v] = win_local[L.pos[v]];
+    lap("winner assignment");
     if (prof)
         std::fprintf(stderr, "[partition] thread time: grow %.3f s, recenter %.3f s, finalize %.3f s\n",
                      g_ns_grow.load() / 1e9, g_ns_recenter.load() / 1e9, g_ns_finalize.load() / 1e9);
