@@ -23,7 +23,7 @@
 //    seeds exist, and each of the 8 x 13 grown states spawns its
 //    finalize() (the expensive part) on any free host thread; the winner
 //    is the first minimum in (restart, round) order exactly as the
-//    reference's strict `<` scan picks it.
+//    reference's strict `<` scan picks it, kept as the passes finish.
 //  * all per-vertex state lives in a BFS-ordered relabelling of the graph
 //    (struct Local), so neighbourhoods are compact in memory; rules that
 //    depend on id order compare original ids, loops whose order matters
@@ -823,10 +823,11 @@ std::vector<uint32_t> partition_graph(const Csr& g, uint32_t k, uint64_t seed, u
     std::function<void(int, int)> chain_step;  // outlives the pool (running tasks call it)
     TaskPool tasks(std::max(1u, threads));
     // the last restarts' chains finish last (their seeds are drawn last):
-    // their grows run on a few threads each
+    // their grows and recenters run on a few threads each (last 2 chains
+    // x 4 threads measured best on 16 cores; 4 chains oversubscribe)
     const unsigned par = std::getenv("PSP_PART_SERIAL") ? 1u : std::min(4u, std::max(1u, threads / 4));
     const char* pl = std::getenv("PSP_PART_PAR_LAST");  // A/B: how many of the last chains
-    const int par_last = pl ? std::atoi(pl) : 4;
+    const int par_last = pl ? std::atoi(pl) : 2;
     const bool serial_recenter = std::getenv("PSP_PART_SERIAL_RECENTER") != nullptr;  // A/B
     auto grow_step = [&](int r, std::vector<uint32_t>& as, std::vector<uint32_t>& hp) {
         if (par > 1 && r >= kRestarts - par_last) P.grow_par(seed_sets[r], as, hp, par);
