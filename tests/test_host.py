@@ -127,6 +127,25 @@ def test_partition_scrambled_ids_match_reference(ref, case):
         assert np.array_equal(got, want), (case, k, seed)
 
 
+@pytest.mark.parametrize("env", [{"PSP_PART_PAR_LAST": "8"}, {"PSP_PART_SERIAL": "1"},
+                                 {"PSP_PART_PAR_LAST": "8", "PSP_PART_SERIAL_RECENTER": "1"}])
+def test_partition_parallel_chains_match_reference(ref, env, monkeypatch):
+    """Every restart chain on 4 threads (grow_par + recenter_par), or all
+    serial: the assignment is the reference's either way, including graphs
+    with unreached pieces and isolated vertices."""
+    from paper_1503_07192_b200 import graphs
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    g = graphs.delaunay(5000, 8)
+    keep = np.random.default_rng(3).random(g.m) < 0.6
+    eu, ev, ew = g.eu[keep], g.ev[keep], g.ew[keep]
+    rgx = ref.graph(g.n, eu, ev, ew)
+    for k, seed in ((29, 4), (200, 1)):
+        want, _ = rgx.partition(k, seed)
+        got = P.partition_graph(P.Graph(g.n, eu, ev, ew), k, seed, threads=16)
+        assert np.array_equal(got, want), (env, k, seed)
+
+
 def test_partition_disconnected_matches_reference(ref):
     # unreached vertices + isolated vertices exercise finalize's fill step
     eu = np.array([0, 1, 2, 5, 6, 8], np.uint32)
